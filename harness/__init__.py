@@ -1,0 +1,221 @@
+"""Seeded synthetic inputs for the TV-reconstruction hot path (input generators only).
+
+Builds the workloads of BASELINE.json configs c1-c5 from the
+conventions of SURVEY.md §8(c): Siddon system matrix (C15), slice-major /
+view-major row order (C4), additive-ellipsoid phantom (C17), noise
+sigma = 0.01*||A x_true||/sqrt(m) (C16), random test point x ~ U[0,1) (seed 3).
+The paper's FORBILD phantom and 3D sphere geometry are not
+available; these seeded inputs stand in for them.
+
+This module holds none of the method's arithmetic.  It is shared by oracle/ and
+by the CUDA path's tests/bench, and imports neither.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "harness.cpp")
+_LIB = os.path.join(_HERE, "libtvrharness.so")
+
+SEED_PHANTOM = 1
+SEED_NOISE = 2
+SEED_X = 3
+
+
+def build(force: bool = False) -> str:
+    """Compile harness.cpp into libtvrharness.so (g++, OpenMP)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c++17",
+                               "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        i64, i32, f64, vp, u64 = (ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+                                  ctypes.c_void_p, ctypes.c_uint64)
+        L.hx_siddon2d.restype = i64
+        L.hx_siddon2d.argtypes = [i32, i32, i32, i32, vp, vp, vp]
+        L.hx_siddon3d.restype = i64
+        L.hx_siddon3d.argtypes = [i32, i32, i32, i32, i32, i32, f64, vp, vp, vp]
+        L.hx_replicate_slices.restype = None
+        L.hx_replicate_slices.argtypes = [i64, i64, vp, vp, vp, i64, i32, vp, vp, vp]
+        L.hx_simulate_projections.restype = None
+        L.hx_simulate_projections.argtypes = [i64, vp, vp, vp, vp, vp]
+        L.hx_phantom.restype = None
+        L.hx_phantom.argtypes = [i32, i32, i32, i32, u64, vp]
+        L.hx_uniform.restype = None
+        L.hx_uniform.argtypes = [i64, u64, vp]
+        L.hx_normal.restype = None
+        L.hx_normal.argtypes = [i64, u64, vp]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ----------------------------------------------------------------- matrices
+@dataclass
+class CSR:
+    """CSR matrix: int64 row_ptr[m+1], int32 col[nnz], fp32 val[nnz]."""
+    n_rows: int
+    n_cols: int
+    row_ptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1])
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+        return sp.csr_matrix((self.val.astype(np.float64), self.col, self.row_ptr),
+                             shape=(self.n_rows, self.n_cols))
+
+
+def siddon_slice(nx: int, ny: int, views: int, bins: int) -> CSR:
+    """One axial slice's Siddon matrix (rows v*bins + b, cols iy*nx + ix); C15."""
+    L = lib()
+    m = views * bins
+    rp = np.zeros(m + 1, np.int64)
+    nnz = L.hx_siddon2d(nx, ny, views, bins, _p(rp), None, None)
+    col = np.empty(nnz, np.int32)
+    val = np.empty(nnz, np.float32)
+    L.hx_siddon2d(nx, ny, views, bins, _p(rp), _p(col), _p(val))
+    return CSR(m, nx * ny, rp, col, val)
+
+
+def siddon_separable(nx: int, ny: int, nz: int, views: int, bins: int) -> CSR:
+    """Slice-separable parallel-beam matrix, slice-major rows (z*V + v)*bins + b (C4)."""
+    s = siddon_slice(nx, ny, views, bins)
+    m = s.n_rows * nz
+    nnz = s.nnz * nz
+    rp = np.empty(m + 1, np.int64)
+    col = np.empty(nnz, np.int32)
+    val = np.empty(nnz, np.float32)
+    lib().hx_replicate_slices(s.n_rows, s.nnz, _p(s.row_ptr), _p(s.col), _p(s.val),
+                              nx * ny, nz, _p(rp), _p(col), _p(val))
+    return CSR(m, nx * ny * nz, rp, col, val)
+
+
+def siddon_tilted(nx: int, ny: int, nz: int, views: int, det_rows: int, det_cols: int,
+                  phimax_deg: float = 10.0) -> CSR:
+    """Non-separable geometry of c5: rays tilted in z by up to +-phimax (C15), view-major rows."""
+    L = lib()
+    m = views * det_rows * det_cols
+    rp = np.zeros(m + 1, np.int64)
+    nnz = L.hx_siddon3d(nx, ny, nz, views, det_rows, det_cols, phimax_deg, _p(rp), None, None)
+    col = np.empty(nnz, np.int32)
+    val = np.empty(nnz, np.float32)
+    L.hx_siddon3d(nx, ny, nz, views, det_rows, det_cols, phimax_deg, _p(rp), _p(col), _p(val))
+    return CSR(m, nx * ny * nz, rp, col, val)
+
+
+# ----------------------------------------------------------- vectors (C17)
+def phantom(nx: int, ny: int, nz: int, n_ell: int, seed: int = SEED_PHANTOM) -> np.ndarray:
+    out = np.empty(nx * ny * nz, np.float32)
+    lib().hx_phantom(nx, ny, nz, n_ell, seed, _p(out))
+    return out
+
+
+def uniform(n: int, seed: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    lib().hx_uniform(n, seed, _p(out))
+    return out
+
+
+def normal(n: int, seed: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    lib().hx_normal(n, seed, _p(out))
+    return out
+
+
+def random_x(n: int, seed: int = SEED_X) -> np.ndarray:
+    """Test point x ~ U[0,1) rounded to fp32 (SURVEY §8(d) c2 'x a random nonnegative vector')."""
+    return uniform(n, seed).astype(np.float32)
+
+
+def simulate_data(A: CSR, x_true: np.ndarray, noise_rel: float = 0.01,
+                  seed: int = SEED_NOISE) -> np.ndarray:
+    """b = A x_true + e, e ~ N(0, sigma^2) i.i.d. over all m rows,
+    sigma = noise_rel*||A x_true||_2/sqrt(m) (C16; Eq.(11)).  Returns fp32."""
+    y = np.empty(A.n_rows, np.float64)
+    lib().hx_simulate_projections(A.n_rows, _p(A.row_ptr), _p(A.col), _p(A.val),
+                                  _p(np.ascontiguousarray(x_true, np.float32)), _p(y))
+    sigma = noise_rel * np.linalg.norm(y) / np.sqrt(A.n_rows)
+    e = sigma * normal(A.n_rows, seed)
+    return (y + e).astype(np.float32)
+
+
+# ---------------------------------------------------------- workload presets
+@dataclass
+class Workload:
+    name: str
+    grid: tuple            # (nx, ny, nz)
+    A: CSR
+    b: np.ndarray
+    x_true: np.ndarray
+    alpha: float = 0.01
+    tau: float = 1e-4
+    lo: float = 0.0
+    hi: float = float("inf")
+    geometry: dict = field(default_factory=dict)
+
+    @property
+    def N(self) -> int:
+        nx, ny, nz = self.grid
+        return nx * ny * nz
+
+
+# BASELINE.json configs (BJ:7-11)
+PRESETS = {
+    "c1": dict(grid=(32, 32, 32), views=12, bins=45, n_ell=6),
+    "c2": dict(grid=(128, 128, 128), views=60, bins=181, n_ell=6),
+    "c3": dict(grid=(256, 256, 256), views=90, bins=363, n_ell=10),
+    "c4": dict(grid=(256, 256, 256), views=90, bins=363, n_ell=10, hi=1.0),
+    "c5": dict(grid=(256, 256, 256), views=120, det=(256, 363), tilt=10.0, n_ell=10),
+}
+
+
+def separable_workload(name: str, grid, views: int, bins: int, n_ell: int,
+                       alpha: float = 0.01, tau: float = 1e-4, lo: float = 0.0,
+                       hi: float = float("inf"), noise_rel: float = 0.01) -> Workload:
+    nx, ny, nz = grid
+    A = siddon_separable(nx, ny, nz, views, bins)
+    xt = phantom(nx, ny, nz, n_ell)
+    b = simulate_data(A, xt, noise_rel)
+    return Workload(name, (nx, ny, nz), A, b, xt, alpha, tau, lo, hi,
+                    dict(kind="separable", views=views, bins=bins))
+
+
+def preset(name: str, **over) -> Workload:
+    p = dict(PRESETS[name])
+    p.update(over)
+    if "det" in p:
+        nx, ny, nz = p["grid"]
+        A = siddon_tilted(nx, ny, nz, p["views"], p["det"][0], p["det"][1], p["tilt"])
+        xt = phantom(nx, ny, nz, p["n_ell"])
+        b = simulate_data(A, xt)
+        return Workload(name, p["grid"], A, b, xt, p.get("alpha", 0.01), p.get("tau", 1e-4),
+                        p.get("lo", 0.0), p.get("hi", float("inf")),
+                        dict(kind="tilted", views=p["views"], det=p["det"], tilt=p["tilt"]))
+    return separable_workload(name, p["grid"], p["views"], p["bins"], p["n_ell"],
+                              p.get("alpha", 0.01), p.get("tau", 1e-4), p.get("lo", 0.0),
+                              p.get("hi", float("inf")))

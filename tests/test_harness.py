@@ -1,0 +1,137 @@
+"""Pins of the seeded input generators (harness/): Siddon geometry,
+phantom and RNG (C17), noise model (C16).  CPU only."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import harness
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden_counts():
+    rows = []
+    for line in open(os.path.join(GOLDEN, "siddon_counts.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, *nums = line.split()
+        rows.append((name, *map(int, nums)))
+    return rows
+
+
+@pytest.mark.parametrize("row", _golden_counts(), ids=lambda r: r[0])
+def test_siddon_slice_counts(row):
+    name, nx, ny, V, nb, nnz, empty, maxrow, nz, total = row
+    s = harness.siddon_slice(nx, ny, V, nb)
+    lens = np.diff(s.row_ptr)
+    assert s.nnz == nnz
+    assert int((lens == 0).sum()) == empty
+    assert int(lens.max()) == maxrow
+    assert s.nnz * nz == total
+
+
+def _chord(nx, ny, V, nb, v, b):
+    """Closed-form length of ray (v, b) inside the half-open box [-nx/2, nx/2) x [-ny/2, ny/2)."""
+    if v == 0:
+        c, s = 1.0, 0.0
+    elif 2 * v == V:
+        c, s = 0.0, 1.0
+    else:
+        th = math.pi * v / V
+        c, s = math.cos(th), math.sin(th)
+    sb = b - 0.5 * (nb - 1)
+    p = (-s * sb, c * sb)
+    d = (c, s)
+    n = (nx, ny)
+    t0, t1 = -math.inf, math.inf
+    for a in range(2):
+        lo, hi = -0.5 * n[a], 0.5 * n[a]
+        if d[a] == 0.0:
+            if not (lo <= p[a] < hi):
+                return 0.0
+        else:
+            ta, tb = (lo - p[a]) / d[a], (hi - p[a]) / d[a]
+            t0, t1 = max(t0, min(ta, tb)), min(t1, max(ta, tb))
+    return max(0.0, t1 - t0)
+
+
+@pytest.mark.parametrize("cfg", [(32, 32, 12, 45), (20, 12, 7, 31), (16, 16, 8, 23)])
+def test_siddon_row_sum_is_chord_length(cfg):
+    nx, ny, V, nb = cfg
+    s = harness.siddon_slice(nx, ny, V, nb)
+    for i in range(s.n_rows):
+        v, b = divmod(i, nb)
+        seg = s.val[s.row_ptr[i]:s.row_ptr[i + 1]].astype(np.float64)
+        chord = _chord(nx, ny, V, nb, v, b)
+        # each fp32 entry carries <= 2^-24 relative rounding
+        assert abs(seg.sum() - chord) <= 1e-12 + len(seg) * 2.0 ** -24 * max(1.0, seg.max(initial=0)), (i, seg.sum(), chord)
+
+
+def test_siddon_axis_aligned_rays_unit_entries_and_structure():
+    nx = ny = 32
+    V, nb = 12, 45
+    s = harness.siddon_slice(nx, ny, V, nb)
+    for v in (0, V // 2):
+        rows = slice(s.row_ptr[v * nb], s.row_ptr[(v + 1) * nb])
+        assert np.all(s.val[rows] == 1.0)
+    # strictly ascending, in-range columns within every row
+    for i in range(s.n_rows):
+        c = s.col[s.row_ptr[i]:s.row_ptr[i + 1]]
+        assert np.all(np.diff(c) > 0)
+        assert c.size == 0 or (c.min() >= 0 and c.max() < nx * ny)
+    # at 0 deg the ray with s_b = -16 runs along voxel row iy = 0 (half-open rule)
+    b = 22 - 16
+    c = s.col[s.row_ptr[b]:s.row_ptr[b + 1]]
+    assert np.array_equal(c, np.arange(32, dtype=np.int32))
+
+
+def test_separable_replication_layout():
+    A = harness.siddon_separable(8, 6, 5, 4, 11)
+    s = harness.siddon_slice(8, 6, 4, 11)
+    assert A.n_rows == 5 * s.n_rows and A.nnz == 5 * s.nnz
+    for z in range(5):
+        r0, r1 = z * s.n_rows, (z + 1) * s.n_rows
+        seg = slice(A.row_ptr[r0], A.row_ptr[r1])
+        assert np.array_equal(A.col[seg], s.col + z * 48)
+        assert np.array_equal(A.val[seg], s.val)
+
+
+def test_tilted_geometry_row_sums_and_layout():
+    A = harness.siddon_tilted(12, 10, 8, 5, 6, 9, 10.0)
+    assert A.n_rows == 5 * 6 * 9
+    for i in range(A.n_rows):
+        c = A.col[A.row_ptr[i]:A.row_ptr[i + 1]]
+        assert np.all(np.diff(c) > 0)
+    # zero tilt reduces to a stack of 2D slices: every row's columns lie in one slice
+    A0 = harness.siddon_tilted(8, 8, 4, 3, 4, 11, 0.0)
+    for i in range(A0.n_rows):
+        c = A0.col[A0.row_ptr[i]:A0.row_ptr[i + 1]]
+        if c.size:
+            assert len(set((c // 64).tolist())) == 1
+
+
+def test_splitmix64_reference_stream():
+    # SplitMix64 (Steele, Lea, Flood 2014) with seed 0: first outputs are
+    # 0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4; uniform() = (z >> 11) * 2^-53.
+    u = harness.uniform(2, 0)
+    assert u[0] == (0xE220A8397B1DCDAF >> 11) * 2.0 ** -53
+    assert u[1] == (0x6E789E6AA1B965F4 >> 11) * 2.0 ** -53
+
+
+def test_normal_moments_and_phantom_range():
+    z = harness.normal(200000, 7)
+    assert abs(z.mean()) < 0.01 and abs(z.std() - 1.0) < 0.01
+    x = harness.phantom(24, 24, 24, 6)
+    assert x.dtype == np.float32 and x.min() >= 0.0 and x.max() <= 1.0
+    assert (x > 0).mean() > 0.05
+    assert np.array_equal(x, harness.phantom(24, 24, 24, 6))
+
+
+def test_noise_level_rule(c1):
+    A = c1.A
+    y = A.to_scipy() @ c1.x_true.astype(np.float64)
+    e = c1.b.astype(np.float64) - y
+    # sigma = 0.01 ||A x_true|| / sqrt(m): ||e|| ~= 0.01 ||A x_true|| (C16)
+    assert abs(np.linalg.norm(e) / np.linalg.norm(y) - 0.01) < 0.001
