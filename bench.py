@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the libtvreg hot path (BASELINE.json metric on its configs[1] workload, c2).
+
+One step = one gradient evaluation (f, grad f) of the smoothed TV objective through the C ABI
+(tvr_objective_grad): A pass with fused residual (a1), A^T pass (a2), fused TV-gradient stencil
+(a4), fp64 reductions (a7).  Inputs (A + A^T = 2.6 GB) are far larger than the 126 MB L2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+N > 1 (torchrun): the volume is split into z-slabs (strong scaling); every step exchanges one
+halo slice with each z-neighbour and all-gathers the fp64 scalars over NCCL.  Timing is CUDA
+events on the library's stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gradient evals/s & HBM GB/s (Ax, A^T r, grad TV_tau); GPBB/UPN time-to-eps"
+UNIT = "gradient evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
+    return ap.parse_args()
+
+
+def workload_desc(name, w):
+    g = w.geometry
+    return dict(workload=f"{name}: {w.grid[0]}x{w.grid[1]}x{w.grid[2]} volume, slice-separable parallel beam, "
+                         f"{g.get('views')} views x {g.get('bins')} bins/slice, Siddon fp32 CSR + transposed CSR, "
+                         f"seeded ellipsoid phantom, 1% noise, alpha={w.alpha}, tau={w.tau}, x ~ U[0,1) seed 3",
+                N=w.N, m=w.A.n_rows, nnz=w.A.nnz, l2="inputs larger than L2 (A + A^T = "
+                f"{2 * 8 * w.A.nnz / 1e9:.2f} GB vs 126 MB L2); no flush needed")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+        self.marks = [None, None]
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def mark(self, i):
+        self.marks[i] = time.time()
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        t0, t1 = self.marks
+        rows = [s for t, s in self.samples if t0 is not None and t0 - 0.06 <= t <= t1 + 0.06]
+        if not rows:
+            rows = [s for _, s in self.samples[-3:]]
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            parts = [p.strip() for p in r.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return dict(sm_mhz=statistics.median(sm), sm_max_mhz=smax, reasons=sorted(reasons),
+                    samples=len(sm))
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_table():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+# ---------------------------------------------------------------- cpu baseline
+def cpu_baseline(w, budget_s=20.0, max_evals=5):
+    import oracle
+    nthreads = os.cpu_count() or 1
+    Po = oracle.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
+                        nthreads=nthreads).use_transpose()
+    import harness
+    x = harness.random_x(w.N)
+    Po.fg(x)  # warm-up
+    t0 = time.perf_counter()
+    n = 0
+    while n < max_evals and (time.perf_counter() - t0) < budget_s:
+        Po.fg(x)
+        n += 1
+    dt = time.perf_counter() - t0
+    return dict(value=n / dt, unit=UNIT, cores=nthreads, kind="oracle",
+                sample=f"{n} full fp64 gradient evaluations of {w.name} (A x row-parallel, A^T r "
+                       f"row-parallel over the oracle's own transposed CSR, TV single-threaded), "
+                       f"{dt:.1f} s on {nthreads} host threads")
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import harness
+    from paper_1105_4002_b200 import tvreg
+    from paper_1105_4002_b200.dist import local_slab, nccl_comm_from_process_group
+
+    torch.cuda.set_device(local_rank)
+    w = harness.preset(args.config)
+    stream = torch.cuda.current_stream()
+    comm = None
+    if world > 1:
+        sl = local_slab(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, world, rank)
+        comm = nccl_comm_from_process_group(world, rank, local_rank)
+        P = tvreg.Problem(sl.row_ptr, sl.col, sl.val, sl.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
+                          n_cols=w.N, world=world, rank=rank, z0=sl.z0, z1=sl.z1, nccl_comm=comm,
+                          device=local_rank, stream=stream.cuda_stream)
+        xfull = harness.random_x(w.N)
+        plane = w.grid[0] * w.grid[1]
+        x_h = np.ascontiguousarray(xfull[sl.z0 * plane:sl.z1 * plane])
+    else:
+        P = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
+                          device=local_rank, stream=stream.cuda_stream)
+        x_h = harness.random_x(w.N)
+    n_loc = P.n
+    x = torch.from_numpy(x_h).cuda()
+    g = torch.empty(n_loc, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        P.objective_grad(x, g)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.15)
+    P.profile(True)
+    P.launch_count(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.mark(0)
+    e0.record(stream)
+    for _ in range(args.steps):
+        P.objective_grad(x, g)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks.mark(1)
+    barrier()
+    launches = P.launch_count()
+    ms_total = e0.elapsed_time(e1)
+    stats = P.kernel_stats()
+    P.profile(False)
+    clk = clocks.stop()
+    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = args.steps / (ms_total / 1e3)   # whole-volume gradient evaluations per second
+
+    # ---- e2e through the host API: H2D x, D2H g and f inside the timed region
+    xh = torch.from_numpy(x_h.copy()).pin_memory()
+    gh = torch.empty(n_loc, dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        P.objective_grad_host(xh.numpy(), gh.numpy())
+    barrier()
+    torch.cuda.synchronize()
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    h0.record(stream)
+    for _ in range(args.steps):
+        P.objective_grad_host(xh.numpy(), gh.numpy())
+    h1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    te = torch.tensor([max(h0.elapsed_time(h1), wall * 1e3)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = dict(value=args.steps / (float(te.item()) / 1e3), unit=UNIT,
+               h2d_bytes_per_step=int(4 * n_loc * world), d2h_bytes_per_step=int((4 * n_loc + 8) * world))
+
+    # ---- roofline of the dominant kernel
+    peak, peak_src = peaks()
+    ktab = {}
+    for name, s in stats.items():
+        if s["launches"] == 0:
+            continue
+        ms = s["ms"] / s["launches"]
+        by = s["bytes"] / s["launches"]
+        gbs = by / (ms / 1e3) / 1e9
+        ktab[name] = dict(launches=s["launches"], ms_per_launch=ms, bytes_per_launch=by,
+                          achieved_gbs=gbs, frac=gbs / peak, share=s["ms"] / ms_total)
+    dom = max(ktab, key=lambda k: stats[k]["ms"])
+    tr = traffic_table().get(f"{args.config}:{dom}")
+    roofline = dict(bound="hbm", kernel=dom, achieved=ktab[dom]["achieved_gbs"], peak=peak,
+                    unit="GB/s", frac=ktab[dom]["achieved_gbs"] / peak, peak_source=peak_src,
+                    traffic=tr, bytes_per_launch=ktab[dom]["bytes_per_launch"],
+                    bytes_model="A pass: 8 nnz + 8(m+1) + 4N + 8m; A^T pass: 8 nnz + 8(N+1) + 4m + 4N "
+                                "(fp32 val, int32 col, int64 row_ptr; SURVEY §8(d))")
+    step_bytes = sum(s["bytes"] for s in stats.values()) / args.steps
+    out = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
+               warmup=args.warmup, ms_per_step=ms_step, higher_is_better=True,
+               scaling="strong" if world > 1 else "weak", vs_baseline=None, dtype="f64",
+               storage_dtype="f32", data="synthetic",
+               config=dict(workload_desc(args.config, w), parallelism=f"zslab{world}" if world > 1 else "single"),
+               roofline=roofline, e2e=e2e, gpu_launches=int(launches), clocks=clk,
+               kernels=ktab, step_hbm_gbs=step_bytes / (ms_step / 1e3) / 1e9,
+               step_frac=step_bytes / (ms_step / 1e3) / 1e9 / peak)
+
+    if rank == 0 and world == 1 and not args.no_solve:
+        out["solvers"] = solver_timings(tvreg, torch)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(w)
+    P.close()
+    if comm:
+        tvreg.nccl_comm_destroy(comm)
+    return out
+
+
+def solver_timings(tvreg, torch):
+    """Time-to-eps of GPBB and UPN on the c1 workload (BJ:7: REL 1e-6 gradient map)."""
+    import harness
+    w = harness.preset("c1")
+    res = {}
+    P = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
+                      stream=torch.cuda.current_stream().cuda_stream)
+    for solver in ("gpbb", "upn"):
+        x = torch.zeros(w.N, device="cuda")
+        r = getattr(P, f"solve_{solver}")(x, max_iters=20000, eps=1e-6)
+        res[solver] = dict(workload="c1 (32^3, 12 views x 45 bins, REL 1e-6)", converged=r.converged,
+                           iters=r.iters, n_f=r.n_f, n_grad=r.n_grad, seconds=r.seconds, f=r.f,
+                           ms_per_iter=1e3 * r.seconds / max(1, r.iters))
+    P.close()
+    return res
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args):
+    """The oracle (plain fp64 CPU) on the same workload; each step one full gradient evaluation,
+    the run bounded to ~2 minutes of CPU time."""
+    import harness
+    import oracle
+    w = harness.preset(args.config)
+    nthreads = os.cpu_count() or 1
+    Po = oracle.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
+                        nthreads=nthreads).use_transpose()
+    x = harness.random_x(w.N)
+    for _ in range(min(args.warmup, 1)):
+        Po.fg(x)
+    t0 = time.perf_counter()
+    n = 0
+    while n < args.steps and (time.perf_counter() - t0) < 120.0:
+        Po.fg(x)
+        n += 1
+    dt = time.perf_counter() - t0
+    v = n / dt
+    sample = (f"{n} of {args.steps} requested full fp64 gradient evaluations of {args.config} "
+              f"(bounded to 120 s), {nthreads} host threads")
+    return dict(impl="reference", metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=n,
+                warmup=args.warmup, ms_per_step=1e3 * dt / max(1, n), higher_is_better=True,
+                scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                config=workload_desc(args.config, w),
+                cpu_baseline=dict(value=v, unit=UNIT, cores=nthreads, kind="oracle", sample=sample),
+                e2e=dict(value=v, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return 0
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,204 @@
+/* libtvreg.h — C ABI of the B200 hot path for accelerated-gradient TV CT reconstruction.
+ *
+ * Paper: J. H. Jorgensen, T. L. Jensen, P. C. Hansen, S. H. Jensen, E. Y. Sidky, X. Pan,
+ * "Accelerated gradient methods for total-variation-based CT image reconstruction"
+ * (arXiv:1105.4002; /root/reference/PAPER.md cited as P:line).
+ *
+ * The library minimises the Huber-smoothed objective
+ *     phi_tau(x) = 1/2 ||A x - b||_2^2 + alpha * sum_j h_tau(||D_j x||_2),   x in Q = [lo, hi]^N
+ * (Eq. (1)-(2); h_tau(t) = t - tau/2 for t >= tau, t^2/(2 tau) otherwise; D_j the
+ * forward-difference gradient at voxel j with zero differences across each axis' last face)
+ * by GPBB (Alg. 1) or UPN (Alg. 3, with BT of Alg. 2),
+ * stopping on the gradient map G_nu (Eq. (10)).
+ *
+ * Conventions for every entry point:
+ *  - Every function returns a tvr_status; no C++ exception crosses this boundary.  On a
+ *    non-OK status tvr_last_error() returns a thread-local message.
+ *  - Volume vectors are fp32, x fastest, then y, then z; in z-slab mode a rank's vectors hold
+ *    only its slices [z0, z1) (N_local = nx*ny*(z1-z0)).  Data vectors are fp32 of m_local.
+ *  - "_dev" pointers are DEVICE pointers on the problem's device, caller-owned (e.g. torch
+ *    tensors' data_ptr()); "_host" pointers are host memory (pinned is fastest).
+ *  - Calls are ordered on the problem's CUDA stream and return once every host-side output
+ *    they report is valid (device outputs are complete when the call returns).
+ *  - In distributed mode every call is collective: all ranks make it in the same order.
+ *  - Arithmetic: fp32 storage; fp64 row accumulators, fp64 per-voxel TV math and fp64
+ *    fixed-order reductions (deterministic run to run).
+ */
+#ifndef LIBTVREG_H
+#define LIBTVREG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TVR_ABI_VERSION 1
+
+typedef enum {
+  TVR_OK = 0,
+  TVR_NOT_CONVERGED = 1,    /* solver reached max_iters; x and the result are still filled in */
+  TVR_E_ARG = -1,           /* invalid argument (NULL, size, tau <= 0, alpha < 0, lo >= hi, ...) */
+  TVR_E_CSR = -2,           /* malformed CSR: row_ptr not monotone / not 0..nnz, column out of
+                               range or not strictly ascending within a row, non-finite value */
+  TVR_E_NOT_SEPARABLE = -3, /* z-slab mode: a local row touches voxels outside the rank's slab */
+  TVR_E_CUDA = -4,          /* CUDA runtime error (message names the call) */
+  TVR_E_NCCL = -5,          /* NCCL error */
+  TVR_E_OOM = -6,           /* device allocation failed */
+  TVR_E_NONFINITE = -7,     /* non-finite objective or gradient */
+  TVR_E_LINESEARCH = -8,    /* GPBB beta < beta_min or BT exceeded bt_max trials */
+  TVR_E_THETA = -9          /* UPN theta outside (0, 1] */
+} tvr_status;
+
+typedef struct tvr_problem tvr_problem; /* opaque, owned by the library */
+
+/* System matrix A in CSR, HOST arrays, read only during tvr_create (caller keeps ownership).
+ * row_ptr[n_rows+1] int64 (row_ptr[0] = 0, row_ptr[n_rows] = nnz, non-decreasing),
+ * col_idx[nnz] int32 GLOBAL voxel indices, strictly ascending within each row,
+ * val[nnz] fp32 finite.  n_cols = nx*ny*nz (global). */
+typedef struct {
+  int64_t n_rows, n_cols, nnz;
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  const float* val;
+} tvr_csr;
+
+typedef struct {
+  int32_t nx, ny, nz; /* global volume; voxel j = (z*ny + y)*nx + x */
+} tvr_grid;
+
+enum { TVR_SHARD_NONE = 0, TVR_SHARD_ZSLAB = 1 };
+
+/* Distribution / placement.  NULL => one GPU, current device, a library-created stream.
+ * ZSLAB: rank owns slices [z0, z1) and the rows of A whose voxels lie there; the TV stencil
+ * exchanges one halo slice with each z-neighbour over NCCL (nccl_comm from
+ * tvr_nccl_comm_init), scalars are all-gathered and summed in rank order. */
+typedef struct {
+  int32_t world, rank, mode;
+  int32_t z0, z1;
+  void* nccl_comm;   /* ncclComm_t or NULL (world == 1) */
+  int32_t device;    /* CUDA device ordinal, or -1 for the current device */
+  void* cuda_stream; /* cudaStream_t to order work on, or NULL for a library-created stream */
+} tvr_dist;
+
+/* Create a problem: validates A (TVR_E_CSR), copies A and b to device memory, builds the
+ * canonical transposed CSR on the device (bit-exact: rows of A^T ascending by source row,
+ * values moved bit for bit), and detects slice-separable structure for slab-staged SpMV.
+ * b_host: m_local fp32 values (host).  alpha >= 0, tau > 0, lo < hi (+-INFINITY allowed). */
+int tvr_create(tvr_problem** out, const tvr_csr* A_local, const float* b_host, tvr_grid grid,
+               double alpha, double tau, double lo, double hi, const tvr_dist* dist);
+void tvr_destroy(tvr_problem* p);
+
+typedef struct {
+  int64_t m_local, n_local, nnz_local; /* local sizes (n_local = voxels owned) */
+  int32_t z0, z1;                      /* owned slices */
+  int32_t slab_staged_A, slab_staged_AT; /* 1 when the smem slice-staged SpMV is used */
+  int64_t device_bytes;                /* device memory held by the problem */
+} tvr_info;
+int tvr_get_info(const tvr_problem* p, tvr_info* info);
+
+/* Objective parts: phi = fidelity + alpha * tv. */
+typedef struct {
+  double fidelity, tv, f;
+} tvr_fparts;
+
+/* f = phi_tau(x) and g = grad phi_tau(x) = A^T(Ax - b) + alpha grad TV_tau(x).
+ * x_dev, g_dev: N_local fp32 device vectors (g_dev may be NULL: value only, no A^T pass).
+ * parts may be NULL. */
+int tvr_objective_grad(tvr_problem* p, const float* x_dev, double* f_out, float* g_dev,
+                       tvr_fparts* parts);
+/* Same computation with HOST x and g (copied inside the call: the end-to-end API). */
+int tvr_objective_grad_host(tvr_problem* p, const float* x_host, double* f_out, float* g_host,
+                            tvr_fparts* parts);
+
+enum { TVR_STOP_REL = 0, TVR_STOP_ABS_PER_N = 1 };
+
+/* GPBB options; tvr_gpbb_default fills K = 2, sigma = 0.1, beta0 = 0.95,
+ * beta_min = 1e-10, eps = 1e-6, TVR_STOP_REL, max_iters = 10000. */
+typedef struct {
+  int64_t max_iters;
+  double eps;
+  int32_t stop_mode; /* REL: ||G_nu(x_k)|| <= eps ||G_1(x_0)||; ABS_PER_N: ||G_nu(x_k)||/N <= eps */
+  int32_t K;
+  double sigma, beta0, beta_min;
+} tvr_gpbb_opts;
+
+/* UPN options; tvr_upn_default fills L0 = 1, mu0 = 1 (mu_bar = L_bar), rho_L = 1.3, bt_max = 200. */
+typedef struct {
+  int64_t max_iters;
+  double eps;
+  int32_t stop_mode;
+  double L0, mu0, rho_L;
+  int32_t bt_max;
+} tvr_upn_opts;
+
+void tvr_gpbb_default(tvr_gpbb_opts* o);
+void tvr_upn_default(tvr_upn_opts* o);
+
+/* One record per accepted iteration (GPBB: the iterate tested at the top of iteration k;
+ * UPN: x_{k}).  step_or_inv_L = theta_k (GPBB) or 1/L_k (UPN). */
+typedef struct {
+  int64_t iter;
+  double f, gmap_rel, gmap_abs_per_n, step_or_inv_L, mu, L;
+  int32_t ls_trials;
+  int32_t _pad;
+} tvr_record;
+
+typedef struct {
+  int32_t converged;
+  int32_t _pad;
+  int64_t iters, n_f, n_grad, n_ls;
+  double f, gmap_rel, gmap_abs_per_n, gmap_ref, seconds, bytes;
+} tvr_result;
+
+/* Solve from x_dev_inout (projected onto Q first); on return it holds the last iterate
+ * tested by the stopping rule.  hist may be NULL; records beyond hist_cap are dropped.
+ * Returns TVR_OK (converged), TVR_NOT_CONVERGED, or an error. */
+int tvr_solve_gpbb(tvr_problem* p, float* x_dev_inout, const tvr_gpbb_opts* opts, tvr_result* res,
+                   tvr_record* hist, int64_t hist_cap);
+int tvr_solve_upn(tvr_problem* p, float* x_dev_inout, const tvr_upn_opts* opts, tvr_result* res,
+                  tvr_record* hist, int64_t hist_cap);
+
+/* ---- inspection hooks (tests) ---- */
+/* y = A x - b (fused residual, the a1 pass); returns 1/2 ||Ax - b||^2 in *fid (nullable). */
+int tvr_residual(tvr_problem* p, const float* x_dev, float* r_dev, double* fid);
+/* w = A^T y using the stored transposed CSR (the a2 pass). y_dev: m_local, w_dev: N_local. */
+int tvr_apply_AT(tvr_problem* p, const float* y_dev, float* w_dev);
+/* TV_tau(x) and, if grad_dev != NULL, grad TV_tau(x). */
+int tvr_tv(tvr_problem* p, const float* x_dev, double* tv_out, float* grad_dev);
+/* ||G_nu(x)||_2 with G_nu(x) = nu (x - P_Q(x - grad f(x)/nu)) (Eq. (10)); G_dev nullable. */
+int tvr_gradient_map(tvr_problem* p, const float* x_dev, double nu, double* norm_out, float* G_dev);
+/* Copy the device transposed CSR to host arrays of n_local+1 / nnz_local entries. */
+int tvr_get_AT(tvr_problem* p, int64_t* row_ptr_host, int32_t* col_host, float* val_host);
+
+/* ---- per-kernel timing (CUDA events on the problem's stream) ---- */
+typedef struct {
+  char name[32];
+  int64_t launches;
+  double total_ms;
+  double bytes; /* algorithmic bytes summed over launches */
+} tvr_kernel_stat;
+int tvr_profile_enable(tvr_problem* p, int on); /* on=1 clears counters and starts recording */
+int tvr_profile_get(tvr_problem* p, tvr_kernel_stat* out, int cap, int* n_out);
+/* Number of kernels launched by the library since tvr_create (or the last reset). */
+int64_t tvr_launch_count(const tvr_problem* p, int reset);
+
+/* ---- NCCL bootstrap (z-slab mode) ---- */
+int tvr_nccl_unique_id_size(void);
+int tvr_nccl_get_unique_id(void* id_out);
+int tvr_nccl_comm_init(void** comm_out, const void* id, int world, int rank, int device);
+int tvr_nccl_comm_destroy(void* comm);
+
+/* Optional device allocator hook (e.g. the PyTorch caching allocator); NULL restores cudaMalloc. */
+typedef void* (*tvr_alloc_fn)(size_t bytes, int device, void* stream, void* ctx);
+typedef void (*tvr_free_fn)(void* ptr, int device, void* stream, void* ctx);
+int tvr_set_allocator(tvr_alloc_fn alloc_fn, tvr_free_fn free_fn, void* ctx);
+
+const char* tvr_last_error(void);
+int tvr_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIBTVREG_H */

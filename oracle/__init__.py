@@ -154,6 +154,18 @@ class Problem:
         nx, ny, nz = self.grid
         return nx * ny * nz
 
+    def use_transpose(self):
+        """Compute A^T y row-parallel over the oracle's own canonical transpose (the
+        multi-core timing mode of SURVEY §8(d)); the default is the scatter over A's rows."""
+        self._T = transpose(self.row_ptr, self.col, self.val, self.N)
+        return self
+
+    def rmatvec(self, y) -> np.ndarray:
+        T = getattr(self, "_T", None)
+        if T is not None:
+            return matvec(T[0], T[1], T[2], y, self.nthreads)
+        return rmatvec(self.row_ptr, self.col, self.val, y, self.N)
+
     # r = A x - b
     def residual(self, x) -> np.ndarray:
         return matvec(self.row_ptr, self.col, self.val, x, self.nthreads) - self.b.astype(np.float64)
@@ -178,7 +190,7 @@ class Problem:
         self.n_g += 1
         r = self.residual(x)
         t, gt = tv(self.grid, x, self.tau, want_grad=True)
-        g = rmatvec(self.row_ptr, self.col, self.val, r, self.N) + self.alpha * gt
+        g = self.rmatvec(r) + self.alpha * gt
         val = 0.5 * float(r @ r) + self.alpha * t
         if not (math.isfinite(val) and np.all(np.isfinite(g))):
             raise NonFiniteError("f/g")

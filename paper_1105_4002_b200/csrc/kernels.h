@@ -1,0 +1,76 @@
+// Internal kernel launchers of libtvreg (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tvr {
+
+struct SpmvArgs {
+  const int64_t* rp;
+  const int32_t* col;
+  const float* val;
+  const float* src;  // gather vector (x for A, r for A^T), local indices
+  const float* b;    // non-null: out = A src - b and sum of squares
+  float* out;
+  const int64_t* item_row;   // nitems+1 row boundaries
+  const int32_t* item_slice; // per item slice id (staged)
+  int64_t nitems;
+  const int64_t* win_lo;     // per slice: first gather index of the slice window
+  const int32_t* win_len;    // per slice: window length
+  int32_t pad_shift, pad_extra;
+  double* partials;
+  unsigned* counter;
+  double* scal;  // non-null: write 1/2-less sum r^2 to scal[0]
+};
+
+cudaError_t launch_spmv(const SpmvArgs& a, int lpr, bool staged, int padmode, int grid, int block,
+                        size_t smem, cudaStream_t st);
+cudaError_t launch_momentum_resid(int64_t m, const float* r1, const float* r0, double beta,
+                                  double* partials, unsigned* counter, double* scal, int grid,
+                                  cudaStream_t st);
+cudaError_t launch_project(int64_t n, float* x, double lo, double hi, int grid, cudaStream_t st);
+cudaError_t launch_gradient_map(int64_t n, const float* x, const float* g, double nu, double lo,
+                                double hi, float* G, double* partials, unsigned* counter,
+                                double* scal, int grid, cudaStream_t st);
+
+struct TVArgs {
+  int nx, ny, nzl;
+  int64_t plane;
+  int zg0, nzg;  // global z of local plane 0; global nz
+  double tau, alpha, lo, hi;
+  // KIND_GRAD
+  const float* w1;
+  const float* w0;  // non-null: w = (1+wbeta) w1 - wbeta w0
+  double wbeta;
+  float* g_out;
+  float* v_out;     // GRAD: optional; TRIAL: required
+  const float* xp;  // BB reductions (with gp)
+  const float* gp;
+  double stop_step; // > 0: gradient-map reduction with this step
+  // KIND_TRIAL
+  const float* tx;
+  const float* tg;
+  const float* xo;  // mu_k reductions
+  double* partials;
+  unsigned* counter;
+  double* scal;     // 6 doubles
+};
+
+cudaError_t launch_tv_grad_plain(const TVArgs& a, const float* x, cudaStream_t st);
+cudaError_t launch_tv_grad_momentum(const TVArgs& a, const float* x1, const float* x0, double beta,
+                                    cudaStream_t st);
+cudaError_t launch_tv_trial(const TVArgs& a, const float* x, const float* g, double s,
+                            cudaStream_t st);
+int tv_num_blocks(int nx, int ny, int nzl);
+cudaError_t launch_halo_fill_trial(const float* x, const float* g, double s, double lo, double hi,
+                                   int64_t plane, int nzl, int has_lo, int has_hi, float* v,
+                                   cudaStream_t st);
+cudaError_t launch_halo_fill_momentum(const float* x1, const float* x0, double beta, int64_t plane,
+                                      int nzl, int has_lo, int has_hi, float* v, cudaStream_t st);
+
+cudaError_t build_transpose(int64_t m, int64_t n, int64_t nnz, const int64_t* rp,
+                            const int32_t* col, const float* val, int64_t* rowT, int32_t* colT,
+                            float* valT, int32_t* scratch_i32_n, int32_t* scratch_col,
+                            float* scratch_val, int64_t* scratch_blocks, cudaStream_t st);
+
+}  // namespace tvr

@@ -1,0 +1,771 @@
+// libtvreg: problem creation, device memory, SpMV plans, pass functions and the C ABI
+// entry points other than the solvers (solvers.cu) and NCCL plumbing (dist.cu).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "problem.h"
+
+namespace tvr {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+const char* kKernelNames[K_COUNT] = {"spmv_A", "spmv_AT", "tv_grad", "tv_trial",
+                                     "momentum", "project", "gmap"};
+
+static tvr_alloc_fn g_alloc = nullptr;
+static tvr_free_fn g_free = nullptr;
+static void* g_alloc_ctx = nullptr;
+
+int dev_alloc(tvr_problem* p, void** ptr, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  void* q = nullptr;
+  if (g_alloc) {
+    q = g_alloc(bytes, p->device, (void*)p->stream, g_alloc_ctx);
+  } else if (cudaMalloc(&q, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    q = nullptr;
+  }
+  if (!q) {
+    set_error("device allocation of " + std::to_string(bytes) + " bytes failed");
+    return TVR_E_OOM;
+  }
+  p->allocs.push_back(q);
+  p->device_bytes += (int64_t)bytes;
+  *ptr = q;
+  return TVR_OK;
+}
+
+static void dev_free_all(tvr_problem* p) {
+  for (void* q : p->allocs) {
+    if (g_free) g_free(q, p->device, (void*)p->stream, g_alloc_ctx);
+    else cudaFree(q);
+  }
+  p->allocs.clear();
+}
+
+int64_t n_local(const tvr_problem* p) { return p->plane * p->nzl; }
+float* volvec(tvr_problem* p, int i) { return p->vol[i]; }
+float* datvec(tvr_problem* p, int i) { return p->dat[i]; }
+
+// --------------------------------------------------------------- timing
+static cudaEvent_t get_event(tvr_problem* p) {
+  if (!p->event_pool.empty()) {
+    cudaEvent_t e = p->event_pool.back();
+    p->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+static void resolve_timings(tvr_problem* p) {
+  for (auto& t : p->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
+      p->kt_ms[t.kid] += ms;
+      p->kt_bytes[t.kid] += t.bytes;
+      p->kt_launches[t.kid] += 1;
+    }
+    p->event_pool.push_back(t.a);
+    p->event_pool.push_back(t.b);
+  }
+  p->pending.clear();
+}
+
+template <class F>
+static int launch(tvr_problem* p, int kid, double bytes, F&& f) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (p->prof) {
+    a = get_event(p);
+    b = get_event(p);
+    cudaEventRecord(a, p->stream);
+  }
+  cudaError_t e = f();
+  if (e != cudaSuccess) {
+    set_error(std::string("kernel ") + kKernelNames[kid] + ": " + cudaGetErrorString(e));
+    return TVR_E_CUDA;
+  }
+  if (p->prof) {
+    cudaEventRecord(b, p->stream);
+    p->pending.push_back({kid, a, b, bytes});
+  }
+  p->launches++;
+  p->bytes_total += bytes;
+  return TVR_OK;
+}
+
+static int elem_grid(tvr_problem* p, int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)p->num_sms * 8));
+}
+
+// ----------------------------------------------------------------- passes
+static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, const float* src,
+                          const float* b, float* out, double* scal) {
+  SpmvArgs a;
+  a.rp = transposed ? p->rpT : p->rp;
+  a.col = transposed ? p->colT : p->col;
+  a.val = transposed ? p->valT : p->val;
+  a.src = src;
+  a.b = b;
+  a.out = out;
+  a.item_row = pl.item_row;
+  a.item_slice = pl.item_slice;
+  a.nitems = pl.nitems;
+  a.win_lo = pl.win_lo;
+  a.win_len = pl.win_len;
+  a.pad_shift = pl.pad_shift;
+  a.pad_extra = pl.pad_extra;
+  a.partials = p->partials;
+  a.counter = p->counter;
+  a.scal = scal;
+  return a;
+}
+
+int pass_residual(tvr_problem* p, const float* x, float* r, int slot) {
+  const SpmvPlan& pl = p->planA;
+  SpmvArgs a = spmv_args(p, pl, false, x, p->b, r, p->dscal + slot);
+  const double bytes = 8.0 * p->nnz + 8.0 * (p->m + 1) + 4.0 * n_local(p) + 8.0 * p->m;
+  return launch(p, K_SPMV_A, bytes, [&] {
+    return launch_spmv(a, pl.lpr, pl.staged, pl.padmode, pl.grid, pl.block, pl.smem, p->stream);
+  });
+}
+
+int pass_AT(tvr_problem* p, const float* r, float* w) {
+  const SpmvPlan& pl = p->planT;
+  SpmvArgs a = spmv_args(p, pl, true, r, nullptr, w, nullptr);
+  const double bytes = 8.0 * p->nnz + 8.0 * (n_local(p) + 1) + 4.0 * p->m + 4.0 * n_local(p);
+  return launch(p, K_SPMV_AT, bytes, [&] {
+    return launch_spmv(a, pl.lpr, pl.staged, pl.padmode, pl.grid, pl.block, pl.smem, p->stream);
+  });
+}
+
+static TVArgs tv_args(tvr_problem* p, int slot) {
+  TVArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.nx = p->nx;
+  a.ny = p->ny;
+  a.nzl = p->nzl;
+  a.plane = p->plane;
+  a.zg0 = p->z0;
+  a.nzg = p->nz;
+  a.tau = p->tau;
+  a.alpha = p->alpha;
+  a.lo = p->lo;
+  a.hi = p->hi;
+  a.partials = p->partials;
+  a.counter = p->counter;
+  a.scal = p->dscal + slot;
+  return a;
+}
+
+int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta, const float* w1,
+                 const float* w0, double wbeta, float* g, float* v_out, const float* xp,
+                 const float* gp, double stop_step, int slot, double alpha) {
+  TVArgs a = tv_args(p, slot);
+  a.alpha = alpha;
+  a.w1 = w1;
+  a.w0 = w0;
+  a.wbeta = wbeta;
+  a.g_out = g;
+  a.v_out = v_out;
+  a.xp = xp;
+  a.gp = gp;
+  a.stop_step = stop_step;
+  const double N = (double)n_local(p);
+  const double bytes = N * (4.0 * (x0 ? 2 : 1) + (w1 ? 4.0 : 0.0) + (w0 ? 4.0 : 0.0) +
+                            (g ? 4.0 : 0.0) + (v_out ? 4.0 : 0.0) + (xp ? 8.0 : 0.0));
+  return launch(p, K_TV_GRAD, bytes, [&] {
+    return x0 ? launch_tv_grad_momentum(a, x, x0, beta, p->stream)
+              : launch_tv_grad_plain(a, x, p->stream);
+  });
+}
+
+int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta, const float* w1,
+                 const float* w0, double wbeta, float* g, float* v_out, const float* xp,
+                 const float* gp, double stop_step, int slot) {
+  return pass_tv_grad(p, x, x0, beta, w1, w0, wbeta, g, v_out, xp, gp, stop_step, slot, p->alpha);
+}
+
+int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, float* v,
+                  double stop_step, const float* xo, int slot) {
+  TVArgs a = tv_args(p, slot);
+  a.v_out = v;
+  a.tx = x;
+  a.tg = g;
+  a.xo = xo;
+  a.stop_step = stop_step;
+  const double N = (double)n_local(p);
+  const double bytes = N * (12.0 + (xo ? 4.0 : 0.0));
+  return launch(p, K_TV_TRIAL, bytes, [&] { return launch_tv_trial(a, x, g, s, p->stream); });
+}
+
+int pass_momentum(tvr_problem* p, const float* r1, const float* r0, double beta, int slot) {
+  const int grid = elem_grid(p, p->m);
+  return launch(p, K_MOMENTUM, 8.0 * p->m, [&] {
+    return launch_momentum_resid(p->m, r1, r0, beta, p->partials, p->counter, p->dscal + slot,
+                                 grid, p->stream);
+  });
+}
+
+int pass_project(tvr_problem* p, float* x) {
+  const int64_t n = n_local(p);
+  const int grid = elem_grid(p, n);
+  return launch(p, K_PROJECT, 8.0 * n,
+                [&] { return launch_project(n, x, p->lo, p->hi, grid, p->stream); });
+}
+
+int pass_gmap(tvr_problem* p, const float* x, const float* g, double nu, float* G, int slot) {
+  const int64_t n = n_local(p);
+  const int grid = elem_grid(p, n);
+  return launch(p, K_GMAP, (G ? 12.0 : 8.0) * n, [&] {
+    return launch_gradient_map(n, x, g, nu, p->lo, p->hi, G, p->partials, p->counter,
+                               p->dscal + slot, grid, p->stream);
+  });
+}
+
+int fetch_scalars(tvr_problem* p, int nslots) {
+  if (p->world > 1) return dist_sum_scalars(p, p->hscal, nslots);
+  TVR_CUDA(cudaMemcpyAsync(p->hscal, p->dscal, sizeof(double) * nslots, cudaMemcpyDeviceToHost,
+                           p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  if (p->prof) resolve_timings(p);
+  return TVR_OK;
+}
+
+void resolve_pending_timings(tvr_problem* p) {
+  if (p->prof) resolve_timings(p);
+}
+
+// ------------------------------------------------------------------ plans
+// Split rows [r0, r1) into items of about `target` nonzeros (at least one row each).
+static void split_rows(const int64_t* rp, int64_t r0, int64_t r1, int64_t target, int32_t slice,
+                       std::vector<int64_t>& rows, std::vector<int32_t>& slices) {
+  int64_t start = r0;
+  while (start < r1) {
+    int64_t end = start + 1;
+    const int64_t lim = rp[start] + target;
+    // binary search the first row boundary reaching lim
+    int64_t lo = start + 1, hi = r1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (rp[mid] >= lim) hi = mid;
+      else lo = mid + 1;
+    }
+    end = std::max(end, lo);
+    rows.push_back(start);
+    slices.push_back(slice);
+    start = end;
+  }
+}
+
+static int upload(tvr_problem* p, void** dst, const void* src, size_t bytes) {
+  TVR_TRY(dev_alloc(p, dst, bytes));
+  TVR_CUDA(cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, p->stream));
+  return TVR_OK;
+}
+
+// rp: host row pointer of the operator (n_rows+1); slices: n_slices+1 row boundaries when
+// separable; windows: per slice gather window (lo, len); pitch padding for the A pass.
+static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& rp, int64_t n_rows,
+                     bool separable, const std::vector<int64_t>& slice_rows,
+                     const std::vector<int64_t>& win_lo, const std::vector<int32_t>& win_len,
+                     int lpr, bool pad) {
+  pl.lpr = lpr;
+  pl.block = 512;
+  size_t smem = 0;
+  int padmode = 0, pad_shift = 0, pad_extra = 0;
+  if (separable) {
+    int32_t maxlen = 0;
+    for (int32_t l : win_len) maxlen = std::max(maxlen, l);
+    if (pad && p->nx >= 32 && (p->nx & (p->nx - 1)) == 0) {
+      padmode = 1;
+      pad_shift = 0;
+      while ((1 << pad_shift) < p->nx) ++pad_shift;
+      pad_extra = ((3 - (p->nx % 32)) % 32 + 32) % 32;
+      smem = sizeof(float) * ((size_t)maxlen + ((size_t)maxlen >> pad_shift) * pad_extra);
+    } else {
+      smem = sizeof(float) * (size_t)maxlen;
+    }
+    int maxsmem = 0;
+    cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+    // leave room for the reduction scratch of the kernel
+    if (smem + 2048 > (size_t)maxsmem) separable = false;
+  }
+  pl.staged = separable;
+  pl.padmode = separable ? padmode : 0;
+  pl.pad_shift = pad_shift;
+  pl.pad_extra = pad_extra;
+  pl.smem = separable ? smem : 0;
+
+  // occupancy-sized persistent grid
+  int occ = 1;
+  {
+    // query via a dry launch configuration: use the runtime's occupancy calculator on the
+    // instantiated kernel is internal to spmv.cu; approximate from smem and threads
+    int smem_per_sm = 0;
+    cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, p->device);
+    const int by_threads = 2048 / pl.block;
+    const int by_smem = pl.smem ? (int)(smem_per_sm / (pl.smem + 1024)) : by_threads;
+    occ = std::max(1, std::min(by_threads, by_smem));
+  }
+  pl.grid = p->num_sms * occ;
+
+  const int64_t nnz = rp[n_rows];
+  std::vector<int64_t> rows;
+  std::vector<int32_t> slices;
+  const int64_t target = std::max<int64_t>(2048, nnz / ((int64_t)pl.grid * 16) + 1);
+  if (separable) {
+    for (size_t z = 0; z + 1 < slice_rows.size(); ++z)
+      split_rows(rp.data(), slice_rows[z], slice_rows[z + 1], target, (int32_t)z, rows, slices);
+  } else {
+    split_rows(rp.data(), 0, n_rows, target, 0, rows, slices);
+  }
+  rows.push_back(n_rows);
+  pl.nitems = (int64_t)slices.size();
+  if (pl.grid > pl.nitems) pl.grid = (int)std::max<int64_t>(1, pl.nitems);
+  TVR_TRY(upload(p, (void**)&pl.item_row, rows.data(), sizeof(int64_t) * rows.size()));
+  TVR_TRY(upload(p, (void**)&pl.item_slice, slices.data(), sizeof(int32_t) * std::max<size_t>(1, slices.size())));
+  if (separable) {
+    TVR_TRY(upload(p, (void**)&pl.win_lo, win_lo.data(), sizeof(int64_t) * win_lo.size()));
+    TVR_TRY(upload(p, (void**)&pl.win_len, win_len.data(), sizeof(int32_t) * win_len.size()));
+  }
+  return TVR_OK;
+}
+
+}  // namespace tvr
+
+using namespace tvr;
+
+// ===================================================================== C ABI
+extern "C" {
+
+const char* tvr_last_error(void) { return g_err.c_str(); }
+int tvr_abi_version(void) { return TVR_ABI_VERSION; }
+
+int tvr_set_allocator(tvr_alloc_fn a, tvr_free_fn f, void* ctx) {
+  if ((a == nullptr) != (f == nullptr)) {
+    set_error("tvr_set_allocator: alloc and free must both be set or both NULL");
+    return TVR_E_ARG;
+  }
+  g_alloc = a;
+  g_free = f;
+  g_alloc_ctx = ctx;
+  return TVR_OK;
+}
+
+void tvr_gpbb_default(tvr_gpbb_opts* o) {
+  if (!o) return;
+  o->max_iters = 10000;
+  o->eps = 1e-6;
+  o->stop_mode = TVR_STOP_REL;
+  o->K = 2;
+  o->sigma = 0.1;
+  o->beta0 = 0.95;
+  o->beta_min = 1e-10;
+}
+
+void tvr_upn_default(tvr_upn_opts* o) {
+  if (!o) return;
+  o->max_iters = 10000;
+  o->eps = 1e-6;
+  o->stop_mode = TVR_STOP_REL;
+  o->L0 = 1.0;
+  o->mu0 = 1.0;
+  o->rho_L = 1.3;
+  o->bt_max = 200;
+}
+
+static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tvr_grid grid,
+                       double alpha, double tau, double lo, double hi, const tvr_dist* dist) {
+  if (!A || !b_host) { set_error("tvr_create: NULL argument"); return TVR_E_ARG; }
+  if (grid.nx <= 0 || grid.ny <= 0 || grid.nz <= 0) { set_error("tvr_create: bad grid"); return TVR_E_ARG; }
+  if (!(tau > 0.0) || !std::isfinite(tau)) { set_error("tvr_create: tau must be > 0"); return TVR_E_ARG; }
+  if (!(alpha >= 0.0) || !std::isfinite(alpha)) { set_error("tvr_create: alpha must be >= 0"); return TVR_E_ARG; }
+  if (!(lo < hi) || std::isnan(lo) || std::isnan(hi)) { set_error("tvr_create: need lo < hi"); return TVR_E_ARG; }
+  p->nx = grid.nx; p->ny = grid.ny; p->nz = grid.nz;
+  p->plane = (int64_t)grid.nx * grid.ny;
+  const int64_t Nglob = p->plane * grid.nz;
+  if (A->n_cols != Nglob) { set_error("tvr_create: A.n_cols != nx*ny*nz"); return TVR_E_ARG; }
+  if (A->n_rows < 0 || A->nnz < 0 || (A->nnz > 0 && (!A->col_idx || !A->val)) || !A->row_ptr) {
+    set_error("tvr_create: bad CSR sizes/pointers");
+    return TVR_E_ARG;
+  }
+  p->alpha = alpha; p->tau = tau; p->lo = lo; p->hi = hi;
+  p->z0 = 0; p->z1 = grid.nz; p->device = -1;
+  cudaStream_t user_stream = nullptr;
+  if (dist) {
+    p->world = dist->world < 1 ? 1 : dist->world;
+    p->rank = dist->rank;
+    p->mode = dist->mode;
+    p->comm = dist->nccl_comm;
+    p->device = dist->device;
+    user_stream = (cudaStream_t)dist->cuda_stream;
+    if (p->mode == TVR_SHARD_ZSLAB) {
+      p->z0 = dist->z0; p->z1 = dist->z1;
+      if (p->z0 < 0 || p->z1 > grid.nz || p->z0 >= p->z1) { set_error("tvr_create: bad slab"); return TVR_E_ARG; }
+    } else if (p->mode != TVR_SHARD_NONE) {
+      set_error("tvr_create: unknown shard mode");
+      return TVR_E_ARG;
+    }
+    if (p->world > 1 && (p->mode != TVR_SHARD_ZSLAB || !p->comm)) {
+      set_error("tvr_create: world > 1 needs ZSLAB mode and an NCCL communicator");
+      return TVR_E_ARG;
+    }
+  }
+  p->nzl = p->z1 - p->z0;
+
+  // ---- validate the CSR (host) ----
+  const int64_t m = A->n_rows, nnz = A->nnz;
+  const int64_t* rp = A->row_ptr;
+  if (rp[0] != 0 || rp[m] != nnz) { set_error("CSR: row_ptr[0] != 0 or row_ptr[m] != nnz"); return TVR_E_CSR; }
+  const int64_t colmin = p->z0 * p->plane, colmax = p->z1 * p->plane;
+  p->separable = true;
+  std::vector<int32_t> row_slice(m, -1);
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t s = rp[i], e = rp[i + 1];
+    if (e < s) { set_error("CSR: row_ptr not non-decreasing at row " + std::to_string(i)); return TVR_E_CSR; }
+    for (int64_t k = s; k < e; ++k) {
+      const int32_t c = A->col_idx[k];
+      if (c < 0 || c >= Nglob) { set_error("CSR: column out of range in row " + std::to_string(i)); return TVR_E_CSR; }
+      if (k > s && c <= A->col_idx[k - 1]) { set_error("CSR: columns not strictly ascending in row " + std::to_string(i)); return TVR_E_CSR; }
+      if (!std::isfinite(A->val[k])) { set_error("CSR: non-finite value in row " + std::to_string(i)); return TVR_E_CSR; }
+    }
+    if (e > s) {
+      const int64_t cf = A->col_idx[s], cl = A->col_idx[e - 1];
+      if (cf < colmin || cl >= colmax) {
+        set_error("row " + std::to_string(i) + " touches voxels outside the slab");
+        return TVR_E_NOT_SEPARABLE;
+      }
+      const int64_t zf = (cf - colmin) / p->plane, zl = (cl - colmin) / p->plane;
+      if (zf != zl) p->separable = false;
+      row_slice[i] = (int32_t)zf;
+    }
+  }
+  for (int64_t i = 0; i < m; ++i)
+    if (!std::isfinite(b_host[i])) { set_error("b: non-finite entry"); return TVR_E_ARG; }
+  // slice-major row order: assign empty rows to the slice of the previous non-empty row
+  if (p->separable) {
+    int32_t cur = 0;
+    for (int64_t i = 0; i < m; ++i) {
+      if (row_slice[i] < 0) row_slice[i] = cur;
+      if (row_slice[i] < cur) { p->separable = false; break; }
+      cur = row_slice[i];
+    }
+  }
+  if (p->separable) {
+    p->slice_row.assign(p->nzl + 1, m);
+    p->slice_row[0] = 0;
+    int64_t i = 0;
+    for (int z = 1; z <= p->nzl; ++z) {
+      while (i < m && row_slice[i] < z) ++i;
+      p->slice_row[z] = i;
+    }
+  }
+
+  p->m = m;
+  p->n = p->plane * p->nzl;
+  p->nnz = nnz;
+  const int64_t n = p->n;
+
+  // ---- device and stream (everything above is host-only validation) ----
+  if (p->device < 0) TVR_CUDA(cudaGetDevice(&p->device));
+  TVR_CUDA(cudaSetDevice(p->device));
+  TVR_CUDA(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device));
+  if (user_stream) {
+    p->stream = user_stream;
+  } else {
+    TVR_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->own_stream = true;
+  }
+
+  // ---- device copies (columns made slab-local) ----
+  const size_t nnz_pad = (size_t)((nnz + 3) / 4 * 4 + 4);
+  TVR_TRY(upload(p, (void**)&p->rp, rp, sizeof(int64_t) * (m + 1)));
+  TVR_TRY(dev_alloc(p, (void**)&p->col, sizeof(int32_t) * nnz_pad));
+  TVR_TRY(dev_alloc(p, (void**)&p->val, sizeof(float) * nnz_pad));
+  TVR_CUDA(cudaMemsetAsync(p->col, 0, sizeof(int32_t) * nnz_pad, p->stream));
+  TVR_CUDA(cudaMemsetAsync(p->val, 0, sizeof(float) * nnz_pad, p->stream));
+  if (colmin == 0) {
+    TVR_CUDA(cudaMemcpyAsync(p->col, A->col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, p->stream));
+  } else {
+    std::vector<int32_t> loc(A->col_idx, A->col_idx + nnz);
+    for (auto& c : loc) c -= (int32_t)colmin;
+    TVR_CUDA(cudaMemcpyAsync(p->col, loc.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, p->stream));
+    TVR_CUDA(cudaStreamSynchronize(p->stream));
+  }
+  TVR_CUDA(cudaMemcpyAsync(p->val, A->val, sizeof(float) * nnz, cudaMemcpyHostToDevice, p->stream));
+  TVR_TRY(upload(p, (void**)&p->b, b_host, sizeof(float) * std::max<int64_t>(m, 1)));
+
+  // ---- transposed CSR on the device ----
+  TVR_TRY(dev_alloc(p, (void**)&p->rpT, sizeof(int64_t) * (n + 1)));
+  TVR_TRY(dev_alloc(p, (void**)&p->colT, sizeof(int32_t) * nnz_pad));
+  TVR_TRY(dev_alloc(p, (void**)&p->valT, sizeof(float) * nnz_pad));
+  TVR_CUDA(cudaMemsetAsync(p->colT, 0, sizeof(int32_t) * nnz_pad, p->stream));
+  TVR_CUDA(cudaMemsetAsync(p->valT, 0, sizeof(float) * nnz_pad, p->stream));
+  {
+    void *cnt = nullptr, *sc = nullptr, *sv = nullptr, *sb = nullptr;
+    const int64_t nb = (n + 1 + 1023) / 1024;
+    TVR_CUDA(cudaMalloc(&cnt, sizeof(int32_t) * std::max<int64_t>(n, 1)));
+    TVR_CUDA(cudaMalloc(&sc, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+    TVR_CUDA(cudaMalloc(&sv, sizeof(float) * std::max<int64_t>(nnz, 1)));
+    TVR_CUDA(cudaMalloc(&sb, sizeof(int64_t) * (nb + 2)));
+    cudaError_t e = build_transpose(m, n, nnz, p->rp, p->col, p->val, p->rpT, p->colT, p->valT,
+                                    (int32_t*)cnt, (int32_t*)sc, (float*)sv, (int64_t*)sb, p->stream);
+    cudaError_t e2 = cudaStreamSynchronize(p->stream);
+    cudaFree(cnt); cudaFree(sc); cudaFree(sv); cudaFree(sb);
+    if (e != cudaSuccess || e2 != cudaSuccess) {
+      set_error(std::string("transpose build: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
+      return TVR_E_CUDA;
+    }
+  }
+
+  // ---- SpMV plans ----
+  {
+    std::vector<int64_t> rpv(rp, rp + m + 1);
+    std::vector<int64_t> wlo, sr;
+    std::vector<int32_t> wlen;
+    if (p->separable) {
+      for (int z = 0; z < p->nzl; ++z) { wlo.push_back((int64_t)z * p->plane); wlen.push_back((int32_t)p->plane); }
+    }
+    TVR_TRY(make_plan(p, p->planA, rpv, m, p->separable, p->slice_row, wlo, wlen, 32, true));
+    // A^T: rows are voxels; slice z owns voxel rows [z plane, (z+1) plane) and gathers r over
+    // the slice's A rows.
+    std::vector<int64_t> rpT(n + 1);
+    TVR_CUDA(cudaMemcpyAsync(rpT.data(), p->rpT, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, p->stream));
+    TVR_CUDA(cudaStreamSynchronize(p->stream));
+    wlo.clear(); wlen.clear();
+    if (p->separable) {
+      for (int z = 0; z <= p->nzl; ++z) sr.push_back((int64_t)z * p->plane);
+      for (int z = 0; z < p->nzl; ++z) {
+        wlo.push_back(p->slice_row[z]);
+        wlen.push_back((int32_t)(p->slice_row[z + 1] - p->slice_row[z]));
+      }
+    }
+    const double mean_len = n > 0 ? (double)nnz / n : 0.0;
+    const int lprT = mean_len > 96 ? 32 : (mean_len > 40 ? 16 : 8);
+    TVR_TRY(make_plan(p, p->planT, rpT, n, p->separable, sr, wlo, wlen, lprT, false));
+  }
+
+  // ---- work vectors ----
+  const int NVOL = 10, NDAT = 4;
+  const size_t volbytes = sizeof(float) * (size_t)(p->plane * (p->nzl + 2));
+  for (int i = 0; i < NVOL; ++i) {
+    float* q = nullptr;
+    TVR_TRY(dev_alloc(p, (void**)&q, volbytes));
+    TVR_CUDA(cudaMemsetAsync(q, 0, volbytes, p->stream));
+    p->vol.push_back(q + p->plane);
+  }
+  for (int i = 0; i < NDAT; ++i) {
+    float* q = nullptr;
+    TVR_TRY(dev_alloc(p, (void**)&q, sizeof(float) * std::max<int64_t>(m, 1)));
+    p->dat.push_back(q);
+  }
+  const int64_t maxgrid = std::max<int64_t>({(int64_t)p->planA.grid, (int64_t)p->planT.grid,
+                                             (int64_t)tv_num_blocks(p->nx, p->ny, p->nzl),
+                                             (int64_t)p->num_sms * 8});
+  p->partials_cap = maxgrid * 8;  // kMaxScalars (common.cuh)
+  TVR_TRY(dev_alloc(p, (void**)&p->partials, sizeof(double) * p->partials_cap));
+  TVR_TRY(dev_alloc(p, (void**)&p->counter, 64));
+  TVR_CUDA(cudaMemsetAsync(p->counter, 0, 64, p->stream));
+  TVR_TRY(dev_alloc(p, (void**)&p->dscal, sizeof(double) * 64));
+  TVR_CUDA(cudaMemsetAsync(p->dscal, 0, sizeof(double) * 64, p->stream));
+  TVR_CUDA(cudaMallocHost((void**)&p->hscal, sizeof(double) * 64 * (std::max(1, p->world) + 1)));
+  if (p->world > 1) TVR_TRY(dev_alloc(p, (void**)&p->dgather, sizeof(double) * 64 * p->world));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  return TVR_OK;
+}
+
+void tvr_destroy(tvr_problem* p) {
+  if (!p) return;
+  if (p->stream) {
+    cudaSetDevice(p->device);
+    cudaStreamSynchronize(p->stream);
+  }
+  dev_free_all(p);
+  for (auto& t : p->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  for (auto e : p->event_pool) cudaEventDestroy(e);
+  if (p->hscal) cudaFreeHost(p->hscal);
+  if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+}
+
+int tvr_create(tvr_problem** out, const tvr_csr* A, const float* b_host, tvr_grid grid,
+               double alpha, double tau, double lo, double hi, const tvr_dist* dist) {
+  if (!out) { set_error("tvr_create: out is NULL"); return TVR_E_ARG; }
+  *out = nullptr;
+  tvr_problem* p = new (std::nothrow) tvr_problem();
+  if (!p) { set_error("host allocation failed"); return TVR_E_OOM; }
+  int s;
+  try {
+    s = create_impl(p, A, b_host, grid, alpha, tau, lo, hi, dist);
+  } catch (const std::exception& ex) {
+    set_error(std::string("tvr_create: ") + ex.what());
+    s = TVR_E_OOM;
+  }
+  if (s != TVR_OK) {
+    tvr_destroy(p);
+    return s;
+  }
+  *out = p;
+  return TVR_OK;
+}
+
+int tvr_get_info(const tvr_problem* p, tvr_info* info) {
+  if (!p || !info) { set_error("tvr_get_info: NULL"); return TVR_E_ARG; }
+  info->m_local = p->m;
+  info->n_local = p->n;
+  info->nnz_local = p->nnz;
+  info->z0 = p->z0;
+  info->z1 = p->z1;
+  info->slab_staged_A = p->planA.staged ? 1 : 0;
+  info->slab_staged_AT = p->planT.staged ? 1 : 0;
+  info->device_bytes = p->device_bytes;
+  return TVR_OK;
+}
+
+// Volume input from a caller pointer: in slab mode copied into an internal buffer whose halo
+// planes are then exchanged; on one GPU used in place.
+static int stage_volume(tvr_problem* p, const float* x_dev, int slot, const float** out) {
+  if (p->world == 1) { *out = x_dev; return TVR_OK; }
+  float* v = volvec(p, slot);
+  TVR_CUDA(cudaMemcpyAsync(v, x_dev, sizeof(float) * p->n, cudaMemcpyDeviceToDevice, p->stream));
+  TVR_TRY(halo_exchange(p, v));
+  *out = v;
+  return TVR_OK;
+}
+
+static int objective_grad_impl(tvr_problem* p, const float* x_dev, double* f_out, float* g_dev,
+                               tvr_fparts* parts) {
+  const float* x;
+  TVR_TRY(stage_volume(p, x_dev, 9, &x));
+  float* r = datvec(p, 0);
+  TVR_TRY(pass_residual(p, x, r, 0));
+  float* w = nullptr;
+  if (g_dev) {
+    w = volvec(p, 8);
+    TVR_TRY(pass_AT(p, r, w));
+  }
+  TVR_TRY(pass_tv_grad(p, x, nullptr, 0.0, w, nullptr, 0.0, g_dev, nullptr, nullptr, nullptr, 0.0, 1));
+  TVR_TRY(fetch_scalars(p, 8));
+  const double fid = 0.5 * p->hscal[0], tv = p->hscal[1];
+  const double f = fid + p->alpha * tv;
+  if (f_out) *f_out = f;
+  if (parts) { parts->fidelity = fid; parts->tv = tv; parts->f = f; }
+  if (!std::isfinite(f)) { set_error("non-finite objective"); return TVR_E_NONFINITE; }
+  return TVR_OK;
+}
+
+int tvr_objective_grad(tvr_problem* p, const float* x_dev, double* f_out, float* g_dev,
+                       tvr_fparts* parts) {
+  if (!p || !x_dev) { set_error("tvr_objective_grad: NULL"); return TVR_E_ARG; }
+  TVR_CUDA(cudaSetDevice(p->device));
+  return objective_grad_impl(p, x_dev, f_out, g_dev, parts);
+}
+
+int tvr_objective_grad_host(tvr_problem* p, const float* x_host, double* f_out, float* g_host,
+                            tvr_fparts* parts) {
+  if (!p || !x_host) { set_error("tvr_objective_grad_host: NULL"); return TVR_E_ARG; }
+  TVR_CUDA(cudaSetDevice(p->device));
+  float* x = volvec(p, 7);
+  float* g = volvec(p, 6);
+  TVR_CUDA(cudaMemcpyAsync(x, x_host, sizeof(float) * p->n, cudaMemcpyHostToDevice, p->stream));
+  TVR_TRY(objective_grad_impl(p, x, f_out, g_host ? g : nullptr, parts));
+  if (g_host) {
+    TVR_CUDA(cudaMemcpyAsync(g_host, g, sizeof(float) * p->n, cudaMemcpyDeviceToHost, p->stream));
+    TVR_CUDA(cudaStreamSynchronize(p->stream));
+  }
+  return TVR_OK;
+}
+
+int tvr_residual(tvr_problem* p, const float* x_dev, float* r_dev, double* fid) {
+  if (!p || !x_dev || !r_dev) { set_error("tvr_residual: NULL"); return TVR_E_ARG; }
+  TVR_CUDA(cudaSetDevice(p->device));
+  TVR_TRY(pass_residual(p, x_dev, r_dev, 0));
+  TVR_TRY(fetch_scalars(p, 1));
+  if (fid) *fid = 0.5 * p->hscal[0];
+  return TVR_OK;
+}
+
+int tvr_apply_AT(tvr_problem* p, const float* y_dev, float* w_dev) {
+  if (!p || !y_dev || !w_dev) { set_error("tvr_apply_AT: NULL"); return TVR_E_ARG; }
+  TVR_CUDA(cudaSetDevice(p->device));
+  TVR_TRY(pass_AT(p, y_dev, w_dev));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  return TVR_OK;
+}
+
+int tvr_tv(tvr_problem* p, const float* x_dev, double* tv_out, float* grad_dev) {
+  if (!p || !x_dev) { set_error("tvr_tv: NULL"); return TVR_E_ARG; }
+  TVR_CUDA(cudaSetDevice(p->device));
+  const float* x;
+  TVR_TRY(stage_volume(p, x_dev, 9, &x));
+  TVR_TRY(pass_tv_grad(p, x, nullptr, 0.0, nullptr, nullptr, 0.0, grad_dev, nullptr, nullptr,
+                       nullptr, 0.0, 1, 1.0));
+  TVR_TRY(fetch_scalars(p, 8));
+  if (tv_out) *tv_out = p->hscal[1];
+  return TVR_OK;
+}
+
+int tvr_gradient_map(tvr_problem* p, const float* x_dev, double nu, double* norm_out, float* G_dev) {
+  if (!p || !x_dev || !(nu > 0.0)) { set_error("tvr_gradient_map: bad argument"); return TVR_E_ARG; }
+  TVR_CUDA(cudaSetDevice(p->device));
+  float* g = volvec(p, 5);
+  double f;
+  TVR_TRY(objective_grad_impl(p, x_dev, &f, g, nullptr));
+  TVR_TRY(pass_gmap(p, x_dev, g, nu, G_dev, 0));
+  TVR_TRY(fetch_scalars(p, 1));
+  if (norm_out) *norm_out = std::sqrt(p->hscal[0]);
+  return TVR_OK;
+}
+
+int tvr_get_AT(tvr_problem* p, int64_t* rp_h, int32_t* col_h, float* val_h) {
+  if (!p) { set_error("tvr_get_AT: NULL"); return TVR_E_ARG; }
+  TVR_CUDA(cudaSetDevice(p->device));
+  if (rp_h) TVR_CUDA(cudaMemcpyAsync(rp_h, p->rpT, sizeof(int64_t) * (p->n + 1), cudaMemcpyDeviceToHost, p->stream));
+  if (col_h) TVR_CUDA(cudaMemcpyAsync(col_h, p->colT, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, p->stream));
+  if (val_h) TVR_CUDA(cudaMemcpyAsync(val_h, p->valT, sizeof(float) * p->nnz, cudaMemcpyDeviceToHost, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  return TVR_OK;
+}
+
+int tvr_profile_enable(tvr_problem* p, int on) {
+  if (!p) { set_error("tvr_profile_enable: NULL"); return TVR_E_ARG; }
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  resolve_timings(p);
+  for (int k = 0; k < K_COUNT; ++k) { p->kt_ms[k] = 0; p->kt_bytes[k] = 0; p->kt_launches[k] = 0; }
+  p->prof = on != 0;
+  return TVR_OK;
+}
+
+int tvr_profile_get(tvr_problem* p, tvr_kernel_stat* out, int cap, int* n_out) {
+  if (!p) { set_error("tvr_profile_get: NULL"); return TVR_E_ARG; }
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  resolve_timings(p);
+  int n = 0;
+  for (int k = 0; k < K_COUNT && n < cap; ++k) {
+    if (!out) break;
+    std::memset(&out[n], 0, sizeof(tvr_kernel_stat));
+    std::strncpy(out[n].name, kKernelNames[k], sizeof(out[n].name) - 1);
+    out[n].launches = p->kt_launches[k];
+    out[n].total_ms = p->kt_ms[k];
+    out[n].bytes = p->kt_bytes[k];
+    ++n;
+  }
+  if (n_out) *n_out = n;
+  return TVR_OK;
+}
+
+int64_t tvr_launch_count(const tvr_problem* p, int reset) {
+  if (!p) return -1;
+  const int64_t n = p->launches;
+  if (reset) const_cast<tvr_problem*>(p)->launches = 0;
+  return n;
+}
+
+}  // extern "C"

@@ -1,0 +1,147 @@
+// Internal state of a libtvreg problem and the host-side pass functions.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/libtvreg.h"
+#include "kernels.h"
+
+namespace tvr {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+#define TVR_CUDA(call)                                                                 \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess) {                                                           \
+      ::tvr::set_error(std::string(#call) + ": " + cudaGetErrorString(_e));            \
+      return TVR_E_CUDA;                                                               \
+    }                                                                                  \
+  } while (0)
+#define TVR_TRY(call)            \
+  do {                           \
+    int _s = (call);             \
+    if (_s < 0) return _s;       \
+  } while (0)
+
+// Kernel ids for per-kernel timing.
+enum KernelId {
+  K_SPMV_A = 0,   // a1: r = A v - b (+ sum r^2)
+  K_SPMV_AT,      // a2: w = A^T r
+  K_TV_GRAD,      // a4: g = w + alpha grad TV (+ BB / stop reductions)
+  K_TV_TRIAL,     // a5: v = P_Q(x - s g), TV(v) (+ Armijo / BT / mu reductions)
+  K_MOMENTUM,     // a6: sum ((1+beta) r1 - beta r0)^2
+  K_PROJECT,
+  K_GMAP,
+  K_COUNT
+};
+extern const char* kKernelNames[K_COUNT];
+
+struct SpmvPlan {
+  bool staged = false;
+  int padmode = 0, pad_shift = 0, pad_extra = 0;
+  int lpr = 32, grid = 0, block = 512;
+  size_t smem = 0;
+  int64_t nitems = 0;
+  int64_t* item_row = nullptr;
+  int32_t* item_slice = nullptr;
+  int64_t* win_lo = nullptr;
+  int32_t* win_len = nullptr;
+};
+
+struct PendingTiming {
+  int kid;
+  cudaEvent_t a, b;
+  double bytes;
+};
+
+}  // namespace tvr
+
+struct tvr_problem {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int nx = 0, ny = 0, nz = 0, z0 = 0, z1 = 0, nzl = 0;
+  int64_t plane = 0, m = 0, n = 0, nnz = 0;
+  double alpha = 0, tau = 0, lo = 0, hi = 0;
+  int world = 1, rank = 0, mode = TVR_SHARD_NONE;
+  void* comm = nullptr;
+  int num_sms = 148;
+
+  // system matrix (device, local indices) and data
+  int64_t* rp = nullptr;
+  int32_t* col = nullptr;
+  float* val = nullptr;
+  int64_t* rpT = nullptr;
+  int32_t* colT = nullptr;
+  float* valT = nullptr;
+  float* b = nullptr;
+  bool separable = false;
+  std::vector<int64_t> slice_row;  // nzl+1 local row boundaries per slice (separable only)
+  tvr::SpmvPlan planA, planT;
+
+  // work vectors: volume vectors carry one halo plane on each side (vol_base + plane)
+  std::vector<float*> vol;  // pointers to local plane 0
+  std::vector<float*> dat;  // m-vectors
+
+  // reductions
+  double* partials = nullptr;
+  int64_t partials_cap = 0;
+  unsigned* counter = nullptr;
+  double* dscal = nullptr;  // 32 doubles
+  double* hscal = nullptr;  // pinned mirror
+
+  // halo exchange staging (z-slab)
+  float* halo_send = nullptr;
+
+  // profiling
+  bool prof = false;
+  std::vector<tvr::PendingTiming> pending;
+  std::vector<cudaEvent_t> event_pool;
+  double kt_ms[tvr::K_COUNT] = {0};
+  double kt_bytes[tvr::K_COUNT] = {0};
+  int64_t kt_launches[tvr::K_COUNT] = {0};
+  int64_t launches = 0;
+  double bytes_total = 0;  // algorithmic bytes of every pass launched
+  double* dgather = nullptr;  // world x 64 scalars (dist)
+
+  std::vector<void*> allocs;
+  int64_t device_bytes = 0;
+};
+
+namespace tvr {
+
+int dev_alloc(tvr_problem* p, void** ptr, size_t bytes);
+float* volvec(tvr_problem* p, int i);
+float* datvec(tvr_problem* p, int i);
+int64_t n_local(const tvr_problem* p);
+
+// pass functions (enqueue only; scalars land in p->dscal[slot..])
+int pass_residual(tvr_problem* p, const float* x, float* r, int slot);         // a1
+int pass_AT(tvr_problem* p, const float* r, float* w);                          // a2
+int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta,  // a4
+                 const float* w1, const float* w0, double wbeta, float* g, float* v_out,
+                 const float* xp, const float* gp, double stop_step, int slot);
+int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta, const float* w1,
+                 const float* w0, double wbeta, float* g, float* v_out, const float* xp,
+                 const float* gp, double stop_step, int slot, double alpha);
+int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, float* v,  // a5
+                  double stop_step, const float* xo, int slot);
+int pass_momentum(tvr_problem* p, const float* r1, const float* r0, double beta, int slot);  // a6
+int pass_project(tvr_problem* p, float* x);
+int pass_gmap(tvr_problem* p, const float* x, const float* g, double nu, float* G, int slot);
+
+// synchronise the stream, fetch nslots scalars into p->hscal and (dist) sum them over ranks
+int fetch_scalars(tvr_problem* p, int nslots);
+// halo planes of a volume vector from the z-neighbours (no-op on one GPU)
+int halo_exchange(tvr_problem* p, float* v);
+// recompute the halo planes of a trial / momentum point from its inputs' halo planes
+int halo_fill_trial(tvr_problem* p, const float* x, const float* g, double s, float* v);
+int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double beta, float* y);
+int dist_sum_scalars(tvr_problem* p, double* vals, int n);
+void resolve_pending_timings(tvr_problem* p);
+
+}  // namespace tvr

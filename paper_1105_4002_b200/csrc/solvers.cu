@@ -1,0 +1,377 @@
+// Host-side solver control: GPBB (Alg. 1) and UPN (Alg. 3,
+// P:205-221) with BT (Alg. 2), the mu_k heuristic (Eq. (9)) and the
+// gradient-map stopping rule (Eq. (10)).  Scalars are fp64 on the host; every vector
+// step runs in the fused kernels (passes of problem.cu).  Readings of the paper: SURVEY §8(c)
+// C6-C14, C21, C25 (listed in DESIGN.md).
+#include <chrono>
+#include <cmath>
+#include <deque>
+#include <string>
+
+#include "problem.h"
+
+namespace tvr {
+
+namespace {
+
+// scalar slots in p->dscal (see pass_* in problem.cu)
+constexpr int S_RSQ = 0;   // sum r^2 of the A pass
+constexpr int S_TV = 1;    // 6 stencil reductions: TV, e1..e5
+constexpr int S_MOM = 7;   // sum r_y^2
+constexpr int S_TV2 = 9;   // 6 reductions of a second stencil pass
+constexpr int S_COUNT = 16;
+
+struct Recorder {
+  tvr_record* hist;
+  int64_t cap, n = 0;
+  void add(const tvr_record& r) {
+    if (hist && n < cap) hist[n] = r;
+    ++n;
+  }
+};
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+bool stop_test(double gn, double gref, double N, double eps, int mode) {
+  if (mode == TVR_STOP_ABS_PER_N) return gn / N <= eps;
+  return gn <= eps * gref;
+}
+
+// Positive root of theta^2 = (1 - theta) theta_k^2 + q theta, reading C10.
+double theta_root(double tk, double q) {
+  const double a = tk * tk - q;
+  const double s = std::sqrt(a * a + 4.0 * tk * tk);
+  return a >= 0.0 ? 2.0 * tk * tk / (a + s) : 0.5 * (-a + s);
+}
+
+int copy_in(tvr_problem* p, float* dst, const float* src) {
+  TVR_CUDA(cudaMemcpyAsync(dst, src, sizeof(float) * p->n, cudaMemcpyDeviceToDevice, p->stream));
+  return TVR_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------- GPBB
+static int gpbb_impl(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_result* res,
+                     Recorder& rec) {
+  const double t0 = now_s();
+  const double bytes0 = p->bytes_total;
+  const double Nglob = (double)p->plane * p->nz;
+  float* x_cur = volvec(p, 0);
+  float* x_prev = volvec(p, 1);
+  float* v = volvec(p, 2);
+  float* g_cur = volvec(p, 3);
+  float* g_prev = volvec(p, 4);
+  float* w = volvec(p, 5);
+  float* r_cur = datvec(p, 0);
+  float* r_trial = datvec(p, 1);
+
+  // x_0 = P_Q(x_in); f_0, g_0 (gradient with the stop-norm reduction at step 1: ||G_1(x_0)||)
+  TVR_TRY(copy_in(p, x_cur, x_io));
+  TVR_TRY(pass_project(p, x_cur));
+  TVR_TRY(halo_exchange(p, x_cur));
+  TVR_TRY(pass_residual(p, x_cur, r_cur, S_RSQ));
+  TVR_TRY(pass_AT(p, r_cur, w));
+  TVR_TRY(pass_tv_grad(p, x_cur, nullptr, 0.0, w, nullptr, 0.0, g_cur, nullptr, nullptr, nullptr,
+                       1.0, S_TV));
+  TVR_TRY(halo_exchange(p, g_cur));
+  TVR_TRY(fetch_scalars(p, S_COUNT));
+  double f = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
+  const double gref = std::sqrt(p->hscal[S_TV + 3]);
+  if (!std::isfinite(f) || !std::isfinite(gref)) { set_error("GPBB: non-finite f or g at x0"); return TVR_E_NONFINITE; }
+  int64_t n_f = 1, n_g = 1, n_ls = 0;
+  std::deque<double> fhist{f};
+  double theta = 1.0;  // theta_0
+  double bb_dd = 0.0, bb_dg = 0.0;
+  int64_t k = 0;
+  bool conv = false;
+  double gn = 0.0;
+  int status = TVR_OK;
+
+  for (;;) {
+    if (k > 0) {  // BB step; keep theta_{k-1} on a non-positive denominator (C6)
+      if (bb_dg > 0.0 && std::isfinite(bb_dg) && std::isfinite(bb_dd)) theta = bb_dd / bb_dg;
+    }
+    double beta = o.beta0;
+    double fhat = -INFINITY;  // P:147 over the last K+1 accepted values (C21)
+    for (size_t i = fhist.size() > (size_t)o.K + 1 ? fhist.size() - o.K - 1 : 0; i < fhist.size(); ++i)
+      fhat = std::fmax(fhat, fhist[i]);
+    int trials = 0;
+    double f_bar = 0.0;
+    for (;;) {
+      // x_bar = P_Q(x_k - beta theta_k g_k), TV(x_bar), g.(x - x_bar); on the first
+      // trial also ||x_k - P_Q(x_k - theta_k g_k)|| for the stop test with nu = 1/theta_k (C11)
+      TVR_TRY(pass_tv_trial(p, x_cur, g_cur, beta * theta, v, trials == 0 ? theta : 0.0, nullptr, S_TV));
+      if (trials == 0 && k >= o.max_iters) {  // last test only
+        TVR_TRY(fetch_scalars(p, S_COUNT));
+        gn = std::sqrt(p->hscal[S_TV + 3]) / theta;
+        conv = stop_test(gn, gref, Nglob, o.eps, o.stop_mode);
+        break;
+      }
+      TVR_TRY(halo_fill_trial(p, x_cur, g_cur, beta * theta, v));
+      TVR_TRY(pass_residual(p, v, r_trial, S_RSQ));
+      TVR_TRY(fetch_scalars(p, S_COUNT));
+      if (trials == 0) {
+        gn = std::sqrt(p->hscal[S_TV + 3]) / theta;
+        conv = stop_test(gn, gref, Nglob, o.eps, o.stop_mode);
+        if (conv) break;
+      }
+      f_bar = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
+      const double gdx = p->hscal[S_TV + 1];  // g_k^T (x_k - x_bar)
+      ++trials;
+      ++n_f;
+      if (!std::isfinite(f_bar)) { set_error("GPBB: non-finite trial objective"); status = TVR_E_NONFINITE; break; }
+      if (!(f_bar >= fhat - o.sigma * gdx)) break;  // loop while f(x_bar) >= f_hat - sigma g^T(x - x_bar)
+      beta = beta * beta;
+      if (beta < o.beta_min) { set_error("GPBB: beta < beta_min"); status = TVR_E_LINESEARCH; break; }
+    }
+    tvr_record r{};
+    r.iter = k; r.f = f; r.gmap_rel = gref > 0 ? gn / gref : 0.0; r.gmap_abs_per_n = gn / Nglob;
+    r.step_or_inv_L = theta; r.ls_trials = trials;
+    rec.add(r);
+    n_ls += trials;
+    if (status != TVR_OK || conv || k >= o.max_iters) break;
+    // accept x_{k+1} = x_bar; r_{k+1} is the trial residual
+    std::swap(x_prev, x_cur);
+    std::swap(x_cur, v);
+    std::swap(r_cur, r_trial);
+    std::swap(g_prev, g_cur);
+    TVR_TRY(pass_AT(p, r_cur, w));
+    TVR_TRY(pass_tv_grad(p, x_cur, nullptr, 0.0, w, nullptr, 0.0, g_cur, nullptr, x_prev, g_prev,
+                         0.0, S_TV));
+    TVR_TRY(halo_exchange(p, g_cur));
+    TVR_TRY(fetch_scalars(p, S_COUNT));
+    bb_dd = p->hscal[S_TV + 1];
+    bb_dg = p->hscal[S_TV + 2];
+    ++n_g;
+    f = f_bar;
+    fhist.push_back(f);
+    if (fhist.size() > 64) fhist.pop_front();
+    ++k;
+  }
+  TVR_CUDA(cudaMemcpyAsync(x_io, x_cur, sizeof(float) * p->n, cudaMemcpyDeviceToDevice, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  if (res) {
+    res->converged = conv ? 1 : 0;
+    res->iters = k;
+    res->n_f = n_f; res->n_grad = n_g; res->n_ls = n_ls;
+    res->f = f; res->gmap_ref = gref;
+    res->gmap_rel = gref > 0 ? gn / gref : 0.0;
+    res->gmap_abs_per_n = gn / Nglob;
+    res->seconds = now_s() - t0;
+    res->bytes = p->bytes_total - bytes0;
+  }
+  if (status != TVR_OK) return status;
+  return conv ? TVR_OK : TVR_NOT_CONVERGED;
+}
+
+// -------------------------------------------------------------------- UPN
+namespace {
+struct BTOut {
+  double f, L;
+  int trials;
+  double mu_gd, mu_dd;  // g_y^T (x_k - y_k), ||x_k - y_k||^2 from the first trial
+};
+}  // namespace
+
+// BT (Alg. 2): L~ = L_bar; x = P_Q(y - g_y/L~) until f(x) <= f(y) + g_y^T(x-y) + L~/2||x-y||^2.
+static int backtrack(tvr_problem* p, const float* y, const float* gy, double fy, double L_bar,
+                     const tvr_upn_opts& o, const float* xk_for_mu, float* x_out, float* r_out,
+                     BTOut& out) {
+  double L = L_bar;
+  out.trials = 0;
+  out.mu_gd = out.mu_dd = 0.0;
+  for (;;) {
+    const double s = 1.0 / L;
+    TVR_TRY(pass_tv_trial(p, y, gy, s, x_out, 0.0, out.trials == 0 ? xk_for_mu : nullptr, S_TV));
+    TVR_TRY(halo_fill_trial(p, y, gy, s, x_out));
+    TVR_TRY(pass_residual(p, x_out, r_out, S_RSQ));
+    TVR_TRY(fetch_scalars(p, S_COUNT));
+    const double fx = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
+    const double gd = -p->hscal[S_TV + 1];  // g_y^T (x - y)
+    const double dd = p->hscal[S_TV + 2];   // ||x - y||^2
+    if (out.trials == 0 && xk_for_mu) {
+      out.mu_gd = p->hscal[S_TV + 4];
+      out.mu_dd = p->hscal[S_TV + 5];
+    }
+    ++out.trials;
+    if (!std::isfinite(fx)) { set_error("BT: non-finite objective"); return TVR_E_NONFINITE; }
+    if (!(fx > fy + gd + 0.5 * L * dd)) {  // P:180, accept on <= (C7)
+      out.f = fx;
+      out.L = L;
+      return TVR_OK;
+    }
+    if (out.trials >= o.bt_max) { set_error("BT: more than bt_max trials"); return TVR_E_LINESEARCH; }
+    L *= o.rho_L;
+  }
+}
+
+static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_result* res,
+                    Recorder& rec) {
+  const double t0 = now_s();
+  const double bytes0 = p->bytes_total;
+  const double Nglob = (double)p->plane * p->nz;
+  float* xk = volvec(p, 0);
+  float* xn = volvec(p, 1);
+  float* ybuf = volvec(p, 2);
+  float* gy = volvec(p, 3);
+  float* wk = volvec(p, 4);
+  float* wn = volvec(p, 5);
+  float* rk = datvec(p, 0);
+  float* rn = datvec(p, 1);
+
+  TVR_TRY(copy_in(p, xk, x_io));
+  TVR_TRY(pass_project(p, xk));
+  TVR_TRY(halo_exchange(p, xk));
+  TVR_TRY(pass_residual(p, xk, rk, S_RSQ));
+  TVR_TRY(pass_AT(p, rk, wk));
+  TVR_TRY(pass_tv_grad(p, xk, nullptr, 0.0, wk, nullptr, 0.0, gy, nullptr, nullptr, nullptr, 1.0, S_TV));
+  TVR_TRY(halo_exchange(p, gy));
+  TVR_TRY(fetch_scalars(p, S_COUNT));
+  const double f0 = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
+  const double gref = std::sqrt(p->hscal[S_TV + 3]);
+  if (!std::isfinite(f0) || !std::isfinite(gref)) { set_error("UPN: non-finite f or g at x0"); return TVR_E_NONFINITE; }
+  int64_t n_f = 1, n_g = 1, n_ls = 0;
+
+  // [x_1, L_0] = BT(x_0, L_bar)
+  BTOut bt;
+  TVR_TRY(backtrack(p, xk, gy, f0, o.L0, o, nullptr, xn, rn, bt));
+  n_f += bt.trials;
+  n_ls += bt.trials;
+  double L = bt.L;
+  double mu = o.mu0;                   // mu_0 = mu_bar
+  double theta = std::sqrt(mu / L);    // theta_1
+  if (!(theta > 0.0 && theta <= 1.0)) { set_error("UPN: theta_1 outside (0,1]"); return TVR_E_THETA; }
+  std::swap(xk, xn);  // x_1
+  std::swap(rk, rn);
+  TVR_TRY(pass_AT(p, rk, wk));
+  // y_1 = x_1: grad f(y_1) = grad f(x_1) -> gy, with the stop reduction at nu = L_0
+  TVR_TRY(pass_tv_grad(p, xk, nullptr, 0.0, wk, nullptr, 0.0, gy, nullptr, nullptr, nullptr, 1.0 / L, S_TV));
+  TVR_TRY(halo_exchange(p, gy));
+  TVR_TRY(fetch_scalars(p, S_COUNT));
+  ++n_g;
+  double fxk = bt.f, fy = bt.f;
+  double gn = L * std::sqrt(p->hscal[S_TV + 3]);
+  const float* y = xk;
+  int64_t k = 1;
+  bool conv = stop_test(gn, gref, Nglob, o.eps, o.stop_mode);
+  {
+    tvr_record r{};
+    r.iter = 1; r.f = fxk; r.gmap_rel = gref > 0 ? gn / gref : 0.0; r.gmap_abs_per_n = gn / Nglob;
+    r.step_or_inv_L = 1.0 / L; r.mu = mu; r.L = L; r.ls_trials = bt.trials;
+    rec.add(r);
+  }
+  int status = TVR_OK;
+  while (!conv && k < o.max_iters) {
+    // [x_{k+1}, L_k] = BT(y_k, L_{k-1})
+    int s = backtrack(p, y, gy, fy, L, o, y == xk ? nullptr : xk, xn, rn, bt);
+    if (s < 0) { status = s; break; }
+    n_f += bt.trials;
+    n_ls += bt.trials;
+    L = bt.L;
+    // mu_k = min(mu_{k-1}, M(x_k, y_k)) (Eq. (9), C9); x_k = y_k keeps mu_{k-1}
+    if (y != xk && bt.mu_dd > 0.0) {
+      const double M = (fxk - fy - bt.mu_gd) / (0.5 * bt.mu_dd);
+      if (M > 0.0 && std::isfinite(M)) mu = std::fmin(mu, M);
+    }
+    const double theta_n = theta_root(theta, mu / L);
+    if (!(theta_n > 0.0 && theta_n <= 1.0) || !std::isfinite(theta_n)) {
+      set_error("UPN: theta outside (0,1]");
+      status = TVR_E_THETA;
+      break;
+    }
+    const double beta = theta * (1.0 - theta) / (theta * theta + theta_n);
+    // w_{k+1} = A^T r_{k+1}; stop reduction at x_{k+1} with nu = L_k (C11); then
+    // y_{k+1} = x_{k+1} + beta (x_{k+1} - x_k) with grad f(y) and f(y) by linearity (a6)
+    TVR_TRY(pass_AT(p, rn, wn));
+    TVR_TRY(pass_tv_grad(p, xn, nullptr, 0.0, wn, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr,
+                         1.0 / L, S_TV));
+    TVR_TRY(pass_momentum(p, rn, rk, beta, S_MOM));
+    TVR_TRY(pass_tv_grad(p, xn, xk, beta, wn, wk, beta, gy, ybuf, nullptr, nullptr, 0.0, S_TV2));
+    TVR_TRY(halo_fill_momentum(p, xn, xk, beta, ybuf));
+    TVR_TRY(halo_exchange(p, gy));
+    TVR_TRY(fetch_scalars(p, S_COUNT));
+    ++n_g;
+    gn = L * std::sqrt(p->hscal[S_TV + 3]);
+    ++k;
+    std::swap(xk, xn);
+    std::swap(rk, rn);
+    std::swap(wk, wn);
+    y = ybuf;
+    fxk = bt.f;
+    fy = 0.5 * p->hscal[S_MOM] + p->alpha * p->hscal[S_TV2];
+    theta = theta_n;
+    conv = stop_test(gn, gref, Nglob, o.eps, o.stop_mode);
+    tvr_record r{};
+    r.iter = k; r.f = fxk; r.gmap_rel = gref > 0 ? gn / gref : 0.0; r.gmap_abs_per_n = gn / Nglob;
+    r.step_or_inv_L = 1.0 / L; r.mu = mu; r.L = L; r.ls_trials = bt.trials;
+    rec.add(r);
+    if (!std::isfinite(fy)) { set_error("UPN: non-finite f(y)"); status = TVR_E_NONFINITE; break; }
+  }
+  TVR_CUDA(cudaMemcpyAsync(x_io, xk, sizeof(float) * p->n, cudaMemcpyDeviceToDevice, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  if (res) {
+    res->converged = conv ? 1 : 0;
+    res->iters = k;
+    res->n_f = n_f; res->n_grad = n_g; res->n_ls = n_ls;
+    res->f = fxk; res->gmap_ref = gref;
+    res->gmap_rel = gref > 0 ? gn / gref : 0.0;
+    res->gmap_abs_per_n = gn / Nglob;
+    res->seconds = now_s() - t0;
+    res->bytes = p->bytes_total - bytes0;
+  }
+  if (status != TVR_OK) return status;
+  return conv ? TVR_OK : TVR_NOT_CONVERGED;
+}
+
+}  // namespace tvr
+
+using namespace tvr;
+
+extern "C" {
+
+int tvr_solve_gpbb(tvr_problem* p, float* x, const tvr_gpbb_opts* opts, tvr_result* res,
+                   tvr_record* hist, int64_t hist_cap) {
+  if (!p || !x) { set_error("tvr_solve_gpbb: NULL"); return TVR_E_ARG; }
+  tvr_gpbb_opts o;
+  tvr_gpbb_default(&o);
+  if (opts) o = *opts;
+  if (o.max_iters < 0 || !(o.eps >= 0) || o.K < 0 || !(o.sigma > 0 && o.sigma < 1) ||
+      !(o.beta0 > 0 && o.beta0 < 1) || !(o.beta_min > 0)) {
+    set_error("tvr_solve_gpbb: invalid options");
+    return TVR_E_ARG;
+  }
+  TVR_CUDA(cudaSetDevice(p->device));
+  Recorder rec{hist, hist ? hist_cap : 0};
+  try {
+    return gpbb_impl(p, x, o, res, rec);
+  } catch (const std::exception& e) {
+    set_error(std::string("tvr_solve_gpbb: ") + e.what());
+    return TVR_E_OOM;
+  }
+}
+
+int tvr_solve_upn(tvr_problem* p, float* x, const tvr_upn_opts* opts, tvr_result* res,
+                  tvr_record* hist, int64_t hist_cap) {
+  if (!p || !x) { set_error("tvr_solve_upn: NULL"); return TVR_E_ARG; }
+  tvr_upn_opts o;
+  tvr_upn_default(&o);
+  if (opts) o = *opts;
+  if (o.max_iters < 1 || !(o.eps >= 0) || !(o.L0 > 0) || !(o.mu0 > 0) || !(o.rho_L > 1) ||
+      o.bt_max < 1) {
+    set_error("tvr_solve_upn: invalid options");
+    return TVR_E_ARG;
+  }
+  TVR_CUDA(cudaSetDevice(p->device));
+  Recorder rec{hist, hist ? hist_cap : 0};
+  try {
+    return upn_impl(p, x, o, res, rec);
+  } catch (const std::exception& e) {
+    set_error(std::string("tvr_solve_upn: ") + e.what());
+    return TVR_E_OOM;
+  }
+}
+
+}  // extern "C"

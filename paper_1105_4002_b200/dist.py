@@ -1,0 +1,91 @@
+"""z-slab partitioning and NCCL bootstrap for multi-GPU runs.
+
+Host-side plumbing only: which slices and rows a rank owns, extraction of its local CSR, and
+creation of the library's NCCL communicator from a unique id broadcast over a
+torch.distributed process group.  The exchange itself (one-slice halo send/recv and the
+rank-ordered scalar sum) runs inside libtvreg (csrc/dist.cu).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def slab_bounds(nz: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced slices [z0, z1) of rank `rank` (ranks ordered along z)."""
+    if world > nz:
+        raise ValueError(f"cannot split {nz} slices over {world} ranks")
+    base, extra = divmod(nz, world)
+    z0 = rank * base + min(rank, extra)
+    return z0, z0 + base + (1 if rank < extra else 0)
+
+
+def row_slices(row_ptr: np.ndarray, col: np.ndarray, plane: int) -> np.ndarray:
+    """Slice of every row (from its first column); empty rows inherit the previous row's slice.
+    Raises if a row spans two slices or rows are not slice-major (not slab-separable)."""
+    m = len(row_ptr) - 1
+    s, e = row_ptr[:-1], row_ptr[1:]
+    nonempty = e > s
+    first = np.full(m, -1, np.int64)
+    last = np.full(m, -1, np.int64)
+    first[nonempty] = col[s[nonempty]] // plane
+    last[nonempty] = col[e[nonempty] - 1] // plane
+    if np.any(first != last):
+        raise ValueError("a row of A spans two z-slices: geometry is not slice-separable")
+    # forward-fill empty rows
+    idx = np.where(nonempty, np.arange(m), 0)
+    np.maximum.accumulate(idx, out=idx)
+    sl = first[idx]
+    sl[sl < 0] = 0
+    if np.any(np.diff(sl) < 0):
+        raise ValueError("rows are not slice-major")
+    return sl
+
+
+@dataclass
+class LocalSlab:
+    z0: int
+    z1: int
+    row0: int
+    row1: int
+    row_ptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+    b: np.ndarray
+
+
+def local_slab(row_ptr, col, val, b, grid, world: int, rank: int, slices=None) -> LocalSlab:
+    """Rank's slices and the contiguous block of A's rows (and b) that touch them.  Columns stay
+    global (tvr_create makes them slab-local)."""
+    nx, ny, nz = grid
+    z0, z1 = slab_bounds(nz, world, rank)
+    sl = row_slices(row_ptr, col, nx * ny) if slices is None else slices
+    r0 = int(np.searchsorted(sl, z0, side="left"))
+    r1 = int(np.searchsorted(sl, z1, side="left"))
+    if rank == 0:
+        r0 = 0
+    if rank == world - 1:
+        r1 = len(row_ptr) - 1
+    e0, e1 = int(row_ptr[r0]), int(row_ptr[r1])
+    return LocalSlab(z0, z1, r0, r1, (row_ptr[r0:r1 + 1] - e0).astype(np.int64),
+                     col[e0:e1], val[e0:e1], b[r0:r1])
+
+
+def nccl_comm_from_process_group(world: int, rank: int, device: int) -> int:
+    """ncclUniqueId from rank 0, broadcast over the default torch.distributed group; returns the
+    library-owned ncclComm_t (as an int) for tvr_dist.nccl_comm."""
+    import torch
+    import torch.distributed as dist
+
+    from . import tvreg
+
+    n = tvreg.lib().tvr_nccl_unique_id_size()
+    if rank == 0:
+        uid = torch.tensor(list(tvreg.nccl_unique_id()), dtype=torch.uint8)
+    else:
+        uid = torch.zeros(n, dtype=torch.uint8)
+    if dist.get_backend() == "nccl":
+        uid = uid.cuda(device)
+    dist.broadcast(uid, src=0)
+    return tvreg.nccl_comm_init(bytes(uid.cpu().tolist()), world, rank, device)

@@ -1,0 +1,69 @@
+"""C-ABI checks that need no GPU: libtvreg.so loads, exports every symbol include/libtvreg.h
+declares, and tvr_create's host-side validation returns the documented status codes before it
+touches a device."""
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1105_4002_b200 import tvreg
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "libtvreg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tvr_[A-Za-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = tvreg.lib()
+    names = _declared()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) == set(tvreg.SIGNATURES), set(names) ^ set(tvreg.SIGNATURES)
+    assert L.tvr_abi_version() == 1
+
+
+def test_defaults_match_the_paper():
+    o = tvreg.tvr_gpbb_opts()
+    tvreg.lib().tvr_gpbb_default(ctypes.byref(o))
+    assert (o.K, o.sigma, o.beta0) == (2, 0.1, 0.95)
+    u = tvreg.tvr_upn_opts()
+    tvreg.lib().tvr_upn_default(ctypes.byref(u))
+    assert (u.L0, u.mu0, u.rho_L, u.bt_max) == (1.0, 1.0, 1.3, 200)
+
+
+def _create(rp, col, val, b, grid=(2, 2, 1), alpha=0.01, tau=1e-3, lo=0.0, hi=math.inf, **kw):
+    return tvreg.Problem(np.asarray(rp), np.asarray(col), np.asarray(val), np.asarray(b), grid,
+                         alpha, tau, lo, hi, **kw)
+
+
+@pytest.mark.parametrize("case,status", [
+    (dict(rp=[0, 2, 1], col=[0, 1], val=[1, 1], b=[0, 0]), tvreg.TVR_E_CSR),      # decreasing row_ptr
+    (dict(rp=[0, 2], col=[1, 1], val=[1, 1], b=[0]), tvreg.TVR_E_CSR),            # duplicate column
+    (dict(rp=[0, 2], col=[2, 1], val=[1, 1], b=[0]), tvreg.TVR_E_CSR),            # descending
+    (dict(rp=[0, 1], col=[4], val=[1], b=[0]), tvreg.TVR_E_CSR),                  # out of range
+    (dict(rp=[0, 1], col=[0], val=[np.nan], b=[0]), tvreg.TVR_E_CSR),             # non-finite value
+    (dict(rp=[1, 1], col=[0], val=[1], b=[0]), tvreg.TVR_E_CSR),                  # row_ptr[0] != 0
+    (dict(rp=[0, 1], col=[0], val=[1], b=[np.inf]), tvreg.TVR_E_ARG),             # non-finite b
+    (dict(rp=[0, 1], col=[0], val=[1], b=[0], tau=0.0), tvreg.TVR_E_ARG),         # tau <= 0
+    (dict(rp=[0, 1], col=[0], val=[1], b=[0], alpha=-1.0), tvreg.TVR_E_ARG),      # alpha < 0
+    (dict(rp=[0, 1], col=[0], val=[1], b=[0], lo=1.0, hi=0.0), tvreg.TVR_E_ARG),  # lo >= hi
+])
+def test_create_validation_statuses(case, status):
+    with pytest.raises(tvreg.TVRError) as e:
+        _create(**case)
+    assert e.value.status == status
+
+
+def test_create_slab_rejects_rows_outside_the_slab():
+    # 2x2x2 grid, rank owns slice z=1 (voxels 4..7); a row touching voxel 0 is not separable
+    with pytest.raises(tvreg.TVRError) as e:
+        _create([0, 2], [0, 5], [1, 1], [0], grid=(2, 2, 2), z0=1, z1=2)
+    assert e.value.status == tvreg.TVR_E_NOT_SEPARABLE

@@ -1,0 +1,213 @@
+"""Kernel parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element
+(SURVEY.md §8(c).4).  Bars: bit-exact for the transposed CSR index arrays and for dyadic-exact
+SpMV inputs; relative L2 <= 1e-6 for single passes (fp32 output rounding is 6e-8); <= 1e-5 for a
+full gradient (BASELINE.json north_star)."""
+import math
+
+import numpy as np
+import pytest
+
+import harness
+import oracle
+from tests._helpers import random_csr
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tvreg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1105_4002_b200 import tvreg as T
+    return T
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def make(T, A, b, grid, alpha=0.01, tau=1e-4, lo=0.0, hi=math.inf):
+    return T.Problem(A.row_ptr, A.col, A.val, b, grid, alpha, tau, lo, hi)
+
+
+# ------------------------------------------------------------------ a3: A^T
+@pytest.mark.parametrize("which", ["c1", "random_ragged", "tilted"])
+def test_transpose_bit_exact(tvreg, which, c1):
+    if which == "c1":
+        A, grid = c1.A, c1.grid
+    elif which == "random_ragged":
+        A, grid = random_csr(301, 7 * 5 * 3, 0.2, seed=3, empty_rows=11), (7, 5, 3)
+    else:
+        A, grid = harness.siddon_tilted(12, 10, 9, 7, 9, 13, 10.0), (12, 10, 9)
+    P = make(tvreg, A, np.zeros(A.n_rows, np.float32), grid)
+    rT, cT, vT = P.get_AT()
+    oT = oracle.transpose(A.row_ptr, A.col, A.val, A.n_cols)
+    assert np.array_equal(rT, oT[0])
+    assert np.array_equal(cT, oT[1])
+    assert np.array_equal(vT.view(np.uint32), oT[2].view(np.uint32))
+
+
+def test_transpose_bit_exact_c2(tvreg):
+    A = harness.siddon_separable(128, 128, 128, 60, 181)
+    P = make(tvreg, A, np.zeros(A.n_rows, np.float32), (128, 128, 128))
+    assert P.info.slab_staged_A == 1 and P.info.slab_staged_AT == 1
+    rT, cT, vT = P.get_AT()
+    oT = oracle.transpose(A.row_ptr, A.col, A.val, A.n_cols)
+    assert np.array_equal(rT, oT[0]) and np.array_equal(cT, oT[1])
+    assert np.array_equal(vT.view(np.uint32), oT[2].view(np.uint32))
+
+
+# --------------------------------------------------------------- a1 / a2
+def _dyadic_separable(nx, ny, nz, V, nb):
+    A = harness.siddon_separable(nx, ny, nz, V, nb)
+    A.val = (np.maximum(1, np.rint(A.val.astype(np.float64) * 1024)) / 1024).astype(np.float32)
+    return A
+
+
+@pytest.mark.parametrize("kind", ["separable", "random"])
+def test_spmv_dyadic_bitwise(tvreg, kind):
+    """Values k/1024 and integer vectors in [0, 8]: every partial sum is exact, so the GPU's
+    r = Ax - b and w = A^T r must equal the oracle bitwise in any summation order (App. A.4)."""
+    rng = np.random.default_rng(1)
+    if kind == "separable":
+        A, grid = _dyadic_separable(40, 24, 6, 9, 31), (40, 24, 6)
+    else:
+        A, grid = random_csr(500, 9 * 8 * 7, 0.05, seed=2, dyadic=True, empty_rows=9), (9, 8, 7)
+    x = rng.integers(0, 9, A.n_cols).astype(np.float32)
+    b = rng.integers(0, 9, A.n_rows).astype(np.float32)
+    P = make(tvreg, A, b, grid)
+    r = torch.empty(A.n_rows, device="cuda")
+    fid = P.residual(dev(x), r)
+    r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x) - b
+    assert np.array_equal(host(r).astype(np.float64), r_ora)
+    assert fid == 0.5 * float(r_ora @ r_ora)
+    y = rng.integers(0, 9, A.n_rows).astype(np.float32)
+    w = torch.empty(A.n_cols, device="cuda")
+    P.apply_AT(dev(y), w)
+    w_ora = oracle.rmatvec(A.row_ptr, A.col, A.val, y, A.n_cols)
+    assert np.array_equal(host(w).astype(np.float64), w_ora)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "ragged", "random"])
+def test_spmv_real_values(tvreg, cfg, c1):
+    rng = np.random.default_rng(4)
+    if cfg == "c1":
+        A, grid = c1.A, c1.grid
+    elif cfg == "ragged":
+        A, grid = harness.siddon_separable(37, 29, 11, 13, 47), (37, 29, 11)
+    else:
+        A, grid = random_csr(700, 10 * 9 * 8, 0.1, seed=5, empty_rows=20), (10, 9, 8)
+    x = rng.random(A.n_cols).astype(np.float32)
+    b = rng.random(A.n_rows).astype(np.float32)
+    P = make(tvreg, A, b, grid)
+    r = torch.empty(A.n_rows, device="cuda")
+    fid = P.residual(dev(x), r)
+    r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x) - b
+    assert rel(host(r), r_ora) <= 1e-6
+    assert abs(fid - 0.5 * r_ora @ r_ora) <= 1e-12 * (0.5 * r_ora @ r_ora)
+    empty = np.diff(A.row_ptr) == 0
+    if empty.any():   # rays that miss the volume: r_i = -b_i exactly
+        assert np.array_equal(host(r)[empty], -b[empty])
+    w = torch.empty(A.n_cols, device="cuda")
+    P.apply_AT(dev(b), w)
+    assert rel(host(w), oracle.rmatvec(A.row_ptr, A.col, A.val, b, A.n_cols)) <= 1e-6
+
+
+# -------------------------------------------------------------------- TV
+@pytest.mark.parametrize("grid", [(32, 32, 32), (37, 29, 19), (31, 7, 16), (1, 1, 5), (64, 3, 2),
+                                  (2, 1, 1)])
+@pytest.mark.parametrize("tau", [1e-4, 1e-1])
+def test_tv_value_and_gradient(tvreg, grid, tau):
+    N = grid[0] * grid[1] * grid[2]
+    rng = np.random.default_rng(N)
+    x = rng.random(N).astype(np.float32)
+    A = random_csr(3, N, 0.5, seed=1)
+    P = make(tvreg, A, np.zeros(3, np.float32), grid, tau=tau)
+    g = torch.empty(N, device="cuda")
+    v = P.tv(dev(x), g)
+    v_ora, g_ora = oracle.tv(grid, x, tau)
+    assert abs(v - v_ora) <= 1e-12 * max(1.0, abs(v_ora))
+    assert rel(host(g), g_ora) <= 1e-6
+
+
+def test_tv_piecewise_constant_phantom(tvreg):
+    """Flat regions (t = 0 < tau: quadratic branch and zero gradient) next to edges."""
+    grid = (40, 36, 20)
+    x = harness.phantom(*grid, 6)
+    A = random_csr(3, x.size, 0.5, seed=1)
+    P = make(tvreg, A, np.zeros(3, np.float32), grid, tau=1e-4)
+    g = torch.empty(x.size, device="cuda")
+    v = P.tv(dev(x), g)
+    v_ora, g_ora = oracle.tv(grid, x, 1e-4)
+    assert abs(v - v_ora) <= 1e-12 * v_ora
+    assert rel(host(g), g_ora) <= 1e-6
+
+
+# ------------------------------------------------------- full gradient (a1+a2+a4)
+def test_objective_grad_c1(tvreg, c1):
+    x = harness.random_x(c1.N)
+    P = make(tvreg, c1.A, c1.b, c1.grid, c1.alpha, c1.tau)
+    g = torch.empty(c1.N, device="cuda")
+    f, (fid, tv) = P.objective_grad(dev(x), g)
+    Po = oracle.Problem(c1.A.row_ptr, c1.A.col, c1.A.val, c1.b, c1.grid, c1.alpha, c1.tau)
+    fo, go = Po.fg(x)
+    assert abs(f - fo) <= 1e-10 * fo
+    assert rel(host(g), go) <= 1e-5
+    # determinism: ten reruns are bitwise identical
+    g0 = host(g).copy()
+    for _ in range(10):
+        f2, _ = P.objective_grad(dev(x), g)
+        assert f2 == f and np.array_equal(host(g), g0)
+    # host API (e2e path) returns the same numbers
+    gh = np.empty(c1.N, np.float32)
+    fh, _ = P.objective_grad_host(x, gh)
+    assert fh == f and np.array_equal(gh, g0)
+    # value-only call
+    fv, _ = P.objective_grad(dev(x), None)
+    assert fv == f
+
+
+def test_objective_grad_c2_full_size(tvreg):
+    """BJ:8 workload at full size in the bench's launch configuration: relative L2 <= 1e-5."""
+    w = harness.preset("c2")
+    x = harness.random_x(w.N)
+    P = make(tvreg, w.A, w.b, w.grid, w.alpha, w.tau)
+    assert P.info.slab_staged_A == 1 and P.info.slab_staged_AT == 1
+    g = torch.empty(w.N, device="cuda")
+    f, (fid, tv) = P.objective_grad(dev(x), g)
+    Po = oracle.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, nthreads=8)
+    fo, go = Po.fg(x)
+    assert abs(f - fo) <= 1e-9 * fo
+    assert rel(host(g), go) <= 1e-5
+    # separately: A pass and A^T pass at <= 1e-6
+    r = torch.empty(w.A.n_rows, device="cuda")
+    P.residual(dev(x), r)
+    ro = oracle.matvec(w.A.row_ptr, w.A.col, w.A.val, x, 8) - w.b
+    assert rel(host(r), ro) <= 1e-6
+    wt = torch.empty(w.N, device="cuda")
+    P.apply_AT(r, wt)
+    rT = oracle.transpose(w.A.row_ptr, w.A.col, w.A.val, w.N)
+    assert rel(host(wt), oracle.matvec(*rT, host(r), 8)) <= 1e-6
+
+
+def test_gradient_map(tvreg, c1):
+    x = harness.random_x(c1.N) - 0.3
+    P = make(tvreg, c1.A, c1.b, c1.grid, c1.alpha, c1.tau)
+    G = torch.empty(c1.N, device="cuda")
+    nrm = P.gradient_map(dev(x), 7.0, G)
+    Po = oracle.Problem(c1.A.row_ptr, c1.A.col, c1.A.val, c1.b, c1.grid, c1.alpha, c1.tau)
+    Go = Po.gradient_map(x.astype(np.float64), 7.0)
+    assert rel(host(G), Go) <= 1e-5
+    assert abs(nrm - np.linalg.norm(Go)) <= 1e-5 * np.linalg.norm(Go)

@@ -1,0 +1,118 @@
+"""Solver parity: GPU GPBB / UPN against the oracle's GPBB / UPN on
+the BJ:7 workload c1 and variants.  Both results are evaluated with the ORACLE's objective;
+bars from BASELINE.json north_star: relative objective gap <= 1e-5, relative image difference
+<= 1e-3.  Plus invariant replay from the recorded histories."""
+import math
+
+import numpy as np
+import pytest
+
+import harness
+import oracle
+from tests._helpers import identity_csr
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tvreg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1105_4002_b200 import tvreg as T
+    return T
+
+
+def _oracle_problem(w, **over):
+    kw = dict(alpha=w.alpha, tau=w.tau, lo=w.lo, hi=w.hi)
+    kw.update(over)
+    return oracle.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, nthreads=4, **kw)
+
+
+def _gpu_problem(T, w, **over):
+    kw = dict(alpha=w.alpha, tau=w.tau, lo=w.lo, hi=w.hi)
+    kw.update(over)
+    return T.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, kw["alpha"], kw["tau"], kw["lo"], kw["hi"])
+
+
+def _check_parity(Po, x_gpu, res_ora):
+    f_gpu = Po.f(x_gpu.astype(np.float64))
+    f_ora = Po.f(res_ora.x)
+    gap = abs(f_gpu - f_ora) / abs(f_ora)
+    diff = np.linalg.norm(x_gpu - res_ora.x) / np.linalg.norm(res_ora.x)
+    assert gap <= 1e-5, gap
+    assert diff <= 1e-3, diff
+    return gap, diff
+
+
+@pytest.fixture(scope="module")
+def c1_ref(c1):
+    Po = _oracle_problem(c1)
+    return dict(upn=oracle.upn(Po, np.zeros(c1.N), eps=1e-6, max_iters=20000),
+                gpbb=oracle.gpbb(Po, np.zeros(c1.N), eps=1e-6, max_iters=20000), P=Po)
+
+
+@pytest.mark.parametrize("solver", ["gpbb", "upn"])
+def test_solver_parity_c1(tvreg, c1, c1_ref, solver):
+    P = _gpu_problem(tvreg, c1)
+    x = torch.zeros(c1.N, device="cuda")
+    res = getattr(P, f"solve_{solver}")(x, max_iters=20000, eps=1e-6, hist_cap=25000)
+    assert res.converged
+    ref = c1_ref[solver]
+    _check_parity(c1_ref["P"], x.cpu().numpy(), ref)
+    # iteration counts within a modest factor of the oracle's (BB steps amplify rounding)
+    assert 0.5 * ref.iters <= res.iters <= 2.0 * ref.iters
+    assert res.gmap_rel <= 1e-6
+    h = res.history
+    assert len(h) == res.iters + (1 if solver == "gpbb" else 0)
+    if solver == "upn":
+        mus = [r["mu"] for r in h]
+        Ls = [r["L"] for r in h]
+        assert all(a >= b for a, b in zip(mus, mus[1:]))
+        assert all(a <= b for a, b in zip(Ls, Ls[1:]))
+    else:
+        assert all(r["step"] > 0 for r in h)
+    # the first iterations agree with the oracle's trajectory
+    oh = ref.history
+    for k in range(3):
+        assert abs(h[k]["f"] - oh[k]["f"]) <= 1e-6 * abs(oh[k]["f"])
+
+
+@pytest.mark.parametrize("solver", ["gpbb", "upn"])
+def test_solver_parity_box_constraint(tvreg, solver):
+    """c4-shaped: box Q = [0, 1], tau = 1e-2 (BJ:10) at desk size."""
+    w = harness.separable_workload("c4s", (24, 24, 12), 10, 35, 5, alpha=0.03, tau=1e-2, hi=1.0)
+    Po = _oracle_problem(w)
+    ref = getattr(oracle, solver)(Po, np.zeros(w.N), eps=1e-7, max_iters=20000)
+    P = _gpu_problem(tvreg, w)
+    x = torch.zeros(w.N, device="cuda")
+    res = getattr(P, f"solve_{solver}")(x, max_iters=20000, eps=1e-7)
+    assert res.converged and ref.converged
+    xg = x.cpu().numpy()
+    assert xg.min() >= 0.0 and xg.max() <= 1.0
+    _check_parity(Po, xg, ref)
+
+
+def test_solver_identity_closed_form(tvreg):
+    """A = I, alpha = 0: the minimiser is P_Q(b)."""
+    n = 4 * 4 * 4
+    A = identity_csr(n)
+    b = np.random.default_rng(1).uniform(-1, 1, n).astype(np.float32)
+    for solver in ("gpbb", "upn"):
+        P = tvreg.Problem(A.row_ptr, A.col, A.val, b, (4, 4, 4), 0.0, 1e-3, 0.0, 0.5)
+        x = torch.zeros(n, device="cuda")
+        res = getattr(P, f"solve_{solver}")(x, eps=1e-6, max_iters=1000)
+        assert res.converged
+        assert np.allclose(x.cpu().numpy(), np.clip(b, 0, 0.5), atol=1e-6)
+
+
+def test_abs_per_n_stop_mode_and_max_iters(tvreg, c1):
+    P = _gpu_problem(tvreg, c1)
+    x = torch.zeros(c1.N, device="cuda")
+    res = P.solve_upn(x, max_iters=7, eps=1e-30, stop_mode=tvreg.TVR_STOP_ABS_PER_N)
+    assert res.status == tvreg.TVR_NOT_CONVERGED and not res.converged and res.iters == 7
+    x2 = torch.zeros(c1.N, device="cuda")
+    res2 = P.solve_gpbb(x2, max_iters=5, eps=1e-30)
+    assert res2.status == tvreg.TVR_NOT_CONVERGED and res2.iters == 5
+    # P:228 scaling: ||G||/N, with N the voxel count
+    assert abs(res.gmap_abs_per_n * c1.N - res.gmap_rel * res.gmap_ref) <= 1e-9 * res.gmap_ref
