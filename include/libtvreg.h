@@ -149,6 +149,7 @@ typedef struct {
   int32_t converged;
   int32_t _pad;
   int64_t iters, n_f, n_grad, n_ls;
+  int64_t n_records; /* records produced (may exceed hist_cap; min(n_records, hist_cap) stored) */
   double f, gmap_rel, gmap_abs_per_n, gmap_ref, seconds, bytes;
 } tvr_result;
 

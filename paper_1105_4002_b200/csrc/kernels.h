@@ -17,14 +17,21 @@ struct SpmvArgs {
   int64_t nitems;
   const int64_t* win_lo;     // per slice: first gather index of the slice window
   const int32_t* win_len;    // per slice: window length
-  int32_t pad_shift, pad_extra;
   double* partials;
   unsigned* counter;
   double* scal;  // non-null: write 1/2-less sum r^2 to scal[0]
 };
 
-cudaError_t launch_spmv(const SpmvArgs& a, int lpr, bool staged, int padmode, int grid, int block,
-                        size_t smem, cudaStream_t st);
+struct SpmvVariant {
+  int lpr = 8;       // lanes per row
+  bool staged = false;
+  int unroll = 2;    // 16-byte chunks in flight per lane
+  int minb = 1;      // __launch_bounds__ min blocks per SM
+};
+bool spmv_variant_exists(const SpmvVariant& v);
+cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int block, size_t smem,
+                        cudaStream_t st);
+int spmv_occupancy(const SpmvVariant& v, int block, size_t smem);
 cudaError_t launch_momentum_resid(int64_t m, const float* r1, const float* r0, double beta,
                                   double* partials, unsigned* counter, double* scal, int grid,
                                   cudaStream_t st);

@@ -2,6 +2,7 @@
 // entry points other than the solvers (solvers.cu) and NCCL plumbing (dist.cu).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -119,8 +120,6 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
   a.nitems = pl.nitems;
   a.win_lo = pl.win_lo;
   a.win_len = pl.win_len;
-  a.pad_shift = pl.pad_shift;
-  a.pad_extra = pl.pad_extra;
   a.partials = p->partials;
   a.counter = p->counter;
   a.scal = scal;
@@ -132,7 +131,7 @@ int pass_residual(tvr_problem* p, const float* x, float* r, int slot) {
   SpmvArgs a = spmv_args(p, pl, false, x, p->b, r, p->dscal + slot);
   const double bytes = 8.0 * p->nnz + 8.0 * (p->m + 1) + 4.0 * n_local(p) + 8.0 * p->m;
   return launch(p, K_SPMV_A, bytes, [&] {
-    return launch_spmv(a, pl.lpr, pl.staged, pl.padmode, pl.grid, pl.block, pl.smem, p->stream);
+    return launch_spmv(a, pl.v, pl.grid, pl.block, pl.smem, p->stream);
   });
 }
 
@@ -141,7 +140,7 @@ int pass_AT(tvr_problem* p, const float* r, float* w) {
   SpmvArgs a = spmv_args(p, pl, true, r, nullptr, w, nullptr);
   const double bytes = 8.0 * p->nnz + 8.0 * (n_local(p) + 1) + 4.0 * p->m + 4.0 * n_local(p);
   return launch(p, K_SPMV_AT, bytes, [&] {
-    return launch_spmv(a, pl.lpr, pl.staged, pl.padmode, pl.grid, pl.block, pl.smem, p->stream);
+    return launch_spmv(a, pl.v, pl.grid, pl.block, pl.smem, p->stream);
   });
 }
 
@@ -264,6 +263,16 @@ static void split_rows(const int64_t* rp, int64_t r0, int64_t r1, int64_t target
   }
 }
 
+// Lanes per row from the mean row length: 16-byte chunks of 4 entries, about one to two
+// chunk pairs per row.
+static int lpr_for(double mean_len) { return mean_len > 160 ? 16 : (mean_len > 24 ? 8 : 4); }
+
+// Tuning overrides (TVR_LPR_A, TVR_LPR_AT, TVR_SPMV_BLOCK, TVR_SPMV_STAGE=0); unset in production.
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
 static int upload(tvr_problem* p, void** dst, const void* src, size_t bytes) {
   TVR_TRY(dev_alloc(p, dst, bytes));
   TVR_CUDA(cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, p->stream));
@@ -276,44 +285,41 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
                      bool separable, const std::vector<int64_t>& slice_rows,
                      const std::vector<int64_t>& win_lo, const std::vector<int32_t>& win_len,
                      int lpr, bool pad) {
-  pl.lpr = lpr;
-  pl.block = 512;
+  pl.v.lpr = lpr;
+  pl.v.unroll = env_int("TVR_SPMV_UNROLL", 2);
+  pl.v.minb = 0;  // chosen below from the shared-memory footprint
+  pl.block = env_int("TVR_SPMV_BLOCK", 512);
+  if (!env_int("TVR_SPMV_STAGE", 1)) separable = false;
   size_t smem = 0;
-  int padmode = 0, pad_shift = 0, pad_extra = 0;
   if (separable) {
     int32_t maxlen = 0;
     for (int32_t l : win_len) maxlen = std::max(maxlen, l);
-    if (pad && p->nx >= 32 && (p->nx & (p->nx - 1)) == 0) {
-      padmode = 1;
-      pad_shift = 0;
-      while ((1 << pad_shift) < p->nx) ++pad_shift;
-      pad_extra = ((3 - (p->nx % 32)) % 32 + 32) % 32;
-      smem = sizeof(float) * ((size_t)maxlen + ((size_t)maxlen >> pad_shift) * pad_extra);
-    } else {
-      smem = sizeof(float) * (size_t)maxlen;
-    }
+    smem = sizeof(float) * ((size_t)maxlen + ((size_t)maxlen >> 5) + 1);  // swz(c) = c + c/32
     int maxsmem = 0;
     cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
     // leave room for the reduction scratch of the kernel
     if (smem + 2048 > (size_t)maxsmem) separable = false;
   }
+  (void)pad;
   pl.staged = separable;
-  pl.padmode = separable ? padmode : 0;
-  pl.pad_shift = pad_shift;
-  pl.pad_extra = pad_extra;
+  pl.v.staged = separable;
   pl.smem = separable ? smem : 0;
-
-  // occupancy-sized persistent grid
-  int occ = 1;
+  // Resident CTAs per SM: as many 512-thread CTAs as fit while leaving >= 80 KB of the 228 KB
+  // L1/smem for L1 (the in-flight 128-bit streaming loads are staged in L1; with ~25 KB left the
+  // A pass at c2 loses half its bandwidth, measured).
   {
-    // query via a dry launch configuration: use the runtime's occupancy calculator on the
-    // instantiated kernel is internal to spmv.cu; approximate from smem and threads
-    int smem_per_sm = 0;
-    cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, p->device);
-    const int by_threads = 2048 / pl.block;
-    const int by_smem = pl.smem ? (int)(smem_per_sm / (pl.smem + 1024)) : by_threads;
-    occ = std::max(1, std::min(by_threads, by_smem));
+    int minb = 1;
+    for (int m = 3; m >= 1; --m)
+      if ((double)m * (pl.smem + 1024) <= (228.0 - 80.0) * 1024) { minb = m; break; }
+    pl.v.minb = env_int("TVR_SPMV_MINB", minb);
   }
+  if (!spmv_variant_exists(pl.v)) {
+    set_error("no SpMV kernel variant for lpr=" + std::to_string(pl.v.lpr));
+    return TVR_E_ARG;
+  }
+
+  // occupancy-sized persistent grid: exactly one wave of resident CTAs
+  const int occ = spmv_occupancy(pl.v, pl.block, pl.smem);
   pl.grid = p->num_sms * occ;
 
   const int64_t nnz = rp[n_rows];
@@ -533,7 +539,9 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     if (p->separable) {
       for (int z = 0; z < p->nzl; ++z) { wlo.push_back((int64_t)z * p->plane); wlen.push_back((int32_t)p->plane); }
     }
-    TVR_TRY(make_plan(p, p->planA, rpv, m, p->separable, p->slice_row, wlo, wlen, 32, true));
+    const double mean_A = m > 0 ? (double)nnz / m : 0.0;
+    TVR_TRY(make_plan(p, p->planA, rpv, m, p->separable, p->slice_row, wlo, wlen,
+                      env_int("TVR_LPR_A", lpr_for(mean_A)), true));
     // A^T: rows are voxels; slice z owns voxel rows [z plane, (z+1) plane) and gathers r over
     // the slice's A rows.
     std::vector<int64_t> rpT(n + 1);
@@ -548,8 +556,8 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
       }
     }
     const double mean_len = n > 0 ? (double)nnz / n : 0.0;
-    const int lprT = mean_len > 96 ? 32 : (mean_len > 40 ? 16 : 8);
-    TVR_TRY(make_plan(p, p->planT, rpT, n, p->separable, sr, wlo, wlen, lprT, false));
+    TVR_TRY(make_plan(p, p->planT, rpT, n, p->separable, sr, wlo, wlen,
+                      env_int("TVR_LPR_AT", lpr_for(mean_len)), false));
   }
 
   // ---- work vectors ----

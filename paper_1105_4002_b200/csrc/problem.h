@@ -42,8 +42,8 @@ extern const char* kKernelNames[K_COUNT];
 
 struct SpmvPlan {
   bool staged = false;
-  int padmode = 0, pad_shift = 0, pad_extra = 0;
-  int lpr = 32, grid = 0, block = 512;
+  SpmvVariant v;
+  int grid = 0, block = 512;
   size_t smem = 0;
   int64_t nitems = 0;
   int64_t* item_row = nullptr;

@@ -156,7 +156,7 @@ static int gpbb_impl(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_re
   if (res) {
     res->converged = conv ? 1 : 0;
     res->iters = k;
-    res->n_f = n_f; res->n_grad = n_g; res->n_ls = n_ls;
+    res->n_f = n_f; res->n_grad = n_g; res->n_ls = n_ls; res->n_records = rec.n;
     res->f = f; res->gmap_ref = gref;
     res->gmap_rel = gref > 0 ? gn / gref : 0.0;
     res->gmap_abs_per_n = gn / Nglob;
@@ -315,7 +315,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   if (res) {
     res->converged = conv ? 1 : 0;
     res->iters = k;
-    res->n_f = n_f; res->n_grad = n_g; res->n_ls = n_ls;
+    res->n_f = n_f; res->n_grad = n_g; res->n_ls = n_ls; res->n_records = rec.n;
     res->f = fxk; res->gmap_ref = gref;
     res->gmap_rel = gref > 0 ? gn / gref : 0.0;
     res->gmap_abs_per_n = gn / Nglob;

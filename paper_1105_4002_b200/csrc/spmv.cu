@@ -10,22 +10,49 @@
 // CTAs walks contiguous item ranges.  For slice-separable matrices (every row of A touches one
 // z-slice; rows slice-major) the gather vector of the current slice is staged in shared memory
 // once per slice change, so the x[col] / r[colT] gathers hit smem instead of L1/L2.
+// Instruction budget per entry: predicate, select, swizzle, LDS, 2 conversions, 1 DFMA.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace tvr {
 
-// Shared-memory index of slice-local column c.  MODE 0: identity; MODE 1: rows of nx voxels
-// padded to a pitch of pitch (nx a power of two, shift = log2 nx) so that y-direction rays
-// (column stride nx) spread over the 32 banks.
-template <int MODE>
-__device__ __forceinline__ int smem_index(int c, int shift, int extra) {
-  if constexpr (MODE == 0) return c;
-  else return c + (c >> shift) * extra;
+// Shared-memory slot of window-local index c: one pad word per 32 (banks spread for the
+// stride-4 lane pattern of the 128-bit loads; simulated on the c2 rows: ~1.7 wavefronts per
+// gather vs ~2.7 for a per-image-row pitch).
+__device__ __forceinline__ int swz(int c) { return c + (c >> 5); }
+
+// Accumulate the (up to) 4 entries of one lane's 16-byte chunk that fall inside the row:
+// entry q is in the row iff lo <= q < hi (lo, hi are 32-bit offsets of the row's ends from the
+// chunk start).  Branch-free: masked entries gather slot 0 and multiply by 0.
+template <bool STAGED>
+__device__ __forceinline__ double chunk_dot(const int4 c, const float4 v, int lo, int hi,
+                                            const float* __restrict__ sm, int wl,
+                                            const float* __restrict__ src, double acc) {
+  const int cc[4] = {c.x, c.y, c.z, c.w};
+  const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const bool in = (q >= lo) & (q < hi);
+    const float val = in ? vv[q] : 0.0f;
+    float xv;
+    if constexpr (STAGED) {
+      xv = sm[swz(in ? cc[q] - wl : 0)];
+    } else {
+      xv = in ? __ldg(src + cc[q]) : 0.0f;
+    }
+    acc = fma((double)val, (double)xv, acc);
+  }
+  return acc;
 }
 
-template <int LPR, bool STAGED, int PADMODE>
-__global__ void __launch_bounds__(512) spmv_kernel(SpmvArgs a) {
+// Groups of LPR lanes own one row at a time; each lane streams 16-byte chunks of col and val
+// (two chunks in flight), gathers from the staged slice (or global memory), accumulates in
+// fp64 and the group reduces with a fixed butterfly.  Row pointers of the next row are
+// prefetched while the current row streams.
+template <int LPR, bool STAGED, int UNR, int MINB>
+__global__ void __launch_bounds__(512, MINB) spmv_kernel(SpmvArgs a) {
   extern __shared__ float stage[];
   const int lane = threadIdx.x & (LPR - 1);
   const int grp = threadIdx.x / LPR;
@@ -33,57 +60,83 @@ __global__ void __launch_bounds__(512) spmv_kernel(SpmvArgs a) {
   const int64_t it0 = (a.nitems * (int64_t)blockIdx.x) / gridDim.x;
   const int64_t it1 = (a.nitems * (int64_t)(blockIdx.x + 1)) / gridDim.x;
   int cur_slice = -1;
-  int64_t win_lo = 0;
+  int wl = 0;
   double sq = 0.0;
   for (int64_t it = it0; it < it1; ++it) {
     if constexpr (STAGED) {
       const int z = a.item_slice[it];
       if (z != cur_slice) {
         __syncthreads();
-        win_lo = a.win_lo[z];
+        const int64_t lo64 = a.win_lo[z];
         const int len = a.win_len[z];
-        const float* src = a.src + win_lo;
-        for (int i = threadIdx.x; i < len; i += blockDim.x)
-          stage[smem_index<PADMODE>(i, a.pad_shift, a.pad_extra)] = __ldg(src + i);
+        const float* src = a.src + lo64;
+        for (int i = threadIdx.x; i < len; i += blockDim.x) stage[swz(i)] = __ldg(src + i);
         __syncthreads();
         cur_slice = z;
+        wl = (int)lo64;
       }
     }
     const int64_t r0 = a.item_row[it], r1 = a.item_row[it + 1];
+    int64_t row = r0 + grp;
+    int64_t s_n = 0, e_n = 0;
+    if (row < r1) {
+      s_n = a.rp[row];
+      e_n = a.rp[row + 1];
+    }
     for (int64_t base = r0; base < r1; base += ngrp) {
-      const int64_t row = base + grp;
-      double acc = 0.0;
-      if (row < r1) {
-        const int64_t s = a.rp[row], e = a.rp[row + 1];
-        for (int64_t k0 = (s & ~int64_t(3)) + 4 * lane; k0 < e; k0 += 4 * LPR) {
-          const int4 c = ld_stream_i4(a.col + k0);
-          const float4 v = ld_stream_f4(a.val + k0);
-          const int cc[4] = {c.x, c.y, c.z, c.w};
-          const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int64_t k = k0 + q;
-            if (k >= s && k < e) {
-              float xv;
-              if constexpr (STAGED)
-                xv = stage[smem_index<PADMODE>(cc[q] - (int)win_lo, a.pad_shift, a.pad_extra)];
-              else
-                xv = __ldg(a.src + cc[q]);
-              acc = fma((double)vv[q], (double)xv, acc);
-            }
-          }
-        }
+      const bool valid = row < r1;
+      const int64_t s = s_n, e = e_n;
+      const int64_t nrow = row + ngrp;
+      if (nrow < r1) {  // prefetch the next row's extent
+        s_n = a.rp[nrow];
+        e_n = a.rp[nrow + 1];
       }
-      acc = group_sum<LPR>(acc);
-      if (row < r1 && lane == 0) {
+      const int64_t kb = s & ~int64_t(3);
+      const int span = (int)(e - kb);
+      int lo = (int)(s - kb) - 4 * lane;
+      int hi = span - 4 * lane;
+      const int nch = valid ? (span + 4 * LPR - 1) / (4 * LPR) : 0;
+      const int32_t* cp = a.col + kb + 4 * lane;
+      const float* vp = a.val + kb + 4 * lane;
+      double acc[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) acc[u] = 0.0;
+      int ch = 0;
+      for (; ch + UNR <= nch; ch += UNR) {  // UNR chunks in flight per lane
+        int4 c[UNR];
+        float4 v[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          c[u] = ld_stream_i4(cp + (ch + u) * 4 * LPR);
+          v[u] = ld_stream_f4(vp + (ch + u) * 4 * LPR);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          acc[u] = chunk_dot<STAGED>(c[u], v[u], lo - 4 * LPR * u, hi - 4 * LPR * u, stage, wl,
+                                     a.src, acc[u]);
+        lo -= 4 * LPR * UNR;
+        hi -= 4 * LPR * UNR;
+      }
+      for (; ch < nch; ++ch) {
+        const int4 c0 = ld_stream_i4(cp + ch * 4 * LPR);
+        const float4 v0 = ld_stream_f4(vp + ch * 4 * LPR);
+        acc[0] = chunk_dot<STAGED>(c0, v0, lo, hi, stage, wl, a.src, acc[0]);
+        lo -= 4 * LPR;
+        hi -= 4 * LPR;
+      }
+#pragma unroll
+      for (int u = 1; u < UNR; ++u) acc[0] += acc[u];
+      const double accr = group_sum<LPR>(acc[0]);
+      if (valid && lane == 0) {
         if (a.b) {
-          const double r = acc - (double)a.b[row];
+          const double r = accr - (double)a.b[row];
           a.out[row] = (float)r;
           sq += r * r;
         } else {
-          a.out[row] = (float)acc;
+          a.out[row] = (float)accr;
         }
       }
+      row = nrow;
     }
   }
   if (a.scal) {
@@ -130,10 +183,10 @@ __global__ void gradient_map_kernel(int64_t n, const float* __restrict__ x,
 }
 
 // ----------------------------------------------------------------- launchers
-template <int LPR, bool STAGED, int PADMODE>
+template <int LPR, bool STAGED, int UNR, int MINB>
 static cudaError_t launch_spmv_t(const SpmvArgs& a, int grid, int block, size_t smem,
                                  cudaStream_t st) {
-  auto k = spmv_kernel<LPR, STAGED, PADMODE>;
+  auto k = spmv_kernel<LPR, STAGED, UNR, MINB>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -142,19 +195,60 @@ static cudaError_t launch_spmv_t(const SpmvArgs& a, int grid, int block, size_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_spmv(const SpmvArgs& a, int lpr, bool staged, int padmode, int grid, int block,
-                        size_t smem, cudaStream_t st) {
-#define TVR_SPMV_CASE(L)                                                            \
-  if (lpr == L) {                                                                   \
-    if (!staged) return launch_spmv_t<L, false, 0>(a, grid, block, 0, st);          \
-    if (padmode == 0) return launch_spmv_t<L, true, 0>(a, grid, block, smem, st);   \
-    return launch_spmv_t<L, true, 1>(a, grid, block, smem, st);                     \
+template <int LPR, bool STAGED, int UNR, int MINB>
+static int occupancy_t(int block, size_t smem) {
+  auto k = spmv_kernel<LPR, STAGED, UNR, MINB>;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, block, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
   }
-  TVR_SPMV_CASE(32)
-  TVR_SPMV_CASE(16)
-  TVR_SPMV_CASE(8)
-#undef TVR_SPMV_CASE
-  return cudaErrorInvalidValue;
+  return n > 0 ? n : 1;
+}
+
+// Dispatch over the instantiated variants: lanes per row {4, 8, 16, 32}, staged or global
+// gather, UNR chunks in flight {2 with min resident CTAs 1-3, 4 with 1}.
+template <class F>
+static auto dispatch(const SpmvVariant& v, F&& f) {
+#define TVR_V(L, S, U, M)                                          \
+  if (v.lpr == L && v.staged == S && v.unroll == U && v.minb == M) \
+    return f(std::integral_constant<int, L>{}, std::integral_constant<bool, S>{}, \
+             std::integral_constant<int, U>{}, std::integral_constant<int, M>{});
+#define TVR_VL(L) TVR_V(L, true, 2, 1) TVR_V(L, false, 2, 1) TVR_V(L, true, 2, 2) TVR_V(L, false, 2, 2) \
+  TVR_V(L, true, 2, 3) TVR_V(L, false, 2, 3) TVR_V(L, true, 4, 1) TVR_V(L, false, 4, 1)
+  TVR_VL(4)
+  TVR_VL(8)
+  TVR_VL(16)
+  TVR_VL(32)
+#undef TVR_VL
+#undef TVR_V
+  return f(std::integral_constant<int, 8>{}, std::integral_constant<bool, false>{},
+           std::integral_constant<int, 2>{}, std::integral_constant<int, 1>{});
+}
+
+bool spmv_variant_exists(const SpmvVariant& v) {
+  if (!(v.lpr == 4 || v.lpr == 8 || v.lpr == 16 || v.lpr == 32)) return false;
+  if (v.unroll == 2) return v.minb >= 1 && v.minb <= 3;
+  return v.unroll == 4 && v.minb == 1;
+}
+
+cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int block, size_t smem,
+                        cudaStream_t st) {
+  if (!spmv_variant_exists(v)) return cudaErrorInvalidValue;
+  return dispatch(v, [&](auto L, auto S, auto U, auto M) {
+    return launch_spmv_t<decltype(L)::value, decltype(S)::value, decltype(U)::value,
+                         decltype(M)::value>(a, grid, block, S ? smem : 0, st);
+  });
+}
+
+int spmv_occupancy(const SpmvVariant& v, int block, size_t smem) {
+  if (!spmv_variant_exists(v)) return 1;
+  return dispatch(v, [&](auto L, auto S, auto U, auto M) {
+    return occupancy_t<decltype(L)::value, decltype(S)::value, decltype(U)::value,
+                       decltype(M)::value>(block, S ? smem : 0);
+  });
 }
 
 cudaError_t launch_momentum_resid(int64_t m, const float* r1, const float* r0, double beta,

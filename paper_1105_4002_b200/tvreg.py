@@ -80,7 +80,7 @@ class tvr_record(ctypes.Structure):
 
 class tvr_result(ctypes.Structure):
     _fields_ = [("converged", c_i32), ("_pad", c_i32), ("iters", c_i64), ("n_f", c_i64),
-                ("n_grad", c_i64), ("n_ls", c_i64), ("f", c_f64), ("gmap_rel", c_f64),
+                ("n_grad", c_i64), ("n_ls", c_i64), ("n_records", c_i64), ("f", c_f64), ("gmap_rel", c_f64),
                 ("gmap_abs_per_n", c_f64), ("gmap_ref", c_f64), ("seconds", c_f64),
                 ("bytes", c_f64)]
 
@@ -333,7 +333,7 @@ class Problem:
         st = fn(self._h, _ptr(x), ctypes.byref(opts), ctypes.byref(res), hist, hist_cap)
         _check(st, fn.__name__, allow=(TVR_OK, TVR_NOT_CONVERGED))
         h = []
-        for i in range(min(hist_cap, res.iters + 1) if hist_cap else 0):
+        for i in range(min(hist_cap, res.n_records) if hist_cap else 0):
             r = hist[i]
             h.append(dict(iter=r.iter, f=r.f, gmap_rel=r.gmap_rel, gmap_abs_per_n=r.gmap_abs_per_n,
                           step=r.step_or_inv_L, mu=r.mu, L=r.L, trials=r.ls_trials))
