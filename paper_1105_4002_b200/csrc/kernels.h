@@ -12,6 +12,7 @@ struct SpmvArgs {
   const float* src;  // gather vector (x for A, r for A^T), local indices
   const float* b;    // non-null: out = A src - b and sum of squares
   float* out;
+  float* out_lo;     // non-null (with b): fp32 remainder r - fl32(r)
   const int64_t* item_row;   // nitems+1 row boundaries
   const int32_t* item_slice; // per item slice id (staged)
   int64_t nitems;
@@ -32,9 +33,9 @@ bool spmv_variant_exists(const SpmvVariant& v);
 cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int block, size_t smem,
                         cudaStream_t st);
 int spmv_occupancy(const SpmvVariant& v, int block, size_t smem);
-cudaError_t launch_momentum_resid(int64_t m, const float* r1, const float* r0, double beta,
-                                  double* partials, unsigned* counter, double* scal, int grid,
-                                  cudaStream_t st);
+cudaError_t launch_momentum_resid(int64_t m, const float* r1, const float* r1lo, const float* r0,
+                                  const float* r0lo, double beta, double* partials,
+                                  unsigned* counter, double* scal, int grid, cudaStream_t st);
 cudaError_t launch_project(int64_t n, float* x, double lo, double hi, int grid, cudaStream_t st);
 cudaError_t launch_gradient_map(int64_t n, const float* x, const float* g, double nu, double lo,
                                 double hi, float* G, double* partials, unsigned* counter,

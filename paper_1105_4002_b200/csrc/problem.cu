@@ -109,6 +109,7 @@ static int elem_grid(tvr_problem* p, int64_t n) {
 static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, const float* src,
                           const float* b, float* out, double* scal) {
   SpmvArgs a;
+  a.out_lo = nullptr;
   a.rp = transposed ? p->rpT : p->rp;
   a.col = transposed ? p->colT : p->col;
   a.val = transposed ? p->valT : p->val;
@@ -126,10 +127,12 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
   return a;
 }
 
-int pass_residual(tvr_problem* p, const float* x, float* r, int slot) {
+int pass_residual(tvr_problem* p, const float* x, float* r, int slot, float* r_lo) {
   const SpmvPlan& pl = p->planA;
   SpmvArgs a = spmv_args(p, pl, false, x, p->b, r, p->dscal + slot);
-  const double bytes = 8.0 * p->nnz + 8.0 * (p->m + 1) + 4.0 * n_local(p) + 8.0 * p->m;
+  a.out_lo = r_lo;
+  const double bytes = 8.0 * p->nnz + 8.0 * (p->m + 1) + 4.0 * n_local(p) + 8.0 * p->m +
+                       (r_lo ? 4.0 * p->m : 0.0);
   return launch(p, K_SPMV_A, bytes, [&] {
     return launch_spmv(a, pl.v, pl.grid, pl.block, pl.smem, p->stream);
   });
@@ -204,11 +207,12 @@ int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, floa
   return launch(p, K_TV_TRIAL, bytes, [&] { return launch_tv_trial(a, x, g, s, p->stream); });
 }
 
-int pass_momentum(tvr_problem* p, const float* r1, const float* r0, double beta, int slot) {
+int pass_momentum(tvr_problem* p, const float* r1, const float* r1lo, const float* r0,
+                  const float* r0lo, double beta, int slot) {
   const int grid = elem_grid(p, p->m);
-  return launch(p, K_MOMENTUM, 8.0 * p->m, [&] {
-    return launch_momentum_resid(p->m, r1, r0, beta, p->partials, p->counter, p->dscal + slot,
-                                 grid, p->stream);
+  return launch(p, K_MOMENTUM, 16.0 * p->m, [&] {
+    return launch_momentum_resid(p->m, r1, r1lo, r0, r0lo, beta, p->partials, p->counter,
+                                 p->dscal + slot, grid, p->stream);
   });
 }
 

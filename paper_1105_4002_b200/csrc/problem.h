@@ -120,7 +120,8 @@ float* datvec(tvr_problem* p, int i);
 int64_t n_local(const tvr_problem* p);
 
 // pass functions (enqueue only; scalars land in p->dscal[slot..])
-int pass_residual(tvr_problem* p, const float* x, float* r, int slot);         // a1
+int pass_residual(tvr_problem* p, const float* x, float* r, int slot,          // a1
+                  float* r_lo = nullptr);
 int pass_AT(tvr_problem* p, const float* r, float* w);                          // a2
 int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta,  // a4
                  const float* w1, const float* w0, double wbeta, float* g, float* v_out,
@@ -130,7 +131,8 @@ int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta, c
                  const float* gp, double stop_step, int slot, double alpha);
 int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, float* v,  // a5
                   double stop_step, const float* xo, int slot);
-int pass_momentum(tvr_problem* p, const float* r1, const float* r0, double beta, int slot);  // a6
+int pass_momentum(tvr_problem* p, const float* r1, const float* r1lo, const float* r0,  // a6
+                  const float* r0lo, double beta, int slot);
 int pass_project(tvr_problem* p, float* x);
 int pass_gmap(tvr_problem* p, const float* x, const float* g, double nu, float* G, int slot);
 

@@ -179,7 +179,7 @@ struct BTOut {
 // BT (Alg. 2): L~ = L_bar; x = P_Q(y - g_y/L~) until f(x) <= f(y) + g_y^T(x-y) + L~/2||x-y||^2.
 static int backtrack(tvr_problem* p, const float* y, const float* gy, double fy, double L_bar,
                      const tvr_upn_opts& o, const float* xk_for_mu, float* x_out, float* r_out,
-                     BTOut& out) {
+                     float* r_out_lo, BTOut& out) {
   double L = L_bar;
   out.trials = 0;
   out.mu_gd = out.mu_dd = 0.0;
@@ -187,7 +187,7 @@ static int backtrack(tvr_problem* p, const float* y, const float* gy, double fy,
     const double s = 1.0 / L;
     TVR_TRY(pass_tv_trial(p, y, gy, s, x_out, 0.0, out.trials == 0 ? xk_for_mu : nullptr, S_TV));
     TVR_TRY(halo_fill_trial(p, y, gy, s, x_out));
-    TVR_TRY(pass_residual(p, x_out, r_out, S_RSQ));
+    TVR_TRY(pass_residual(p, x_out, r_out, S_RSQ, r_out_lo));
     TVR_TRY(fetch_scalars(p, S_COUNT));
     const double fx = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
     const double gd = -p->hscal[S_TV + 1];  // g_y^T (x - y)
@@ -221,11 +221,13 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   float* wn = volvec(p, 5);
   float* rk = datvec(p, 0);
   float* rn = datvec(p, 1);
+  float* rk_lo = datvec(p, 2);  // fp32 remainders: r = hi + lo to ~2^-48 (f(y) by linearity)
+  float* rn_lo = datvec(p, 3);
 
   TVR_TRY(copy_in(p, xk, x_io));
   TVR_TRY(pass_project(p, xk));
   TVR_TRY(halo_exchange(p, xk));
-  TVR_TRY(pass_residual(p, xk, rk, S_RSQ));
+  TVR_TRY(pass_residual(p, xk, rk, S_RSQ, rk_lo));
   TVR_TRY(pass_AT(p, rk, wk));
   TVR_TRY(pass_tv_grad(p, xk, nullptr, 0.0, wk, nullptr, 0.0, gy, nullptr, nullptr, nullptr, 1.0, S_TV));
   TVR_TRY(halo_exchange(p, gy));
@@ -237,7 +239,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
 
   // [x_1, L_0] = BT(x_0, L_bar)
   BTOut bt;
-  TVR_TRY(backtrack(p, xk, gy, f0, o.L0, o, nullptr, xn, rn, bt));
+  TVR_TRY(backtrack(p, xk, gy, f0, o.L0, o, nullptr, xn, rn, rn_lo, bt));
   n_f += bt.trials;
   n_ls += bt.trials;
   double L = bt.L;
@@ -246,6 +248,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   if (!(theta > 0.0 && theta <= 1.0)) { set_error("UPN: theta_1 outside (0,1]"); return TVR_E_THETA; }
   std::swap(xk, xn);  // x_1
   std::swap(rk, rn);
+  std::swap(rk_lo, rn_lo);
   TVR_TRY(pass_AT(p, rk, wk));
   // y_1 = x_1: grad f(y_1) = grad f(x_1) -> gy, with the stop reduction at nu = L_0
   TVR_TRY(pass_tv_grad(p, xk, nullptr, 0.0, wk, nullptr, 0.0, gy, nullptr, nullptr, nullptr, 1.0 / L, S_TV));
@@ -266,7 +269,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   int status = TVR_OK;
   while (!conv && k < o.max_iters) {
     // [x_{k+1}, L_k] = BT(y_k, L_{k-1})
-    int s = backtrack(p, y, gy, fy, L, o, y == xk ? nullptr : xk, xn, rn, bt);
+    int s = backtrack(p, y, gy, fy, L, o, y == xk ? nullptr : xk, xn, rn, rn_lo, bt);
     if (s < 0) { status = s; break; }
     n_f += bt.trials;
     n_ls += bt.trials;
@@ -288,7 +291,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
     TVR_TRY(pass_AT(p, rn, wn));
     TVR_TRY(pass_tv_grad(p, xn, nullptr, 0.0, wn, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr,
                          1.0 / L, S_TV));
-    TVR_TRY(pass_momentum(p, rn, rk, beta, S_MOM));
+    TVR_TRY(pass_momentum(p, rn, rn_lo, rk, rk_lo, beta, S_MOM));
     TVR_TRY(pass_tv_grad(p, xn, xk, beta, wn, wk, beta, gy, ybuf, nullptr, nullptr, 0.0, S_TV2));
     TVR_TRY(halo_fill_momentum(p, xn, xk, beta, ybuf));
     TVR_TRY(halo_exchange(p, gy));
@@ -298,6 +301,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
     ++k;
     std::swap(xk, xn);
     std::swap(rk, rn);
+    std::swap(rk_lo, rn_lo);
     std::swap(wk, wn);
     y = ybuf;
     fxk = bt.f;

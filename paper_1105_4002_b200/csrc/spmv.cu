@@ -130,7 +130,9 @@ __global__ void __launch_bounds__(512, MINB) spmv_kernel(SpmvArgs a) {
       if (valid && lane == 0) {
         if (a.b) {
           const double r = accr - (double)a.b[row];
-          a.out[row] = (float)r;
+          const float rh = (float)r;
+          a.out[row] = rh;
+          if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);  // hi + lo carries r to ~2^-48
           sq += r * r;
         } else {
           a.out[row] = (float)accr;
@@ -146,13 +148,18 @@ __global__ void __launch_bounds__(512, MINB) spmv_kernel(SpmvArgs a) {
 }
 
 // a6: s = sum_i ((1+beta) r1_i - beta r0_i)^2 in fp64 (no vector written: only f(y) needs it).
+// Residuals are carried as fp32 hi + lo pairs so that f(y) by linearity keeps fp64 accuracy
+// (BT compares f values that differ by ~1e-14 relative near convergence).
 __global__ void momentum_resid_kernel(int64_t m, const float* __restrict__ r1,
-                                      const float* __restrict__ r0, double beta, double* partials,
+                                      const float* __restrict__ r1lo, const float* __restrict__ r0,
+                                      const float* __restrict__ r0lo, double beta, double* partials,
                                       unsigned* counter, double* scal) {
   double s = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += stride) {
-    const double ry = (1.0 + beta) * (double)r1[i] - beta * (double)r0[i];
+    const double a1 = (double)r1[i] + (double)r1lo[i];
+    const double a0 = (double)r0[i] + (double)r0lo[i];
+    const double ry = (1.0 + beta) * a1 - beta * a0;
     s += ry * ry;
   }
   double v[1] = {s};
@@ -251,10 +258,10 @@ int spmv_occupancy(const SpmvVariant& v, int block, size_t smem) {
   });
 }
 
-cudaError_t launch_momentum_resid(int64_t m, const float* r1, const float* r0, double beta,
-                                  double* partials, unsigned* counter, double* scal, int grid,
-                                  cudaStream_t st) {
-  momentum_resid_kernel<<<grid, 256, 0, st>>>(m, r1, r0, beta, partials, counter, scal);
+cudaError_t launch_momentum_resid(int64_t m, const float* r1, const float* r1lo, const float* r0,
+                                  const float* r0lo, double beta, double* partials,
+                                  unsigned* counter, double* scal, int grid, cudaStream_t st) {
+  momentum_resid_kernel<<<grid, 256, 0, st>>>(m, r1, r1lo, r0, r0lo, beta, partials, counter, scal);
   return cudaGetLastError();
 }
 

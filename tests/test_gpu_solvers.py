@@ -80,13 +80,15 @@ def test_solver_parity_c1(tvreg, c1, c1_ref, solver):
 
 @pytest.mark.parametrize("solver", ["gpbb", "upn"])
 def test_solver_parity_box_constraint(tvreg, solver):
-    """c4-shaped: box Q = [0, 1], tau = 1e-2 (BJ:10) at desk size."""
+    """c4-shaped: box Q = [0, 1], tau = 1e-2 (BJ:10) at desk size.  fp32 storage of the iterate
+    puts an accuracy floor near ||G||/||G_0|| = 1.2e-6 on this problem (emulated
+    on CPU), so the GPU solves to 3e-6 against an oracle reference at 1e-7."""
     w = harness.separable_workload("c4s", (24, 24, 12), 10, 35, 5, alpha=0.03, tau=1e-2, hi=1.0)
     Po = _oracle_problem(w)
     ref = getattr(oracle, solver)(Po, np.zeros(w.N), eps=1e-7, max_iters=20000)
     P = _gpu_problem(tvreg, w)
     x = torch.zeros(w.N, device="cuda")
-    res = getattr(P, f"solve_{solver}")(x, max_iters=20000, eps=1e-7)
+    res = getattr(P, f"solve_{solver}")(x, max_iters=20000, eps=3e-6)
     assert res.converged and ref.converged
     xg = x.cpu().numpy()
     assert xg.min() >= 0.0 and xg.max() <= 1.0
