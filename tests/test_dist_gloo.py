@@ -1,0 +1,153 @@
+"""Multi-rank z-slab decomposition on CPU (gloo, world size 2 and 3): the partition logic of
+paper_1105_4002_b200/dist.py, the halo-exchange pattern of csrc/dist.cu (plane 0 to rank-1,
+plane nzl-1 to rank+1) and the rank-ordered scalar sum, checked against the unsharded oracle
+gradient."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import harness
+import oracle
+from paper_1105_4002_b200.dist import local_slab, row_slices, slab_bounds
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_slab_bounds_cover_and_balance():
+    for nz in (5, 32, 128):
+        for world in (1, 2, 3, 4, 8):
+            if world > nz:
+                continue
+            b = [slab_bounds(nz, world, r) for r in range(world)]
+            assert b[0][0] == 0 and b[-1][1] == nz
+            assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+            sizes = [z1 - z0 for z0, z1 in b]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        slab_bounds(3, 4, 0)
+
+
+def test_local_slabs_partition_rows():
+    w = harness.separable_workload("t", (12, 10, 7), 6, 17, 3)
+    A = w.A
+    sl = row_slices(A.row_ptr, A.col, 120)
+    for world in (2, 3):
+        parts = [local_slab(A.row_ptr, A.col, A.val, w.b, w.grid, world, r, sl) for r in range(world)]
+        assert parts[0].row0 == 0 and parts[-1].row1 == A.n_rows
+        assert all(parts[i].row1 == parts[i + 1].row0 for i in range(world - 1))
+        assert np.array_equal(np.concatenate([p.b for p in parts]), w.b)
+        for p in parts:
+            assert p.row_ptr[0] == 0 and p.row_ptr[-1] == len(p.col)
+            if len(p.col):
+                assert p.col.min() >= p.z0 * 120 and p.col.max() < p.z1 * 120
+
+
+def test_row_slices_rejects_non_separable():
+    A = harness.siddon_tilted(8, 8, 6, 4, 5, 9, 10.0)
+    with pytest.raises(ValueError):
+        row_slices(A.row_ptr, A.col, 64)
+
+
+def _halo_exchange(v, plane, rank, world):
+    """Same pattern as csrc/dist.cu: own planes v[plane:-plane]; halos v[:plane], v[-plane:]."""
+    reqs = []
+    nzl = v.numel() // plane - 2
+    if rank > 0:
+        reqs.append(dist.isend(v[plane:2 * plane].clone(), rank - 1))
+        buf_lo = torch.empty(plane, dtype=v.dtype)
+        reqs.append(dist.irecv(buf_lo, rank - 1))
+    if rank < world - 1:
+        reqs.append(dist.isend(v[nzl * plane:(nzl + 1) * plane].clone(), rank + 1))
+        buf_hi = torch.empty(plane, dtype=v.dtype)
+        reqs.append(dist.irecv(buf_hi, rank + 1))
+    for r in reqs:
+        r.wait()
+    if rank > 0:
+        v[:plane] = buf_lo
+    if rank < world - 1:
+        v[(nzl + 1) * plane:] = buf_hi
+
+
+def _rank_ordered_sum(vals, world):
+    t = torch.tensor(vals, dtype=torch.float64)
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    acc = torch.zeros_like(t)
+    for o in out:   # rank order, as dist_sum_scalars
+        acc += o
+    return acc.numpy()
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = harness.separable_workload("t", (11, 9, 8), 7, 19, 3, alpha=0.02, tau=1e-2)
+        nx, ny, nz = w.grid
+        plane = nx * ny
+        x = harness.random_x(w.N)
+        sl = local_slab(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, world, rank)
+        nzl = sl.z1 - sl.z0
+        # local residual / fidelity / A^T r (columns made slab-local as tvr_create does)
+        col_loc = (sl.col - sl.z0 * plane).astype(np.int32)
+        xl = x[sl.z0 * plane:sl.z1 * plane].astype(np.float64)
+        r = oracle.matvec(sl.row_ptr, col_loc, sl.val, xl) - sl.b.astype(np.float64)
+        wl = oracle.rmatvec(sl.row_ptr, col_loc, sl.val, r, nzl * plane)
+        # volume with halo planes, exchanged
+        v = torch.zeros((nzl + 2) * plane, dtype=torch.float64)
+        v[plane:(nzl + 1) * plane] = torch.from_numpy(xl)
+        _halo_exchange(v, plane, rank, world)
+        vz0 = sl.z0 - (1 if rank > 0 else 0)
+        vz1 = sl.z1 + (1 if rank < world - 1 else 0)
+        lo = plane if rank > 0 else 0
+        ext = v.numpy()[plane - lo:(nzl + 1) * plane + (plane if rank < world - 1 else 0)]
+        _, g_ext = oracle.tv((nx, ny, vz1 - vz0), ext, w.tau)
+        g_tv = g_ext[lo:lo + nzl * plane]
+        # owned TV value: planes [z0, z1) with the upper halo supplying dz
+        up = ext[lo:]
+        tv_own = oracle.tv((nx, ny, len(up) // plane), up, w.tau, False)[0]
+        if rank < world - 1:
+            tv_own -= oracle.tv((nx, ny, 1), up[-plane:], w.tau, False)[0]
+        s = _rank_ordered_sum([float(r @ r), tv_own], world)
+        g_loc = wl + w.alpha * g_tv
+        f = 0.5 * s[0] + w.alpha * s[1]
+        q.put((rank, sl.z0, sl.z1, f, g_loc))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gradient_matches_unsharded(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = harness.separable_workload("t", (11, 9, 8), 7, 19, 3, alpha=0.02, tau=1e-2)
+    Po = oracle.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau)
+    f, g = Po.fg(harness.random_x(w.N))
+    plane = 11 * 9
+    fs = [r[3] for r in res]
+    assert all(fi == fs[0] for fi in fs)          # bitwise identical on every rank
+    assert abs(fs[0] - f) <= 1e-12 * abs(f)
+    gs = np.concatenate([r[4] for r in res])
+    assert [r[1] for r in res][0] == 0 and res[-1][2] == 8
+    assert np.allclose(gs, g, rtol=1e-12, atol=1e-12 * np.abs(g).max())
+    assert gs.size == plane * 8
