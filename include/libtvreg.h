@@ -93,7 +93,8 @@ void tvr_destroy(tvr_problem* p);
 typedef struct {
   int64_t m_local, n_local, nnz_local; /* local sizes (n_local = voxels owned) */
   int32_t z0, z1;                      /* owned slices */
-  int32_t slab_staged_A, slab_staged_AT; /* 1 when the smem slice-staged SpMV is used */
+  int32_t slab_staged_A, slab_staged_AT; /* SpMV kernel: 0 global gathers, 1 slice staged in
+                                           smem, 2 slice staged + TMA bulk-copy pipeline */
   int64_t device_bytes;                /* device memory held by the problem */
 } tvr_info;
 int tvr_get_info(const tvr_problem* p, tvr_info* info);

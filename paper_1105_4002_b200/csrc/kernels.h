@@ -33,6 +33,39 @@ bool spmv_variant_exists(const SpmvVariant& v);
 cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int block, size_t smem,
                         cudaStream_t st);
 int spmv_occupancy(const SpmvVariant& v, int block, size_t smem);
+
+// TMA bulk-copy pipelined SpMV (spmv_tma.cu): tiles of whole rows inside one slice.
+constexpr int kTmaConsumerWarps = 8;
+constexpr int kTmaProducerWarps = 4;  // divides kTmaConsumerWarps (stage count is a multiple)
+struct TmaSpmvArgs {
+  const int64_t* rp;
+  const int32_t* col;
+  const float* val;
+  const float* src;
+  const float* b;
+  float* out;
+  float* out_lo;
+  const int64_t* tile_row;   // ntiles+1 row boundaries
+  const int64_t* tile_k0;    // per tile: first entry, rounded down to a multiple of 4
+  const int64_t* tile_k1;    // per tile: end entry, rounded up to a multiple of 4
+  const int32_t* tile_slice;
+  int64_t ntiles;
+  const int64_t* bounds;     // ascending tile indices that start a new slice (bounds[0] = 0)
+  int64_t nbounds;
+  const int64_t* win_lo;
+  const int32_t* win_len;
+  int32_t win_cap;    // floats of the (swizzled) window buffer
+  int32_t tile_nnz;   // capacity of a stage in entries (multiple of 4)
+  int32_t tile_rows;  // capacity of a stage in rows
+  int32_t stages;
+  uint32_t piece;     // bytes per bulk copy of the col / val streams (multiple of 16)
+  double* partials;
+  unsigned* counter;
+  double* scal;
+};
+size_t tma_spmv_smem_bytes(int win_cap, int tile_nnz, int tile_rows, int stages);
+cudaError_t launch_spmv_tma(const TmaSpmvArgs& a, int lpr, int grid, size_t smem, cudaStream_t st);
+
 cudaError_t launch_momentum_resid(int64_t m, const float* r1, const float* r1lo, const float* r0,
                                   const float* r0lo, double beta, double* partials,
                                   unsigned* counter, double* scal, int grid, cudaStream_t st);
@@ -70,6 +103,7 @@ cudaError_t launch_tv_grad_momentum(const TVArgs& a, const float* x1, const floa
 cudaError_t launch_tv_trial(const TVArgs& a, const float* x, const float* g, double s,
                             cudaStream_t st);
 int tv_num_blocks(int nx, int ny, int nzl);
+int tv_set_grid(int num_sms);  // size the persistent stencil grid for the current device
 cudaError_t launch_halo_fill_trial(const float* x, const float* g, double s, double lo, double hi,
                                    int64_t plane, int nzl, int has_lo, int has_hi, float* v,
                                    cudaStream_t st);

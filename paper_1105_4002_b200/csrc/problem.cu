@@ -127,23 +127,55 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
   return a;
 }
 
+// Launch one SpMV pass with the plan's kernel: the TMA bulk-copy pipeline when planned, else the
+// register-streaming kernel.
+static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed, const float* src,
+                            const float* b, float* out, float* out_lo, double* scal) {
+  if (pl.tma.on) {
+    TmaSpmvArgs t;
+    t.rp = transposed ? p->rpT : p->rp;
+    t.col = transposed ? p->colT : p->col;
+    t.val = transposed ? p->valT : p->val;
+    t.src = src;
+    t.b = b;
+    t.out = out;
+    t.out_lo = out_lo;
+    t.tile_row = pl.tma.tile_row;
+    t.tile_k0 = pl.tma.tile_k0;
+    t.tile_k1 = pl.tma.tile_k1;
+    t.tile_slice = pl.tma.tile_slice;
+    t.ntiles = pl.tma.ntiles;
+    t.bounds = pl.tma.bounds;
+    t.nbounds = pl.tma.nbounds;
+    t.win_lo = pl.win_lo;
+    t.win_len = pl.win_len;
+    t.win_cap = pl.tma.win_cap;
+    t.tile_nnz = pl.tma.tile_nnz;
+    t.tile_rows = pl.tma.tile_rows;
+    t.stages = pl.tma.stages;
+    t.piece = pl.tma.piece;
+    t.partials = p->partials;
+    t.counter = p->counter;
+    t.scal = scal;
+    return launch_spmv_tma(t, pl.v.lpr, pl.tma.grid, pl.tma.smem, p->stream);
+  }
+  SpmvArgs a = spmv_args(p, pl, transposed, src, b, out, scal);
+  a.out_lo = out_lo;
+  return launch_spmv(a, pl.v, pl.grid, pl.block, pl.smem, p->stream);
+}
+
 int pass_residual(tvr_problem* p, const float* x, float* r, int slot, float* r_lo) {
-  const SpmvPlan& pl = p->planA;
-  SpmvArgs a = spmv_args(p, pl, false, x, p->b, r, p->dscal + slot);
-  a.out_lo = r_lo;
   const double bytes = 8.0 * p->nnz + 8.0 * (p->m + 1) + 4.0 * n_local(p) + 8.0 * p->m +
                        (r_lo ? 4.0 * p->m : 0.0);
   return launch(p, K_SPMV_A, bytes, [&] {
-    return launch_spmv(a, pl.v, pl.grid, pl.block, pl.smem, p->stream);
+    return run_spmv(p, p->planA, false, x, p->b, r, r_lo, p->dscal + slot);
   });
 }
 
 int pass_AT(tvr_problem* p, const float* r, float* w) {
-  const SpmvPlan& pl = p->planT;
-  SpmvArgs a = spmv_args(p, pl, true, r, nullptr, w, nullptr);
   const double bytes = 8.0 * p->nnz + 8.0 * (n_local(p) + 1) + 4.0 * p->m + 4.0 * n_local(p);
   return launch(p, K_SPMV_AT, bytes, [&] {
-    return launch_spmv(a, pl.v, pl.grid, pl.block, pl.smem, p->stream);
+    return run_spmv(p, p->planT, true, r, nullptr, w, nullptr, nullptr);
   });
 }
 
@@ -283,6 +315,74 @@ static int upload(tvr_problem* p, void** dst, const void* src, size_t bytes) {
   return TVR_OK;
 }
 
+// Tiles for the TMA pipeline: runs of whole rows inside one slice whose 16-byte-aligned entry
+// span fits a stage (tile_nnz entries) and whose row count fits tile_rows.  Stages fill the
+// shared memory left after the slice window.  Disabled (register kernel) if a row does not fit.
+static int make_tma_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& rp,
+                         const std::vector<int64_t>& slice_rows, size_t win_cap) {
+  TmaPlan& t = pl.tma;
+  t.on = false;
+  // Opt-in: measured slower than the register-streaming kernel at c2 (profiles/r01/tma.md).
+  if (!env_int("TVR_SPMV_TMA", 0)) return TVR_OK;
+  int maxsmem = 0;
+  cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+  t.tile_nnz = env_int("TVR_TMA_TILE", 1024);
+  t.piece = (uint32_t)env_int("TVR_TMA_PIECE", 1 << 20) & ~15u;
+  if (t.piece < 16) t.piece = 16;
+  t.tile_rows = 256;
+  t.win_cap = (int)win_cap;
+  // Stage count: a multiple of the consumer-warp count.  Tile i goes to warp i % NC and stage
+  // i % S; with S % NC != 0 a warp could wait on a stage two phases ahead, which an mbarrier
+  // parity wait cannot tell from the previous phase (it would read a stale tile).
+  // (Consumers take tiles dynamically, which needs S >= NC; producers own tiles i = p mod NP,
+  // which needs S % NP == 0.)
+  int stages = 0;
+  const int smax = env_int("TVR_TMA_STAGES", 4 * kTmaConsumerWarps);
+  for (int s = (smax / kTmaProducerWarps) * kTmaProducerWarps; s >= kTmaConsumerWarps;
+       s -= kTmaProducerWarps)
+    if (tma_spmv_smem_bytes(t.win_cap, t.tile_nnz, t.tile_rows, s) + 4096 <= (size_t)maxsmem) {
+      stages = s;
+      break;
+    }
+  if (stages < kTmaConsumerWarps) return TVR_OK;
+  t.stages = stages;
+  t.smem = tma_spmv_smem_bytes(t.win_cap, t.tile_nnz, t.tile_rows, stages);
+  std::vector<int64_t> row, k0, k1;
+  std::vector<int32_t> sl;
+  auto span = [&](int64_t r0, int64_t r1) {
+    return ((rp[r1] + 3) & ~int64_t(3)) - (rp[r0] & ~int64_t(3));
+  };
+  for (size_t z = 0; z + 1 < slice_rows.size(); ++z) {
+    int64_t r = slice_rows[z];
+    const int64_t rend = slice_rows[z + 1];
+    while (r < rend) {
+      int64_t e = r + 1;
+      if (span(r, e) > t.tile_nnz) return TVR_OK;  // a row longer than a stage
+      while (e < rend && e - r < t.tile_rows && span(r, e + 1) <= t.tile_nnz) ++e;
+      row.push_back(r);
+      k0.push_back(rp[r] & ~int64_t(3));
+      k1.push_back((rp[e] + 3) & ~int64_t(3));
+      sl.push_back((int32_t)z);
+      r = e;
+    }
+  }
+  if (row.empty()) return TVR_OK;
+  row.push_back(slice_rows.back());
+  t.ntiles = (int64_t)sl.size();
+  t.grid = (int)std::min<int64_t>(p->num_sms, t.ntiles);
+  TVR_TRY(upload(p, (void**)&t.tile_row, row.data(), sizeof(int64_t) * row.size()));
+  TVR_TRY(upload(p, (void**)&t.tile_k0, k0.data(), sizeof(int64_t) * k0.size()));
+  TVR_TRY(upload(p, (void**)&t.tile_k1, k1.data(), sizeof(int64_t) * k1.size()));
+  TVR_TRY(upload(p, (void**)&t.tile_slice, sl.data(), sizeof(int32_t) * sl.size()));
+  std::vector<int64_t> bounds;
+  for (size_t i = 0; i < sl.size(); ++i)
+    if (i == 0 || sl[i] != sl[i - 1]) bounds.push_back((int64_t)i);
+  t.nbounds = (int64_t)bounds.size();
+  TVR_TRY(upload(p, (void**)&t.bounds, bounds.data(), sizeof(int64_t) * bounds.size()));
+  t.on = true;
+  return TVR_OK;
+}
+
 // rp: host row pointer of the operator (n_rows+1); slices: n_slices+1 row boundaries when
 // separable; windows: per slice gather window (lo, len); pitch padding for the A pass.
 static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& rp, int64_t n_rows,
@@ -344,6 +444,7 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
   if (separable) {
     TVR_TRY(upload(p, (void**)&pl.win_lo, win_lo.data(), sizeof(int64_t) * win_lo.size()));
     TVR_TRY(upload(p, (void**)&pl.win_len, win_len.data(), sizeof(int32_t) * win_len.size()));
+    TVR_TRY(make_tma_plan(p, pl, rp, slice_rows, pl.smem / sizeof(float)));
   }
   return TVR_OK;
 }
@@ -495,8 +596,12 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   }
 
   // ---- device copies (columns made slab-local) ----
+  // Padding: 16-byte chunk loads and TMA bulk copies of whole 16-byte units may read up to 3
+  // entries past the end of col/val/b and 2 past row_ptr (the pads are zero, never used).
   const size_t nnz_pad = (size_t)((nnz + 3) / 4 * 4 + 4);
-  TVR_TRY(upload(p, (void**)&p->rp, rp, sizeof(int64_t) * (m + 1)));
+  TVR_TRY(dev_alloc(p, (void**)&p->rp, sizeof(int64_t) * (m + 3)));
+  TVR_CUDA(cudaMemsetAsync(p->rp, 0, sizeof(int64_t) * (m + 3), p->stream));
+  TVR_CUDA(cudaMemcpyAsync(p->rp, rp, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, p->stream));
   TVR_TRY(dev_alloc(p, (void**)&p->col, sizeof(int32_t) * nnz_pad));
   TVR_TRY(dev_alloc(p, (void**)&p->val, sizeof(float) * nnz_pad));
   TVR_CUDA(cudaMemsetAsync(p->col, 0, sizeof(int32_t) * nnz_pad, p->stream));
@@ -510,10 +615,13 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     TVR_CUDA(cudaStreamSynchronize(p->stream));
   }
   TVR_CUDA(cudaMemcpyAsync(p->val, A->val, sizeof(float) * nnz, cudaMemcpyHostToDevice, p->stream));
-  TVR_TRY(upload(p, (void**)&p->b, b_host, sizeof(float) * std::max<int64_t>(m, 1)));
+  TVR_TRY(dev_alloc(p, (void**)&p->b, sizeof(float) * (m + 4)));
+  TVR_CUDA(cudaMemsetAsync(p->b, 0, sizeof(float) * (m + 4), p->stream));
+  TVR_CUDA(cudaMemcpyAsync(p->b, b_host, sizeof(float) * m, cudaMemcpyHostToDevice, p->stream));
 
   // ---- transposed CSR on the device ----
-  TVR_TRY(dev_alloc(p, (void**)&p->rpT, sizeof(int64_t) * (n + 1)));
+  TVR_TRY(dev_alloc(p, (void**)&p->rpT, sizeof(int64_t) * (n + 3)));
+  TVR_CUDA(cudaMemsetAsync(p->rpT, 0, sizeof(int64_t) * (n + 3), p->stream));
   TVR_TRY(dev_alloc(p, (void**)&p->colT, sizeof(int32_t) * nnz_pad));
   TVR_TRY(dev_alloc(p, (void**)&p->valT, sizeof(float) * nnz_pad));
   TVR_CUDA(cudaMemsetAsync(p->colT, 0, sizeof(int32_t) * nnz_pad, p->stream));
@@ -578,6 +686,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     TVR_TRY(dev_alloc(p, (void**)&q, sizeof(float) * std::max<int64_t>(m, 1)));
     p->dat.push_back(q);
   }
+  tv_set_grid(p->num_sms);
   const int64_t maxgrid = std::max<int64_t>({(int64_t)p->planA.grid, (int64_t)p->planT.grid,
                                              (int64_t)tv_num_blocks(p->nx, p->ny, p->nzl),
                                              (int64_t)p->num_sms * 8});
@@ -635,8 +744,8 @@ int tvr_get_info(const tvr_problem* p, tvr_info* info) {
   info->nnz_local = p->nnz;
   info->z0 = p->z0;
   info->z1 = p->z1;
-  info->slab_staged_A = p->planA.staged ? 1 : 0;
-  info->slab_staged_AT = p->planT.staged ? 1 : 0;
+  info->slab_staged_A = p->planA.tma.on ? 2 : (p->planA.staged ? 1 : 0);
+  info->slab_staged_AT = p->planT.tma.on ? 2 : (p->planT.staged ? 1 : 0);
   info->device_bytes = p->device_bytes;
   return TVR_OK;
 }

@@ -40,7 +40,22 @@ enum KernelId {
 };
 extern const char* kKernelNames[K_COUNT];
 
+struct TmaPlan {
+  bool on = false;
+  int grid = 0, stages = 0, tile_nnz = 0, tile_rows = 0, win_cap = 0;
+  uint32_t piece = 1u << 20;
+  size_t smem = 0;
+  int64_t ntiles = 0;
+  int64_t* tile_row = nullptr;
+  int64_t* tile_k0 = nullptr;
+  int64_t* tile_k1 = nullptr;
+  int32_t* tile_slice = nullptr;
+  int64_t* bounds = nullptr;
+  int64_t nbounds = 0;
+};
+
 struct SpmvPlan {
+  TmaPlan tma;
   bool staged = false;
   SpmvVariant v;
   int grid = 0, block = 512;

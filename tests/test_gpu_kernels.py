@@ -62,7 +62,7 @@ def test_transpose_bit_exact(tvreg, which, c1):
 def test_transpose_bit_exact_c2(tvreg):
     A = harness.siddon_separable(128, 128, 128, 60, 181)
     P = make(tvreg, A, np.zeros(A.n_rows, np.float32), (128, 128, 128))
-    assert P.info.slab_staged_A == 1 and P.info.slab_staged_AT == 1
+    assert P.info.slab_staged_A >= 1 and P.info.slab_staged_AT >= 1
     rT, cT, vT = P.get_AT()
     oT = oracle.transpose(A.row_ptr, A.col, A.val, A.n_cols)
     assert np.array_equal(rT, oT[0]) and np.array_equal(cT, oT[1])
@@ -184,7 +184,7 @@ def test_objective_grad_c2_full_size(tvreg):
     w = harness.preset("c2")
     x = harness.random_x(w.N)
     P = make(tvreg, w.A, w.b, w.grid, w.alpha, w.tau)
-    assert P.info.slab_staged_A == 1 and P.info.slab_staged_AT == 1
+    assert P.info.slab_staged_A >= 1 and P.info.slab_staged_AT >= 1
     g = torch.empty(w.N, device="cuda")
     f, (fid, tv) = P.objective_grad(dev(x), g)
     Po = oracle.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, nthreads=8)
@@ -211,3 +211,33 @@ def test_gradient_map(tvreg, c1):
     Go = Po.gradient_map(x.astype(np.float64), 7.0)
     assert rel(host(G), Go) <= 1e-5
     assert abs(nrm - np.linalg.norm(Go)) <= 1e-5 * np.linalg.norm(Go)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "ragged"])
+def test_tma_pipeline_matches_register_kernel_bitwise(tvreg, cfg, c1, monkeypatch):
+    """The TMA bulk-copy SpMV and the register-streaming SpMV use the same per-row summation
+    order, so r, 1/2||r||^2 and A^T r agree bitwise; the staged-window kernel is exercised too."""
+    if cfg == "c1":
+        A, b, grid = c1.A, c1.b, c1.grid
+    else:
+        A = harness.siddon_separable(37, 29, 11, 13, 47)
+        b = np.random.default_rng(2).random(A.n_rows).astype(np.float32)
+        grid = (37, 29, 11)
+    x = dev(harness.random_x(A.n_cols))
+    outs = {}
+    for mode in ("tma", "reg", "global"):
+        monkeypatch.setenv("TVR_SPMV_TMA", "1" if mode == "tma" else "0")
+        monkeypatch.setenv("TVR_SPMV_STAGE", "0" if mode == "global" else "1")
+        P = make(tvreg, A, b, grid)
+        assert P.info.slab_staged_A == {"tma": 2, "reg": 1, "global": 0}[mode]
+        r = torch.empty(A.n_rows, device="cuda")
+        fid = P.residual(x, r)
+        w = torch.empty(A.n_cols, device="cuda")
+        P.apply_AT(r, w)
+        outs[mode] = (host(r).copy(), fid, host(w).copy())
+        P.close()
+    for mode in ("reg", "global"):
+        assert np.array_equal(outs[mode][0], outs["tma"][0])
+        # the fp64 sum of r^2 is split differently over CTAs: equal to rounding only
+        assert abs(outs[mode][1] - outs["tma"][1]) <= 1e-13 * outs["tma"][1]
+        assert np.array_equal(outs[mode][2], outs["tma"][2])
