@@ -8,6 +8,7 @@ namespace tvr {
 struct SpmvArgs {
   const int64_t* rp;
   const int32_t* col;
+  const uint16_t* col16;  // 16-bit window offsets (SpmvVariant::idx16)
   const float* val;
   const float* src;  // gather vector (x for A, r for A^T), local indices
   const float* b;    // non-null: out = A src - b and sum of squares
@@ -28,7 +29,10 @@ struct SpmvVariant {
   bool staged = false;
   int unroll = 2;    // 16-byte chunks in flight per lane
   int minb = 1;      // __launch_bounds__ min blocks per SM
+  bool idx16 = false;  // 16-bit column offsets inside the staged slice window (6 B per entry)
 };
+cudaError_t launch_compress_cols(const SpmvArgs& a, const int32_t* col, uint16_t* col16, bool expand,
+                                 int32_t* col_out, cudaStream_t st);
 bool spmv_variant_exists(const SpmvVariant& v);
 cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int block, size_t smem,
                         cudaStream_t st);

@@ -40,6 +40,16 @@ int dev_alloc(tvr_problem* p, void** ptr, size_t bytes) {
   return TVR_OK;
 }
 
+void dev_free(tvr_problem* p, void* q) {
+  for (size_t i = 0; i < p->allocs.size(); ++i)
+    if (p->allocs[i] == q) {
+      if (g_free) g_free(q, p->device, (void*)p->stream, g_alloc_ctx);
+      else cudaFree(q);
+      p->allocs.erase(p->allocs.begin() + i);
+      return;
+    }
+}
+
 static void dev_free_all(tvr_problem* p) {
   for (void* q : p->allocs) {
     if (g_free) g_free(q, p->device, (void*)p->stream, g_alloc_ctx);
@@ -112,6 +122,7 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
   a.out_lo = nullptr;
   a.rp = transposed ? p->rpT : p->rp;
   a.col = transposed ? p->colT : p->col;
+  a.col16 = transposed ? p->colT16 : p->col16;
   a.val = transposed ? p->valT : p->val;
   a.src = src;
   a.b = b;
@@ -164,16 +175,20 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
   return launch_spmv(a, pl.v, pl.grid, pl.block, pl.smem, p->stream);
 }
 
+// Algorithmic bytes per entry: fp32 value + int32 column, or + 16-bit column offset.
+static double entry_bytes(const SpmvPlan& pl) { return pl.v.idx16 ? 6.0 : 8.0; }
+
 int pass_residual(tvr_problem* p, const float* x, float* r, int slot, float* r_lo) {
-  const double bytes = 8.0 * p->nnz + 8.0 * (p->m + 1) + 4.0 * n_local(p) + 8.0 * p->m +
-                       (r_lo ? 4.0 * p->m : 0.0);
+  const double bytes = entry_bytes(p->planA) * p->nnz + 8.0 * (p->m + 1) + 4.0 * n_local(p) +
+                       8.0 * p->m + (r_lo ? 4.0 * p->m : 0.0);
   return launch(p, K_SPMV_A, bytes, [&] {
     return run_spmv(p, p->planA, false, x, p->b, r, r_lo, p->dscal + slot);
   });
 }
 
 int pass_AT(tvr_problem* p, const float* r, float* w) {
-  const double bytes = 8.0 * p->nnz + 8.0 * (n_local(p) + 1) + 4.0 * p->m + 4.0 * n_local(p);
+  const double bytes =
+      entry_bytes(p->planT) * p->nnz + 8.0 * (n_local(p) + 1) + 4.0 * p->m + 4.0 * n_local(p);
   return launch(p, K_SPMV_AT, bytes, [&] {
     return run_spmv(p, p->planT, true, r, nullptr, w, nullptr, nullptr);
   });
@@ -301,7 +316,12 @@ static void split_rows(const int64_t* rp, int64_t r0, int64_t r1, int64_t target
 
 // Lanes per row from the mean row length: 16-byte chunks of 4 entries, about one to two
 // chunk pairs per row.
-static int lpr_for(double mean_len) { return mean_len > 160 ? 16 : (mean_len > 24 ? 8 : 4); }
+// Measured at c2 (scripts/sweep_spmv.py): 4-entry chunks: LPR 8 for rows of 76 and 115;
+// 8-entry chunks (16-bit columns): LPR 8 for 115, LPR 4 for 76.
+static int lpr_for(double mean_len, int chunk) {
+  const double per_chunk_rows = mean_len / chunk;  // chunks per row
+  return per_chunk_rows > 40 ? 16 : (per_chunk_rows > 12 ? 8 : 4);
+}
 
 // Tuning overrides (TVR_LPR_A, TVR_LPR_AT, TVR_SPMV_BLOCK, TVR_SPMV_STAGE=0); unset in production.
 static int env_int(const char* name, int dflt) {
@@ -388,8 +408,7 @@ static int make_tma_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t
 static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& rp, int64_t n_rows,
                      bool separable, const std::vector<int64_t>& slice_rows,
                      const std::vector<int64_t>& win_lo, const std::vector<int32_t>& win_len,
-                     int lpr, bool pad) {
-  pl.v.lpr = lpr;
+                     double mean_len, const char* lpr_env, bool pad) {
   pl.v.unroll = env_int("TVR_SPMV_UNROLL", 2);
   pl.v.minb = 0;  // chosen below from the shared-memory footprint
   pl.block = env_int("TVR_SPMV_BLOCK", 512);
@@ -408,12 +427,22 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
   pl.staged = separable;
   pl.v.staged = separable;
   pl.smem = separable ? smem : 0;
+  // 16-bit column offsets inside the slice window whenever every window fits 2^16 entries
+  // (c2 and c3 both do): 6 instead of 8 HBM bytes per entry.  The TMA path streams int32.
+  {
+    int32_t maxlen = 0;
+    for (int32_t l : win_len) maxlen = std::max(maxlen, l);
+    pl.v.idx16 = separable && maxlen <= 65536 && env_int("TVR_IDX16", 1) != 0 &&
+                 env_int("TVR_SPMV_TMA", 0) == 0;
+  }
+  pl.v.lpr = env_int(lpr_env, lpr_for(mean_len, pl.v.idx16 ? 8 : 4));
   // Resident CTAs per SM: as many 512-thread CTAs as fit while leaving >= 80 KB of the 228 KB
   // L1/smem for L1 (the in-flight 128-bit streaming loads are staged in L1; with ~25 KB left the
-  // A pass at c2 loses half its bandwidth, measured).
+  // A pass at c2 loses half its bandwidth, measured).  The 16-bit kernel spills at the 40
+  // registers of 3 CTAs and is faster with 2 (scripts/sweep_spmv.py).
   {
     int minb = 1;
-    for (int m = 3; m >= 1; --m)
+    for (int m = pl.v.idx16 ? 2 : 3; m >= 1; --m)
       if ((double)m * (pl.smem + 1024) <= (228.0 - 80.0) * 1024) { minb = m; break; }
     pl.v.minb = env_int("TVR_SPMV_MINB", minb);
   }
@@ -598,7 +627,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   // ---- device copies (columns made slab-local) ----
   // Padding: 16-byte chunk loads and TMA bulk copies of whole 16-byte units may read up to 3
   // entries past the end of col/val/b and 2 past row_ptr (the pads are zero, never used).
-  const size_t nnz_pad = (size_t)((nnz + 3) / 4 * 4 + 4);
+  const size_t nnz_pad = (size_t)((nnz + 7) / 8 * 8 + 8);  // 8-entry chunks of the 16-bit kernel
   TVR_TRY(dev_alloc(p, (void**)&p->rp, sizeof(int64_t) * (m + 3)));
   TVR_CUDA(cudaMemsetAsync(p->rp, 0, sizeof(int64_t) * (m + 3), p->stream));
   TVR_CUDA(cudaMemcpyAsync(p->rp, rp, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, p->stream));
@@ -653,7 +682,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     }
     const double mean_A = m > 0 ? (double)nnz / m : 0.0;
     TVR_TRY(make_plan(p, p->planA, rpv, m, p->separable, p->slice_row, wlo, wlen,
-                      env_int("TVR_LPR_A", lpr_for(mean_A)), true));
+                      mean_A, "TVR_LPR_A", true));
     // A^T: rows are voxels; slice z owns voxel rows [z plane, (z+1) plane) and gathers r over
     // the slice's A rows.
     std::vector<int64_t> rpT(n + 1);
@@ -669,8 +698,23 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     }
     const double mean_len = n > 0 ? (double)nnz / n : 0.0;
     TVR_TRY(make_plan(p, p->planT, rpT, n, p->separable, sr, wlo, wlen,
-                      env_int("TVR_LPR_AT", lpr_for(mean_len)), false));
+                      mean_len, "TVR_LPR_AT", false));
   }
+  // ---- 16-bit column offsets for the staged plans ----
+  p->nnz_pad = nnz_pad;
+  for (int which = 0; which < 2; ++which) {
+    SpmvPlan& pl = which ? p->planT : p->planA;
+    if (!pl.v.idx16) continue;
+    uint16_t** dst = which ? &p->colT16 : &p->col16;
+    TVR_TRY(dev_alloc(p, (void**)dst, sizeof(uint16_t) * nnz_pad));
+    TVR_CUDA(cudaMemsetAsync(*dst, 0, sizeof(uint16_t) * nnz_pad, p->stream));
+    SpmvArgs a = spmv_args(p, pl, which == 1, nullptr, nullptr, nullptr, nullptr);
+    TVR_CUDA(launch_compress_cols(a, which ? p->colT : p->col, *dst, false, nullptr, p->stream));
+  }
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  // the int32 columns are no longer read by any pass: release them (c3: 7.7 GB each)
+  if (p->planA.v.idx16) { dev_free(p, p->col); p->col = nullptr; }
+  if (p->planT.v.idx16) { dev_free(p, p->colT); p->colT = nullptr; }
 
   // ---- work vectors ----
   const int NVOL = 10, NDAT = 4;
@@ -849,7 +893,20 @@ int tvr_get_AT(tvr_problem* p, int64_t* rp_h, int32_t* col_h, float* val_h) {
   if (!p) { set_error("tvr_get_AT: NULL"); return TVR_E_ARG; }
   TVR_CUDA(cudaSetDevice(p->device));
   if (rp_h) TVR_CUDA(cudaMemcpyAsync(rp_h, p->rpT, sizeof(int64_t) * (p->n + 1), cudaMemcpyDeviceToHost, p->stream));
-  if (col_h) TVR_CUDA(cudaMemcpyAsync(col_h, p->colT, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, p->stream));
+  if (col_h && p->colT16) {
+    // the device holds 16-bit window offsets: expand them back to the canonical int32 columns
+    int32_t* tmp = nullptr;
+    TVR_CUDA(cudaMalloc(&tmp, sizeof(int32_t) * std::max<int64_t>(p->nnz, 1)));
+    SpmvArgs a = spmv_args(p, p->planT, true, nullptr, nullptr, nullptr, nullptr);
+    cudaError_t e = launch_compress_cols(a, nullptr, p->colT16, true, tmp, p->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(col_h, tmp, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    cudaFree(tmp);
+    if (e != cudaSuccess) { set_error(std::string("tvr_get_AT: ") + cudaGetErrorString(e)); return TVR_E_CUDA; }
+  } else if (col_h) {
+    TVR_CUDA(cudaMemcpyAsync(col_h, p->colT, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, p->stream));
+  }
   if (val_h) TVR_CUDA(cudaMemcpyAsync(val_h, p->valT, sizeof(float) * p->nnz, cudaMemcpyDeviceToHost, p->stream));
   TVR_CUDA(cudaStreamSynchronize(p->stream));
   return TVR_OK;

@@ -93,6 +93,9 @@ struct tvr_problem {
   int64_t* rpT = nullptr;
   int32_t* colT = nullptr;
   float* valT = nullptr;
+  uint16_t* col16 = nullptr;   // 16-bit window offsets (planA.v.idx16)
+  uint16_t* colT16 = nullptr;  // (planT.v.idx16)
+  size_t nnz_pad = 0;
   float* b = nullptr;
   bool separable = false;
   std::vector<int64_t> slice_row;  // nzl+1 local row boundaries per slice (separable only)
@@ -130,6 +133,7 @@ struct tvr_problem {
 namespace tvr {
 
 int dev_alloc(tvr_problem* p, void** ptr, size_t bytes);
+void dev_free(tvr_problem* p, void* ptr);
 float* volvec(tvr_problem* p, int i);
 float* datvec(tvr_problem* p, int i);
 int64_t n_local(const tvr_problem* p);

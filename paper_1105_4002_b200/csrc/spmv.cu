@@ -147,6 +147,158 @@ __global__ void __launch_bounds__(512, MINB) spmv_kernel(SpmvArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// 16-bit column variant for slice-staged matrices: every column is stored as its offset inside
+// the slice window (< 65536), so one 16-byte load carries 8 columns and the entry costs 6 bytes
+// of HBM instead of 8.  Chunks are 8 entries (one int4 of columns + two float4 of values).
+__device__ __forceinline__ double chunk8_dot(const int4 c, const float4 v0, const float4 v1, int lo,
+                                             int hi, const float* __restrict__ sm, double acc) {
+  const uint32_t cw[4] = {(uint32_t)c.x, (uint32_t)c.y, (uint32_t)c.z, (uint32_t)c.w};
+  const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+  double pr[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const bool in = (q >= lo) & (q < hi);
+    const int cidx = (int)((cw[q >> 1] >> (16 * (q & 1))) & 0xffffu);  // little-endian halves
+    const float val = in ? vv[q] : 0.0f;
+    const float xv = sm[swz(in ? cidx : 0)];
+    pr[q] = (double)val * (double)xv;  // exact: 24-bit x 24-bit significands fit fp64
+  }
+  // pairwise tree (depth 3) instead of an 8-deep fma chain: shorter dependency latency
+  return acc + (((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7])));
+}
+
+template <int LPR, int UNR, int MINB>
+__global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
+  extern __shared__ float stage[];
+  const int lane = threadIdx.x & (LPR - 1);
+  const int grp = threadIdx.x / LPR;
+  const int ngrp = blockDim.x / LPR;
+  const int64_t it0 = (a.nitems * (int64_t)blockIdx.x) / gridDim.x;
+  const int64_t it1 = (a.nitems * (int64_t)(blockIdx.x + 1)) / gridDim.x;
+  int cur_slice = -1;
+  double sq = 0.0;
+  for (int64_t it = it0; it < it1; ++it) {
+    const int z = a.item_slice[it];
+    if (z != cur_slice) {
+      __syncthreads();
+      const int64_t lo64 = a.win_lo[z];
+      const int len = a.win_len[z];
+      const float* src = a.src + lo64;
+      for (int i = threadIdx.x; i < len; i += blockDim.x) stage[swz(i)] = __ldg(src + i);
+      __syncthreads();
+      cur_slice = z;
+    }
+    const int64_t r0 = a.item_row[it], r1 = a.item_row[it + 1];
+    int64_t row = r0 + grp;
+    int64_t s_n = 0, e_n = 0;
+    if (row < r1) {
+      s_n = a.rp[row];
+      e_n = a.rp[row + 1];
+    }
+    for (int64_t base = r0; base < r1; base += ngrp) {
+      const bool valid = row < r1;
+      const int64_t s = s_n, e = e_n;
+      const int64_t nrow = row + ngrp;
+      if (nrow < r1) {
+        s_n = a.rp[nrow];
+        e_n = a.rp[nrow + 1];
+      }
+      const int64_t kb = s & ~int64_t(7);
+      const int span = (int)(e - kb);
+      int lo = (int)(s - kb) - 8 * lane;
+      int hi = span - 8 * lane;
+      const int nch = valid ? (span + 8 * LPR - 1) / (8 * LPR) : 0;
+      const uint16_t* cp = a.col16 + kb + 8 * lane;
+      const float* vp = a.val + kb + 8 * lane;
+      double acc[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) acc[u] = 0.0;
+      int ch = 0;
+      for (; ch + UNR <= nch; ch += UNR) {
+        int4 c[UNR];
+        float4 va[UNR], vb[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          c[u] = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + (ch + u) * 8 * LPR));
+          va[u] = ld_stream_f4(vp + (ch + u) * 8 * LPR);
+          vb[u] = ld_stream_f4(vp + (ch + u) * 8 * LPR + 4);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          acc[u] = chunk8_dot(c[u], va[u], vb[u], lo - 8 * LPR * u, hi - 8 * LPR * u, stage, acc[u]);
+        lo -= 8 * LPR * UNR;
+        hi -= 8 * LPR * UNR;
+      }
+      for (; ch < nch; ++ch) {
+        const int4 c0 = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + ch * 8 * LPR));
+        const float4 va0 = ld_stream_f4(vp + ch * 8 * LPR);
+        const float4 vb0 = ld_stream_f4(vp + ch * 8 * LPR + 4);
+        acc[0] = chunk8_dot(c0, va0, vb0, lo, hi, stage, acc[0]);
+        lo -= 8 * LPR;
+        hi -= 8 * LPR;
+      }
+#pragma unroll
+      for (int u = 1; u < UNR; ++u) acc[0] += acc[u];
+      const double accr = group_sum<LPR>(acc[0]);
+      if (valid && lane == 0) {
+        if (a.b) {
+          const double r = accr - (double)a.b[row];
+          const float rh = (float)r;
+          a.out[row] = rh;
+          if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
+          sq += r * r;
+        } else {
+          a.out[row] = (float)accr;
+        }
+      }
+      row = nrow;
+    }
+  }
+  if (a.scal) {
+    double v[1] = {sq};
+    reduce_to_scalars<1>(v, a.partials, a.counter, a.scal);
+  }
+}
+
+// col16[k] = col[k] - win_lo[slice of k's row]: the 16-bit window offsets of a staged plan.
+__global__ void compress_cols_kernel(int64_t nitems, const int64_t* __restrict__ item_row,
+                                     const int32_t* __restrict__ item_slice,
+                                     const int64_t* __restrict__ win_lo,
+                                     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                     uint16_t* __restrict__ col16) {
+  for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int64_t base = win_lo[item_slice[it]];
+    const int64_t k0 = rp[item_row[it]], k1 = rp[item_row[it + 1]];
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) col16[k] = (uint16_t)(col[k] - base);
+  }
+}
+
+// Inverse: the canonical int32 columns (for tvr_get_AT / inspection).
+__global__ void expand_cols_kernel(int64_t nitems, const int64_t* __restrict__ item_row,
+                                   const int32_t* __restrict__ item_slice,
+                                   const int64_t* __restrict__ win_lo, const int64_t* __restrict__ rp,
+                                   const uint16_t* __restrict__ col16, int32_t* __restrict__ col) {
+  for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int64_t base = win_lo[item_slice[it]];
+    const int64_t k0 = rp[item_row[it]], k1 = rp[item_row[it + 1]];
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) col[k] = (int32_t)(base + col16[k]);
+  }
+}
+
+cudaError_t launch_compress_cols(const SpmvArgs& a, const int32_t* col, uint16_t* col16, bool expand,
+                                 int32_t* col_out, cudaStream_t st) {
+  const int grid = a.nitems < 148 * 16 ? (int)a.nitems : 148 * 16;
+  if (grid <= 0) return cudaSuccess;
+  if (expand)
+    expand_cols_kernel<<<grid, 256, 0, st>>>(a.nitems, a.item_row, a.item_slice, a.win_lo, a.rp, col16,
+                                             col_out);
+  else
+    compress_cols_kernel<<<grid, 256, 0, st>>>(a.nitems, a.item_row, a.item_slice, a.win_lo, a.rp, col,
+                                               col16);
+  return cudaGetLastError();
+}
+
 // a6: s = sum_i ((1+beta) r1_i - beta r0_i)^2 in fp64 (no vector written: only f(y) needs it).
 // Residuals are carried as fp32 hi + lo pairs so that f(y) by linearity keeps fp64 accuracy
 // (BT compares f values that differ by ~1e-14 relative near convergence).
@@ -235,7 +387,22 @@ static auto dispatch(const SpmvVariant& v, F&& f) {
            std::integral_constant<int, 2>{}, std::integral_constant<int, 1>{});
 }
 
+// 16-bit variants: staged only, UNR 2, lanes per row {4, 8, 16}, min resident CTAs {1, 2, 3}.
+template <class F>
+static auto dispatch16(const SpmvVariant& v, F&& f) {
+#define TVR_V16(L, M) \
+  if (v.lpr == L && v.minb == M) return f(spmv16_kernel<L, 2, M>);
+  TVR_V16(4, 1) TVR_V16(4, 2) TVR_V16(4, 3)
+  TVR_V16(8, 1) TVR_V16(8, 2) TVR_V16(8, 3)
+  TVR_V16(16, 1) TVR_V16(16, 2) TVR_V16(16, 3)
+#undef TVR_V16
+  return f(spmv16_kernel<8, 2, 1>);
+}
+
 bool spmv_variant_exists(const SpmvVariant& v) {
+  if (v.idx16)
+    return v.staged && v.unroll == 2 && (v.lpr == 4 || v.lpr == 8 || v.lpr == 16) && v.minb >= 1 &&
+           v.minb <= 3;
   if (!(v.lpr == 4 || v.lpr == 8 || v.lpr == 16 || v.lpr == 32)) return false;
   if (v.unroll == 2) return v.minb >= 1 && v.minb <= 3;
   return v.unroll == 4 && v.minb == 1;
@@ -244,6 +411,16 @@ bool spmv_variant_exists(const SpmvVariant& v) {
 cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int block, size_t smem,
                         cudaStream_t st) {
   if (!spmv_variant_exists(v)) return cudaErrorInvalidValue;
+  if (v.idx16) {
+    return dispatch16(v, [&](auto k) {
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      k<<<grid, block, smem, st>>>(a);
+      return cudaGetLastError();
+    });
+  }
   return dispatch(v, [&](auto L, auto S, auto U, auto M) {
     return launch_spmv_t<decltype(L)::value, decltype(S)::value, decltype(U)::value,
                          decltype(M)::value>(a, grid, block, S ? smem : 0, st);
@@ -252,6 +429,17 @@ cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int b
 
 int spmv_occupancy(const SpmvVariant& v, int block, size_t smem) {
   if (!spmv_variant_exists(v)) return 1;
+  if (v.idx16) {
+    return dispatch16(v, [&](auto k) {
+      if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int n = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, block, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 1;
+      }
+      return n > 0 ? n : 1;
+    });
+  }
   return dispatch(v, [&](auto L, auto S, auto U, auto M) {
     return occupancy_t<decltype(L)::value, decltype(S)::value, decltype(U)::value,
                        decltype(M)::value>(block, S ? smem : 0);

@@ -225,19 +225,28 @@ def test_tma_pipeline_matches_register_kernel_bitwise(tvreg, cfg, c1, monkeypatc
         grid = (37, 29, 11)
     x = dev(harness.random_x(A.n_cols))
     outs = {}
-    for mode in ("tma", "reg", "global"):
+    for mode in ("tma", "reg", "global", "reg16"):
         monkeypatch.setenv("TVR_SPMV_TMA", "1" if mode == "tma" else "0")
         monkeypatch.setenv("TVR_SPMV_STAGE", "0" if mode == "global" else "1")
+        monkeypatch.setenv("TVR_IDX16", "1" if mode == "reg16" else "0")
         P = make(tvreg, A, b, grid)
-        assert P.info.slab_staged_A == {"tma": 2, "reg": 1, "global": 0}[mode]
+        assert P.info.slab_staged_A == {"tma": 2, "reg": 1, "global": 0, "reg16": 1}[mode]
         r = torch.empty(A.n_rows, device="cuda")
         fid = P.residual(x, r)
         w = torch.empty(A.n_cols, device="cuda")
         P.apply_AT(r, w)
         outs[mode] = (host(r).copy(), fid, host(w).copy())
+        if mode == "reg16":   # the 16-bit device columns expand back to the canonical A^T
+            rT, cT, vT = P.get_AT()
+            oT = oracle.transpose(A.row_ptr, A.col, A.val, A.n_cols)
+            assert np.array_equal(cT, oT[1]) and np.array_equal(rT, oT[0])
         P.close()
-    for mode in ("reg", "global"):
+    for mode in ("reg", "global"):   # same 4-entry chunk order: bitwise
         assert np.array_equal(outs[mode][0], outs["tma"][0])
         # the fp64 sum of r^2 is split differently over CTAs: equal to rounding only
         assert abs(outs[mode][1] - outs["tma"][1]) <= 1e-13 * outs["tma"][1]
         assert np.array_equal(outs[mode][2], outs["tma"][2])
+    # 16-bit columns use 8-entry chunks (another fp64 summation order): equal to fp32 rounding
+    assert rel(outs["reg16"][0], outs["reg"][0]) <= 1e-7
+    assert abs(outs["reg16"][1] - outs["reg"][1]) <= 1e-13 * outs["reg"][1]
+    assert rel(outs["reg16"][2], outs["reg"][2]) <= 1e-7
