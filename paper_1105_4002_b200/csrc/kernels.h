@@ -16,9 +16,14 @@ struct SpmvArgs {
   float* out_lo;     // non-null (with b): fp32 remainder r - fl32(r)
   const int64_t* item_row;   // nitems+1 row boundaries
   const int32_t* item_slice; // per item slice id (staged)
+  const int64_t* slice_item_end;  // per slice: one past its last item (16-bit kernel)
   int64_t nitems;
   const int64_t* win_lo;     // per slice: first gather index of the slice window
   const int32_t* win_len;    // per slice: window length
+  int32_t parts, part_len;   // window parts (16-bit kernel): parts * part_len >= window length
+  int64_t nrows;
+  const uint16_t* part_off;  // (parts-1) x nrows row-relative starts of parts 1..parts-1
+  double* part_acc;          // nrows fp64 partial row sums between parts
   double* partials;
   unsigned* counter;
   double* scal;  // non-null: write 1/2-less sum r^2 to scal[0]
@@ -30,9 +35,12 @@ struct SpmvVariant {
   int unroll = 2;    // 16-byte chunks in flight per lane
   int minb = 1;      // __launch_bounds__ min blocks per SM
   bool idx16 = false;  // 16-bit column offsets inside the staged slice window (6 B per entry)
+  bool parts = false;  // (idx16, staged) window cut into parts: spmv16_parts_kernel
 };
 cudaError_t launch_compress_cols(const SpmvArgs& a, const int32_t* col, uint16_t* col16, bool expand,
                                  int32_t* col_out, cudaStream_t st);
+cudaError_t launch_parts_rows(const SpmvArgs& a, bool expand, const int32_t* col, uint16_t* col16,
+                              uint16_t* part_off, int32_t* col_out, cudaStream_t st);
 bool spmv_variant_exists(const SpmvVariant& v);
 cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int block, size_t smem,
                         cudaStream_t st);

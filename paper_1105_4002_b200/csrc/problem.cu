@@ -129,9 +129,15 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
   a.out = out;
   a.item_row = pl.item_row;
   a.item_slice = pl.item_slice;
+  a.slice_item_end = pl.slice_item_end;
   a.nitems = pl.nitems;
   a.win_lo = pl.win_lo;
   a.win_len = pl.win_len;
+  a.parts = pl.parts;
+  a.part_len = pl.part_len > 0 ? pl.part_len : (1 << 30);
+  a.nrows = pl.nrows;
+  a.part_off = pl.part_off;
+  a.part_acc = pl.part_acc;
   a.partials = p->partials;
   a.counter = p->counter;
   a.scal = scal;
@@ -412,29 +418,47 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
   pl.v.unroll = env_int("TVR_SPMV_UNROLL", 2);
   pl.v.minb = 0;  // chosen below from the shared-memory footprint
   pl.block = env_int("TVR_SPMV_BLOCK", 512);
-  if (!env_int("TVR_SPMV_STAGE", 1)) separable = false;
+  // Slice-structured matrices (every row inside one slice window) admit:
+  //  * 16-bit column offsets inside the window: 6 instead of 8 HBM bytes per entry (any window of
+  //    <= 65536 entries: c2 and c3);
+  //  * staging the window in shared memory when it fits (c2 both passes, c3 A^T); a larger
+  //    window (c3's 256 KB x-slice) is gathered from global memory (mostly L1 hits), or, with
+  //    TVR_PART_CAP set, cut into parts staged one after another (measured slower at c3).
+  // The TMA path and TVR_IDX16=0 use int32 columns with whole staged windows only.
   size_t smem = 0;
-  if (separable) {
-    int32_t maxlen = 0;
-    for (int32_t l : win_len) maxlen = std::max(maxlen, l);
-    smem = sizeof(float) * ((size_t)maxlen + ((size_t)maxlen >> 5) + 1);  // swz(c) = c + c/32
+  bool staged = separable && env_int("TVR_SPMV_STAGE", 1) != 0;
+  pl.parts = 1;
+  pl.part_len = 0;
+  int32_t maxlen = 0;
+  for (int32_t l : win_len) maxlen = std::max(maxlen, l);
+  const bool want16 = separable && maxlen <= 65536 && env_int("TVR_IDX16", 1) != 0 &&
+                      env_int("TVR_SPMV_TMA", 0) == 0;
+  if (staged) {
+    int32_t wlen = maxlen;
+    const int32_t cap = want16 ? std::min(65536, std::max(1024, env_int("TVR_PART_CAP", 65536))) : maxlen;
+    if (want16 && maxlen > cap) {
+      pl.parts = (maxlen + cap - 1) / cap;
+      pl.part_len = ((maxlen + pl.parts - 1) / pl.parts + 31) / 32 * 32;
+      wlen = pl.part_len;
+    } else if (want16) {
+      pl.part_len = (maxlen + 31) / 32 * 32;
+    }
+    smem = sizeof(float) * ((size_t)wlen + ((size_t)wlen >> 5) + 1);  // swz(c) = c + c/32
     int maxsmem = 0;
     cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
     // leave room for the reduction scratch of the kernel
-    if (smem + 2048 > (size_t)maxsmem) separable = false;
+    if (smem + 2048 > (size_t)maxsmem) {
+      staged = false;
+      pl.parts = 1;
+    }
   }
+  if (want16 && !staged) pl.part_len = (maxlen + 31) / 32 * 32;
   (void)pad;
-  pl.staged = separable;
-  pl.v.staged = separable;
-  pl.smem = separable ? smem : 0;
-  // 16-bit column offsets inside the slice window whenever every window fits 2^16 entries
-  // (c2 and c3 both do): 6 instead of 8 HBM bytes per entry.  The TMA path streams int32.
-  {
-    int32_t maxlen = 0;
-    for (int32_t l : win_len) maxlen = std::max(maxlen, l);
-    pl.v.idx16 = separable && maxlen <= 65536 && env_int("TVR_IDX16", 1) != 0 &&
-                 env_int("TVR_SPMV_TMA", 0) == 0;
-  }
+  pl.staged = staged;
+  pl.v.staged = staged;
+  pl.smem = staged ? smem : 0;
+  pl.v.idx16 = want16;
+  pl.v.parts = want16 && staged && pl.parts > 1;
   pl.v.lpr = env_int(lpr_env, lpr_for(mean_len, pl.v.idx16 ? 8 : 4));
   // Resident CTAs per SM: as many 512-thread CTAs as fit while leaving >= 80 KB of the 228 KB
   // L1/smem for L1 (the in-flight 128-bit streaming loads are staged in L1; with ~25 KB left the
@@ -473,8 +497,11 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
   if (separable) {
     TVR_TRY(upload(p, (void**)&pl.win_lo, win_lo.data(), sizeof(int64_t) * win_lo.size()));
     TVR_TRY(upload(p, (void**)&pl.win_len, win_len.data(), sizeof(int32_t) * win_len.size()));
-    TVR_TRY(make_tma_plan(p, pl, rp, slice_rows, pl.smem / sizeof(float)));
+    std::vector<int64_t> zend(win_lo.size(), 0);
+    for (size_t i = 0; i < slices.size(); ++i) zend[slices[i]] = (int64_t)i + 1;
+    TVR_TRY(upload(p, (void**)&pl.slice_item_end, zend.data(), sizeof(int64_t) * std::max<size_t>(1, zend.size())));
   }
+  if (staged) TVR_TRY(make_tma_plan(p, pl, rp, slice_rows, pl.smem / sizeof(float)));
   return TVR_OK;
 }
 
@@ -708,8 +735,14 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     uint16_t** dst = which ? &p->colT16 : &p->col16;
     TVR_TRY(dev_alloc(p, (void**)dst, sizeof(uint16_t) * nnz_pad));
     TVR_CUDA(cudaMemsetAsync(*dst, 0, sizeof(uint16_t) * nnz_pad, p->stream));
+    pl.nrows = which ? n : m;
+    if (pl.parts > 1) {
+      TVR_TRY(dev_alloc(p, (void**)&pl.part_off, sizeof(uint16_t) * (pl.parts - 1) * pl.nrows));
+      TVR_TRY(dev_alloc(p, (void**)&pl.part_acc, sizeof(double) * pl.nrows));
+    }
     SpmvArgs a = spmv_args(p, pl, which == 1, nullptr, nullptr, nullptr, nullptr);
-    TVR_CUDA(launch_compress_cols(a, which ? p->colT : p->col, *dst, false, nullptr, p->stream));
+    TVR_CUDA(launch_parts_rows(a, false, which ? p->colT : p->col, *dst, pl.part_off, nullptr,
+                               p->stream));
   }
   TVR_CUDA(cudaStreamSynchronize(p->stream));
   // the int32 columns are no longer read by any pass: release them (c3: 7.7 GB each)
@@ -898,7 +931,7 @@ int tvr_get_AT(tvr_problem* p, int64_t* rp_h, int32_t* col_h, float* val_h) {
     int32_t* tmp = nullptr;
     TVR_CUDA(cudaMalloc(&tmp, sizeof(int32_t) * std::max<int64_t>(p->nnz, 1)));
     SpmvArgs a = spmv_args(p, p->planT, true, nullptr, nullptr, nullptr, nullptr);
-    cudaError_t e = launch_compress_cols(a, nullptr, p->colT16, true, tmp, p->stream);
+    cudaError_t e = launch_parts_rows(a, true, nullptr, p->colT16, p->planT.part_off, tmp, p->stream);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(col_h, tmp, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, p->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);

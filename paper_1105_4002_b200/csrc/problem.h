@@ -56,6 +56,10 @@ struct TmaPlan {
 
 struct SpmvPlan {
   TmaPlan tma;
+  int parts = 1, part_len = 0;       // slice-window parts (16-bit kernel)
+  uint16_t* part_off = nullptr;      // (parts-1) x nrows
+  double* part_acc = nullptr;        // nrows
+  int64_t nrows = 0;
   bool staged = false;
   SpmvVariant v;
   int grid = 0, block = 512;
@@ -63,6 +67,7 @@ struct SpmvPlan {
   int64_t nitems = 0;
   int64_t* item_row = nullptr;
   int32_t* item_slice = nullptr;
+  int64_t* slice_item_end = nullptr;
   int64_t* win_lo = nullptr;
   int32_t* win_len = nullptr;
 };

@@ -151,8 +151,12 @@ __global__ void __launch_bounds__(512, MINB) spmv_kernel(SpmvArgs a) {
 // 16-bit column variant for slice-staged matrices: every column is stored as its offset inside
 // the slice window (< 65536), so one 16-byte load carries 8 columns and the entry costs 6 bytes
 // of HBM instead of 8.  Chunks are 8 entries (one int4 of columns + two float4 of values).
+// STAGED: gather from the shared-memory window; otherwise from global memory at gbase (the
+// window start), for windows too large to stage (c3's 256 KB x-slice, mostly L1-resident).
+template <bool STAGED>
 __device__ __forceinline__ double chunk8_dot(const int4 c, const float4 v0, const float4 v1, int lo,
-                                             int hi, const float* __restrict__ sm, double acc) {
+                                             int hi, const float* __restrict__ sm,
+                                             const float* __restrict__ gbase, double acc) {
   const uint32_t cw[4] = {(uint32_t)c.x, (uint32_t)c.y, (uint32_t)c.z, (uint32_t)c.w};
   const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
   double pr[8];
@@ -161,14 +165,18 @@ __device__ __forceinline__ double chunk8_dot(const int4 c, const float4 v0, cons
     const bool in = (q >= lo) & (q < hi);
     const int cidx = (int)((cw[q >> 1] >> (16 * (q & 1))) & 0xffffu);  // little-endian halves
     const float val = in ? vv[q] : 0.0f;
-    const float xv = sm[swz(in ? cidx : 0)];
+    float xv;
+    if constexpr (STAGED) xv = sm[swz(in ? cidx : 0)];
+    else xv = in ? __ldg(gbase + cidx) : 0.0f;
     pr[q] = (double)val * (double)xv;  // exact: 24-bit x 24-bit significands fit fp64
   }
   // pairwise tree (depth 3) instead of an 8-deep fma chain: shorter dependency latency
   return acc + (((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7])));
 }
 
-template <int LPR, int UNR, int MINB>
+// Main 16-bit kernel: whole slice window staged in shared memory (STAGED) or gathered from
+// global memory at the window start.  The CTA restages only when the slice changes.
+template <int LPR, int UNR, int MINB, bool STAGED>
 __global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
   extern __shared__ float stage[];
   const int lane = threadIdx.x & (LPR - 1);
@@ -177,16 +185,19 @@ __global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
   const int64_t it0 = (a.nitems * (int64_t)blockIdx.x) / gridDim.x;
   const int64_t it1 = (a.nitems * (int64_t)(blockIdx.x + 1)) / gridDim.x;
   int cur_slice = -1;
+  const float* gbase = a.src;
   double sq = 0.0;
   for (int64_t it = it0; it < it1; ++it) {
     const int z = a.item_slice[it];
     if (z != cur_slice) {
-      __syncthreads();
       const int64_t lo64 = a.win_lo[z];
-      const int len = a.win_len[z];
-      const float* src = a.src + lo64;
-      for (int i = threadIdx.x; i < len; i += blockDim.x) stage[swz(i)] = __ldg(src + i);
-      __syncthreads();
+      gbase = a.src + lo64;
+      if constexpr (STAGED) {
+        __syncthreads();
+        const int len = a.win_len[z];
+        for (int i = threadIdx.x; i < len; i += blockDim.x) stage[swz(i)] = __ldg(gbase + i);
+        __syncthreads();
+      }
       cur_slice = z;
     }
     const int64_t r0 = a.item_row[it], r1 = a.item_row[it + 1];
@@ -226,7 +237,8 @@ __global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u)
-          acc[u] = chunk8_dot(c[u], va[u], vb[u], lo - 8 * LPR * u, hi - 8 * LPR * u, stage, acc[u]);
+          acc[u] = chunk8_dot<STAGED>(c[u], va[u], vb[u], lo - 8 * LPR * u, hi - 8 * LPR * u, stage,
+                                      gbase, acc[u]);
         lo -= 8 * LPR * UNR;
         hi -= 8 * LPR * UNR;
       }
@@ -234,7 +246,7 @@ __global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
         const int4 c0 = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + ch * 8 * LPR));
         const float4 va0 = ld_stream_f4(vp + ch * 8 * LPR);
         const float4 vb0 = ld_stream_f4(vp + ch * 8 * LPR + 4);
-        acc[0] = chunk8_dot(c0, va0, vb0, lo, hi, stage, acc[0]);
+        acc[0] = chunk8_dot<STAGED>(c0, va0, vb0, lo, hi, stage, gbase, acc[0]);
         lo -= 8 * LPR;
         hi -= 8 * LPR;
       }
@@ -259,6 +271,160 @@ __global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
     double v[1] = {sq};
     reduce_to_scalars<1>(v, a.partials, a.counter, a.scal);
   }
+}
+
+// Window parts (opt-in, TVR_PART_CAP): a slice window larger than the shared-memory budget is
+// cut into `parts` pieces of part_len entries.  Columns ascend within a row, so each row's
+// entries are contiguous per part; part_off[(p-1) nrows + row] is the row-relative start of
+// part p.  The CTA stages part p and runs all rows of its slice segment on it, carrying the fp64
+// partial sum of each row in part_acc (same thread every part, so no synchronisation needed);
+// the last part finalises the row.  Measured slower than global gathers for c3's x-slice
+// (every part re-walks each row with half-empty chunks), so not the default.
+template <int LPR, int UNR, int MINB, bool STAGED>
+__global__ void __launch_bounds__(512, MINB) spmv16_parts_kernel(SpmvArgs a) {
+  extern __shared__ float stage[];
+  const int lane = threadIdx.x & (LPR - 1);
+  const int grp = threadIdx.x / LPR;
+  const int ngrp = blockDim.x / LPR;
+  const int64_t it0 = (a.nitems * (int64_t)blockIdx.x) / gridDim.x;
+  const int64_t it1 = (a.nitems * (int64_t)(blockIdx.x + 1)) / gridDim.x;
+  const int P = a.parts;
+  double sq = 0.0;
+  for (int64_t sa = it0; sa < it1;) {
+    const int z = a.item_slice[sa];
+    const int64_t zend = a.slice_item_end[z];
+    const int64_t sb = zend < it1 ? zend : it1;  // slice segment [sa, sb) of this CTA
+    const int64_t wlo = a.win_lo[z];
+    const int wlen = a.win_len[z];
+  for (int p = 0; p < P; ++p) {
+    const int plo = p * a.part_len;
+    const float* gbase = a.src + wlo + plo;
+    if constexpr (STAGED) {
+      const int plen = min(a.part_len, wlen - plo);
+      __syncthreads();
+      for (int i = threadIdx.x; i < plen; i += blockDim.x) stage[swz(i)] = __ldg(gbase + i);
+      __syncthreads();
+    }
+  for (int64_t it = sa; it < sb; ++it) {
+    const int64_t r0 = a.item_row[it], r1 = a.item_row[it + 1];
+    // entry range of `row` inside part p
+    auto extent = [&](int64_t rr, int64_t& s_, int64_t& e_) {
+      const int64_t rs = a.rp[rr];
+      s_ = rs + (p > 0 ? (int64_t)a.part_off[(int64_t)(p - 1) * a.nrows + rr] : 0);
+      e_ = (p == P - 1) ? a.rp[rr + 1] : rs + (int64_t)a.part_off[(int64_t)p * a.nrows + rr];
+    };
+    int64_t row = r0 + grp;
+    int64_t s_n = 0, e_n = 0;
+    if (row < r1) extent(row, s_n, e_n);
+    for (int64_t base = r0; base < r1; base += ngrp) {
+      const bool valid = row < r1;
+      const int64_t s = s_n, e = e_n;
+      const int64_t nrow = row + ngrp;
+      if (nrow < r1) extent(nrow, s_n, e_n);  // prefetch the next row's extent
+      const int64_t kb = s & ~int64_t(7);
+      const int span = (int)(e - kb);
+      int lo = (int)(s - kb) - 8 * lane;
+      int hi = span - 8 * lane;
+      const int nch = valid ? (span + 8 * LPR - 1) / (8 * LPR) : 0;
+      const uint16_t* cp = a.col16 + kb + 8 * lane;
+      const float* vp = a.val + kb + 8 * lane;
+      double acc[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) acc[u] = 0.0;
+      int ch = 0;
+      for (; ch + UNR <= nch; ch += UNR) {
+        int4 c[UNR];
+        float4 va[UNR], vb[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          c[u] = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + (ch + u) * 8 * LPR));
+          va[u] = ld_stream_f4(vp + (ch + u) * 8 * LPR);
+          vb[u] = ld_stream_f4(vp + (ch + u) * 8 * LPR + 4);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          acc[u] = chunk8_dot<STAGED>(c[u], va[u], vb[u], lo - 8 * LPR * u, hi - 8 * LPR * u, stage,
+                                      gbase, acc[u]);
+        lo -= 8 * LPR * UNR;
+        hi -= 8 * LPR * UNR;
+      }
+      for (; ch < nch; ++ch) {
+        const int4 c0 = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + ch * 8 * LPR));
+        const float4 va0 = ld_stream_f4(vp + ch * 8 * LPR);
+        const float4 vb0 = ld_stream_f4(vp + ch * 8 * LPR + 4);
+        acc[0] = chunk8_dot<STAGED>(c0, va0, vb0, lo, hi, stage, gbase, acc[0]);
+        lo -= 8 * LPR;
+        hi -= 8 * LPR;
+      }
+#pragma unroll
+      for (int u = 1; u < UNR; ++u) acc[0] += acc[u];
+      double accr = group_sum<LPR>(acc[0]);
+      if (valid && lane == 0) {
+        if (p > 0) accr += a.part_acc[row];
+        if (p < P - 1) {
+          a.part_acc[row] = accr;
+        } else if (a.b) {
+          const double r = accr - (double)a.b[row];
+          const float rh = (float)r;
+          a.out[row] = rh;
+          if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
+          sq += r * r;
+        } else {
+          a.out[row] = (float)accr;
+        }
+      }
+      row = nrow;
+    }
+  }  // items
+  }  // parts
+    sa = sb;
+  }  // slice segments
+  if (a.scal) {
+    double v[1] = {sq};
+    reduce_to_scalars<1>(v, a.partials, a.counter, a.scal);
+  }
+}
+
+// Per row of a staged plan with window parts: part_off (row-relative start of parts 1..P-1) and
+// col16[k] = (col[k] - win_lo) - part * part_len.  With expand, the inverse (canonical int32
+// columns from col16 and part_off).
+__global__ void parts_rows_kernel(int64_t nitems, const int64_t* __restrict__ item_row,
+                                  const int32_t* __restrict__ item_slice,
+                                  const int64_t* __restrict__ win_lo, const int64_t* __restrict__ rp,
+                                  int parts, int part_len, int64_t nrows, bool expand,
+                                  const int32_t* __restrict__ col, uint16_t* __restrict__ col16,
+                                  uint16_t* __restrict__ part_off, int32_t* __restrict__ col_out) {
+  for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int64_t base = win_lo[item_slice[it]];
+    for (int64_t row = item_row[it] + threadIdx.x; row < item_row[it + 1]; row += blockDim.x) {
+      const int64_t s = rp[row], e = rp[row + 1];
+      int q = 1;  // next boundary to record
+      for (int64_t k = s; k < e; ++k) {
+        int pk;
+        if (!expand) {
+          const int64_t off = (int64_t)col[k] - base;
+          pk = (int)(off / part_len);
+          while (q <= pk && q < parts) part_off[(int64_t)(q - 1) * nrows + row] = (uint16_t)(k - s), ++q;
+          col16[k] = (uint16_t)(off - (int64_t)pk * part_len);
+        } else {
+          pk = 0;
+          while (pk + 1 < parts && (k - s) >= (int64_t)part_off[(int64_t)pk * nrows + row]) ++pk;
+          col_out[k] = (int32_t)(base + (int64_t)pk * part_len + col16[k]);
+        }
+      }
+      if (!expand)
+        for (; q < parts; ++q) part_off[(int64_t)(q - 1) * nrows + row] = (uint16_t)(e - s);
+    }
+  }
+}
+
+cudaError_t launch_parts_rows(const SpmvArgs& a, bool expand, const int32_t* col, uint16_t* col16,
+                              uint16_t* part_off, int32_t* col_out, cudaStream_t st) {
+  const int grid = a.nitems < 148 * 16 ? (int)a.nitems : 148 * 16;
+  if (grid <= 0) return cudaSuccess;
+  parts_rows_kernel<<<grid, 128, 0, st>>>(a.nitems, a.item_row, a.item_slice, a.win_lo, a.rp, a.parts,
+                                          a.part_len, a.nrows, expand, col, col16, part_off, col_out);
+  return cudaGetLastError();
 }
 
 // col16[k] = col[k] - win_lo[slice of k's row]: the 16-bit window offsets of a staged plan.
@@ -387,22 +553,24 @@ static auto dispatch(const SpmvVariant& v, F&& f) {
            std::integral_constant<int, 2>{}, std::integral_constant<int, 1>{});
 }
 
-// 16-bit variants: staged only, UNR 2, lanes per row {4, 8, 16}, min resident CTAs {1, 2, 3}.
+// 16-bit variants: UNR 2, lanes per row {4, 8, 16}, min resident CTAs {1, 2, 3}, window staged
+// in shared memory or gathered from global memory.
 template <class F>
 static auto dispatch16(const SpmvVariant& v, F&& f) {
-#define TVR_V16(L, M) \
-  if (v.lpr == L && v.minb == M) return f(spmv16_kernel<L, 2, M>);
+#define TVR_V16(L, M)                                                                 \
+  if (v.lpr == L && v.minb == M)                                                      \
+    return v.parts ? f(spmv16_parts_kernel<L, 2, M, true>)                            \
+                   : (v.staged ? f(spmv16_kernel<L, 2, M, true>) : f(spmv16_kernel<L, 2, M, false>));
   TVR_V16(4, 1) TVR_V16(4, 2) TVR_V16(4, 3)
   TVR_V16(8, 1) TVR_V16(8, 2) TVR_V16(8, 3)
   TVR_V16(16, 1) TVR_V16(16, 2) TVR_V16(16, 3)
 #undef TVR_V16
-  return f(spmv16_kernel<8, 2, 1>);
+  return f(spmv16_kernel<8, 2, 1, true>);
 }
 
 bool spmv_variant_exists(const SpmvVariant& v) {
   if (v.idx16)
-    return v.staged && v.unroll == 2 && (v.lpr == 4 || v.lpr == 8 || v.lpr == 16) && v.minb >= 1 &&
-           v.minb <= 3;
+    return v.unroll == 2 && (v.lpr == 4 || v.lpr == 8 || v.lpr == 16) && v.minb >= 1 && v.minb <= 3;
   if (!(v.lpr == 4 || v.lpr == 8 || v.lpr == 16 || v.lpr == 32)) return false;
   if (v.unroll == 2) return v.minb >= 1 && v.minb <= 3;
   return v.unroll == 4 && v.minb == 1;

@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtvreg.so")
+# TVR_LIB_PATH: load another in-tree build (A/B timing of kernel revisions); default libtvreg.so
+LIB_PATH = os.environ.get("TVR_LIB_PATH") or os.path.join(_PKG, "libtvreg.so")
 
 # ---------------------------------------------------------------- status codes
 TVR_OK = 0

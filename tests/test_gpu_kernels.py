@@ -250,3 +250,28 @@ def test_tma_pipeline_matches_register_kernel_bitwise(tvreg, cfg, c1, monkeypatc
     assert rel(outs["reg16"][0], outs["reg"][0]) <= 1e-7
     assert abs(outs["reg16"][1] - outs["reg"][1]) <= 1e-13 * outs["reg"][1]
     assert rel(outs["reg16"][2], outs["reg"][2]) <= 1e-7
+
+
+@pytest.mark.parametrize("cap", [1024, 300, 128])
+def test_window_parts_match_oracle(tvreg, c1, cap, monkeypatch):
+    """Slice windows cut into parts (the c3 A pass path): rows' entries split at part boundaries,
+    fp64 partial sums carried between parts; dyadic data makes the result exact."""
+    monkeypatch.setenv("TVR_PART_CAP", str(cap))
+    A = _dyadic_separable(32, 32, 6, 12, 45)
+    rng = np.random.default_rng(7)
+    x = rng.integers(0, 9, A.n_cols).astype(np.float32)
+    b = rng.integers(0, 9, A.n_rows).astype(np.float32)
+    P = make(tvreg, A, b, (32, 32, 6))
+    assert P.info.slab_staged_A == 1 and P.info.slab_staged_AT == 1
+    r = torch.empty(A.n_rows, device="cuda")
+    fid = P.residual(dev(x), r)
+    r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x) - b
+    assert np.array_equal(host(r).astype(np.float64), r_ora)
+    assert fid == 0.5 * float(r_ora @ r_ora)
+    w = torch.empty(A.n_cols, device="cuda")
+    P.apply_AT(dev(b), w)
+    assert np.array_equal(host(w).astype(np.float64), oracle.rmatvec(A.row_ptr, A.col, A.val, b, A.n_cols))
+    rT, cT, vT = P.get_AT()
+    oT = oracle.transpose(A.row_ptr, A.col, A.val, A.n_cols)
+    assert np.array_equal(rT, oT[0]) and np.array_equal(cT, oT[1])
+    assert np.array_equal(vT.view(np.uint32), oT[2].view(np.uint32))
