@@ -270,6 +270,7 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0 and world == 1 and not args.no_solve:
         out["solvers"] = solver_timings(tvreg, torch)
+        out["c3_gradient"] = large_config_line(tvreg, torch)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(w)
     P.close()
@@ -278,19 +279,54 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
-def solver_timings(tvreg, torch):
-    """Time-to-eps of GPBB and UPN on the c1 workload (BJ:7: REL 1e-6 gradient map)."""
+def solver_timings(tvreg, torch, configs=("c1", "c2")):
+    """Time-to-eps of GPBB and UPN (BJ:7: gradient map 1e-6 relative to ||G_1(x_0)||, x_0 = 0),
+    with the algorithmic HBM GB/s of the whole solve (bytes of every pass / wall time)."""
     import harness
-    w = harness.preset("c1")
-    res = {}
+    out = {}
+    for cfg in configs:
+        w = harness.preset(cfg)
+        P = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
+                          stream=torch.cuda.current_stream().cuda_stream)
+        for solver in ("gpbb", "upn"):
+            x = torch.zeros(w.N, device="cuda")
+            r = getattr(P, f"solve_{solver}")(x, max_iters=20000, eps=1e-6)
+            out[f"{cfg}_{solver}"] = dict(
+                workload=f"{cfg} {w.grid[0]}^3, REL 1e-6", converged=r.converged, iters=r.iters,
+                n_f=r.n_f, n_grad=r.n_grad, seconds=r.seconds, f=r.f, gmap_rel=r.gmap_rel,
+                ms_per_iter=1e3 * r.seconds / max(1, r.iters), solve_hbm_gbs=r.bytes / r.seconds / 1e9)
+        P.close()
+        del w
+    return out
+
+
+def large_config_line(tvreg, torch, cfg="c3", steps=10):
+    """Gradient evaluations on the 256^3 workload (BJ:9), for context beside the c2 headline."""
+    import harness
+    w = harness.preset(cfg)
+    stream = torch.cuda.current_stream()
     P = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
-                      stream=torch.cuda.current_stream().cuda_stream)
-    for solver in ("gpbb", "upn"):
-        x = torch.zeros(w.N, device="cuda")
-        r = getattr(P, f"solve_{solver}")(x, max_iters=20000, eps=1e-6)
-        res[solver] = dict(workload="c1 (32^3, 12 views x 45 bins, REL 1e-6)", converged=r.converged,
-                           iters=r.iters, n_f=r.n_f, n_grad=r.n_grad, seconds=r.seconds, f=r.f,
-                           ms_per_iter=1e3 * r.seconds / max(1, r.iters))
+                      stream=stream.cuda_stream)
+    x = torch.from_numpy(harness.random_x(w.N)).cuda()
+    g = torch.empty(w.N, device="cuda")
+    for _ in range(3):
+        P.objective_grad(x, g)
+    P.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        P.objective_grad(x, g)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    st = P.kernel_stats()
+    peak, _ = peaks()
+    kt = {k: dict(ms_per_launch=v["ms"] / v["launches"],
+                  achieved_gbs=v["bytes"] / v["ms"] / 1e6, frac=v["bytes"] / v["ms"] / 1e6 / peak)
+          for k, v in st.items() if v["launches"]}
+    res = dict(workload=f"{cfg}: {w.grid[0]}^3, nnz {w.A.nnz}", value=1e3 / ms, unit=UNIT,
+               ms_per_step=ms, steps=steps, kernels=kt)
     P.close()
     return res
 
