@@ -79,17 +79,21 @@ __global__ void __launch_bounds__(512, MINB) spmv_kernel(SpmvArgs a) {
     const int64_t r0 = a.item_row[it], r1 = a.item_row[it + 1];
     int64_t row = r0 + grp;
     int64_t s_n = 0, e_n = 0;
+    float b_n = 0.0f;
     if (row < r1) {
       s_n = a.rp[row];
       e_n = a.rp[row + 1];
+      if (a.b) b_n = __ldg(a.b + row);
     }
     for (int64_t base = r0; base < r1; base += ngrp) {
       const bool valid = row < r1;
       const int64_t s = s_n, e = e_n;
+      const float bv = b_n;
       const int64_t nrow = row + ngrp;
-      if (nrow < r1) {  // prefetch the next row's extent
+      if (nrow < r1) {  // prefetch the next row's extent and data value
         s_n = a.rp[nrow];
         e_n = a.rp[nrow + 1];
+        if (a.b) b_n = __ldg(a.b + nrow);
       }
       const int64_t kb = s & ~int64_t(3);
       const int span = (int)(e - kb);
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(512, MINB) spmv_kernel(SpmvArgs a) {
       const double accr = group_sum<LPR>(acc[0]);
       if (valid && lane == 0) {
         if (a.b) {
-          const double r = accr - (double)a.b[row];
+          const double r = accr - (double)bv;
           const float rh = (float)r;
           a.out[row] = rh;
           if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);  // hi + lo carries r to ~2^-48
@@ -203,17 +207,21 @@ __global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
     const int64_t r0 = a.item_row[it], r1 = a.item_row[it + 1];
     int64_t row = r0 + grp;
     int64_t s_n = 0, e_n = 0;
+    float b_n = 0.0f;
     if (row < r1) {
       s_n = a.rp[row];
       e_n = a.rp[row + 1];
+      if (a.b) b_n = __ldg(a.b + row);
     }
     for (int64_t base = r0; base < r1; base += ngrp) {
       const bool valid = row < r1;
       const int64_t s = s_n, e = e_n;
+      const float bv = b_n;
       const int64_t nrow = row + ngrp;
-      if (nrow < r1) {
+      if (nrow < r1) {  // prefetch the next row's extent and data value
         s_n = a.rp[nrow];
         e_n = a.rp[nrow + 1];
+        if (a.b) b_n = __ldg(a.b + nrow);
       }
       const int64_t kb = s & ~int64_t(7);
       const int span = (int)(e - kb);
@@ -255,7 +263,7 @@ __global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
       const double accr = group_sum<LPR>(acc[0]);
       if (valid && lane == 0) {
         if (a.b) {
-          const double r = accr - (double)a.b[row];
+          const double r = accr - (double)bv;
           const float rh = (float)r;
           a.out[row] = rh;
           if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
