@@ -470,6 +470,8 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
       if ((double)m * (pl.smem + 1024) <= (228.0 - 80.0) * 1024) { minb = m; break; }
     pl.v.minb = env_int("TVR_SPMV_MINB", minb);
   }
+  // 3 chunks in flight for the staged 16-bit kernel at 2 CTAs/SM (1-3% faster than 2 at c2)
+  if (pl.v.idx16 && staged && !pl.v.parts && pl.v.minb == 2) pl.v.unroll = env_int("TVR_SPMV_UNROLL", 3);
   if (!spmv_variant_exists(pl.v)) {
     set_error("no SpMV kernel variant for lpr=" + std::to_string(pl.v.lpr));
     return TVR_E_ARG;
