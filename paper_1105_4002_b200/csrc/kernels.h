@@ -42,6 +42,7 @@ cudaError_t launch_compress_cols(const SpmvArgs& a, const int32_t* col, uint16_t
 cudaError_t launch_parts_rows(const SpmvArgs& a, bool expand, const int32_t* col, uint16_t* col16,
                               uint16_t* part_off, int32_t* col_out, cudaStream_t st);
 bool spmv_variant_exists(const SpmvVariant& v);
+cudaError_t ensure_smem_attr(const void* func, size_t smem);
 cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int block, size_t smem,
                         cudaStream_t st);
 int spmv_occupancy(const SpmvVariant& v, int block, size_t smem);

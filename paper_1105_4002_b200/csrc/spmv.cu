@@ -11,6 +11,8 @@
 // z-slice; rows slice-major) the gather vector of the current slice is staged in shared memory
 // once per slice change, so the x[col] / r[colT] gathers hit smem instead of L1/L2.
 // Instruction budget per entry: predicate, select, swizzle, LDS, 2 conversions, 1 DFMA.
+#include <map>
+#include <mutex>
 #include <type_traits>
 
 #include "common.cuh"
@@ -518,14 +520,28 @@ __global__ void gradient_map_kernel(int64_t n, const float* __restrict__ x,
 }
 
 // ----------------------------------------------------------------- launchers
+// Raise a kernel's dynamic shared-memory limit once per (function, device, size) instead of a
+// driver call on every launch (host overhead of the synchronous per-call API).
+cudaError_t ensure_smem_attr(const void* func, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{func, dev}];
+  if (have >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) have = smem;
+  return e;
+}
+
 template <int LPR, bool STAGED, int UNR, int MINB>
 static cudaError_t launch_spmv_t(const SpmvArgs& a, int grid, int block, size_t smem,
                                  cudaStream_t st) {
   auto k = spmv_kernel<LPR, STAGED, UNR, MINB>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+  cudaError_t e = ensure_smem_attr((const void*)k, smem);
+  if (e != cudaSuccess) return e;
   k<<<grid, block, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -599,10 +615,8 @@ cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int b
   if (!spmv_variant_exists(v)) return cudaErrorInvalidValue;
   if (v.idx16) {
     return dispatch16(v, [&](auto k) {
-      if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-      }
+      cudaError_t e = ensure_smem_attr((const void*)k, smem);
+      if (e != cudaSuccess) return e;
       k<<<grid, block, smem, st>>>(a);
       return cudaGetLastError();
     });

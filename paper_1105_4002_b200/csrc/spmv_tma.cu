@@ -297,7 +297,7 @@ __global__ void __launch_bounds__((kTmaConsumerWarps + kTmaProducerWarps) * 32, 
 cudaError_t launch_spmv_tma(const TmaSpmvArgs& a, int lpr, int grid, size_t smem, cudaStream_t st) {
   if (a.stages < kTmaConsumerWarps || a.stages % kTmaProducerWarps != 0) return cudaErrorInvalidValue;
   auto go = [&](auto kern) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_smem_attr((const void*)kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<grid, (kTmaConsumerWarps + kTmaProducerWarps) * 32, smem, st>>>(a);
     return cudaGetLastError();
