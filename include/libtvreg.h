@@ -14,8 +14,9 @@
  * Conventions for every entry point:
  *  - Every function returns a tvr_status; no C++ exception crosses this boundary.  On a
  *    non-OK status tvr_last_error() returns a thread-local message.
- *  - Volume vectors are fp32, x fastest, then y, then z; in z-slab mode a rank's vectors hold
- *    only its slices [z0, z1) (N_local = nx*ny*(z1-z0)).  Data vectors are fp32 of m_local.
+ *  - Volume vectors are fp32, x fastest, then y, then z; in z-slab and views mode a rank's
+ *    vectors hold only its slices [z0, z1) (N_local = nx*ny*(z1-z0)).  Data vectors are fp32
+ *    of m_local (the rank's rows of A).
  *  - "_dev" pointers are DEVICE pointers on the problem's device, caller-owned (e.g. torch
  *    tensors' data_ptr()); "_host" pointers are host memory (pinned is fastest).
  *  - Calls are ordered on the problem's CUDA stream and return once every host-side output
@@ -34,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TVR_ABI_VERSION 1
+#define TVR_ABI_VERSION 2
 
 typedef enum {
   TVR_OK = 0,
@@ -42,7 +43,8 @@ typedef enum {
   TVR_E_ARG = -1,           /* invalid argument (NULL, size, tau <= 0, alpha < 0, lo >= hi, ...) */
   TVR_E_CSR = -2,           /* malformed CSR: row_ptr not monotone / not 0..nnz, column out of
                                range or not strictly ascending within a row, non-finite value */
-  TVR_E_NOT_SEPARABLE = -3, /* z-slab mode: a local row touches voxels outside the rank's slab */
+  TVR_E_NOT_SEPARABLE = -3, /* z-slab mode: a local row touches voxels outside the rank's slab
+                               (non-separable geometry: use TVR_SHARD_VIEWS) */
   TVR_E_CUDA = -4,          /* CUDA runtime error (message names the call) */
   TVR_E_NCCL = -5,          /* NCCL error */
   TVR_E_OOM = -6,           /* device allocation failed */
@@ -68,12 +70,19 @@ typedef struct {
   int32_t nx, ny, nz; /* global volume; voxel j = (z*ny + y)*nx + x */
 } tvr_grid;
 
-enum { TVR_SHARD_NONE = 0, TVR_SHARD_ZSLAB = 1 };
+enum { TVR_SHARD_NONE = 0, TVR_SHARD_ZSLAB = 1, TVR_SHARD_VIEWS = 2 };
 
 /* Distribution / placement.  NULL => one GPU, current device, a library-created stream.
- * ZSLAB: rank owns slices [z0, z1) and the rows of A whose voxels lie there; the TV stencil
- * exchanges one halo slice with each z-neighbour over NCCL (nccl_comm from
- * tvr_nccl_comm_init), scalars are all-gathered and summed in rank order. */
+ * ZSLAB (P1, slice-separable geometry): rank owns slices [z0, z1) and the rows
+ *   of A whose voxels lie there; A and A^T need no communication.
+ * VIEWS (P2, any geometry, e.g. rays tilted in z, BJ:11): rank owns an arbitrary block of A's
+ *   rows (normally a contiguous range of projection views) with GLOBAL columns, and slices
+ *   [z0, z1) of every volume vector.  Before each A pass the slabs of the point are
+ *   all-gathered into a full-volume buffer; the A^T pass produces a full-volume partial
+ *   A_p^T r_p that is reduce-scattered (fp32 sum) to the slabs.
+ * In both modes the TV stencil exchanges one halo slice with each z-neighbour over NCCL
+ * (nccl_comm from tvr_nccl_comm_init) and scalars are all-gathered and summed in rank order.
+ * The slabs must tile [0, nz) in rank order (rank r's z1 = rank r+1's z0). */
 typedef struct {
   int32_t world, rank, mode;
   int32_t z0, z1;
@@ -96,6 +105,8 @@ typedef struct {
   int32_t slab_staged_A, slab_staged_AT; /* SpMV kernel: 0 global gathers, 1 slice staged in
                                            smem, 2 slice staged + TMA bulk-copy pipeline */
   int64_t device_bytes;                /* device memory held by the problem */
+  int64_t n_cols_local;                /* columns of the local A (= rows of its A^T): N_local,
+                                          or N in VIEWS mode */
 } tvr_info;
 int tvr_get_info(const tvr_problem* p, tvr_info* info);
 
@@ -165,13 +176,15 @@ int tvr_solve_upn(tvr_problem* p, float* x_dev_inout, const tvr_upn_opts* opts, 
 /* ---- inspection hooks (tests) ---- */
 /* y = A x - b (fused residual, the a1 pass); returns 1/2 ||Ax - b||^2 in *fid (nullable). */
 int tvr_residual(tvr_problem* p, const float* x_dev, float* r_dev, double* fid);
-/* w = A^T y using the stored transposed CSR (the a2 pass). y_dev: m_local, w_dev: N_local. */
+/* w = A^T y using the stored transposed CSR (the a2 pass). y_dev: m_local, w_dev: N_local
+ * (VIEWS mode: the rank's slab of sum_p A_p^T y_p; collective). */
 int tvr_apply_AT(tvr_problem* p, const float* y_dev, float* w_dev);
 /* TV_tau(x) and, if grad_dev != NULL, grad TV_tau(x). */
 int tvr_tv(tvr_problem* p, const float* x_dev, double* tv_out, float* grad_dev);
 /* ||G_nu(x)||_2 with G_nu(x) = nu (x - P_Q(x - grad f(x)/nu)) (Eq. (10)); G_dev nullable. */
 int tvr_gradient_map(tvr_problem* p, const float* x_dev, double nu, double* norm_out, float* G_dev);
-/* Copy the device transposed CSR to host arrays of n_local+1 / nnz_local entries. */
+/* Copy the device transposed CSR to host arrays of n_cols_local+1 / nnz_local entries
+ * (n_cols_local = N_local, or N in VIEWS mode, where A^T of the local rows spans the volume). */
 int tvr_get_AT(tvr_problem* p, int64_t* row_ptr_host, int32_t* col_host, float* val_host);
 
 /* ---- per-kernel timing (CUDA events on the problem's stream) ---- */

@@ -184,20 +184,28 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
 // Algorithmic bytes per entry: fp32 value + int32 column, or + 16-bit column offset.
 static double entry_bytes(const SpmvPlan& pl) { return pl.v.idx16 ? 6.0 : 8.0; }
 
+// x: a slab volume vector.  VIEWS mode gathers the whole point first (gather_volume).
 int pass_residual(tvr_problem* p, const float* x, float* r, int slot, float* r_lo) {
-  const double bytes = entry_bytes(p->planA) * p->nnz + 8.0 * (p->m + 1) + 4.0 * n_local(p) +
+  const float* src = x;
+  TVR_TRY(gather_volume(p, x, &src));
+  const double bytes = entry_bytes(p->planA) * p->nnz + 8.0 * (p->m + 1) + 4.0 * p->ncol +
                        8.0 * p->m + (r_lo ? 4.0 * p->m : 0.0);
   return launch(p, K_SPMV_A, bytes, [&] {
-    return run_spmv(p, p->planA, false, x, p->b, r, r_lo, p->dscal + slot);
+    return run_spmv(p, p->planA, false, src, p->b, r, r_lo, p->dscal + slot);
   });
 }
 
+// w: a slab volume vector.  VIEWS mode computes the full-volume partial A_p^T r_p and
+// reduce-scatters it to the slabs.
 int pass_AT(tvr_problem* p, const float* r, float* w) {
+  float* dst = views_dist(p) ? p->wfull : w;
   const double bytes =
-      entry_bytes(p->planT) * p->nnz + 8.0 * (n_local(p) + 1) + 4.0 * p->m + 4.0 * n_local(p);
-  return launch(p, K_SPMV_AT, bytes, [&] {
-    return run_spmv(p, p->planT, true, r, nullptr, w, nullptr, nullptr);
-  });
+      entry_bytes(p->planT) * p->nnz + 8.0 * (p->ncol + 1) + 4.0 * p->m + 4.0 * p->ncol;
+  TVR_TRY(launch(p, K_SPMV_AT, bytes, [&] {
+    return run_spmv(p, p->planT, true, r, nullptr, dst, nullptr, nullptr);
+  }));
+  if (views_dist(p)) TVR_TRY(reduce_scatter_volume(p, dst, w));
+  return TVR_OK;
 }
 
 static TVArgs tv_args(tvr_problem* p, int slot) {
@@ -575,25 +583,33 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     p->comm = dist->nccl_comm;
     p->device = dist->device;
     user_stream = (cudaStream_t)dist->cuda_stream;
-    if (p->mode == TVR_SHARD_ZSLAB) {
+    if (p->mode == TVR_SHARD_ZSLAB || p->mode == TVR_SHARD_VIEWS) {
       p->z0 = dist->z0; p->z1 = dist->z1;
       if (p->z0 < 0 || p->z1 > grid.nz || p->z0 >= p->z1) { set_error("tvr_create: bad slab"); return TVR_E_ARG; }
     } else if (p->mode != TVR_SHARD_NONE) {
       set_error("tvr_create: unknown shard mode");
       return TVR_E_ARG;
     }
-    if (p->world > 1 && (p->mode != TVR_SHARD_ZSLAB || !p->comm)) {
-      set_error("tvr_create: world > 1 needs ZSLAB mode and an NCCL communicator");
+    if (p->world > 1 && (p->mode == TVR_SHARD_NONE || !p->comm)) {
+      set_error("tvr_create: world > 1 needs ZSLAB or VIEWS mode and an NCCL communicator");
+      return TVR_E_ARG;
+    }
+    if (p->rank < 0 || p->rank >= p->world) { set_error("tvr_create: bad rank"); return TVR_E_ARG; }
+    if (p->world == 1 && (p->z0 != 0 || p->z1 != grid.nz) && p->mode == TVR_SHARD_VIEWS) {
+      set_error("tvr_create: VIEWS mode on one rank owns every slice");
       return TVR_E_ARG;
     }
   }
   p->nzl = p->z1 - p->z0;
+  const bool views = p->mode == TVR_SHARD_VIEWS;
+  p->zA0 = views ? 0 : p->z0;
+  p->nzA = views ? grid.nz : p->nzl;
 
   // ---- validate the CSR (host) ----
   const int64_t m = A->n_rows, nnz = A->nnz;
   const int64_t* rp = A->row_ptr;
   if (rp[0] != 0 || rp[m] != nnz) { set_error("CSR: row_ptr[0] != 0 or row_ptr[m] != nnz"); return TVR_E_CSR; }
-  const int64_t colmin = p->z0 * p->plane, colmax = p->z1 * p->plane;
+  const int64_t colmin = p->zA0 * p->plane, colmax = (p->zA0 + p->nzA) * p->plane;
   p->separable = true;
   std::vector<int32_t> row_slice(m, -1);
   for (int64_t i = 0; i < m; ++i) {
@@ -628,10 +644,10 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     }
   }
   if (p->separable) {
-    p->slice_row.assign(p->nzl + 1, m);
+    p->slice_row.assign(p->nzA + 1, m);
     p->slice_row[0] = 0;
     int64_t i = 0;
-    for (int z = 1; z <= p->nzl; ++z) {
+    for (int z = 1; z <= p->nzA; ++z) {
       while (i < m && row_slice[i] < z) ++i;
       p->slice_row[z] = i;
     }
@@ -639,8 +655,9 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
 
   p->m = m;
   p->n = p->plane * p->nzl;
+  p->ncol = p->plane * p->nzA;
   p->nnz = nnz;
-  const int64_t n = p->n;
+  const int64_t n = p->ncol;  // rows of the local A^T
 
   // ---- device and stream (everything above is host-only validation) ----
   if (p->device < 0) TVR_CUDA(cudaGetDevice(&p->device));
@@ -707,7 +724,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     std::vector<int64_t> wlo, sr;
     std::vector<int32_t> wlen;
     if (p->separable) {
-      for (int z = 0; z < p->nzl; ++z) { wlo.push_back((int64_t)z * p->plane); wlen.push_back((int32_t)p->plane); }
+      for (int z = 0; z < p->nzA; ++z) { wlo.push_back((int64_t)z * p->plane); wlen.push_back((int32_t)p->plane); }
     }
     const double mean_A = m > 0 ? (double)nnz / m : 0.0;
     TVR_TRY(make_plan(p, p->planA, rpv, m, p->separable, p->slice_row, wlo, wlen,
@@ -719,8 +736,8 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     TVR_CUDA(cudaStreamSynchronize(p->stream));
     wlo.clear(); wlen.clear();
     if (p->separable) {
-      for (int z = 0; z <= p->nzl; ++z) sr.push_back((int64_t)z * p->plane);
-      for (int z = 0; z < p->nzl; ++z) {
+      for (int z = 0; z <= p->nzA; ++z) sr.push_back((int64_t)z * p->plane);
+      for (int z = 0; z < p->nzA; ++z) {
         wlo.push_back(p->slice_row[z]);
         wlen.push_back((int32_t)(p->slice_row[z + 1] - p->slice_row[z]));
       }
@@ -764,6 +781,13 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     float* q = nullptr;
     TVR_TRY(dev_alloc(p, (void**)&q, sizeof(float) * std::max<int64_t>(m, 1)));
     p->dat.push_back(q);
+  }
+  if (views_dist(p)) {
+    // every rank's slab bounds, all-gathered from the callers' tvr_dist (the slabs must tile
+    // [0, nz) in rank order)
+    TVR_TRY(dev_alloc(p, (void**)&p->xfull, sizeof(float) * p->ncol));
+    TVR_TRY(dev_alloc(p, (void**)&p->wfull, sizeof(float) * p->ncol));
+    TVR_TRY(views_slab_table(p));
   }
   tv_set_grid(p->num_sms);
   const int64_t maxgrid = std::max<int64_t>({(int64_t)p->planA.grid, (int64_t)p->planT.grid,
@@ -826,6 +850,7 @@ int tvr_get_info(const tvr_problem* p, tvr_info* info) {
   info->slab_staged_A = p->planA.tma.on ? 2 : (p->planA.staged ? 1 : 0);
   info->slab_staged_AT = p->planT.tma.on ? 2 : (p->planT.staged ? 1 : 0);
   info->device_bytes = p->device_bytes;
+  info->n_cols_local = p->ncol;
   return TVR_OK;
 }
 
@@ -927,7 +952,7 @@ int tvr_gradient_map(tvr_problem* p, const float* x_dev, double nu, double* norm
 int tvr_get_AT(tvr_problem* p, int64_t* rp_h, int32_t* col_h, float* val_h) {
   if (!p) { set_error("tvr_get_AT: NULL"); return TVR_E_ARG; }
   TVR_CUDA(cudaSetDevice(p->device));
-  if (rp_h) TVR_CUDA(cudaMemcpyAsync(rp_h, p->rpT, sizeof(int64_t) * (p->n + 1), cudaMemcpyDeviceToHost, p->stream));
+  if (rp_h) TVR_CUDA(cudaMemcpyAsync(rp_h, p->rpT, sizeof(int64_t) * (p->ncol + 1), cudaMemcpyDeviceToHost, p->stream));
   if (col_h && p->colT16) {
     // the device holds 16-bit window offsets: expand them back to the canonical int32 columns
     int32_t* tmp = nullptr;

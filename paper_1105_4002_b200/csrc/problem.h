@@ -86,6 +86,10 @@ struct tvr_problem {
   bool own_stream = false;
   int nx = 0, ny = 0, nz = 0, z0 = 0, z1 = 0, nzl = 0;
   int64_t plane = 0, m = 0, n = 0, nnz = 0;
+  // columns of the local A (= rows of its A^T) and the slices they span: the slab (n, z0, nzl)
+  // in NONE / ZSLAB mode, the whole volume (N, 0, nz) in VIEWS mode
+  int64_t ncol = 0;
+  int zA0 = 0, nzA = 0;
   double alpha = 0, tau = 0, lo = 0, hi = 0;
   int world = 1, rank = 0, mode = TVR_SHARD_NONE;
   void* comm = nullptr;
@@ -119,6 +123,11 @@ struct tvr_problem {
 
   // halo exchange staging (z-slab)
   float* halo_send = nullptr;
+  // VIEWS mode with world > 1: full-volume gather target of the A pass and full-volume partial
+  // A_p^T r_p before the reduce-scatter; per-rank slab offsets / sizes (elements)
+  float* xfull = nullptr;
+  float* wfull = nullptr;
+  std::vector<int64_t> slab_off, slab_cnt;
 
   // profiling
   bool prof = false;
@@ -168,6 +177,12 @@ int halo_exchange(tvr_problem* p, float* v);
 int halo_fill_trial(tvr_problem* p, const float* x, const float* g, double s, float* v);
 int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double beta, float* y);
 int dist_sum_scalars(tvr_problem* p, double* vals, int n);
+// VIEWS mode: the A pass's source (slab -> full volume, all-gathered) and the A^T pass's
+// target (full-volume partial -> slab, reduce-scattered); identity on one rank
+bool views_dist(const tvr_problem* p);
+int views_slab_table(tvr_problem* p);
+int gather_volume(tvr_problem* p, const float* slab, const float** full);
+int reduce_scatter_volume(tvr_problem* p, const float* full, float* slab);
 void resolve_pending_timings(tvr_problem* p);
 
 }  // namespace tvr

@@ -1,9 +1,15 @@
-"""z-slab partitioning and NCCL bootstrap for multi-GPU runs.
+"""Partitioning and NCCL bootstrap for multi-GPU runs.
 
-Host-side plumbing only: which slices and rows a rank owns, extraction of its local CSR, and
-creation of the library's NCCL communicator from a unique id broadcast over a
-torch.distributed process group.  The exchange itself (one-slice halo send/recv and the
-rank-ordered scalar sum) runs inside libtvreg (csrc/dist.cu).
+P1 (z-slab, slice-separable geometry): a rank owns slices [z0, z1) and the rows of A whose
+voxels lie there.  P2 (views, any geometry, e.g. c5's tilted rays): a rank owns a contiguous
+range of projection views (rows view-major, C4) with global columns, plus a z-slab of every
+volume vector.
+
+Host-side plumbing only: which slices / views and rows a rank owns, extraction of its local
+CSR, and creation of the library's NCCL communicator from a unique id broadcast over a
+torch.distributed process group.  The exchanges themselves (halo send/recv, rank-ordered
+scalar sum, and in P2 the all-gather of the point and reduce-scatter of A^T r) run inside
+libtvreg (csrc/dist.cu).
 """
 from __future__ import annotations
 
@@ -70,6 +76,36 @@ def local_slab(row_ptr, col, val, b, grid, world: int, rank: int, slices=None) -
     e0, e1 = int(row_ptr[r0]), int(row_ptr[r1])
     return LocalSlab(z0, z1, r0, r1, (row_ptr[r0:r1 + 1] - e0).astype(np.int64),
                      col[e0:e1], val[e0:e1], b[r0:r1])
+
+
+@dataclass
+class LocalViews:
+    v0: int
+    v1: int
+    z0: int
+    z1: int
+    row0: int
+    row1: int
+    row_ptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+    b: np.ndarray
+
+
+def local_views(row_ptr, col, val, b, grid, n_views: int, world: int, rank: int) -> LocalViews:
+    """P2: the rank's views [v0, v1) (balanced like slab_bounds), their rows (view-major: view v
+    owns rows [v R, (v+1) R), R = m / n_views) with GLOBAL columns, and the rank's z-slab of the
+    volume vectors."""
+    m = len(row_ptr) - 1
+    if n_views <= 0 or m % n_views:
+        raise ValueError(f"{m} rows are not {n_views} equal views")
+    R = m // n_views
+    v0, v1 = slab_bounds(n_views, world, rank)
+    z0, z1 = slab_bounds(grid[2], world, rank)
+    r0, r1 = v0 * R, v1 * R
+    e0, e1 = int(row_ptr[r0]), int(row_ptr[r1])
+    return LocalViews(v0, v1, z0, z1, r0, r1, (row_ptr[r0:r1 + 1] - e0).astype(np.int64),
+                      col[e0:e1], val[e0:e1], b[r0:r1])
 
 
 def nccl_comm_from_process_group(world: int, rank: int, device: int) -> int:

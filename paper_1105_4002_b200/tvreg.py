@@ -33,6 +33,7 @@ STATUS_NAMES = {v: k for k, v in globals().items() if k.startswith("TVR_") and i
 
 TVR_SHARD_NONE = 0
 TVR_SHARD_ZSLAB = 1
+TVR_SHARD_VIEWS = 2
 TVR_STOP_REL = 0
 TVR_STOP_ABS_PER_N = 1
 
@@ -56,7 +57,7 @@ class tvr_dist(ctypes.Structure):
 class tvr_info(ctypes.Structure):
     _fields_ = [("m_local", c_i64), ("n_local", c_i64), ("nnz_local", c_i64), ("z0", c_i32),
                 ("z1", c_i32), ("slab_staged_A", c_i32), ("slab_staged_AT", c_i32),
-                ("device_bytes", c_i64)]
+                ("device_bytes", c_i64), ("n_cols_local", c_i64)]
 
 
 class tvr_fparts(ctypes.Structure):
@@ -243,7 +244,9 @@ class Problem:
     def __init__(self, row_ptr, col, val, b, grid, alpha: float, tau: float, lo: float = 0.0,
                  hi: float = math.inf, *, n_cols: int | None = None, world: int = 1, rank: int = 0,
                  z0: int | None = None, z1: int | None = None, nccl_comm: int | None = None,
-                 device: int = -1, stream: int | None = None):
+                 device: int = -1, stream: int | None = None, shard: str | None = None):
+        """shard: None (ZSLAB when world > 1 or z0 is given, else NONE), "zslab" or "views"
+        (rows of any geometry, global columns; see tvr_dist in include/libtvreg.h)."""
         L = lib()
         self._keep = [np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
                       np.ascontiguousarray(val, np.float32), np.ascontiguousarray(b, np.float32)]
@@ -253,8 +256,12 @@ class Problem:
         csr = tvr_csr(len(rp) - 1, n_cols if n_cols is not None else nx * ny * nz, int(rp[-1]),
                       rp.ctypes.data, cl.ctypes.data, vl.ctypes.data)
         dist = None
-        if world > 1 or z0 is not None or stream is not None or device >= 0:
-            dist = tvr_dist(world, rank, TVR_SHARD_ZSLAB if (world > 1 or z0 is not None) else TVR_SHARD_NONE,
+        if shard is None:
+            mode = TVR_SHARD_ZSLAB if (world > 1 or z0 is not None) else TVR_SHARD_NONE
+        else:
+            mode = {"none": TVR_SHARD_NONE, "zslab": TVR_SHARD_ZSLAB, "views": TVR_SHARD_VIEWS}[shard]
+        if mode != TVR_SHARD_NONE or stream is not None or device >= 0:
+            dist = tvr_dist(world, rank, mode,
                             0 if z0 is None else z0, nz if z1 is None else z1,
                             nccl_comm, device, stream)
         h = c_vp()
@@ -321,7 +328,7 @@ class Problem:
         return v.value
 
     def get_AT(self):
-        rp = np.empty(self.n + 1, np.int64)
+        rp = np.empty(self.info.n_cols_local + 1, np.int64)
         cl = np.empty(self.nnz, np.int32)
         vl = np.empty(self.nnz, np.float32)
         _check(lib().tvr_get_AT(self._h, rp.ctypes.data, cl.ctypes.data, vl.ctypes.data), "tvr_get_AT")

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(tvreg.SIGNATURES), set(names) ^ set(tvreg.SIGNATURES)
-    assert L.tvr_abi_version() == 1
+    assert L.tvr_abi_version() == 2
 
 
 def test_defaults_match_the_paper():
@@ -67,3 +67,16 @@ def test_create_slab_rejects_rows_outside_the_slab():
     with pytest.raises(tvreg.TVRError) as e:
         _create([0, 2], [0, 5], [1, 1], [0], grid=(2, 2, 2), z0=1, z1=2)
     assert e.value.status == tvreg.TVR_E_NOT_SEPARABLE
+
+
+@pytest.mark.parametrize("kw", [
+    dict(shard="views", z0=1, z1=2),                  # one VIEWS rank must own every slice
+    dict(shard="views", world=2, rank=0, z0=0, z1=1),  # world > 1 needs an NCCL communicator
+    dict(shard="views", z0=0, z1=3),                  # slab past nz
+    dict(shard="zslab", world=2, rank=2, z0=0, z1=1, nccl_comm=1),  # rank out of range
+])
+def test_create_views_mode_validation(kw):
+    # host-side checks, before any CUDA call: a tilted row (voxels 0 and 5) is fine in VIEWS mode
+    with pytest.raises(tvreg.TVRError) as e:
+        _create([0, 2], [0, 5], [1, 1], [0], grid=(2, 2, 2), **kw)
+    assert e.value.status == tvreg.TVR_E_ARG

@@ -13,7 +13,7 @@ import torch.multiprocessing as mp
 
 import harness
 import oracle
-from paper_1105_4002_b200.dist import local_slab, row_slices, slab_bounds
+from paper_1105_4002_b200.dist import local_slab, local_views, row_slices, slab_bounds
 
 
 def _free_port():
@@ -89,6 +89,28 @@ def _rank_ordered_sum(vals, world):
     return acc.numpy()
 
 
+def _tv_slab(xl, nxy, z0, z1, tau, rank, world):
+    """Owned TV value and TV gradient of a slab from its halo-exchanged volume (csrc/tv.cu's
+    decomposition: planes [z0, z1), the upper halo supplying dz of the last owned plane)."""
+    nx, ny = nxy
+    plane = nx * ny
+    nzl = z1 - z0
+    v = torch.zeros((nzl + 2) * plane, dtype=torch.float64)
+    v[plane:(nzl + 1) * plane] = torch.from_numpy(xl)
+    _halo_exchange(v, plane, rank, world)
+    vz0 = z0 - (1 if rank > 0 else 0)
+    vz1 = z1 + (1 if rank < world - 1 else 0)
+    lo = plane if rank > 0 else 0
+    ext = v.numpy()[plane - lo:(nzl + 1) * plane + (plane if rank < world - 1 else 0)]
+    _, g_ext = oracle.tv((nx, ny, vz1 - vz0), ext, tau)
+    g_tv = g_ext[lo:lo + nzl * plane]
+    up = ext[lo:]
+    tv_own = oracle.tv((nx, ny, len(up) // plane), up, tau, False)[0]
+    if rank < world - 1:
+        tv_own -= oracle.tv((nx, ny, 1), up[-plane:], tau, False)[0]
+    return tv_own, g_tv
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -105,21 +127,7 @@ def _worker(rank, world, port, q):
         xl = x[sl.z0 * plane:sl.z1 * plane].astype(np.float64)
         r = oracle.matvec(sl.row_ptr, col_loc, sl.val, xl) - sl.b.astype(np.float64)
         wl = oracle.rmatvec(sl.row_ptr, col_loc, sl.val, r, nzl * plane)
-        # volume with halo planes, exchanged
-        v = torch.zeros((nzl + 2) * plane, dtype=torch.float64)
-        v[plane:(nzl + 1) * plane] = torch.from_numpy(xl)
-        _halo_exchange(v, plane, rank, world)
-        vz0 = sl.z0 - (1 if rank > 0 else 0)
-        vz1 = sl.z1 + (1 if rank < world - 1 else 0)
-        lo = plane if rank > 0 else 0
-        ext = v.numpy()[plane - lo:(nzl + 1) * plane + (plane if rank < world - 1 else 0)]
-        _, g_ext = oracle.tv((nx, ny, vz1 - vz0), ext, w.tau)
-        g_tv = g_ext[lo:lo + nzl * plane]
-        # owned TV value: planes [z0, z1) with the upper halo supplying dz
-        up = ext[lo:]
-        tv_own = oracle.tv((nx, ny, len(up) // plane), up, w.tau, False)[0]
-        if rank < world - 1:
-            tv_own -= oracle.tv((nx, ny, 1), up[-plane:], w.tau, False)[0]
+        tv_own, g_tv = _tv_slab(xl, (nx, ny), sl.z0, sl.z1, w.tau, rank, world)
         s = _rank_ordered_sum([float(r @ r), tv_own], world)
         g_loc = wl + w.alpha * g_tv
         f = 0.5 * s[0] + w.alpha * s[1]
@@ -151,3 +159,89 @@ def test_sharded_gradient_matches_unsharded(world):
     assert [r[1] for r in res][0] == 0 and res[-1][2] == 8
     assert np.allclose(gs, g, rtol=1e-12, atol=1e-12 * np.abs(g).max())
     assert gs.size == plane * 8
+
+
+# ---------------------------------------------------------------- P2: views sharding
+# csrc/dist.cu's VIEWS mode: all-gather of the point (ragged slabs: one broadcast per rank),
+# local A pass over the rank's views with global columns, full-volume A_p^T r_p, reduce to each
+# slab's owner (ragged: one reduce per rank), then the z-slab TV as in P1.
+_TILT = dict(grid=(10, 9, 8), views=6, det=(5, 13), tilt=10.0)
+
+
+def _tilted():
+    nx, ny, nz = _TILT["grid"]
+    A = harness.siddon_tilted(nx, ny, nz, _TILT["views"], *_TILT["det"], _TILT["tilt"])
+    b = harness.simulate_data(A, harness.phantom(nx, ny, nz, 3))
+    return A, b
+
+
+def test_local_views_partition_rows():
+    A, b = _tilted()
+    for world in (2, 3, 4):
+        parts = [local_views(A.row_ptr, A.col, A.val, b, _TILT["grid"], _TILT["views"], world, r)
+                 for r in range(world)]
+        assert parts[0].row0 == 0 and parts[-1].row1 == A.n_rows
+        assert all(parts[i].row1 == parts[i + 1].row0 for i in range(world - 1))
+        assert parts[0].z0 == 0 and parts[-1].z1 == _TILT["grid"][2]
+        assert np.array_equal(np.concatenate([p.b for p in parts]), b)
+        assert np.array_equal(np.concatenate([p.col for p in parts]), A.col)
+    with pytest.raises(ValueError):
+        local_views(A.row_ptr, A.col, A.val, b, _TILT["grid"], 7, 2, 0)
+
+
+def _views_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A, b = _tilted()
+        nx, ny, nz = _TILT["grid"]
+        plane, N = nx * ny, nx * ny * nz
+        alpha, tau = 0.02, 1e-2
+        lv = local_views(A.row_ptr, A.col, A.val, b, _TILT["grid"], _TILT["views"], world, rank)
+        bounds = [slab_bounds(nz, world, r) for r in range(world)]
+        x = harness.random_x(N).astype(np.float64)
+        xl = x[lv.z0 * plane:lv.z1 * plane].copy()
+        # all-gather the point: one broadcast per rank into its slab of the full buffer
+        full = torch.zeros(N, dtype=torch.float64)
+        for r, (z0, z1) in enumerate(bounds):
+            piece = torch.from_numpy(xl) if r == rank else torch.zeros((z1 - z0) * plane, dtype=torch.float64)
+            dist.broadcast(piece, src=r)
+            full[z0 * plane:z1 * plane] = piece
+        r_loc = oracle.matvec(lv.row_ptr, lv.col, lv.val, full.numpy()) - lv.b.astype(np.float64)
+        w_part = torch.from_numpy(oracle.rmatvec(lv.row_ptr, lv.col, lv.val, r_loc, N))
+        # reduce-scatter: each slab summed onto its owner
+        w_slab = None
+        for r, (z0, z1) in enumerate(bounds):
+            piece = w_part[z0 * plane:z1 * plane].clone()
+            dist.reduce(piece, dst=r)
+            if r == rank:
+                w_slab = piece.numpy()
+        tv_own, g_tv = _tv_slab(xl, (nx, ny), lv.z0, lv.z1, tau, rank, world)
+        s = _rank_ordered_sum([float(r_loc @ r_loc), tv_own], world)
+        q.put((rank, lv.z0, lv.z1, 0.5 * s[0] + alpha * s[1], w_slab + alpha * g_tv))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_views_sharded_gradient_matches_unsharded(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_views_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A, b = _tilted()
+    Po = oracle.Problem(A.row_ptr, A.col, A.val, b, _TILT["grid"], 0.02, 1e-2)
+    f, g = Po.fg(harness.random_x(A.n_cols))
+    fs = [r[3] for r in res]
+    assert all(fi == fs[0] for fi in fs)
+    assert abs(fs[0] - f) <= 1e-12 * abs(f)
+    gs = np.concatenate([r[4] for r in res])
+    assert gs.size == g.size
+    assert np.allclose(gs, g, rtol=1e-12, atol=1e-12 * np.abs(g).max())

@@ -275,3 +275,47 @@ def test_window_parts_match_oracle(tvreg, c1, cap, monkeypatch):
     oT = oracle.transpose(A.row_ptr, A.col, A.val, A.n_cols)
     assert np.array_equal(rT, oT[0]) and np.array_equal(cT, oT[1])
     assert np.array_equal(vT.view(np.uint32), oT[2].view(np.uint32))
+
+
+# ------------------------------------------------------- VIEWS mode (§8(e) P2) on one GPU
+def test_views_mode_one_rank_matches_unsharded(tvreg):
+    grid = (12, 10, 9)
+    A = harness.siddon_tilted(*grid, 8, 9, 13, 10.0)
+    b = harness.simulate_data(A, harness.phantom(*grid, 3))
+    x = dev(harness.random_x(A.n_cols))
+    P0 = make(tvreg, A, b, grid)
+    P1 = tvreg.Problem(A.row_ptr, A.col, A.val, b, grid, 0.01, 1e-4, 0.0, math.inf, shard="views",
+                       z0=0, z1=grid[2])
+    assert P1.info.n_cols_local == A.n_cols
+    g0 = torch.empty_like(x)
+    g1 = torch.empty_like(x)
+    f0, _ = P0.objective_grad(x, g0)
+    f1, _ = P1.objective_grad(x, g1)
+    assert f0 == f1
+    assert torch.equal(g0, g1)
+
+
+def test_views_row_blocks_sum_to_full_AT(tvreg):
+    """Per-rank pieces of P2 on one GPU: each view block's A_p^T y_p spans the whole volume and
+    their sum is A^T y; each block's residual is its rows of A x - b."""
+    from paper_1105_4002_b200.dist import local_views
+    grid = (12, 10, 9)
+    views = 8
+    A = harness.siddon_tilted(*grid, views, 9, 13, 10.0)
+    b = harness.simulate_data(A, harness.phantom(*grid, 3))
+    xh = harness.random_x(A.n_cols)
+    y = harness.normal(A.n_rows, 7).astype(np.float32)
+    w_sum = np.zeros(A.n_cols)
+    for rank in range(3):
+        lv = local_views(A.row_ptr, A.col, A.val, b, grid, views, 3, rank)
+        P = tvreg.Problem(lv.row_ptr, lv.col, lv.val, lv.b, grid, 0.01, 1e-4, 0.0, math.inf,
+                          shard="views", z0=0, z1=grid[2])
+        w = torch.empty(A.n_cols, device="cuda")
+        P.apply_AT(dev(y[lv.row0:lv.row1]), w)
+        w_sum += host(w)
+        r = torch.empty(lv.row1 - lv.row0, device="cuda")
+        P.residual(dev(xh), r)
+        ro = oracle.matvec(lv.row_ptr, lv.col, lv.val, xh.astype(np.float64)) - lv.b
+        assert rel(host(r), ro) <= 1e-6
+    wo = oracle.rmatvec(A.row_ptr, A.col, A.val, y.astype(np.float64), A.n_cols)
+    assert rel(w_sum, wo) <= 1e-6
