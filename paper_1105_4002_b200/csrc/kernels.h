@@ -91,6 +91,7 @@ struct TVArgs {
   int nx, ny, nzl;
   int64_t plane;
   int zg0, nzg;  // global z of local plane 0; global nz
+  int zc;        // planes per work item (set by the launcher)
   double tau, alpha, lo, hi;
   // KIND_GRAD
   const float* w1;
