@@ -24,6 +24,22 @@ __device__ __forceinline__ float4 ld_stream_f4(const float* p) {
   return r;
 }
 
+// 256-bit streaming load (sm_100: LDG.E.256): a lane's 8 consecutive fp32 values in one
+// request, so the 32-byte sectors of the value stream are fetched once (two 128-bit loads at a
+// 32-byte lane stride each touch every sector half-used, and without L1 allocation the sector
+// comes from L2 twice).
+struct f8 {
+  float4 lo, hi;
+};
+__device__ __forceinline__ f8 ld_stream_f8(const float* p) {
+  f8 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r.lo.x), "=f"(r.lo.y), "=f"(r.lo.z), "=f"(r.lo.w), "=f"(r.hi.x),
+                 "=f"(r.hi.y), "=f"(r.hi.z), "=f"(r.hi.w)
+               : "l"(p));
+  return r;
+}
+
 // Fixed-order butterfly reduction inside a group of G lanes (G power of two <= 32):
 // deterministic for a fixed launch configuration.
 template <int G>

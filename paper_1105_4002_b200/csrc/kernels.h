@@ -45,7 +45,48 @@ bool spmv_variant_exists(const SpmvVariant& v);
 cudaError_t ensure_smem_attr(const void* func, size_t smem);
 cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int block, size_t smem,
                         cudaStream_t st);
+// padded-row 16-bit kernel (rows start on 8-entry boundaries, zero-padded)
+cudaError_t launch_spmv16p(const SpmvArgs& a, const SpmvVariant& v, int grid, int block,
+                           size_t smem, cudaStream_t st);
+int spmv16p_occupancy(const SpmvVariant& v, int block, size_t smem);
+cudaError_t launch_pad_rows(int64_t m, const int64_t* rp, const int64_t* rpp, const uint16_t* col16,
+                            const float* val, uint16_t* col16p, float* valp, cudaStream_t st);
 int spmv_occupancy(const SpmvVariant& v, int block, size_t smem);
+
+// Row-agnostic SpMV (spmv_flat.cu): warps stream items as tiles of 32 x 8 entries with a
+// head-mask segmented reduction.
+struct FlatArgs {
+  const int64_t* rp;
+  const int32_t* col;      // int32 global columns (!idx16)
+  const uint16_t* col16;   // 16-bit window offsets (idx16)
+  const float* val;
+  const uint8_t* head;     // per 8-entry chunk: bit q set iff entry 8c+q starts a nonempty row
+  const float* src;
+  const float* b;          // non-null: out = A src - b, sum r^2
+  float* out;
+  float* out_lo;
+  const int64_t* item_row;  // nitems+1 row boundaries (items never straddle a slice)
+  const int64_t* item_nz;   // per item: nonempty rows before item_row[k] (index into nzr)
+  const int32_t* item_slice;
+  const int64_t* slice_item_end;  // per slice: one past its last item
+  int64_t nitems;
+  const int32_t* nzr;       // nonempty rows in order
+  const int32_t* empty_rows;
+  int64_t n_empty;
+  const int64_t* win_lo;    // per slice gather window (staged: shared memory; else base offset)
+  const int32_t* win_len;
+  double* partials;
+  unsigned* counter;
+  double* scal;
+};
+struct FlatVariant {
+  bool staged = false;
+  bool idx16 = false;
+  int unroll = 2;  // tiles of loads in flight per warp
+};
+cudaError_t launch_spmv_flat(const FlatArgs& a, const FlatVariant& v, int grid, int block,
+                             size_t smem, cudaStream_t st);
+int spmv_flat_occupancy(const FlatVariant& v, int block, size_t smem);
 
 // TMA bulk-copy pipelined SpMV (spmv_tma.cu): tiles of whole rows inside one slice.
 constexpr int kTmaConsumerWarps = 8;

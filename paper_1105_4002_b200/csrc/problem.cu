@@ -176,8 +176,41 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     t.scal = scal;
     return launch_spmv_tma(t, pl.v.lpr, pl.tma.grid, pl.tma.smem, p->stream);
   }
+  if (pl.flat.on) {
+    const FlatPlan& f = pl.flat;
+    FlatArgs a;
+    a.rp = transposed ? p->rpT : p->rp;
+    a.col = transposed ? p->colT : p->col;
+    a.col16 = transposed ? p->colT16 : p->col16;
+    a.val = transposed ? p->valT : p->val;
+    a.head = f.head;
+    a.src = src;
+    a.b = b;
+    a.out = out;
+    a.out_lo = out_lo;
+    a.item_row = f.item_row;
+    a.item_nz = f.item_nz;
+    a.item_slice = f.item_slice;
+    a.slice_item_end = f.slice_item_end;
+    a.nitems = f.nitems;
+    a.nzr = f.nzr;
+    a.empty_rows = f.empty_rows;
+    a.n_empty = f.n_empty;
+    a.win_lo = f.win_lo;
+    a.win_len = f.win_len;
+    a.partials = p->partials;
+    a.counter = p->counter;
+    a.scal = scal;
+    return launch_spmv_flat(a, f.v, f.grid, f.block, f.smem, p->stream);
+  }
   SpmvArgs a = spmv_args(p, pl, transposed, src, b, out, scal);
   a.out_lo = out_lo;
+  if (pl.pad) {
+    a.rp = pl.rpp;
+    a.col16 = pl.col16p;
+    a.val = pl.valp;
+    return launch_spmv16p(a, pl.v, pl.pad_grid, pl.block, pl.smem, p->stream);
+  }
   return launch_spmv(a, pl.v, pl.grid, pl.block, pl.smem, p->stream);
 }
 
@@ -345,7 +378,7 @@ static int env_int(const char* name, int dflt) {
 
 static int upload(tvr_problem* p, void** dst, const void* src, size_t bytes) {
   TVR_TRY(dev_alloc(p, dst, bytes));
-  TVR_CUDA(cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, p->stream));
+  if (src && bytes) TVR_CUDA(cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, p->stream));
   return TVR_OK;
 }
 
@@ -414,6 +447,76 @@ static int make_tma_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t
   t.nbounds = (int64_t)bounds.size();
   TVR_TRY(upload(p, (void**)&t.bounds, bounds.data(), sizeof(int64_t) * bounds.size()));
   t.on = true;
+  return TVR_OK;
+}
+
+// Row-agnostic plan (spmv_flat.cu): items of about TVR_FLAT_ITEM entries (default 2048) that
+// never straddle a slice, the per-chunk head mask, the nonempty-row map and the empty rows.
+// Uses the per-row plan's window staging (pl.staged, pl.smem) and column format (pl.v.idx16).
+static int make_flat_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& rp,
+                          int64_t n_rows, bool separable, const std::vector<int64_t>& slice_rows,
+                          const std::vector<int64_t>& win_lo, const std::vector<int32_t>& win_len,
+                          size_t nnz_pad) {
+  FlatPlan& f = pl.flat;
+  f.on = false;
+  if (!env_int("TVR_SPMV_FLAT", 0) || pl.tma.on || pl.v.parts) return TVR_OK;
+  if (n_rows >= ((int64_t)1 << 31)) return TVR_OK;  // nzr holds int32 row ids
+  // int32 columns are slab-local voxel ids: gathered from global memory (no window)
+  f.v.staged = pl.staged && pl.v.idx16;
+  f.v.idx16 = pl.v.idx16;
+  f.v.unroll = env_int("TVR_FLAT_UNROLL", 2);
+  f.block = env_int("TVR_FLAT_BLOCK", 512);
+  f.smem = f.v.staged ? pl.smem : 0;
+  f.grid = p->num_sms * spmv_flat_occupancy(f.v, f.block, f.smem);
+  const int64_t nnz = rp[n_rows];
+  // head mask, nonempty-row map, empty rows
+  std::vector<uint8_t> head(nnz_pad / 8, 0);
+  std::vector<int32_t> nzr, empty;
+  std::vector<int64_t> nz_before(n_rows + 1, 0);
+  for (int64_t r = 0; r < n_rows; ++r) {
+    nz_before[r + 1] = nz_before[r];
+    if (rp[r + 1] > rp[r]) {
+      head[rp[r] >> 3] |= (uint8_t)(1u << (rp[r] & 7));
+      nzr.push_back((int32_t)r);
+      nz_before[r + 1]++;
+    } else {
+      empty.push_back((int32_t)r);
+    }
+  }
+  // items
+  const int64_t target = std::max<int64_t>(64, env_int("TVR_FLAT_ITEM", 2048));
+  std::vector<int64_t> rows;
+  std::vector<int32_t> slices;
+  if (separable) {
+    for (size_t z = 0; z + 1 < slice_rows.size(); ++z)
+      split_rows(rp.data(), slice_rows[z], slice_rows[z + 1], target, (int32_t)z, rows, slices);
+  } else {
+    split_rows(rp.data(), 0, n_rows, target, 0, rows, slices);
+  }
+  rows.push_back(n_rows);
+  f.nitems = (int64_t)slices.size();
+  std::vector<int64_t> inz(f.nitems);
+  for (int64_t k = 0; k < f.nitems; ++k) inz[k] = nz_before[rows[k]];
+  const size_t nslices = separable ? win_lo.size() : 1;
+  std::vector<int64_t> zend(nslices, 0);
+  for (size_t i = 0; i < slices.size(); ++i) zend[slices[i]] = (int64_t)i + 1;
+  for (size_t z = 1; z < nslices; ++z) zend[z] = std::max(zend[z], zend[z - 1]);
+  std::vector<int64_t> wlo = separable && f.v.idx16 ? win_lo : std::vector<int64_t>(nslices, 0);
+  std::vector<int32_t> wlen = separable && f.v.idx16 ? win_len : std::vector<int32_t>(nslices, 0);
+  if (f.grid > f.nitems) f.grid = (int)std::max<int64_t>(1, f.nitems);
+  TVR_TRY(upload(p, (void**)&f.head, head.data(), head.size()));
+  TVR_TRY(upload(p, (void**)&f.nzr, nzr.data(), sizeof(int32_t) * nzr.size()));
+  TVR_TRY(upload(p, (void**)&f.empty_rows, empty.data(), sizeof(int32_t) * empty.size()));
+  f.n_empty = (int64_t)empty.size();
+  TVR_TRY(upload(p, (void**)&f.item_row, rows.data(), sizeof(int64_t) * rows.size()));
+  TVR_TRY(upload(p, (void**)&f.item_nz, inz.data(), sizeof(int64_t) * inz.size()));
+  TVR_TRY(upload(p, (void**)&f.item_slice, slices.data(), sizeof(int32_t) * slices.size()));
+  TVR_TRY(upload(p, (void**)&f.slice_item_end, zend.data(), sizeof(int64_t) * zend.size()));
+  TVR_TRY(upload(p, (void**)&f.win_lo, wlo.data(), sizeof(int64_t) * wlo.size()));
+  TVR_TRY(upload(p, (void**)&f.win_len, wlen.data(), sizeof(int32_t) * wlen.size()));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));  // host vectors die here
+  f.on = true;
+  (void)nnz;
   return TVR_OK;
 }
 
@@ -512,6 +615,8 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
     TVR_TRY(upload(p, (void**)&pl.slice_item_end, zend.data(), sizeof(int64_t) * std::max<size_t>(1, zend.size())));
   }
   if (staged) TVR_TRY(make_tma_plan(p, pl, rp, slice_rows, pl.smem / sizeof(float)));
+  TVR_TRY(make_flat_plan(p, pl, rp, n_rows, separable, slice_rows, win_lo, win_len,
+                         (size_t)((rp[n_rows] + 7) / 8 * 8 + 8)));
   return TVR_OK;
 }
 
@@ -764,6 +869,30 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
                                p->stream));
   }
   TVR_CUDA(cudaStreamSynchronize(p->stream));
+  // ---- padded-row copies for the 16-bit kernel (TVR_SPMV_PAD=0 disables) ----
+  for (int which = 0; which < 2; ++which) {
+    SpmvPlan& pl = which ? p->planT : p->planA;
+    if (!pl.v.idx16 || pl.v.parts || pl.tma.on || pl.flat.on || !env_int("TVR_SPMV_PAD", 1)) continue;
+    const int64_t rows = which ? n : m;
+    std::vector<int64_t> rph(rows + 1), rpp(rows + 1);
+    TVR_CUDA(cudaMemcpyAsync(rph.data(), which ? p->rpT : p->rp, sizeof(int64_t) * (rows + 1),
+                             cudaMemcpyDeviceToHost, p->stream));
+    TVR_CUDA(cudaStreamSynchronize(p->stream));
+    rpp[0] = 0;
+    for (int64_t r = 0; r < rows; ++r) rpp[r + 1] = rpp[r] + (rph[r + 1] - rph[r] + 7) / 8 * 8;
+    const size_t cap = (size_t)rpp[rows] + 8 * 16 * 4 + 8;  // slack: chunks read past the last row
+    TVR_TRY(upload(p, (void**)&pl.rpp, rpp.data(), sizeof(int64_t) * (rows + 1)));
+    TVR_TRY(dev_alloc(p, (void**)&pl.col16p, sizeof(uint16_t) * cap));
+    TVR_TRY(dev_alloc(p, (void**)&pl.valp, sizeof(float) * cap));
+    TVR_CUDA(cudaMemsetAsync(pl.col16p, 0, sizeof(uint16_t) * cap, p->stream));
+    TVR_CUDA(cudaMemsetAsync(pl.valp, 0, sizeof(float) * cap, p->stream));
+    TVR_CUDA(launch_pad_rows(rows, which ? p->rpT : p->rp, pl.rpp, which ? p->colT16 : p->col16,
+                             which ? p->valT : p->val, pl.col16p, pl.valp, p->stream));
+    TVR_CUDA(cudaStreamSynchronize(p->stream));
+    pl.pad_grid = std::min<int64_t>((int64_t)p->num_sms * spmv16p_occupancy(pl.v, pl.block, pl.smem),
+                                    std::max<int64_t>(1, pl.nitems));
+    pl.pad = true;
+  }
   // the int32 columns are no longer read by any pass: release them (c3: 7.7 GB each)
   if (p->planA.v.idx16) { dev_free(p, p->col); p->col = nullptr; }
   if (p->planT.v.idx16) { dev_free(p, p->colT); p->colT = nullptr; }

@@ -54,8 +54,34 @@ struct TmaPlan {
   int64_t nbounds = 0;
 };
 
+// Row-agnostic SpMV plan (spmv_flat.cu): warp-sized items, head mask, nonempty-row map.
+struct FlatPlan {
+  bool on = false;
+  FlatVariant v;
+  int grid = 0, block = 512;
+  size_t smem = 0;
+  int64_t nitems = 0;
+  int64_t* item_row = nullptr;
+  int64_t* item_nz = nullptr;
+  int32_t* item_slice = nullptr;
+  int64_t* slice_item_end = nullptr;
+  int64_t* win_lo = nullptr;  // one zero entry when the matrix has no slice windows
+  int32_t* win_len = nullptr;
+  uint8_t* head = nullptr;
+  int32_t* nzr = nullptr;
+  int32_t* empty_rows = nullptr;
+  int64_t n_empty = 0;
+};
+
 struct SpmvPlan {
   TmaPlan tma;
+  FlatPlan flat;
+  // padded-row copy for spmv16p_kernel (rows on 8-entry boundaries, zero pads)
+  bool pad = false;
+  int pad_grid = 0;
+  int64_t* rpp = nullptr;
+  uint16_t* col16p = nullptr;
+  float* valp = nullptr;
   int parts = 1, part_len = 0;       // slice-window parts (16-bit kernel)
   uint16_t* part_off = nullptr;      // (parts-1) x nrows
   double* part_acc = nullptr;        // nrows

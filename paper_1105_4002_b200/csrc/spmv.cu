@@ -285,6 +285,178 @@ __global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
   }
 }
 
+// Padded-row 16-bit kernel: the device copy starts every row on an 8-entry boundary and
+// zero-pads it to a multiple of 8 entries (pad: value 0, offset 0).  A lane's 8-entry chunk is
+// then entirely inside its row or entirely past it, so the per-entry range tests of
+// spmv16_kernel (compare, select value, select gather index: ~5 instructions per entry) become
+// one select per chunk.  Chunks past the row load whatever follows (valid memory: the arrays
+// carry 8 LPR UNR entries of slack) and are discarded.
+template <bool STAGED>
+__device__ __forceinline__ double chunk8_sum(const int4 c, const float4 v0, const float4 v1,
+                                             const float* __restrict__ sm,
+                                             const float* __restrict__ gbase) {
+  const uint32_t cw[4] = {(uint32_t)c.x, (uint32_t)c.y, (uint32_t)c.z, (uint32_t)c.w};
+  const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+  double pr[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int cidx = (int)((cw[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+    float xv;
+    if constexpr (STAGED) xv = sm[swz(cidx)];
+    else xv = __ldg(gbase + cidx);
+    pr[q] = (double)vv[q] * (double)xv;  // exact
+  }
+  return ((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
+}
+
+template <int LPR, int UNR, bool STAGED>
+__global__ void __launch_bounds__(512, 2) spmv16p_kernel(SpmvArgs a) {
+  extern __shared__ float stage[];
+  const int lane = threadIdx.x & (LPR - 1);
+  const int grp = threadIdx.x / LPR;
+  const int ngrp = blockDim.x / LPR;
+  const int64_t it0 = (a.nitems * (int64_t)blockIdx.x) / gridDim.x;
+  const int64_t it1 = (a.nitems * (int64_t)(blockIdx.x + 1)) / gridDim.x;
+  int cur_slice = -1;
+  const float* gbase = a.src;
+  double sq = 0.0;
+  for (int64_t it = it0; it < it1; ++it) {
+    const int z = a.item_slice[it];
+    if (z != cur_slice) {
+      gbase = a.src + a.win_lo[z];
+      if constexpr (STAGED) {
+        __syncthreads();
+        const int len = a.win_len[z];
+        for (int i = threadIdx.x; i < len; i += blockDim.x) stage[swz(i)] = __ldg(gbase + i);
+        __syncthreads();
+      }
+      cur_slice = z;
+    }
+    const int64_t r0 = a.item_row[it], r1 = a.item_row[it + 1];
+    int64_t row = r0 + grp;
+    int64_t s_n = 0, e_n = 0;
+    float b_n = 0.0f;
+    if (row < r1) {
+      s_n = a.rp[row];
+      e_n = a.rp[row + 1];
+      if (STAGED && a.b) b_n = __ldg(a.b + row);
+    }
+    for (int64_t base = r0; base < r1; base += ngrp) {
+      const bool valid = row < r1;
+      const int64_t s = s_n;
+      const int span = (int)(e_n - s_n);  // padded: a multiple of 8
+      const float bv = b_n;
+      const int64_t nrow = row + ngrp;
+      if (nrow < r1) {
+        s_n = a.rp[nrow];
+        e_n = a.rp[nrow + 1];
+        if (STAGED && a.b) b_n = __ldg(a.b + nrow);
+      }
+      const int nch = valid ? (span + 8 * LPR - 1) / (8 * LPR) : 0;
+      const int lim = span - 8 * lane;  // chunk k of this lane is in the row iff k 8 LPR < lim
+      const uint16_t* cp = a.col16 + s + 8 * lane;
+      const float* vp = a.val + s + 8 * lane;
+      double acc[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) acc[u] = 0.0;
+      int ch = 0;
+      for (; ch + UNR <= nch; ch += UNR) {
+        int4 c[UNR];
+        float4 va[UNR], vb[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          c[u] = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + (ch + u) * 8 * LPR));
+          va[u] = ld_stream_f4(vp + (ch + u) * 8 * LPR);
+          vb[u] = ld_stream_f4(vp + (ch + u) * 8 * LPR + 4);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const double t = chunk8_sum<STAGED>(c[u], va[u], vb[u], stage, gbase);
+          acc[u] += ((ch + u) * 8 * LPR < lim) ? t : 0.0;
+        }
+      }
+      for (; ch < nch; ++ch) {
+        const int4 c0 = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + ch * 8 * LPR));
+        const float4 va0 = ld_stream_f4(vp + ch * 8 * LPR);
+        const float4 vb0 = ld_stream_f4(vp + ch * 8 * LPR + 4);
+        const double t = chunk8_sum<STAGED>(c0, va0, vb0, stage, gbase);
+        acc[0] += (ch * 8 * LPR < lim) ? t : 0.0;
+      }
+#pragma unroll
+      for (int u = 1; u < UNR; ++u) acc[0] += acc[u];
+      const double accr = group_sum<LPR>(acc[0]);
+      if (valid && lane == 0) {
+        if (a.b) {
+          const double r = accr - (double)(STAGED ? bv : __ldg(a.b + row));
+          const float rh = (float)r;
+          a.out[row] = rh;
+          if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
+          sq += r * r;
+        } else {
+          a.out[row] = (float)accr;
+        }
+      }
+      row = nrow;
+    }
+  }
+  if (a.scal) {
+    double v[1] = {sq};
+    reduce_to_scalars<1>(v, a.partials, a.counter, a.scal);
+  }
+}
+
+// Padded copy of a 16-bit CSR: row r's entries move from rp[r] to rpp[r] (an 8-entry boundary),
+// pads to rpp[r+1] are zero.  One warp per row.
+__global__ void pad_rows_kernel(int64_t m, const int64_t* rp, const int64_t* rpp,
+                                const uint16_t* col16, const float* val, uint16_t* col16p,
+                                float* valp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < m; r += nw) {
+    const int64_t s = rp[r], len = rp[r + 1] - s, d = rpp[r], plen = rpp[r + 1] - d;
+    for (int64_t k = lane; k < plen; k += 32) {
+      col16p[d + k] = k < len ? col16[s + k] : (uint16_t)0;
+      valp[d + k] = k < len ? val[s + k] : 0.0f;
+    }
+  }
+}
+
+cudaError_t launch_pad_rows(int64_t m, const int64_t* rp, const int64_t* rpp, const uint16_t* col16,
+                            const float* val, uint16_t* col16p, float* valp, cudaStream_t st) {
+  pad_rows_kernel<<<1184, 256, 0, st>>>(m, rp, rpp, col16, val, col16p, valp);
+  return cudaGetLastError();
+}
+
+template <class F>
+static cudaError_t dispatch16p(const SpmvVariant& v, F&& f) {
+#define TVR_VP(L, U)                                                                   \
+  if (v.lpr == L && v.unroll == U)                                                     \
+    return v.staged ? f(spmv16p_kernel<L, U, true>) : f(spmv16p_kernel<L, U, false>);
+  TVR_VP(4, 2) TVR_VP(4, 3) TVR_VP(4, 4) TVR_VP(8, 2) TVR_VP(8, 3) TVR_VP(16, 2)
+#undef TVR_VP
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_spmv16p(const SpmvArgs& a, const SpmvVariant& v, int grid, int block,
+                           size_t smem, cudaStream_t st) {
+  return dispatch16p(v, [&](auto k) -> cudaError_t {
+    cudaError_t e = ensure_smem_attr((const void*)k, smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, block, smem, st>>>(a);
+    return cudaGetLastError();
+  });
+}
+
+int spmv16p_occupancy(const SpmvVariant& v, int block, size_t smem) {
+  int occ = 0;
+  dispatch16p(v, [&](auto k) -> cudaError_t {
+    ensure_smem_attr((const void*)k, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, block, smem);
+  });
+  return occ > 0 ? occ : 1;
+}
+
 // Window parts (opt-in, TVR_PART_CAP): a slice window larger than the shared-memory budget is
 // cut into `parts` pieces of part_len entries.  Columns ascend within a row, so each row's
 // entries are contiguous per part; part_off[(p-1) nrows + row] is the row-relative start of

@@ -9,7 +9,7 @@ import pytest
 
 import harness
 import oracle
-from tests._helpers import random_csr
+from tests._helpers import SmallCSR, random_csr
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -225,6 +225,7 @@ def test_tma_pipeline_matches_register_kernel_bitwise(tvreg, cfg, c1, monkeypatc
         grid = (37, 29, 11)
     x = dev(harness.random_x(A.n_cols))
     outs = {}
+    monkeypatch.setenv("TVR_SPMV_FLAT", "0")  # the per-row kernels (the flat one: test_flat_*)
     for mode in ("tma", "reg", "global", "reg16"):
         monkeypatch.setenv("TVR_SPMV_TMA", "1" if mode == "tma" else "0")
         monkeypatch.setenv("TVR_SPMV_STAGE", "0" if mode == "global" else "1")
@@ -250,6 +251,74 @@ def test_tma_pipeline_matches_register_kernel_bitwise(tvreg, cfg, c1, monkeypatc
     assert rel(outs["reg16"][0], outs["reg"][0]) <= 1e-7
     assert abs(outs["reg16"][1] - outs["reg"][1]) <= 1e-13 * outs["reg"][1]
     assert rel(outs["reg16"][2], outs["reg"][2]) <= 1e-7
+
+
+def _row_length_zoo(n_cols, seed):
+    """Rows of 0, 1, 2, 3, 7, 8, 9, 31, 255, 256, 257 and 600 entries in random order, dyadic
+    values: rows inside one chunk, rows ending on chunk / tile edges, rows spanning several
+    256-entry tiles, empty rows."""
+    rng = np.random.default_rng(seed)
+    lens = rng.permutation(np.repeat([0, 1, 2, 3, 7, 8, 9, 31, 255, 256, 257, 600], 6))
+    rp, cols, vals = [0], [], []
+    for L in lens:
+        c = np.sort(rng.choice(n_cols, size=L, replace=False))
+        cols.extend(c.tolist())
+        vals.extend((rng.integers(1, 2049, size=L) / 1024.0).tolist())
+        rp.append(rp[-1] + L)
+    return SmallCSR(rp, cols, vals, n_cols)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "ragged", "zoo"])
+def test_flat_spmv_variants(tvreg, cfg, c1, monkeypatch):
+    """The row-agnostic SpMV (spmv_flat.cu): staged / global gather, 1 or 2 tiles in flight,
+    16-bit or int32 columns and any item size share one summation order, so they agree bitwise;
+    they match the oracle (bitwise on dyadic data) and the per-row kernel to fp32 rounding."""
+    rng = np.random.default_rng(11)
+    if cfg == "c1":
+        A, grid = c1.A, c1.grid
+        x = harness.random_x(A.n_cols)
+        b = c1.b
+    elif cfg == "ragged":
+        A, grid = harness.siddon_separable(37, 29, 11, 13, 47), (37, 29, 11)
+        x = harness.random_x(A.n_cols)
+        b = rng.random(A.n_rows).astype(np.float32)
+    else:
+        grid = (16, 16, 4)
+        A = _row_length_zoo(16 * 16 * 4, 3)
+        x = rng.integers(0, 9, A.n_cols).astype(np.float32)
+        b = rng.integers(0, 9, A.n_rows).astype(np.float32)
+    modes = {"flat": {}, "global": {"TVR_SPMV_STAGE": "0"}, "unr1": {"TVR_FLAT_UNROLL": "1"},
+             "int32": {"TVR_IDX16": "0"}, "items64": {"TVR_FLAT_ITEM": "64"},
+             "perrow": {"TVR_SPMV_FLAT": "0"}}
+    outs = {}
+    for mode, env in modes.items():
+        for k in ("TVR_SPMV_STAGE", "TVR_FLAT_UNROLL", "TVR_IDX16", "TVR_FLAT_ITEM", "TVR_SPMV_FLAT"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        P = make(tvreg, A, b, grid)
+        r = torch.empty(A.n_rows, device="cuda")
+        fid = P.residual(dev(x), r)
+        w = torch.empty(A.n_cols, device="cuda")
+        P.apply_AT(dev(b), w)
+        outs[mode] = (host(r).copy(), fid, host(w).copy())
+        P.close()
+    r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x.astype(np.float64)) - b
+    w_ora = oracle.rmatvec(A.row_ptr, A.col, A.val, b.astype(np.float64), A.n_cols)
+    for mode in ("global", "unr1", "int32", "items64"):
+        assert np.array_equal(outs[mode][0], outs["flat"][0]), mode
+        assert np.array_equal(outs[mode][2], outs["flat"][2]), mode
+        assert abs(outs[mode][1] - outs["flat"][1]) <= 1e-13 * outs["flat"][1]
+    if cfg == "zoo":  # dyadic: exact
+        assert np.array_equal(outs["flat"][0].astype(np.float64), r_ora)
+        assert np.array_equal(outs["flat"][2].astype(np.float64), w_ora)
+        assert outs["flat"][1] == 0.5 * float(r_ora @ r_ora)
+    assert rel(outs["flat"][0], r_ora) <= 1e-6 and rel(outs["flat"][2], w_ora) <= 1e-6
+    assert rel(outs["flat"][0], outs["perrow"][0]) <= 1e-7
+    assert rel(outs["flat"][2], outs["perrow"][2]) <= 1e-7
+    empty = np.diff(A.row_ptr) == 0
+    if empty.any():
+        assert np.array_equal(outs["flat"][0][empty], -b[empty])
 
 
 @pytest.mark.parametrize("cap", [1024, 300, 128])
