@@ -145,8 +145,21 @@ typedef struct {
   int32_t bt_max;
 } tvr_upn_opts;
 
+/* GP options: the paper's baseline comparator, Eq. (6), x_{k+1} = P_Q(x_k - g_k/L_k)
+ * with L_k found by BT (Alg. 2) starting from L_{k-1} (the oracle's
+ * gp() follows the same steps).  tvr_gp_default fills L0 = 1, rho_L = 1.3, bt_max = 200,
+ * eps = 1e-6, TVR_STOP_REL, max_iters = 10000. */
+typedef struct {
+  int64_t max_iters;
+  double eps;
+  int32_t stop_mode;
+  double L0, rho_L;
+  int32_t bt_max;
+} tvr_gp_opts;
+
 void tvr_gpbb_default(tvr_gpbb_opts* o);
 void tvr_upn_default(tvr_upn_opts* o);
+void tvr_gp_default(tvr_gp_opts* o);
 
 /* One record per accepted iteration (GPBB: the iterate tested at the top of iteration k;
  * UPN: x_{k}).  step_or_inv_L = theta_k (GPBB) or 1/L_k (UPN). */
@@ -172,6 +185,10 @@ int tvr_solve_gpbb(tvr_problem* p, float* x_dev_inout, const tvr_gpbb_opts* opts
                    tvr_record* hist, int64_t hist_cap);
 int tvr_solve_upn(tvr_problem* p, float* x_dev_inout, const tvr_upn_opts* opts, tvr_result* res,
                   tvr_record* hist, int64_t hist_cap);
+/* GP (f1): same conventions as tvr_solve_upn; records carry 1/L_k, the stop test runs at x_{k+1}
+ * with nu = L_k (as UPN, C11). */
+int tvr_solve_gp(tvr_problem* p, float* x_dev_inout, const tvr_gp_opts* opts, tvr_result* res,
+                 tvr_record* hist, int64_t hist_cap);
 
 /* ---- inspection hooks (tests) ---- */
 /* y = A x - b (fused residual, the a1 pass); returns 1/2 ||Ax - b||^2 in *fid (nullable). */

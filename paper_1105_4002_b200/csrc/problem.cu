@@ -652,6 +652,16 @@ void tvr_gpbb_default(tvr_gpbb_opts* o) {
   o->beta_min = 1e-10;
 }
 
+void tvr_gp_default(tvr_gp_opts* o) {
+  if (!o) return;
+  o->max_iters = 10000;
+  o->eps = 1e-6;
+  o->stop_mode = TVR_STOP_REL;
+  o->L0 = 1.0;
+  o->rho_L = 1.3;
+  o->bt_max = 200;
+}
+
 void tvr_upn_default(tvr_upn_opts* o) {
   if (!o) return;
   o->max_iters = 10000;

@@ -330,6 +330,81 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   return conv ? TVR_OK : TVR_NOT_CONVERGED;
 }
 
+// --------------------------------------------------------------------- GP
+// Eq. (6) with theta_k = 1/L_k from BT (Alg. 2) warm-started at L_{k-1}: the paper's
+// baseline comparator, step for step as the oracle's gp().
+static int gp_impl(tvr_problem* p, float* x_io, const tvr_gp_opts& o, tvr_result* res,
+                   Recorder& rec) {
+  const double t0 = now_s();
+  const double bytes0 = p->bytes_total;
+  const double Nglob = (double)p->plane * p->nz;
+  float* xk = volvec(p, 0);
+  float* xn = volvec(p, 1);
+  float* g = volvec(p, 3);
+  float* w = volvec(p, 5);
+  float* rk = datvec(p, 0);
+  float* rn = datvec(p, 1);
+
+  TVR_TRY(copy_in(p, xk, x_io));
+  TVR_TRY(pass_project(p, xk));
+  TVR_TRY(halo_exchange(p, xk));
+  TVR_TRY(pass_residual(p, xk, rk, S_RSQ));
+  TVR_TRY(pass_AT(p, rk, w));
+  TVR_TRY(pass_tv_grad(p, xk, nullptr, 0.0, w, nullptr, 0.0, g, nullptr, nullptr, nullptr, 1.0, S_TV));
+  TVR_TRY(halo_exchange(p, g));
+  TVR_TRY(fetch_scalars(p, S_COUNT));
+  double f = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
+  const double gref = std::sqrt(p->hscal[S_TV + 3]);
+  if (!std::isfinite(f) || !std::isfinite(gref)) { set_error("GP: non-finite f or g at x0"); return TVR_E_NONFINITE; }
+  int64_t n_f = 1, n_g = 1, n_ls = 0, k = 0;
+  tvr_upn_opts bo;  // BT parameters
+  tvr_upn_default(&bo);
+  bo.rho_L = o.rho_L;
+  bo.bt_max = o.bt_max;
+  double L = o.L0, gn = gref;
+  bool conv = false;
+  int status = TVR_OK;
+  for (;;) {
+    BTOut bt;
+    const int s = backtrack(p, xk, g, f, L, bo, nullptr, xn, rn, nullptr, bt);
+    if (s < 0) { status = s; break; }
+    n_f += bt.trials;
+    n_ls += bt.trials;
+    L = bt.L;
+    ++k;
+    std::swap(xk, xn);
+    std::swap(rk, rn);
+    f = bt.f;
+    TVR_TRY(pass_AT(p, rk, w));
+    TVR_TRY(pass_tv_grad(p, xk, nullptr, 0.0, w, nullptr, 0.0, g, nullptr, nullptr, nullptr,
+                         1.0 / L, S_TV));
+    TVR_TRY(halo_exchange(p, g));
+    TVR_TRY(fetch_scalars(p, S_COUNT));
+    ++n_g;
+    gn = L * std::sqrt(p->hscal[S_TV + 3]);
+    tvr_record r{};
+    r.iter = k; r.f = f; r.gmap_rel = gref > 0 ? gn / gref : 0.0; r.gmap_abs_per_n = gn / Nglob;
+    r.step_or_inv_L = 1.0 / L; r.L = L; r.ls_trials = bt.trials;
+    rec.add(r);
+    conv = stop_test(gn, gref, Nglob, o.eps, o.stop_mode);
+    if (conv || k >= o.max_iters) break;
+  }
+  TVR_CUDA(cudaMemcpyAsync(x_io, xk, sizeof(float) * p->n, cudaMemcpyDeviceToDevice, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  if (res) {
+    res->converged = conv ? 1 : 0;
+    res->iters = k;
+    res->n_f = n_f; res->n_grad = n_g; res->n_ls = n_ls; res->n_records = rec.n;
+    res->f = f; res->gmap_ref = gref;
+    res->gmap_rel = gref > 0 ? gn / gref : 0.0;
+    res->gmap_abs_per_n = gn / Nglob;
+    res->seconds = now_s() - t0;
+    res->bytes = p->bytes_total - bytes0;
+  }
+  if (status != TVR_OK) return status;
+  return conv ? TVR_OK : TVR_NOT_CONVERGED;
+}
+
 }  // namespace tvr
 
 using namespace tvr;
@@ -374,6 +449,26 @@ int tvr_solve_upn(tvr_problem* p, float* x, const tvr_upn_opts* opts, tvr_result
     return upn_impl(p, x, o, res, rec);
   } catch (const std::exception& e) {
     set_error(std::string("tvr_solve_upn: ") + e.what());
+    return TVR_E_OOM;
+  }
+}
+
+int tvr_solve_gp(tvr_problem* p, float* x, const tvr_gp_opts* opts, tvr_result* res,
+                 tvr_record* hist, int64_t hist_cap) {
+  if (!p || !x) { set_error("tvr_solve_gp: NULL"); return TVR_E_ARG; }
+  tvr_gp_opts o;
+  tvr_gp_default(&o);
+  if (opts) o = *opts;
+  if (o.max_iters < 1 || !(o.eps >= 0) || !(o.L0 > 0) || !(o.rho_L > 1) || o.bt_max < 1) {
+    set_error("tvr_solve_gp: invalid options");
+    return TVR_E_ARG;
+  }
+  TVR_CUDA(cudaSetDevice(p->device));
+  Recorder rec{hist, hist ? hist_cap : 0};
+  try {
+    return gp_impl(p, x, o, res, rec);
+  } catch (const std::exception& e) {
+    set_error(std::string("tvr_solve_gp: ") + e.what());
     return TVR_E_OOM;
   }
 }

@@ -74,6 +74,11 @@ class tvr_upn_opts(ctypes.Structure):
                 ("mu0", c_f64), ("rho_L", c_f64), ("bt_max", c_i32)]
 
 
+class tvr_gp_opts(ctypes.Structure):
+    _fields_ = [("max_iters", c_i64), ("eps", c_f64), ("stop_mode", c_i32), ("L0", c_f64),
+                ("rho_L", c_f64), ("bt_max", c_i32)]
+
+
 class tvr_record(ctypes.Structure):
     _fields_ = [("iter", c_i64), ("f", c_f64), ("gmap_rel", c_f64), ("gmap_abs_per_n", c_f64),
                 ("step_or_inv_L", c_f64), ("mu", c_f64), ("L", c_f64), ("ls_trials", c_i32),
@@ -107,9 +112,12 @@ SIGNATURES = {
                                                ctypes.POINTER(tvr_fparts)]),
     "tvr_gpbb_default": (None, [ctypes.POINTER(tvr_gpbb_opts)]),
     "tvr_upn_default": (None, [ctypes.POINTER(tvr_upn_opts)]),
+    "tvr_gp_default": (None, [ctypes.POINTER(tvr_gp_opts)]),
     "tvr_solve_gpbb": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(tvr_gpbb_opts),
                                       ctypes.POINTER(tvr_result), ctypes.POINTER(tvr_record), c_i64]),
     "tvr_solve_upn": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(tvr_upn_opts),
+                                     ctypes.POINTER(tvr_result), ctypes.POINTER(tvr_record), c_i64]),
+    "tvr_solve_gp": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(tvr_gp_opts),
                                      ctypes.POINTER(tvr_result), ctypes.POINTER(tvr_record), c_i64]),
     "tvr_residual": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(c_f64)]),
     "tvr_apply_AT": (ctypes.c_int, [c_vp, c_vp, c_vp]),
@@ -357,6 +365,12 @@ class Problem:
                   rho_L=1.3, bt_max=200, hist_cap=0) -> SolveResult:
         o = tvr_upn_opts(max_iters, eps, stop_mode, L0, L0 if mu0 is None else mu0, rho_L, bt_max)
         return self._solve(lib().tvr_solve_upn, o, x, hist_cap)
+
+    def solve_gp(self, x, max_iters=10000, eps=1e-6, stop_mode=TVR_STOP_REL, L0=1.0, rho_L=1.3,
+                 bt_max=200, hist_cap=0) -> SolveResult:
+        """Gradient projection with BT steps (the paper's comparator, Eq. (6))."""
+        o = tvr_gp_opts(max_iters, eps, stop_mode, L0, rho_L, bt_max)
+        return self._solve(lib().tvr_solve_gp, o, x, hist_cap)
 
     # ---- timing
     def profile(self, on: bool = True):

@@ -118,3 +118,23 @@ def test_abs_per_n_stop_mode_and_max_iters(tvreg, c1):
     assert res2.status == tvreg.TVR_NOT_CONVERGED and res2.iters == 5
     # P:228 scaling: ||G||/N, with N the voxel count
     assert abs(res.gmap_abs_per_n * c1.N - res.gmap_rel * res.gmap_ref) <= 1e-9 * res.gmap_ref
+
+
+def test_gp_parity_c1(tvreg, c1):
+    """GP (f1, Eq. (6) with BT steps): 150 iterations on c1 against the oracle's gp(): same L_k
+    sequence, f_k to fp32-storage accuracy, monotone f, and the final iterate within the
+    north_star bars."""
+    Po = _oracle_problem(c1)
+    ref = oracle.gp(Po, np.zeros(c1.N), eps=0.0, max_iters=150)
+    P = _gpu_problem(tvreg, c1)
+    x = torch.zeros(c1.N, device="cuda")
+    res = P.solve_gp(x, max_iters=150, eps=0.0, hist_cap=200)
+    assert not res.converged and res.iters == 150
+    h, oh = res.history, ref.history
+    assert len(h) == 150
+    assert [r["L"] for r in h] == [r["L"] for r in oh]
+    for k in range(150):
+        assert abs(h[k]["f"] - oh[k]["f"]) <= 1e-6 * abs(oh[k]["f"])
+    fs = [r["f"] for r in h]
+    assert all(a >= b for a, b in zip(fs, fs[1:]))  # BT's sufficient decrease
+    _check_parity(Po, x.cpu().numpy(), ref)
