@@ -52,6 +52,8 @@ def lib():
         L.hx_siddon2d.argtypes = [i32, i32, i32, i32, vp, vp, vp]
         L.hx_siddon3d.restype = i64
         L.hx_siddon3d.argtypes = [i32, i32, i32, i32, i32, i32, f64, vp, vp, vp]
+        L.hx_siddon_sphere.restype = i64
+        L.hx_siddon_sphere.argtypes = [i32, i32, i32, i32, i32, i32, vp, vp, vp]
         L.hx_replicate_slices.restype = None
         L.hx_replicate_slices.argtypes = [i64, i64, vp, vp, vp, i64, i32, vp, vp, vp]
         L.hx_simulate_projections.restype = None
@@ -128,6 +130,19 @@ def siddon_tilted(nx: int, ny: int, nz: int, views: int, det_rows: int, det_cols
     return CSR(m, nx * ny * nz, rp, col, val)
 
 
+def siddon_sphere(nx: int, ny: int, nz: int, views: int, det_rows: int, det_cols: int) -> CSR:
+    """The paper's geometry (f2): parallel beam, view directions on a golden spiral over
+    the half sphere, det_rows x det_cols unit pixels; view-major rows."""
+    L = lib()
+    m = views * det_rows * det_cols
+    rp = np.zeros(m + 1, np.int64)
+    nnz = L.hx_siddon_sphere(nx, ny, nz, views, det_rows, det_cols, _p(rp), None, None)
+    col = np.empty(nnz, np.int32)
+    val = np.empty(nnz, np.float32)
+    L.hx_siddon_sphere(nx, ny, nz, views, det_rows, det_cols, _p(rp), _p(col), _p(val))
+    return CSR(m, nx * ny * nz, rp, col, val)
+
+
 # ----------------------------------------------------------- vectors (C17)
 def phantom(nx: int, ny: int, nz: int, n_ell: int, seed: int = SEED_PHANTOM) -> np.ndarray:
     out = np.empty(nx * ny * nz, np.float32)
@@ -191,6 +206,9 @@ PRESETS = {
     "c3": dict(grid=(256, 256, 256), views=90, bins=363, n_ell=10),
     "c4": dict(grid=(256, 256, 256), views=90, bins=363, n_ell=10, hi=1.0),
     "c5": dict(grid=(256, 256, 256), views=120, det=(256, 363), tilt=10.0, n_ell=10),
+    # the paper's own experiment shape: 64^3, 55 / 19 views of 91^2
+    "f2many": dict(grid=(64, 64, 64), views=55, det=(91, 91), sphere=True, n_ell=10),
+    "f2few": dict(grid=(64, 64, 64), views=19, det=(91, 91), sphere=True, n_ell=10),
 }
 
 
@@ -208,6 +226,14 @@ def separable_workload(name: str, grid, views: int, bins: int, n_ell: int,
 def preset(name: str, **over) -> Workload:
     p = dict(PRESETS[name])
     p.update(over)
+    if p.get("sphere"):
+        nx, ny, nz = p["grid"]
+        A = siddon_sphere(nx, ny, nz, p["views"], p["det"][0], p["det"][1])
+        xt = phantom(nx, ny, nz, p["n_ell"])
+        b = simulate_data(A, xt)
+        return Workload(name, p["grid"], A, b, xt, p.get("alpha", 0.01), p.get("tau", 1e-4),
+                        p.get("lo", 0.0), p.get("hi", float("inf")),
+                        dict(kind="sphere", views=p["views"], det=p["det"]))
     if "det" in p:
         nx, ny, nz = p["grid"]
         A = siddon_tilted(nx, ny, nz, p["views"], p["det"][0], p["det"][1], p["tilt"])

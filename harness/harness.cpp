@@ -206,6 +206,55 @@ int64_t hx_siddon3d(int nx, int ny, int nz, int V, int R, int C, double phimax_d
   return row_ptr[m];
 }
 
+// 3D parallel beam with view directions spread over the unit sphere (the paper's own
+// geometry).  Reading: golden-spiral directions on the half sphere (d and -d
+// give the same parallel projection): cos(theta_v) = 1 - (v + 1/2)/V, azimuth v * pi (3 - sqrt 5).
+// Detector R x C of unit pixels centred on the origin, spanned by u = (a x d)/|a x d| (a = e_z,
+// or e_x when d is within ~26 deg of e_z) and w = d x u.  Rows view-major: (v R + r) C + c.
+int64_t hx_siddon_sphere(int nx, int ny, int nz, int V, int R, int C, int64_t* row_ptr,
+                         int32_t* col, float* val) {
+  const int n[3] = {nx, ny, nz};
+  const int64_t m = (int64_t)V * R * C;
+  std::vector<int64_t> cnt(col && val ? 0 : m, 0);
+  const double golden = M_PI * (3.0 - std::sqrt(5.0));
+#pragma omp parallel
+  {
+    std::vector<double> ts;
+    std::vector<Seg> segs;
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t i = 0; i < m; ++i) {
+      const int v = (int)(i / ((int64_t)R * C));
+      const int r = (int)((i / C) % R), cc = (int)(i % C);
+      const double ct = 1.0 - (v + 0.5) / (double)V, st = std::sqrt(std::max(0.0, 1.0 - ct * ct));
+      const double ph = golden * v;
+      const double d[3] = {st * std::cos(ph), st * std::sin(ph), ct};
+      const double a[3] = {std::fabs(ct) < 0.9 ? 0.0 : 1.0, 0.0, std::fabs(ct) < 0.9 ? 1.0 : 0.0};
+      double u[3] = {a[1] * d[2] - a[2] * d[1], a[2] * d[0] - a[0] * d[2], a[0] * d[1] - a[1] * d[0]};
+      const double un = std::sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+      for (double& q : u) q /= un;
+      const double w[3] = {d[1] * u[2] - d[2] * u[1], d[2] * u[0] - d[0] * u[2],
+                           d[0] * u[1] - d[1] * u[0]};
+      const double pa = (double)cc - 0.5 * (C - 1), pb = (double)r - 0.5 * (R - 1);
+      const double p0[3] = {pa * u[0] + pb * w[0], pa * u[1] + pb * w[1], pa * u[2] + pb * w[2]};
+      trace_ray(p0, d, n, 3, ts, segs);
+      if (col && val) {
+        int64_t off = row_ptr[i];
+        for (size_t k = 0; k < segs.size(); ++k) {
+          col[off + k] = (int32_t)segs[k].col;
+          val[off + k] = (float)segs[k].len;
+        }
+      } else {
+        cnt[i] = (int64_t)segs.size();
+      }
+    }
+  }
+  if (!(col && val)) {
+    row_ptr[0] = 0;
+    for (int64_t i = 0; i < m; ++i) row_ptr[i + 1] = row_ptr[i] + cnt[i];
+  }
+  return row_ptr[m];
+}
+
 // Simulated projections y = A x (fp64 accumulation of fp32 entries): the
 // "forward mapping of the discretized image" of the simulation setup
 // (Eq. (11)).  Data generation only.

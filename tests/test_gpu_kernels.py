@@ -43,12 +43,14 @@ def make(T, A, b, grid, alpha=0.01, tau=1e-4, lo=0.0, hi=math.inf):
 
 
 # ------------------------------------------------------------------ a3: A^T
-@pytest.mark.parametrize("which", ["c1", "random_ragged", "tilted"])
+@pytest.mark.parametrize("which", ["c1", "random_ragged", "tilted", "sphere"])
 def test_transpose_bit_exact(tvreg, which, c1):
     if which == "c1":
         A, grid = c1.A, c1.grid
     elif which == "random_ragged":
         A, grid = random_csr(301, 7 * 5 * 3, 0.2, seed=3, empty_rows=11), (7, 5, 3)
+    elif which == "sphere":
+        A, grid = harness.siddon_sphere(14, 12, 10, 9, 19, 21), (14, 12, 10)
     else:
         A, grid = harness.siddon_tilted(12, 10, 9, 7, 9, 13, 10.0), (12, 10, 9)
     P = make(tvreg, A, np.zeros(A.n_rows, np.float32), grid)
@@ -388,3 +390,20 @@ def test_views_row_blocks_sum_to_full_AT(tvreg):
         assert rel(host(r), ro) <= 1e-6
     wo = oracle.rmatvec(A.row_ptr, A.col, A.val, y.astype(np.float64), A.n_cols)
     assert rel(w_sum, wo) <= 1e-6
+
+
+def test_objective_grad_sphere_geometry(tvreg):
+    """f2: the paper's geometry (parallel beam, directions over the sphere) is
+    non-separable: int32 columns, global gathers; gradient parity with the oracle."""
+    grid = (20, 18, 16)
+    A = harness.siddon_sphere(*grid, 9, 29, 29)
+    b = harness.simulate_data(A, harness.phantom(*grid, 4))
+    x = harness.random_x(A.n_cols)
+    P = make(tvreg, A, b, grid)
+    assert P.info.slab_staged_A == 0
+    g = torch.empty(A.n_cols, device="cuda")
+    f, _ = P.objective_grad(dev(x), g)
+    Po = oracle.Problem(A.row_ptr, A.col, A.val, b, grid, 0.01, 1e-4)
+    fo, go = Po.fg(x.astype(np.float64))
+    assert abs(f - fo) <= 1e-9 * abs(fo)
+    assert rel(host(g), go) <= 1e-5

@@ -135,3 +135,52 @@ def test_noise_level_rule(c1):
     e = c1.b.astype(np.float64) - y
     # sigma = 0.01 ||A x_true|| / sqrt(m): ||e|| ~= 0.01 ||A x_true|| (C16)
     assert abs(np.linalg.norm(e) / np.linalg.norm(y) - 0.01) < 0.001
+
+
+def _box_chord(p0, d, n):
+    """Length of p0 + t d (|d| = 1) inside the centred box prod [-n_a/2, n_a/2] (slab method)."""
+    t0, t1 = -np.inf, np.inf
+    for a in range(3):
+        h = 0.5 * n[a]
+        if d[a] == 0.0:
+            if not (-h <= p0[a] <= h):
+                return 0.0
+            continue
+        ta, tb = sorted(((-h - p0[a]) / d[a], (h - p0[a]) / d[a]))
+        t0, t1 = max(t0, ta), min(t1, tb)
+    return max(0.0, t1 - t0)
+
+
+def test_sphere_geometry_row_sums_are_box_chords():
+    """f2: every row of the golden-spiral parallel-beam matrix sums to the length of its
+    ray inside the volume (closed form by slabs), so Siddon drops or duplicates no segment."""
+    nx, ny, nz, V, R, C = 6, 5, 4, 7, 9, 11
+    A = harness.siddon_sphere(nx, ny, nz, V, R, C)
+    assert A.n_rows == V * R * C and A.n_cols == nx * ny * nz
+    rows = np.repeat(np.arange(A.n_rows), np.diff(A.row_ptr))
+    sums = np.bincount(rows, weights=A.val.astype(np.float64), minlength=A.n_rows)
+    golden = np.pi * (3.0 - np.sqrt(5.0))
+    for i in range(A.n_rows):
+        v, r, c = i // (R * C), (i // C) % R, i % C
+        ct = 1.0 - (v + 0.5) / V
+        st = np.sqrt(1.0 - ct * ct)
+        d = np.array([st * np.cos(golden * v), st * np.sin(golden * v), ct])
+        a = np.array([0.0, 0.0, 1.0]) if abs(ct) < 0.9 else np.array([1.0, 0.0, 0.0])
+        u = np.cross(a, d)
+        u /= np.linalg.norm(u)
+        w = np.cross(d, u)
+        p0 = (c - 0.5 * (C - 1)) * u + (r - 0.5 * (R - 1)) * w
+        assert abs(sums[i] - _box_chord(p0, d, (nx, ny, nz))) <= 1e-5, i
+    # columns strictly ascending within rows, lengths positive
+    for i in range(A.n_rows):
+        cs = A.col[A.row_ptr[i]:A.row_ptr[i + 1]]
+        assert np.all(np.diff(cs) > 0)
+    assert np.all(A.val > 0)
+
+
+def test_f2_presets_match_the_paper_sizes():
+    """64^3 voxels, 55 or 19 views of 91^2 pixels (m = 455,455 / 157,339 rows)."""
+    for name, views in (("f2many", 55), ("f2few", 19)):
+        p = harness.PRESETS[name]
+        assert p["grid"] == (64, 64, 64) and p["views"] == views and p["det"] == (91, 91)
+    assert 55 * 91 * 91 == 455455 and 19 * 91 * 91 == 157339
