@@ -216,6 +216,15 @@ int tvr_profile_get(tvr_problem* p, tvr_kernel_stat* out, int cap, int* n_out);
 /* Number of kernels launched by the library since tvr_create (or the last reset). */
 int64_t tvr_launch_count(const tvr_problem* p, int reset);
 
+/* Solver control.  HOST: the scalar logic of every line-search / BT trial runs
+ * on the host after a device->host fetch of the pass reductions.  DEVICE: a whole solve is one
+ * CUDA graph with conditional while / if nodes; single-thread control kernels take the same
+ * decisions in the same fp64 arithmetic (identical iterates), the host waits once.  DEVICE
+ * applies to one-GPU problems (world == 1; others use HOST).  Default DEVICE; the environment
+ * variable TVR_CONTROL=host|device overrides. */
+enum { TVR_CONTROL_HOST = 0, TVR_CONTROL_DEVICE = 1 };
+int tvr_set_control(tvr_problem* p, int mode);
+
 /* ---- NCCL bootstrap (z-slab mode) ---- */
 int tvr_nccl_unique_id_size(void);
 int tvr_nccl_get_unique_id(void* id_out);

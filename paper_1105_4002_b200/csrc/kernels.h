@@ -150,6 +150,9 @@ struct TVArgs {
   double* partials;
   unsigned* counter;
   double* scal;     // 6 doubles
+  // non-null (device-side control): [0] trial step s / momentum beta, [1] stop_step, [2] wbeta,
+  // read by the kernel at launch instead of the values above
+  const double* dparam;
 };
 
 cudaError_t launch_tv_grad_plain(const TVArgs& a, const float* x, cudaStream_t st);

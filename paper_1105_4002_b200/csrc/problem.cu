@@ -262,8 +262,9 @@ static TVArgs tv_args(tvr_problem* p, int slot) {
 
 int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta, const float* w1,
                  const float* w0, double wbeta, float* g, float* v_out, const float* xp,
-                 const float* gp, double stop_step, int slot, double alpha) {
+                 const float* gp, double stop_step, int slot, double alpha, const double* dparam) {
   TVArgs a = tv_args(p, slot);
+  a.dparam = dparam;
   a.alpha = alpha;
   a.w1 = w1;
   a.w0 = w0;
@@ -289,8 +290,9 @@ int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta, c
 }
 
 int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, float* v,
-                  double stop_step, const float* xo, int slot) {
+                  double stop_step, const float* xo, int slot, const double* dparam) {
   TVArgs a = tv_args(p, slot);
+  a.dparam = dparam;
   a.v_out = v;
   a.tx = x;
   a.tg = g;
@@ -1135,6 +1137,15 @@ int tvr_profile_get(tvr_problem* p, tvr_kernel_stat* out, int cap, int* n_out) {
     ++n;
   }
   if (n_out) *n_out = n;
+  return TVR_OK;
+}
+
+int tvr_set_control(tvr_problem* p, int mode) {
+  if (!p || (mode != TVR_CONTROL_HOST && mode != TVR_CONTROL_DEVICE)) {
+    set_error("tvr_set_control: bad argument");
+    return TVR_E_ARG;
+  }
+  p->control = mode;
   return TVR_OK;
 }
 

@@ -118,6 +118,7 @@ struct tvr_problem {
   int zA0 = 0, nzA = 0;
   double alpha = 0, tau = 0, lo = 0, hi = 0;
   int world = 1, rank = 0, mode = TVR_SHARD_NONE;
+  int control = TVR_CONTROL_DEVICE;  // solver control (tvr_set_control)
   void* comm = nullptr;
   int num_sms = 148;
 
@@ -187,9 +188,11 @@ int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta,  
                  const float* xp, const float* gp, double stop_step, int slot);
 int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta, const float* w1,
                  const float* w0, double wbeta, float* g, float* v_out, const float* xp,
-                 const float* gp, double stop_step, int slot, double alpha);
+                 const float* gp, double stop_step, int slot, double alpha,
+                 const double* dparam = nullptr);  // dparam: device-side (beta, stop_step, wbeta)
 int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, float* v,  // a5
-                  double stop_step, const float* xo, int slot);
+                  double stop_step, const float* xo, int slot,
+                  const double* dparam = nullptr);  // dparam: device-side (s, stop_step)
 int pass_momentum(tvr_problem* p, const float* r1, const float* r1lo, const float* r0,  // a6
                   const float* r0lo, double beta, int slot);
 int pass_project(tvr_problem* p, float* x);

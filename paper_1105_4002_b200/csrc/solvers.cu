@@ -3,23 +3,21 @@
 // gradient-map stopping rule (Eq. (10)).  Scalars are fp64 on the host; every vector
 // step runs in the fused kernels (passes of problem.cu).  Readings of the paper: SURVEY §8(c)
 // C6-C14, C21, C25 (listed in DESIGN.md).
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <deque>
 #include <string>
 
+#include "control.h"
 #include "problem.h"
+#include "solver_slots.h"
 
 namespace tvr {
 
 namespace {
 
-// scalar slots in p->dscal (see pass_* in problem.cu)
-constexpr int S_RSQ = 0;   // sum r^2 of the A pass
-constexpr int S_TV = 1;    // 6 stencil reductions: TV, e1..e5
-constexpr int S_MOM = 7;   // sum r_y^2
-constexpr int S_TV2 = 9;   // 6 reductions of a second stencil pass
-constexpr int S_COUNT = 16;
 
 struct Recorder {
   tvr_record* hist;
@@ -53,6 +51,12 @@ int copy_in(tvr_problem* p, float* dst, const float* src) {
 
 }  // namespace
 
+bool use_device_control(const tvr_problem* p);
+static int gpbb_device(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_result* res,
+                       Recorder& rec, double t0, double bytes0, float* x_cur, float* x_prev,
+                       float* v, float* g_cur, float* g_prev, float* w, float* r_cur,
+                       float* r_trial, double f, double gref);
+
 // ------------------------------------------------------------------- GPBB
 static int gpbb_impl(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_result* res,
                      Recorder& rec) {
@@ -81,6 +85,9 @@ static int gpbb_impl(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_re
   double f = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
   const double gref = std::sqrt(p->hscal[S_TV + 3]);
   if (!std::isfinite(f) || !std::isfinite(gref)) { set_error("GPBB: non-finite f or g at x0"); return TVR_E_NONFINITE; }
+  if (use_device_control(p) && o.K + 1 <= 64)
+    return gpbb_device(p, x_io, o, res, rec, t0, bytes0, x_cur, x_prev, v, g_cur, g_prev, w, r_cur,
+                       r_trial, f, gref);
   int64_t n_f = 1, n_g = 1, n_ls = 0;
   std::deque<double> fhist{f};
   double theta = 1.0;  // theta_0
@@ -165,6 +172,173 @@ static int gpbb_impl(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_re
   }
   if (status != TVR_OK) return status;
   return conv ? TVR_OK : TVR_NOT_CONVERGED;
+}
+
+// -------------------------------------------- device-side control
+// A solve as one CUDA graph: conditional WHILE nodes for the iterations and the line search, an
+// IF node for the accepted step; single-thread control kernels (control.cu) take the host
+// controller's decisions on the device.  One GPU only (the distributed scalar sum is a host
+// rank-ordered sum).
+
+namespace {
+
+// Append a conditional node to the capture in progress on p->stream; returns its body graph.
+int capture_conditional(tvr_problem* p, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type,
+                        cudaGraph_t* body) {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaGraph_t g;
+  TVR_CUDA(cudaStreamGetCaptureInfo(p->stream, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = type;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  TVR_CUDA(cudaGraphAddNode(&node, g, deps, nd, &np));
+  TVR_CUDA(cudaStreamUpdateCaptureDependencies(p->stream, &node, 1, cudaStreamSetCaptureDependencies));
+  *body = np.conditional.phGraph_out[0];
+  return TVR_OK;
+}
+
+// Capture f() (pass functions on p->stream) into `body`; returns the algorithmic bytes the
+// captured passes move per execution.  Profiling events and launch counters are suspended.
+template <class F>
+int capture_body(tvr_problem* p, cudaGraph_t body, double* bytes, F&& f) {
+  const bool prof = p->prof;
+  const int64_t launches = p->launches;
+  const double b0 = p->bytes_total;
+  p->prof = false;
+  TVR_CUDA(cudaStreamBeginCaptureToGraph(p->stream, body, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeRelaxed));
+  const int st = f();
+  cudaGraph_t out = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(p->stream, &out);
+  p->prof = prof;
+  if (bytes) *bytes = p->bytes_total - b0;
+  p->bytes_total = b0;
+  p->launches = launches;
+  if (st < 0) return st;
+  TVR_CUDA(e);
+  return TVR_OK;
+}
+
+struct GraphGuard {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  ~GraphGuard() {
+    if (ex) cudaGraphExecDestroy(ex);
+    if (g) cudaGraphDestroy(g);
+  }
+};
+
+}  // namespace
+
+bool use_device_control(const tvr_problem* p) {
+  if (p->world > 1) return false;
+  const char* e = std::getenv("TVR_CONTROL");
+  if (e && *e) return std::string(e) == "device";
+  return p->control == TVR_CONTROL_DEVICE;
+}
+
+// GPBB with device-side control.  Same entry state as gpbb_impl after its x_0 pass; returns the
+// same result fields.
+static int gpbb_device(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_result* res,
+                       Recorder& rec, double t0, double bytes0, float* x_cur, float* x_prev,
+                       float* v, float* g_cur, float* g_prev, float* w, float* r_cur,
+                       float* r_trial, double f, double gref) {
+  const double Nglob = (double)p->plane * p->nz;
+  GpbbDev hd{};
+  hd.eps = o.eps; hd.sigma = o.sigma; hd.beta0 = o.beta0; hd.beta_min = o.beta_min;
+  hd.gref = gref; hd.N = Nglob; hd.alpha = p->alpha;
+  hd.max_iters = o.max_iters; hd.K = o.K; hd.stop_mode = o.stop_mode;
+  hd.f = f; hd.theta = 1.0;  // theta_0
+  hd.fhist[0] = f; hd.nh = 1;
+  hd.rec_cap = rec.hist ? rec.cap : 0;
+  GpbbDev* d = nullptr;
+  tvr_record* drec = nullptr;
+  struct Free {
+    void* a; void* b;
+    ~Free() { if (a) cudaFree(a); if (b) cudaFree(b); }
+  } fr{nullptr, nullptr};
+  TVR_CUDA(cudaMalloc(&d, sizeof(GpbbDev)));
+  fr.a = d;
+  if (hd.rec_cap > 0) {
+    TVR_CUDA(cudaMalloc(&drec, sizeof(tvr_record) * hd.rec_cap));
+    fr.b = drec;
+  }
+  hd.rec = drec;
+  TVR_CUDA(cudaMemcpyAsync(d, &hd, sizeof(hd), cudaMemcpyHostToDevice, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+
+  GraphGuard gg;
+  TVR_CUDA(cudaGraphCreate(&gg.g, 0));
+  GpbbHandles h;
+  TVR_CUDA(cudaGraphConditionalHandleCreate(&h.outer, gg.g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h.outer;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t outer;
+  TVR_CUDA(cudaGraphAddNode(&outer, gg.g, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0], body_ls = nullptr, body_acc = nullptr;
+  TVR_CUDA(cudaGraphConditionalHandleCreate(&h.ls, body, 0, 0));
+  TVR_CUDA(cudaGraphConditionalHandleCreate(&h.acc, body, 0, 0));
+  const size_t vb = sizeof(float) * p->n, db = sizeof(float) * p->m;
+  double bytes_ls = 0.0, bytes_acc = 0.0;
+  TVR_TRY(capture_body(p, body, nullptr, [&]() -> int {
+    TVR_CUDA(launch_gpbb_begin(d, h, p->stream));
+    TVR_TRY(capture_conditional(p, h.ls, cudaGraphCondTypeWhile, &body_ls));
+    TVR_TRY(capture_conditional(p, h.acc, cudaGraphCondTypeIf, &body_acc));
+    return TVR_OK;
+  }));
+  // one line-search trial: x_bar = P_Q(x_k - beta theta_k g_k) with TV and Armijo reductions,
+  // r = A x_bar - b, then the decision
+  TVR_TRY(capture_body(p, body_ls, &bytes_ls, [&]() -> int {
+    TVR_TRY(pass_tv_trial(p, x_cur, g_cur, 0.0, v, 0.0, nullptr, S_TV, d->dparam));
+    TVR_TRY(pass_residual(p, v, r_trial, S_RSQ));
+    TVR_CUDA(launch_gpbb_ls(d, p->dscal, h, p->stream));
+    return TVR_OK;
+  }));
+  // accepted step: rotate the state by copies, gradient at x_{k+1} with BB reductions
+  TVR_TRY(capture_body(p, body_acc, &bytes_acc, [&]() -> int {
+    TVR_CUDA(cudaMemcpyAsync(x_prev, x_cur, vb, cudaMemcpyDeviceToDevice, p->stream));
+    TVR_CUDA(cudaMemcpyAsync(g_prev, g_cur, vb, cudaMemcpyDeviceToDevice, p->stream));
+    TVR_CUDA(cudaMemcpyAsync(x_cur, v, vb, cudaMemcpyDeviceToDevice, p->stream));
+    TVR_CUDA(cudaMemcpyAsync(r_cur, r_trial, db, cudaMemcpyDeviceToDevice, p->stream));
+    TVR_TRY(pass_AT(p, r_cur, w));
+    TVR_TRY(pass_tv_grad(p, x_cur, nullptr, 0.0, w, nullptr, 0.0, g_cur, nullptr, x_prev, g_prev,
+                         0.0, S_TV));
+    TVR_CUDA(launch_gpbb_accept(d, p->dscal, p->stream));
+    return TVR_OK;
+  }));
+  TVR_CUDA(cudaGraphInstantiate(&gg.ex, gg.g, 0));
+  TVR_CUDA(cudaGraphLaunch(gg.ex, p->stream));
+  TVR_CUDA(cudaMemcpyAsync(&hd, d, sizeof(hd), cudaMemcpyDeviceToHost, p->stream));
+  TVR_CUDA(cudaMemcpyAsync(x_io, x_cur, vb, cudaMemcpyDeviceToDevice, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  if (drec && hd.n_rec > 0) {
+    TVR_CUDA(cudaMemcpy(rec.hist, drec, sizeof(tvr_record) * std::min(hd.n_rec, hd.rec_cap),
+                        cudaMemcpyDeviceToHost));
+  }
+  rec.n = hd.n_rec;
+  p->bytes_total += (double)hd.ls_execs * bytes_ls + (double)hd.n_g * (bytes_acc + 4.0 * vb + 2.0 * db);
+  p->launches += 2 * hd.ls_execs + 3 * hd.n_g;
+  if (res) {
+    res->converged = hd.conv ? 1 : 0;
+    res->iters = hd.k;
+    res->n_f = 1 + hd.n_f; res->n_grad = 1 + hd.n_g; res->n_ls = hd.n_ls; res->n_records = rec.n;
+    res->f = hd.f; res->gmap_ref = gref;
+    res->gmap_rel = gref > 0 ? hd.gn / gref : 0.0;
+    res->gmap_abs_per_n = hd.gn / Nglob;
+    res->seconds = now_s() - t0;
+    res->bytes = p->bytes_total - bytes0;
+  }
+  if (hd.status == TVR_E_NONFINITE) { set_error("GPBB: non-finite trial objective"); return TVR_E_NONFINITE; }
+  if (hd.status == TVR_E_LINESEARCH) { set_error("GPBB: beta < beta_min"); return TVR_E_LINESEARCH; }
+  return hd.conv ? TVR_OK : TVR_NOT_CONVERGED;
 }
 
 // -------------------------------------------------------------------- UPN

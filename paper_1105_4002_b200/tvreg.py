@@ -34,6 +34,8 @@ STATUS_NAMES = {v: k for k, v in globals().items() if k.startswith("TVR_") and i
 TVR_SHARD_NONE = 0
 TVR_SHARD_ZSLAB = 1
 TVR_SHARD_VIEWS = 2
+TVR_CONTROL_HOST = 0
+TVR_CONTROL_DEVICE = 1
 TVR_STOP_REL = 0
 TVR_STOP_ABS_PER_N = 1
 
@@ -120,6 +122,7 @@ SIGNATURES = {
     "tvr_solve_gp": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(tvr_gp_opts),
                                      ctypes.POINTER(tvr_result), ctypes.POINTER(tvr_record), c_i64]),
     "tvr_residual": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(c_f64)]),
+    "tvr_set_control": (ctypes.c_int, [c_vp, ctypes.c_int]),
     "tvr_apply_AT": (ctypes.c_int, [c_vp, c_vp, c_vp]),
     "tvr_tv": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(c_f64), c_vp]),
     "tvr_gradient_map": (ctypes.c_int, [c_vp, c_vp, c_f64, ctypes.POINTER(c_f64), c_vp]),
@@ -343,6 +346,11 @@ class Problem:
         return rp, cl, vl
 
     # ---- solvers
+    def set_control(self, mode: str):
+        """Solver control: "device" (one CUDA graph per solve, default) or "host"."""
+        _check(lib().tvr_set_control(self._h, {"host": TVR_CONTROL_HOST,
+                                               "device": TVR_CONTROL_DEVICE}[mode]), "tvr_set_control")
+
     def _solve(self, fn, opts, x, hist_cap):
         res = tvr_result()
         hist = (tvr_record * hist_cap)() if hist_cap else None
