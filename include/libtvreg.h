@@ -216,13 +216,16 @@ int tvr_profile_get(tvr_problem* p, tvr_kernel_stat* out, int cap, int* n_out);
 /* Number of kernels launched by the library since tvr_create (or the last reset). */
 int64_t tvr_launch_count(const tvr_problem* p, int reset);
 
-/* Solver control.  HOST: the scalar logic of every line-search / BT trial runs
- * on the host after a device->host fetch of the pass reductions.  DEVICE: a whole solve is one
- * CUDA graph with conditional while / if nodes; single-thread control kernels take the same
- * decisions in the same fp64 arithmetic (identical iterates), the host waits once.  DEVICE
- * applies to one-GPU problems (world == 1; others use HOST).  Default DEVICE; the environment
- * variable TVR_CONTROL=host|device overrides. */
-enum { TVR_CONTROL_HOST = 0, TVR_CONTROL_DEVICE = 1 };
+/* Solver control for GPBB and UPN.  HOST: the scalar logic of every line-search
+ * / BT trial runs on the host after a device->host fetch of the pass reductions.  DEVICE: a whole
+ * solve is one CUDA graph with conditional while / if nodes; single-thread control kernels take
+ * the same decisions in the same fp64 arithmetic (identical iterates), the host waits once; the
+ * state rotates by device copies.  DEVICE applies to one-GPU problems (world == 1; others use
+ * HOST).  AUTO (default): DEVICE below 2^25 matrix entries, where launch and synchronisation
+ * latency is a visible part of an iteration (c1: -11 to -16 % per iteration), HOST above (c2:
+ * kernel-bound, the copies cost 1-4 %).  The environment variable TVR_CONTROL=host|device
+ * overrides. */
+enum { TVR_CONTROL_HOST = 0, TVR_CONTROL_DEVICE = 1, TVR_CONTROL_AUTO = 2 };
 int tvr_set_control(tvr_problem* p, int mode);
 
 /* ---- NCCL bootstrap (z-slab mode) ---- */

@@ -34,6 +34,31 @@ struct GpbbHandles {
   cudaGraphConditionalHandle outer, ls, acc;
 };
 
+struct UpnDev {
+  double eps, gref, N, alpha, rho_L;
+  int64_t max_iters;
+  int32_t bt_max, stop_mode;
+  // state (names as upn_impl)
+  double L, mu, theta, theta_n, beta, fxk, fy, gn;
+  double bt_f, bt_L, mu_gd, mu_dd;
+  int64_t k, n_f, n_g, n_ls, bt_execs;
+  int32_t bt_trials, conv, status, first;  // first: y_k = x_k (no mu_k update, C9)
+  double dp_trial[3];  // BT trial: s = 1/L~
+  double dp_stop[3];   // stop-test stencil at x_{k+1}: stop_step = 1/L_k
+  double dp_mom[3];    // momentum point: beta (source and w blend)
+  tvr_record* rec;
+  int64_t rec_cap, n_rec;
+};
+
+struct UpnHandles {
+  cudaGraphConditionalHandle outer, bt, rest;
+};
+
+cudaError_t launch_upn_bt_begin(UpnDev* d, UpnHandles h, cudaStream_t st);
+cudaError_t launch_upn_bt(UpnDev* d, const double* scal, UpnHandles h, cudaStream_t st);
+cudaError_t launch_upn_mid(UpnDev* d, UpnHandles h, cudaStream_t st);
+cudaError_t launch_upn_end(UpnDev* d, const double* scal, UpnHandles h, cudaStream_t st);
+
 cudaError_t launch_gpbb_begin(GpbbDev* d, GpbbHandles h, cudaStream_t st);
 cudaError_t launch_gpbb_ls(GpbbDev* d, const double* scal, GpbbHandles h, cudaStream_t st);
 cudaError_t launch_gpbb_accept(GpbbDev* d, const double* scal, cudaStream_t st);

@@ -122,7 +122,8 @@ cudaError_t launch_spmv_tma(const TmaSpmvArgs& a, int lpr, int grid, size_t smem
 
 cudaError_t launch_momentum_resid(int64_t m, const float* r1, const float* r1lo, const float* r0,
                                   const float* r0lo, double beta, double* partials,
-                                  unsigned* counter, double* scal, int grid, cudaStream_t st);
+                                  unsigned* counter, double* scal, int grid, cudaStream_t st,
+                                  const double* dbeta = nullptr);  // dbeta: device-side beta
 cudaError_t launch_project(int64_t n, float* x, double lo, double hi, int grid, cudaStream_t st);
 cudaError_t launch_gradient_map(int64_t n, const float* x, const float* g, double nu, double lo,
                                 double hi, float* G, double* partials, unsigned* counter,
@@ -151,7 +152,9 @@ struct TVArgs {
   unsigned* counter;
   double* scal;     // 6 doubles
   // non-null (device-side control): [0] trial step s / momentum beta, [1] stop_step, [2] wbeta,
-  // read by the kernel at launch instead of the values above
+  // read by the kernel at launch instead of the values above.  The instantiation (which optional
+  // reductions exist) is still chosen from the host-side fields, so a call site whose stop step is
+  // decided on the device passes a positive placeholder stop_step.
   const double* dparam;
 };
 

@@ -304,11 +304,11 @@ int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, floa
 }
 
 int pass_momentum(tvr_problem* p, const float* r1, const float* r1lo, const float* r0,
-                  const float* r0lo, double beta, int slot) {
+                  const float* r0lo, double beta, int slot, const double* dbeta) {
   const int grid = elem_grid(p, p->m);
   return launch(p, K_MOMENTUM, 16.0 * p->m, [&] {
     return launch_momentum_resid(p->m, r1, r1lo, r0, r0lo, beta, p->partials, p->counter,
-                                 p->dscal + slot, grid, p->stream);
+                                 p->dscal + slot, grid, p->stream, dbeta);
   });
 }
 
@@ -1141,7 +1141,7 @@ int tvr_profile_get(tvr_problem* p, tvr_kernel_stat* out, int cap, int* n_out) {
 }
 
 int tvr_set_control(tvr_problem* p, int mode) {
-  if (!p || (mode != TVR_CONTROL_HOST && mode != TVR_CONTROL_DEVICE)) {
+  if (!p || (mode != TVR_CONTROL_HOST && mode != TVR_CONTROL_DEVICE && mode != TVR_CONTROL_AUTO)) {
     set_error("tvr_set_control: bad argument");
     return TVR_E_ARG;
   }

@@ -118,7 +118,7 @@ struct tvr_problem {
   int zA0 = 0, nzA = 0;
   double alpha = 0, tau = 0, lo = 0, hi = 0;
   int world = 1, rank = 0, mode = TVR_SHARD_NONE;
-  int control = TVR_CONTROL_DEVICE;  // solver control (tvr_set_control)
+  int control = TVR_CONTROL_AUTO;  // solver control (tvr_set_control)
   void* comm = nullptr;
   int num_sms = 148;
 
@@ -194,7 +194,7 @@ int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, floa
                   double stop_step, const float* xo, int slot,
                   const double* dparam = nullptr);  // dparam: device-side (s, stop_step)
 int pass_momentum(tvr_problem* p, const float* r1, const float* r1lo, const float* r0,  // a6
-                  const float* r0lo, double beta, int slot);
+                  const float* r0lo, double beta, int slot, const double* dbeta = nullptr);
 int pass_project(tvr_problem* p, float* x);
 int pass_gmap(tvr_problem* p, const float* x, const float* g, double nu, float* G, int slot);
 

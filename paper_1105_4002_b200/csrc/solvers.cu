@@ -57,6 +57,15 @@ static int gpbb_device(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_
                        float* v, float* g_cur, float* g_prev, float* w, float* r_cur,
                        float* r_trial, double f, double gref);
 
+struct UpnState {
+  float *xk, *xn, *ybuf, *gy, *wk, *wn, *rk, *rn, *rk_lo, *rn_lo;
+  double L, mu, theta, fxk, fy, gn, gref;
+  int64_t k, n_f, n_g, n_ls;
+  bool conv;
+};
+static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnState& st,
+                      int* status);
+
 // ------------------------------------------------------------------- GPBB
 static int gpbb_impl(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_result* res,
                      Recorder& rec) {
@@ -239,6 +248,7 @@ bool use_device_control(const tvr_problem* p) {
   if (p->world > 1) return false;
   const char* e = std::getenv("TVR_CONTROL");
   if (e && *e) return std::string(e) == "device";
+  if (p->control == TVR_CONTROL_AUTO) return p->nnz < ((int64_t)1 << 25);
   return p->control == TVR_CONTROL_DEVICE;
 }
 
@@ -297,7 +307,8 @@ static int gpbb_device(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_
   // one line-search trial: x_bar = P_Q(x_k - beta theta_k g_k) with TV and Armijo reductions,
   // r = A x_bar - b, then the decision
   TVR_TRY(capture_body(p, body_ls, &bytes_ls, [&]() -> int {
-    TVR_TRY(pass_tv_trial(p, x_cur, g_cur, 0.0, v, 0.0, nullptr, S_TV, d->dparam));
+    TVR_TRY(pass_tv_trial(p, x_cur, g_cur, 0.0, v, 1.0 /* stop: decided on the device */, nullptr,
+                          S_TV, d->dparam));
     TVR_TRY(pass_residual(p, v, r_trial, S_RSQ));
     TVR_CUDA(launch_gpbb_ls(d, p->dscal, h, p->stream));
     return TVR_OK;
@@ -339,6 +350,98 @@ static int gpbb_device(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_
   if (hd.status == TVR_E_NONFINITE) { set_error("GPBB: non-finite trial objective"); return TVR_E_NONFINITE; }
   if (hd.status == TVR_E_LINESEARCH) { set_error("GPBB: beta < beta_min"); return TVR_E_LINESEARCH; }
   return hd.conv ? TVR_OK : TVR_NOT_CONVERGED;
+}
+
+// UPN iterations k >= 1 with device-side control (one graph launch); st holds the host state
+// after x_1 and is updated in place.  *status receives a solver error (TVR_OK otherwise).
+static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnState& st,
+                      int* status) {
+  *status = TVR_OK;
+  UpnDev hd{};
+  hd.eps = o.eps; hd.gref = st.gref; hd.N = (double)p->plane * p->nz; hd.alpha = p->alpha;
+  hd.rho_L = o.rho_L; hd.max_iters = o.max_iters; hd.bt_max = o.bt_max; hd.stop_mode = o.stop_mode;
+  hd.L = st.L; hd.mu = st.mu; hd.theta = st.theta; hd.fxk = st.fxk; hd.fy = st.fy; hd.gn = st.gn;
+  hd.k = st.k; hd.first = 1;
+  hd.rec_cap = rec.hist ? std::max<int64_t>(0, rec.cap - rec.n) : 0;
+  UpnDev* d = nullptr;
+  tvr_record* drec = nullptr;
+  struct Free {
+    void* a; void* b;
+    ~Free() { if (a) cudaFree(a); if (b) cudaFree(b); }
+  } fr{nullptr, nullptr};
+  TVR_CUDA(cudaMalloc(&d, sizeof(UpnDev)));
+  fr.a = d;
+  if (hd.rec_cap > 0) {
+    TVR_CUDA(cudaMalloc(&drec, sizeof(tvr_record) * hd.rec_cap));
+    fr.b = drec;
+  }
+  hd.rec = drec;
+  const size_t vb = sizeof(float) * p->n, db = sizeof(float) * p->m;
+  // y_1 = x_1 lives in ybuf from here on
+  TVR_CUDA(cudaMemcpyAsync(st.ybuf, st.xk, vb, cudaMemcpyDeviceToDevice, p->stream));
+  TVR_CUDA(cudaMemcpyAsync(d, &hd, sizeof(hd), cudaMemcpyHostToDevice, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+
+  GraphGuard gg;
+  TVR_CUDA(cudaGraphCreate(&gg.g, 0));
+  UpnHandles h;
+  TVR_CUDA(cudaGraphConditionalHandleCreate(&h.outer, gg.g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h.outer;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t outer;
+  TVR_CUDA(cudaGraphAddNode(&outer, gg.g, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0], body_bt = nullptr, body_rest = nullptr;
+  TVR_CUDA(cudaGraphConditionalHandleCreate(&h.bt, body, 0, 0));
+  TVR_CUDA(cudaGraphConditionalHandleCreate(&h.rest, body, 0, 0));
+  double bytes_bt = 0.0, bytes_rest = 0.0;
+  TVR_TRY(capture_body(p, body, nullptr, [&]() -> int {
+    TVR_CUDA(launch_upn_bt_begin(d, h, p->stream));
+    TVR_TRY(capture_conditional(p, h.bt, cudaGraphCondTypeWhile, &body_bt));
+    TVR_CUDA(launch_upn_mid(d, h, p->stream));
+    TVR_TRY(capture_conditional(p, h.rest, cudaGraphCondTypeIf, &body_rest));
+    return TVR_OK;
+  }));
+  // one BT trial: x = P_Q(y - g_y/L~), its TV and BT / mu reductions, r = A x - b
+  TVR_TRY(capture_body(p, body_bt, &bytes_bt, [&]() -> int {
+    TVR_TRY(pass_tv_trial(p, st.ybuf, st.gy, 0.0, st.xn, 0.0, st.xk, S_TV, d->dp_trial));
+    TVR_TRY(pass_residual(p, st.xn, st.rn, S_RSQ, st.rn_lo));
+    TVR_CUDA(launch_upn_bt(d, p->dscal, h, p->stream));
+    return TVR_OK;
+  }));
+  // w_{k+1}, stop reduction at x_{k+1}, y_{k+1} with f(y), grad f(y) by linearity (a6)
+  TVR_TRY(capture_body(p, body_rest, &bytes_rest, [&]() -> int {
+    TVR_TRY(pass_AT(p, st.rn, st.wn));
+    TVR_TRY(pass_tv_grad(p, st.xn, nullptr, 0.0, st.wn, nullptr, 0.0, nullptr, nullptr, nullptr,
+                         nullptr, 1.0 /* 1/L_k on the device */, S_TV, p->alpha, d->dp_stop));
+    TVR_TRY(pass_momentum(p, st.rn, st.rn_lo, st.rk, st.rk_lo, 0.0, S_MOM, d->dp_mom));
+    TVR_TRY(pass_tv_grad(p, st.xn, st.xk, 0.0, st.wn, st.wk, 0.0, st.gy, st.ybuf, nullptr, nullptr,
+                         0.0, S_TV2, p->alpha, d->dp_mom));
+    TVR_CUDA(cudaMemcpyAsync(st.xk, st.xn, vb, cudaMemcpyDeviceToDevice, p->stream));
+    TVR_CUDA(cudaMemcpyAsync(st.rk, st.rn, db, cudaMemcpyDeviceToDevice, p->stream));
+    TVR_CUDA(cudaMemcpyAsync(st.rk_lo, st.rn_lo, db, cudaMemcpyDeviceToDevice, p->stream));
+    TVR_CUDA(cudaMemcpyAsync(st.wk, st.wn, vb, cudaMemcpyDeviceToDevice, p->stream));
+    TVR_CUDA(launch_upn_end(d, p->dscal, h, p->stream));
+    return TVR_OK;
+  }));
+  TVR_CUDA(cudaGraphInstantiate(&gg.ex, gg.g, 0));
+  TVR_CUDA(cudaGraphLaunch(gg.ex, p->stream));
+  TVR_CUDA(cudaMemcpyAsync(&hd, d, sizeof(hd), cudaMemcpyDeviceToHost, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  if (drec && hd.n_rec > 0)
+    TVR_CUDA(cudaMemcpy(rec.hist + rec.n, drec, sizeof(tvr_record) * std::min(hd.n_rec, hd.rec_cap),
+                        cudaMemcpyDeviceToHost));
+  rec.n += hd.n_rec;
+  p->bytes_total += (double)hd.bt_execs * bytes_bt + (double)hd.n_g * (bytes_rest + 4.0 * vb + 4.0 * db);
+  p->launches += 2 * hd.bt_execs + 4 * hd.n_g;
+  st.L = hd.L; st.mu = hd.mu; st.theta = hd.theta; st.fxk = hd.fxk; st.fy = hd.fy; st.gn = hd.gn;
+  st.k = hd.k; st.n_f += hd.n_f; st.n_g += hd.n_g; st.n_ls += hd.n_ls; st.conv = hd.conv != 0;
+  if (hd.status == TVR_E_NONFINITE) { set_error("UPN: non-finite objective"); *status = TVR_E_NONFINITE; }
+  if (hd.status == TVR_E_LINESEARCH) { set_error("BT: more than bt_max trials"); *status = TVR_E_LINESEARCH; }
+  if (hd.status == TVR_E_THETA) { set_error("UPN: theta outside (0,1]"); *status = TVR_E_THETA; }
+  return TVR_OK;
 }
 
 // -------------------------------------------------------------------- UPN
@@ -441,7 +544,14 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
     rec.add(r);
   }
   int status = TVR_OK;
-  while (!conv && k < o.max_iters) {
+  if (!conv && k < o.max_iters && use_device_control(p)) {
+    UpnState us{xk, xn, ybuf, gy, wk, wn, rk, rn, rk_lo, rn_lo, L, mu, theta, fxk, fy, gn, gref,
+                k, n_f, n_g, n_ls, conv};
+    TVR_TRY(upn_device(p, o, rec, us, &status));
+    L = us.L; mu = us.mu; theta = us.theta; fxk = us.fxk; fy = us.fy; gn = us.gn;
+    k = us.k; n_f = us.n_f; n_g = us.n_g; n_ls = us.n_ls; conv = us.conv;
+  }
+  while (!conv && k < o.max_iters && status == TVR_OK) {
     // [x_{k+1}, L_k] = BT(y_k, L_{k-1})
     int s = backtrack(p, y, gy, fy, L, o, y == xk ? nullptr : xk, xn, rn, rn_lo, bt);
     if (s < 0) { status = s; break; }

@@ -667,7 +667,8 @@ cudaError_t launch_compress_cols(const SpmvArgs& a, const int32_t* col, uint16_t
 __global__ void momentum_resid_kernel(int64_t m, const float* __restrict__ r1,
                                       const float* __restrict__ r1lo, const float* __restrict__ r0,
                                       const float* __restrict__ r0lo, double beta, double* partials,
-                                      unsigned* counter, double* scal) {
+                                      unsigned* counter, double* scal, const double* dbeta) {
+  if (dbeta) beta = *dbeta;  // device-side control
   double s = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += stride) {
@@ -832,8 +833,10 @@ int spmv_occupancy(const SpmvVariant& v, int block, size_t smem) {
 
 cudaError_t launch_momentum_resid(int64_t m, const float* r1, const float* r1lo, const float* r0,
                                   const float* r0lo, double beta, double* partials,
-                                  unsigned* counter, double* scal, int grid, cudaStream_t st) {
-  momentum_resid_kernel<<<grid, 256, 0, st>>>(m, r1, r1lo, r0, r0lo, beta, partials, counter, scal);
+                                  unsigned* counter, double* scal, int grid, cudaStream_t st,
+                                  const double* dbeta) {
+  momentum_resid_kernel<<<grid, 256, 0, st>>>(m, r1, r1lo, r0, r0lo, beta, partials, counter, scal,
+                                              dbeta);
   return cudaGetLastError();
 }
 

@@ -36,6 +36,7 @@ TVR_SHARD_ZSLAB = 1
 TVR_SHARD_VIEWS = 2
 TVR_CONTROL_HOST = 0
 TVR_CONTROL_DEVICE = 1
+TVR_CONTROL_AUTO = 2
 TVR_STOP_REL = 0
 TVR_STOP_ABS_PER_N = 1
 
@@ -347,9 +348,10 @@ class Problem:
 
     # ---- solvers
     def set_control(self, mode: str):
-        """Solver control: "device" (one CUDA graph per solve, default) or "host"."""
-        _check(lib().tvr_set_control(self._h, {"host": TVR_CONTROL_HOST,
-                                               "device": TVR_CONTROL_DEVICE}[mode]), "tvr_set_control")
+        """Solver control: "device" (one CUDA graph per solve), "host", or "auto" (default: device
+        below 2^25 matrix entries); SURVEY f3."""
+        _check(lib().tvr_set_control(self._h, {"host": TVR_CONTROL_HOST, "device": TVR_CONTROL_DEVICE,
+                                               "auto": TVR_CONTROL_AUTO}[mode]), "tvr_set_control")
 
     def _solve(self, fn, opts, x, hist_cap):
         res = tvr_result()

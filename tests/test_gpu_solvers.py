@@ -140,17 +140,19 @@ def test_gp_parity_c1(tvreg, c1):
     _check_parity(Po, x.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("solver", ["gpbb", "upn"])
 @pytest.mark.parametrize("case", ["c1", "box"])
-def test_device_control_matches_host_control_gpbb(tvreg, c1, case):
-    """f3: GPBB as one CUDA graph with conditional nodes and device control kernels takes the host
-    controller's decisions in the same fp64 arithmetic: identical iterates, counts and history."""
+def test_device_control_matches_host_control(tvreg, c1, case, solver):
+    """f3: a solve as one CUDA graph with conditional nodes and device control kernels takes the
+    host controller's decisions in the same fp64 arithmetic: identical iterates, counts, history."""
     kw = {} if case == "c1" else dict(alpha=0.03, tau=1e-2, hi=1.0)
     outs = {}
     for mode in ("host", "device"):
         P = _gpu_problem(tvreg, c1, **kw)
         P.set_control(mode)
         x = torch.zeros(c1.N, device="cuda")
-        res = P.solve_gpbb(x, max_iters=20000, eps=1e-6 if case == "c1" else 3e-6, hist_cap=25000)
+        res = getattr(P, f"solve_{solver}")(x, max_iters=20000, eps=1e-6 if case == "c1" else 3e-6,
+                                            hist_cap=25000)
         outs[mode] = (res, x.clone())
         P.close()
     (rh, xh), (rd, xd) = outs["host"], outs["device"]
@@ -161,15 +163,17 @@ def test_device_control_matches_host_control_gpbb(tvreg, c1, case):
     assert rd.history == rh.history
 
 
-def test_device_control_max_iters_and_restart(tvreg, c1):
-    """max_iters stops the device loop like the host loop (stop test only at k = max_iters), and a
-    second solve on the same problem starts from fresh controller state."""
+@pytest.mark.parametrize("solver", ["gpbb", "upn"])
+def test_device_control_max_iters_and_restart(tvreg, c1, solver):
+    """max_iters stops the device loop like the host loop, and a second solve on the same problem
+    starts from fresh controller state."""
     P = _gpu_problem(tvreg, c1)
     res = []
     for mode in ("host", "device", "device"):
         P.set_control(mode)
         x = torch.zeros(c1.N, device="cuda")
-        res.append((P.solve_gpbb(x, max_iters=7, eps=1e-12, hist_cap=20), x.clone()))
+        res.append((getattr(P, f"solve_{solver}")(x, max_iters=7, eps=1e-12, hist_cap=20), x.clone()))
     for r, x in res[1:]:
-        assert not r.converged and r.iters == 7 and len(r.history) == 8
+        assert not r.converged and r.iters == 7
+        assert len(r.history) == (8 if solver == "gpbb" else 7)
         assert r.history == res[0][0].history and torch.equal(x, res[0][1])
