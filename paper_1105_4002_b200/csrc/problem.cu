@@ -147,7 +147,24 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
 // Launch one SpMV pass with the plan's kernel: the TMA bulk-copy pipeline when planned, else the
 // register-streaming kernel.
 static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed, const float* src,
-                            const float* b, float* out, float* out_lo, double* scal) {
+                            const float* b, float* out, float* out_lo, double* scal,
+                            int64_t it_lo = 0, int64_t it_hi = -1) {
+  if (it_hi >= 0) {  // items [it_lo, it_hi) only (per-row kernels; the e2e pipeline's chunks)
+    SpmvArgs a = spmv_args(p, pl, transposed, src, b, out, scal);
+    a.out_lo = out_lo;
+    a.item_row += it_lo;
+    a.item_slice += it_lo;
+    a.nitems = it_hi - it_lo;
+    if (pl.pad) {
+      a.rp = pl.rpp;
+      a.col16 = pl.col16p;
+      a.val = pl.valp;
+      return launch_spmv16p(a, pl.v, (int)std::min<int64_t>(pl.pad_grid, std::max<int64_t>(1, a.nitems)),
+                            pl.block, pl.smem, p->stream);
+    }
+    return launch_spmv(a, pl.v, (int)std::min<int64_t>(pl.grid, std::max<int64_t>(1, a.nitems)),
+                       pl.block, pl.smem, p->stream);
+  }
   if (pl.tma.on) {
     TmaSpmvArgs t;
     t.rp = transposed ? p->rpT : p->rp;
@@ -614,7 +631,9 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
     TVR_TRY(upload(p, (void**)&pl.win_len, win_len.data(), sizeof(int32_t) * win_len.size()));
     std::vector<int64_t> zend(win_lo.size(), 0);
     for (size_t i = 0; i < slices.size(); ++i) zend[slices[i]] = (int64_t)i + 1;
+    for (size_t z = 1; z < zend.size(); ++z) zend[z] = std::max(zend[z], zend[z - 1]);
     TVR_TRY(upload(p, (void**)&pl.slice_item_end, zend.data(), sizeof(int64_t) * std::max<size_t>(1, zend.size())));
+    pl.h_slice_item_end = zend;
   }
   if (staged) TVR_TRY(make_tma_plan(p, pl, rp, slice_rows, pl.smem / sizeof(float)));
   TVR_TRY(make_flat_plan(p, pl, rp, n_rows, separable, slice_rows, win_lo, win_len,
@@ -953,6 +972,9 @@ void tvr_destroy(tvr_problem* p) {
     cudaStreamSynchronize(p->stream);
   }
   dev_free_all(p);
+  for (auto e : p->pipe_ev) cudaEventDestroy(e);
+  if (p->s_in) cudaStreamDestroy(p->s_in);
+  if (p->s_out) cudaStreamDestroy(p->s_out);
   for (auto& t : p->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
   for (auto e : p->event_pool) cudaEventDestroy(e);
   if (p->hscal) cudaFreeHost(p->hscal);
@@ -1034,10 +1056,110 @@ int tvr_objective_grad(tvr_problem* p, const float* x_dev, double* f_out, float*
   return objective_grad_impl(p, x_dev, f_out, g_dev, parts);
 }
 
+static bool pinned(const void* ptr) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// End-to-end gradient with the transfers overlapped (one GPU, slice-separable A, per-row SpMV
+// kernels, pinned host buffers): the volume is cut into C slab chunks; chunk c's x goes up on a
+// copy stream while the previous chunks compute, its A pass (rows of its slices), A^T pass (its
+// voxels) and stencil (its planes; needs the first plane of chunk c+1) run as soon as their
+// inputs are there, and its g goes down on a second copy stream.  Per-element results are the
+// unchunked passes' (same kernels, same rows); the fidelity and TV sums are added per chunk in
+// chunk order (equal to the single-launch sums to rounding).
+static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double* f_out, float* gh,
+                                         tvr_fparts* parts, int C) {
+  const int nz = p->nzl;
+  const int64_t plane = p->plane;
+  float* x = volvec(p, 7);
+  float* g = volvec(p, 6);
+  float* w = volvec(p, 8);
+  float* r = datvec(p, 0);
+  if (!p->s_in) {
+    TVR_CUDA(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+    TVR_CUDA(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+    p->pipe_ev.resize(2 * 16 + 2);
+    for (auto& e : p->pipe_ev) TVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t ev_start = p->pipe_ev[0], ev_done = p->pipe_ev[1];
+  auto ev_in = [&](int c) { return p->pipe_ev[2 + c]; };
+  auto ev_g = [&](int c) { return p->pipe_ev[2 + 16 + c]; };
+  std::vector<int> z(C + 1);
+  for (int c = 0; c <= C; ++c) z[c] = (int)((int64_t)nz * c / C);
+  constexpr int SA = 16, ST = 24;  // scalar slots: A chunk c at SA + c, stencil chunk c at ST + 6 c
+  TVR_CUDA(cudaEventRecord(ev_start, p->stream));
+  TVR_CUDA(cudaStreamWaitEvent(p->s_in, ev_start, 0));
+  TVR_CUDA(cudaStreamWaitEvent(p->s_out, ev_start, 0));
+  for (int c = 0; c < C; ++c) {
+    const size_t off = (size_t)z[c] * plane, cnt = (size_t)(z[c + 1] - z[c]) * plane;
+    TVR_CUDA(cudaMemcpyAsync(x + off, xh + off, sizeof(float) * cnt, cudaMemcpyHostToDevice, p->s_in));
+    TVR_CUDA(cudaEventRecord(ev_in(c), p->s_in));
+  }
+  auto items = [](const SpmvPlan& pl, int z0, int z1, int64_t& lo, int64_t& hi) {
+    lo = z0 > 0 ? pl.h_slice_item_end[z0 - 1] : 0;
+    hi = pl.h_slice_item_end[z1 - 1];
+  };
+  const double bytes_row = entry_bytes(p->planA) * (double)p->nnz / nz;  // per slice, for counters
+  for (int c = 0; c < C; ++c) {
+    TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_in(c), 0));
+    int64_t lo, hi;
+    items(p->planA, z[c], z[c + 1], lo, hi);
+    TVR_TRY(launch(p, K_SPMV_A, bytes_row * (z[c + 1] - z[c]), [&] {
+      return run_spmv(p, p->planA, false, x, p->b, r, nullptr, p->dscal + SA + c, lo, hi);
+    }));
+    if (gh) {
+      items(p->planT, z[c], z[c + 1], lo, hi);
+      TVR_TRY(launch(p, K_SPMV_AT, bytes_row * (z[c + 1] - z[c]), [&] {
+        return run_spmv(p, p->planT, true, r, nullptr, w, nullptr, nullptr, lo, hi);
+      }));
+    }
+    if (c + 1 < C) TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_in(c + 1), 0));  // plane z[c+1]
+    TVArgs a = tv_args(p, ST + 6 * c);
+    const int64_t off = (int64_t)z[c] * plane;
+    a.zg0 = p->z0 + z[c];
+    a.nzl = z[c + 1] - z[c];
+    a.w1 = gh ? w + off : nullptr;
+    a.g_out = gh ? g + off : nullptr;
+    const double N = (double)a.nzl * plane;
+    TVR_TRY(launch(p, K_TV_GRAD, N * (gh ? 12.0 : 8.0),
+                   [&] { return launch_tv_grad_plain(a, x + off, p->stream); }));
+    if (gh) {
+      TVR_CUDA(cudaEventRecord(ev_g(c), p->stream));
+      TVR_CUDA(cudaStreamWaitEvent(p->s_out, ev_g(c), 0));
+      TVR_CUDA(cudaMemcpyAsync(gh + off, g + off, sizeof(float) * N, cudaMemcpyDeviceToHost, p->s_out));
+    }
+  }
+  TVR_CUDA(cudaEventRecord(ev_done, p->s_out));
+  TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_done, 0));
+  TVR_CUDA(cudaMemcpyAsync(p->hscal, p->dscal, sizeof(double) * 64, cudaMemcpyDeviceToHost, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  resolve_pending_timings(p);
+  double rsq = 0.0, tv = 0.0;
+  for (int c = 0; c < C; ++c) {
+    rsq += p->hscal[SA + c];
+    tv += p->hscal[ST + 6 * c];
+  }
+  const double fid = 0.5 * rsq, f = fid + p->alpha * tv;
+  if (f_out) *f_out = f;
+  if (parts) { parts->fidelity = fid; parts->tv = tv; parts->f = f; }
+  if (!std::isfinite(f)) { set_error("non-finite objective"); return TVR_E_NONFINITE; }
+  return TVR_OK;
+}
+
 int tvr_objective_grad_host(tvr_problem* p, const float* x_host, double* f_out, float* g_host,
                             tvr_fparts* parts) {
   if (!p || !x_host) { set_error("tvr_objective_grad_host: NULL"); return TVR_E_ARG; }
   TVR_CUDA(cudaSetDevice(p->device));
+  const int C = std::min(env_int("TVR_E2E_CHUNKS", 2), std::min(6, p->nzl));  // 6: dscal slots
+  if (C > 1 && p->world == 1 && p->separable && !p->planA.tma.on && !p->planT.tma.on &&
+      !p->planA.flat.on && !p->planT.flat.on && !p->planA.v.parts && !p->planT.v.parts &&
+      pinned(x_host) && (!g_host || pinned(g_host)))
+    return objective_grad_host_pipelined(p, x_host, f_out, g_host, parts, C);
   float* x = volvec(p, 7);
   float* g = volvec(p, 6);
   TVR_CUDA(cudaMemcpyAsync(x, x_host, sizeof(float) * p->n, cudaMemcpyHostToDevice, p->stream));

@@ -94,6 +94,7 @@ struct SpmvPlan {
   int64_t* item_row = nullptr;
   int32_t* item_slice = nullptr;
   int64_t* slice_item_end = nullptr;
+  std::vector<int64_t> h_slice_item_end;  // host copy (slice-chunked launches of the e2e pipeline)
   int64_t* win_lo = nullptr;
   int32_t* win_len = nullptr;
 };
@@ -155,6 +156,10 @@ struct tvr_problem {
   float* xfull = nullptr;
   float* wfull = nullptr;
   std::vector<int64_t> slab_off, slab_cnt;
+
+  // e2e pipeline of tvr_objective_grad_host (created on first use)
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;
 
   // profiling
   bool prof = false;
