@@ -76,9 +76,12 @@ __global__ void __launch_bounds__(512, MINB) spmv_kernel(SpmvArgs a) {
   int cur_slice = -1;
   int wl = 0;
   double sq = 0.0;
-  for (int64_t it = it0; it < it1; ++it) {
+  // rows of one slice segment (the CTA's items of one slice) walked as one range (see spmv16p)
+  for (int64_t it = it0; it < it1;) {
+    const int z = a.item_slice[it];
+    int64_t it_end = it + 1;
+    while (it_end < it1 && a.item_slice[it_end] == z) ++it_end;
     if constexpr (STAGED) {
-      const int z = a.item_slice[it];
       if (z != cur_slice) {
         __syncthreads();
         const int64_t lo64 = a.win_lo[z];
@@ -90,7 +93,7 @@ __global__ void __launch_bounds__(512, MINB) spmv_kernel(SpmvArgs a) {
         wl = (int)lo64;
       }
     }
-    const int64_t r0 = a.item_row[it], r1 = a.item_row[it + 1];
+    const int64_t r0 = a.item_row[it], r1 = a.item_row[it_end];
     int64_t row = r0 + grp;
     int64_t s_n = 0, e_n = 0;
     float b_n = 0.0f;
@@ -158,6 +161,7 @@ __global__ void __launch_bounds__(512, MINB) spmv_kernel(SpmvArgs a) {
       }
       row = nrow;
     }
+    it = it_end;
   }
   if (a.scal) {
     double v[1] = {sq};
@@ -205,8 +209,12 @@ __global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
   int cur_slice = -1;
   const float* gbase = a.src;
   double sq = 0.0;
-  for (int64_t it = it0; it < it1; ++it) {
+  // Rows of one slice segment (the CTA's items of one slice) are walked as one range: per-item
+  // rounds left groups idle whenever an item had fewer rows than the CTA has groups.
+  for (int64_t it = it0; it < it1;) {
     const int z = a.item_slice[it];
+    int64_t it_end = it + 1;
+    while (it_end < it1 && a.item_slice[it_end] == z) ++it_end;
     if (z != cur_slice) {
       const int64_t lo64 = a.win_lo[z];
       gbase = a.src + lo64;
@@ -218,7 +226,7 @@ __global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
       }
       cur_slice = z;
     }
-    const int64_t r0 = a.item_row[it], r1 = a.item_row[it + 1];
+    const int64_t r0 = a.item_row[it], r1 = a.item_row[it_end];
     int64_t row = r0 + grp;
     int64_t s_n = 0, e_n = 0;
     // b is prefetched with the next row's extent in the staged kernel (A pass -3% at c2); the
@@ -290,6 +298,7 @@ __global__ void __launch_bounds__(512, MINB) spmv16_kernel(SpmvArgs a) {
       }
       row = nrow;
     }
+    it = it_end;
   }
   if (a.scal) {
     double v[1] = {sq};
@@ -332,8 +341,12 @@ __global__ void __launch_bounds__(512, 2) spmv16p_kernel(SpmvArgs a) {
   int cur_slice = -1;
   const float* gbase = a.src;
   double sq = 0.0;
-  for (int64_t it = it0; it < it1; ++it) {
+  // Rows of one slice segment (the CTA's items of one slice) are walked as one range: per-item
+  // rounds left groups idle whenever an item had fewer rows than the CTA has groups.
+  for (int64_t it = it0; it < it1;) {
     const int z = a.item_slice[it];
+    int64_t it_end = it + 1;
+    while (it_end < it1 && a.item_slice[it_end] == z) ++it_end;
     if (z != cur_slice) {
       gbase = a.src + a.win_lo[z];
       if constexpr (STAGED) {
@@ -344,7 +357,7 @@ __global__ void __launch_bounds__(512, 2) spmv16p_kernel(SpmvArgs a) {
       }
       cur_slice = z;
     }
-    const int64_t r0 = a.item_row[it], r1 = a.item_row[it + 1];
+    const int64_t r0 = a.item_row[it], r1 = a.item_row[it_end];
     int64_t row = r0 + grp;
     int64_t s_n = 0, e_n = 0;
     float b_n = 0.0f;
@@ -410,6 +423,7 @@ __global__ void __launch_bounds__(512, 2) spmv16p_kernel(SpmvArgs a) {
       }
       row = nrow;
     }
+    it = it_end;
   }
   if (a.scal) {
     double v[1] = {sq};
