@@ -49,6 +49,12 @@ cudaError_t launch_spmv(const SpmvArgs& a, const SpmvVariant& v, int grid, int b
 cudaError_t launch_spmv16p(const SpmvArgs& a, const SpmvVariant& v, int grid, int block,
                            size_t smem, cudaStream_t st);
 int spmv16p_occupancy(const SpmvVariant& v, int block, size_t smem);
+// padded-row int32 kernel (global columns; rows on 4-entry boundaries, zero-padded)
+cudaError_t launch_spmv32p(const SpmvArgs& a, const SpmvVariant& v, int grid, int block,
+                           cudaStream_t st);
+int spmv32p_occupancy(const SpmvVariant& v, int block);
+cudaError_t launch_pad_rows32(int64_t m, const int64_t* rp, const int64_t* rpp, const int32_t* col,
+                              const float* val, int32_t* colp, float* valp, cudaStream_t st);
 cudaError_t launch_pad_rows(int64_t m, const int64_t* rp, const int64_t* rpp, const uint16_t* col16,
                             const float* val, uint16_t* col16p, float* valp, cudaStream_t st);
 int spmv_occupancy(const SpmvVariant& v, int block, size_t smem);

@@ -158,9 +158,11 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     if (pl.pad) {
       a.rp = pl.rpp;
       a.col16 = pl.col16p;
+      a.col = pl.col32p;
       a.val = pl.valp;
-      return launch_spmv16p(a, pl.v, (int)std::min<int64_t>(pl.pad_grid, std::max<int64_t>(1, a.nitems)),
-                            pl.block, pl.smem, p->stream);
+      const int g = (int)std::min<int64_t>(pl.pad_grid, std::max<int64_t>(1, a.nitems));
+      return pl.v.idx16 ? launch_spmv16p(a, pl.v, g, pl.block, pl.smem, p->stream)
+                        : launch_spmv32p(a, pl.v, g, pl.block, p->stream);
     }
     return launch_spmv(a, pl.v, (int)std::min<int64_t>(pl.grid, std::max<int64_t>(1, a.nitems)),
                        pl.block, pl.smem, p->stream);
@@ -225,8 +227,10 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
   if (pl.pad) {
     a.rp = pl.rpp;
     a.col16 = pl.col16p;
+    a.col = pl.col32p;
     a.val = pl.valp;
-    return launch_spmv16p(a, pl.v, pl.pad_grid, pl.block, pl.smem, p->stream);
+    return pl.v.idx16 ? launch_spmv16p(a, pl.v, pl.pad_grid, pl.block, pl.smem, p->stream)
+                      : launch_spmv32p(a, pl.v, pl.pad_grid, pl.block, p->stream);
   }
   return launch_spmv(a, pl.v, pl.grid, pl.block, pl.smem, p->stream);
 }
@@ -900,28 +904,44 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
                                p->stream));
   }
   TVR_CUDA(cudaStreamSynchronize(p->stream));
-  // ---- padded-row copies for the 16-bit kernel (TVR_SPMV_PAD=0 disables) ----
+  // ---- padded-row copies (TVR_SPMV_PAD=0 disables): 16-bit plans pad rows to 8 entries,
+  // int32 global-gather plans to 4; skipped when the copy would not fit in free device memory
   for (int which = 0; which < 2; ++which) {
     SpmvPlan& pl = which ? p->planT : p->planA;
-    if (!pl.v.idx16 || pl.v.parts || pl.tma.on || pl.flat.on || !env_int("TVR_SPMV_PAD", 1)) continue;
+    const bool p16 = pl.v.idx16, p32 = !pl.v.idx16 && !pl.staged;
+    if (!(p16 || p32) || pl.v.parts || pl.tma.on || pl.flat.on || !env_int("TVR_SPMV_PAD", 1)) continue;
+    const int q = p16 ? 8 : 4;  // chunk entries
     const int64_t rows = which ? n : m;
     std::vector<int64_t> rph(rows + 1), rpp(rows + 1);
     TVR_CUDA(cudaMemcpyAsync(rph.data(), which ? p->rpT : p->rp, sizeof(int64_t) * (rows + 1),
                              cudaMemcpyDeviceToHost, p->stream));
     TVR_CUDA(cudaStreamSynchronize(p->stream));
     rpp[0] = 0;
-    for (int64_t r = 0; r < rows; ++r) rpp[r + 1] = rpp[r] + (rph[r + 1] - rph[r] + 7) / 8 * 8;
-    const size_t cap = (size_t)rpp[rows] + 8 * 16 * 4 + 8;  // slack: chunks read past the last row
+    for (int64_t r = 0; r < rows; ++r) rpp[r + 1] = rpp[r] + (rph[r + 1] - rph[r] + q - 1) / q * q;
+    const size_t cap = (size_t)rpp[rows] + (size_t)q * 32 * 4 + 8;  // slack: chunks read past the last row
+    const size_t need = cap * (p16 ? 6 : 8) + sizeof(int64_t) * (rows + 1);
+    size_t fr = 0, tot = 0;
+    TVR_CUDA(cudaMemGetInfo(&fr, &tot));
+    if (need + ((size_t)1 << 30) > fr) continue;  // keep 1 GB of headroom
     TVR_TRY(upload(p, (void**)&pl.rpp, rpp.data(), sizeof(int64_t) * (rows + 1)));
-    TVR_TRY(dev_alloc(p, (void**)&pl.col16p, sizeof(uint16_t) * cap));
     TVR_TRY(dev_alloc(p, (void**)&pl.valp, sizeof(float) * cap));
-    TVR_CUDA(cudaMemsetAsync(pl.col16p, 0, sizeof(uint16_t) * cap, p->stream));
     TVR_CUDA(cudaMemsetAsync(pl.valp, 0, sizeof(float) * cap, p->stream));
-    TVR_CUDA(launch_pad_rows(rows, which ? p->rpT : p->rp, pl.rpp, which ? p->colT16 : p->col16,
-                             which ? p->valT : p->val, pl.col16p, pl.valp, p->stream));
+    if (p16) {
+      TVR_TRY(dev_alloc(p, (void**)&pl.col16p, sizeof(uint16_t) * cap));
+      TVR_CUDA(cudaMemsetAsync(pl.col16p, 0, sizeof(uint16_t) * cap, p->stream));
+      TVR_CUDA(launch_pad_rows(rows, which ? p->rpT : p->rp, pl.rpp, which ? p->colT16 : p->col16,
+                               which ? p->valT : p->val, pl.col16p, pl.valp, p->stream));
+      pl.pad_grid = std::min<int64_t>((int64_t)p->num_sms * spmv16p_occupancy(pl.v, pl.block, pl.smem),
+                                      std::max<int64_t>(1, pl.nitems));
+    } else {
+      TVR_TRY(dev_alloc(p, (void**)&pl.col32p, sizeof(int32_t) * cap));
+      TVR_CUDA(cudaMemsetAsync(pl.col32p, 0, sizeof(int32_t) * cap, p->stream));
+      TVR_CUDA(launch_pad_rows32(rows, which ? p->rpT : p->rp, pl.rpp, which ? p->colT : p->col,
+                                 which ? p->valT : p->val, pl.col32p, pl.valp, p->stream));
+      pl.pad_grid = std::min<int64_t>((int64_t)p->num_sms * spmv32p_occupancy(pl.v, pl.block),
+                                      std::max<int64_t>(1, pl.nitems));
+    }
     TVR_CUDA(cudaStreamSynchronize(p->stream));
-    pl.pad_grid = std::min<int64_t>((int64_t)p->num_sms * spmv16p_occupancy(pl.v, pl.block, pl.smem),
-                                    std::max<int64_t>(1, pl.nitems));
     pl.pad = true;
   }
   // the int32 columns are no longer read by any pass: release them (c3: 7.7 GB each)

@@ -80,7 +80,8 @@ struct SpmvPlan {
   bool pad = false;
   int pad_grid = 0;
   int64_t* rpp = nullptr;
-  uint16_t* col16p = nullptr;
+  uint16_t* col16p = nullptr;  // 16-bit plans
+  int32_t* col32p = nullptr;   // int32 global-gather plans
   float* valp = nullptr;
   int parts = 1, part_len = 0;       // slice-window parts (16-bit kernel)
   uint16_t* part_off = nullptr;      // (parts-1) x nrows

@@ -484,6 +484,136 @@ int spmv16p_occupancy(const SpmvVariant& v, int block, size_t smem) {
   return occ > 0 ? occ : 1;
 }
 
+// Padded-row int32 kernel (global columns: non-separable geometry or TVR_IDX16=0): rows start on
+// 4-entry boundaries, zero-padded, one select per 4-entry chunk (as spmv16p_kernel); gathers
+// from global memory (L1).
+template <int LPR, int UNR>
+__global__ void __launch_bounds__(512, 2) spmv32p_kernel(SpmvArgs a) {
+  const int lane = threadIdx.x & (LPR - 1);
+  const int grp = threadIdx.x / LPR;
+  const int ngrp = blockDim.x / LPR;
+  const int64_t it0 = (a.nitems * (int64_t)blockIdx.x) / gridDim.x;
+  const int64_t it1 = (a.nitems * (int64_t)(blockIdx.x + 1)) / gridDim.x;
+  double sq = 0.0;
+  // the CTA's whole item range is one row range (no slice windows in the global-gather kernel)
+  const int64_t r0 = it0 < it1 ? a.item_row[it0] : 0, r1 = it0 < it1 ? a.item_row[it1] : 0;
+  int64_t row = r0 + grp;
+  int64_t s_n = 0, e_n = 0;
+  if (row < r1) {
+    s_n = a.rp[row];
+    e_n = a.rp[row + 1];
+  }
+  for (int64_t base = r0; base < r1; base += ngrp) {
+    const bool valid = row < r1;
+    const int64_t s = s_n;
+    const int span = (int)(e_n - s_n);  // padded: a multiple of 4
+    const int64_t nrow = row + ngrp;
+    if (nrow < r1) {
+      s_n = a.rp[nrow];
+      e_n = a.rp[nrow + 1];
+    }
+    const int nch = valid ? (span + 4 * LPR - 1) / (4 * LPR) : 0;
+    const int lim = span - 4 * lane;
+    const int32_t* cp = a.col + s + 4 * lane;
+    const float* vp = a.val + s + 4 * lane;
+    double acc[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) acc[u] = 0.0;
+    int ch = 0;
+    auto chunk = [&](const int4 c, const float4 v) {
+      const double p0 = (double)v.x * (double)__ldg(a.src + c.x);
+      const double p1 = (double)v.y * (double)__ldg(a.src + c.y);
+      const double p2 = (double)v.z * (double)__ldg(a.src + c.z);
+      const double p3 = (double)v.w * (double)__ldg(a.src + c.w);
+      return (p0 + p1) + (p2 + p3);
+    };
+    for (; ch + UNR <= nch; ch += UNR) {
+      int4 c[UNR];
+      float4 v[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        c[u] = ld_stream_i4(cp + (ch + u) * 4 * LPR);
+        v[u] = ld_stream_f4(vp + (ch + u) * 4 * LPR);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const double t = chunk(c[u], v[u]);
+        acc[u] += ((ch + u) * 4 * LPR < lim) ? t : 0.0;
+      }
+    }
+    for (; ch < nch; ++ch) {
+      const double t = chunk(ld_stream_i4(cp + ch * 4 * LPR), ld_stream_f4(vp + ch * 4 * LPR));
+      acc[0] += (ch * 4 * LPR < lim) ? t : 0.0;
+    }
+#pragma unroll
+    for (int u = 1; u < UNR; ++u) acc[0] += acc[u];
+    const double accr = group_sum<LPR>(acc[0]);
+    if (valid && lane == 0) {
+      if (a.b) {
+        const double r = accr - (double)__ldg(a.b + row);
+        const float rh = (float)r;
+        a.out[row] = rh;
+        if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
+        sq += r * r;
+      } else {
+        a.out[row] = (float)accr;
+      }
+    }
+    row = nrow;
+  }
+  if (a.scal) {
+    double v[1] = {sq};
+    reduce_to_scalars<1>(v, a.partials, a.counter, a.scal);
+  }
+}
+
+__global__ void pad_rows32_kernel(int64_t m, const int64_t* rp, const int64_t* rpp, const int32_t* col,
+                                  const float* val, int32_t* colp, float* valp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < m; r += nw) {
+    const int64_t s = rp[r], len = rp[r + 1] - s, d = rpp[r], plen = rpp[r + 1] - d;
+    for (int64_t k = lane; k < plen; k += 32) {
+      colp[d + k] = k < len ? col[s + k] : 0;
+      valp[d + k] = k < len ? val[s + k] : 0.0f;
+    }
+  }
+}
+
+cudaError_t launch_pad_rows32(int64_t m, const int64_t* rp, const int64_t* rpp, const int32_t* col,
+                              const float* val, int32_t* colp, float* valp, cudaStream_t st) {
+  pad_rows32_kernel<<<1184, 256, 0, st>>>(m, rp, rpp, col, val, colp, valp);
+  return cudaGetLastError();
+}
+
+template <class F>
+static cudaError_t dispatch32p(const SpmvVariant& v, F&& f) {
+  if (v.lpr == 4) return f(spmv32p_kernel<4, 2>);
+  if (v.lpr == 8) return f(spmv32p_kernel<8, 2>);
+  if (v.lpr == 16) return f(spmv32p_kernel<16, 2>);
+  if (v.lpr == 32) return f(spmv32p_kernel<32, 2>);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_spmv32p(const SpmvArgs& a, const SpmvVariant& v, int grid, int block,
+                           cudaStream_t st) {
+  return dispatch32p(v, [&](auto k) -> cudaError_t {
+    cudaError_t e = ensure_smem_attr((const void*)k, 0);
+    if (e != cudaSuccess) return e;
+    k<<<grid, block, 0, st>>>(a);
+    return cudaGetLastError();
+  });
+}
+
+int spmv32p_occupancy(const SpmvVariant& v, int block) {
+  int occ = 0;
+  dispatch32p(v, [&](auto k) -> cudaError_t {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, block, 0);
+  });
+  return occ > 0 ? occ : 1;
+}
+
 // Window parts (opt-in, TVR_PART_CAP): a slice window larger than the shared-memory budget is
 // cut into `parts` pieces of part_len entries.  Columns ascend within a row, so each row's
 // entries are contiguous per part; part_off[(p-1) nrows + row] is the row-relative start of
