@@ -7,9 +7,10 @@ One step = one gradient evaluation (f, grad f) of the smoothed TV objective thro
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
 
-N > 1 (torchrun): the volume is split into z-slabs (strong scaling); every step exchanges one
-halo slice with each z-neighbour and all-gathers the fp64 scalars over NCCL.  Timing is CUDA
-events on the library's stream, max over ranks.
+N > 1 (torchrun): weak scaling over z-slabs: every GPU holds one full c2-sized slab of a volume
+N times taller (harness.weak_slab), every step exchanges one halo slice with each z-neighbour and
+all-gathers the fp64 scalars over NCCL; value = c2-sized gradient evaluations per second summed
+over GPUs.  Timing is CUDA events on the library's stream, max over ranks.
 """
 from __future__ import annotations
 
@@ -162,22 +163,26 @@ def run_ours(args, rank, world, local_rank):
 
     import harness
     from paper_1105_4002_b200 import tvreg
-    from paper_1105_4002_b200.dist import local_slab, nccl_comm_from_process_group
+    from paper_1105_4002_b200.dist import nccl_comm_from_process_group
 
     torch.cuda.set_device(local_rank)
-    w = harness.preset(args.config)
     stream = torch.cuda.current_stream()
     comm = None
     if world > 1:
-        sl = local_slab(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, world, rank)
+        # Weak scaling over z-slabs: every rank holds one full c2-sized slab of
+        # a volume nz*world slices tall; the TV halo exchange and the rank-ordered scalar sum are
+        # the real data-path collectives.  value = c2-sized gradient evaluations per second,
+        # summed over ranks.
+        sl = harness.weak_slab(args.config, world, rank)
         comm = nccl_comm_from_process_group(world, rank, local_rank)
-        P = tvreg.Problem(sl.row_ptr, sl.col, sl.val, sl.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
-                          n_cols=w.N, world=world, rank=rank, z0=sl.z0, z1=sl.z1, nccl_comm=comm,
+        N = sl.grid[0] * sl.grid[1] * sl.grid[2]
+        P = tvreg.Problem(sl.row_ptr, sl.col, sl.val, sl.b, sl.grid, sl.alpha, sl.tau, sl.lo, sl.hi,
+                          n_cols=N, world=world, rank=rank, z0=sl.z0, z1=sl.z1, nccl_comm=comm,
                           device=local_rank, stream=stream.cuda_stream)
-        xfull = harness.random_x(w.N)
-        plane = w.grid[0] * w.grid[1]
-        x_h = np.ascontiguousarray(xfull[sl.z0 * plane:sl.z1 * plane])
+        x_h = harness.random_x(P.n)
+        w = harness.preset(args.config) if rank == 0 else None  # rank 0: config text only
     else:
+        w = harness.preset(args.config)
         P = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
                           device=local_rank, stream=stream.cuda_stream)
         x_h = harness.random_x(w.N)
@@ -230,7 +235,9 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = args.steps / (ms_total / 1e3)   # whole-volume gradient evaluations per second
+    # gradient evaluations of c2-sized volumes per second over the whole job (weak scaling:
+    # world slabs per step)
+    value = world * args.steps / (ms_total / 1e3)
 
     # ---- e2e through the host API: H2D x, D2H g and f inside the timed region
     xh = torch.from_numpy(x_h.copy()).pin_memory()
@@ -250,7 +257,7 @@ def run_ours(args, rank, world, local_rank):
     te = torch.tensor([max(h0.elapsed_time(h1), wall * 1e3)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e = dict(value=args.steps / (float(te.item()) / 1e3), unit=UNIT,
+    e2e = dict(value=world * args.steps / (float(te.item()) / 1e3), unit=UNIT,
                h2d_bytes_per_step=int(4 * n_loc * world), d2h_bytes_per_step=int((4 * n_loc + 8) * world))
 
     # ---- roofline of the dominant kernel
@@ -278,9 +285,14 @@ def run_ours(args, rank, world, local_rank):
     out = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=ms_step, higher_is_better=True,
                ms_per_step_instrumented=ms_total_prof / args.steps,
-               scaling="strong" if world > 1 else "weak", vs_baseline=None, dtype="f64",
+               scaling="weak", vs_baseline=None, dtype="f64",
                storage_dtype="f32", data="synthetic",
-               config=dict(workload_desc(args.config, w), parallelism=f"zslab{world}" if world > 1 else "single"),
+               config=(dict(workload_desc(args.config, w),
+                            parallelism=f"zslab{world}" if world > 1 else "single",
+                            **({"weak_scaling": f"one {args.config} slab per GPU: volume "
+                                f"{w.grid[0]}x{w.grid[1]}x{w.grid[2] * world}, value = {args.config} "
+                                "gradient evaluations per second summed over GPUs"} if world > 1 else {}))
+                       if w is not None else {}),
                roofline=roofline, e2e=e2e, gpu_launches=int(launches), clocks=clk,
                kernels=ktab, step_hbm_gbs=step_bytes / (ms_step / 1e3) / 1e9,
                step_frac=step_bytes / (ms_step / 1e3) / 1e9 / peak)

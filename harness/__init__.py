@@ -223,6 +223,40 @@ def separable_workload(name: str, grid, views: int, bins: int, n_ell: int,
                     dict(kind="separable", views=views, bins=bins))
 
 
+@dataclass
+class SlabWorkload:
+    """One rank's part of a weak-scaled slice-separable workload: the preset's volume repeated
+    `world` times along z (global grid nx x ny x (nz world)); this rank owns slices [z0, z1) and
+    their rows, columns global."""
+    grid: tuple
+    z0: int
+    z1: int
+    row_ptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+    b: np.ndarray
+    alpha: float
+    tau: float
+    lo: float
+    hi: float
+
+
+def weak_slab(name: str, world: int, rank: int) -> SlabWorkload:
+    """Rank `rank`'s slab of preset `name` weak-scaled over `world` ranks (separable presets):
+    the phantom is drawn on the tall volume, the noise seed differs per rank."""
+    p = dict(PRESETS[name])
+    nx, ny, nz = p["grid"]
+    A = siddon_separable(nx, ny, nz, p["views"], p["bins"])
+    z0, z1 = rank * nz, (rank + 1) * nz
+    plane = nx * ny
+    xt = phantom(nx, ny, nz * world, p["n_ell"])[z0 * plane:z1 * plane]
+    b = simulate_data(A, xt, seed=SEED_NOISE + 1000 * rank)
+    col = (A.col.astype(np.int64) + z0 * plane).astype(np.int32)
+    return SlabWorkload((nx, ny, nz * world), z0, z1, A.row_ptr, col, A.val, b,
+                        p.get("alpha", 0.01), p.get("tau", 1e-4), p.get("lo", 0.0),
+                        p.get("hi", float("inf")))
+
+
 def preset(name: str, **over) -> Workload:
     p = dict(PRESETS[name])
     p.update(over)

@@ -245,3 +245,19 @@ def test_views_sharded_gradient_matches_unsharded(world):
     gs = np.concatenate([r[4] for r in res])
     assert gs.size == g.size
     assert np.allclose(gs, g, rtol=1e-12, atol=1e-12 * np.abs(g).max())
+
+
+def test_weak_slab_tiles_a_tall_volume():
+    """bench.py's weak scaling (harness.weak_slab): rank r owns slices [r nz, (r+1) nz) of a
+    volume world times taller, with the preset's slice matrix and global columns."""
+    w = harness.preset("c1")
+    nx, ny, nz = w.grid
+    plane = nx * ny
+    for world in (1, 2, 3):
+        for rank in range(world):
+            sl = harness.weak_slab("c1", world, rank)
+            assert sl.grid == (nx, ny, nz * world) and (sl.z0, sl.z1) == (rank * nz, (rank + 1) * nz)
+            assert np.array_equal(sl.row_ptr, w.A.row_ptr) and np.array_equal(sl.val, w.A.val)
+            assert np.array_equal(sl.col, w.A.col + rank * nz * plane)
+            assert sl.b.shape == (w.A.n_rows,)
+    assert np.array_equal(harness.weak_slab("c1", 1, 0).b, w.b)  # world 1: the c1 workload itself
