@@ -86,7 +86,8 @@ enum { TVR_SHARD_NONE = 0, TVR_SHARD_ZSLAB = 1, TVR_SHARD_VIEWS = 2 };
 typedef struct {
   int32_t world, rank, mode;
   int32_t z0, z1;
-  void* nccl_comm;   /* ncclComm_t or NULL (world == 1) */
+  void* nccl_comm;   /* communicator from tvr_nccl_comm_init / tvr_local_comm_create, or NULL
+                        (world == 1) */
   int32_t device;    /* CUDA device ordinal, or -1 for the current device */
   void* cuda_stream; /* cudaStream_t to order work on, or NULL for a library-created stream */
 } tvr_dist;
@@ -227,6 +228,13 @@ int64_t tvr_launch_count(const tvr_problem* p, int reset);
  * overrides. */
 enum { TVR_CONTROL_HOST = 0, TVR_CONTROL_DEVICE = 1, TVR_CONTROL_AUTO = 2 };
 int tvr_set_control(tvr_problem* p, int mode);
+
+/* In-process thread communicator (testing the multi-rank paths on one GPU): ranks are host
+ * threads of one process, each with its own tvr_problem (same or different devices); every
+ * collective is a host barrier, device-to-device copies from the peers' buffers and a second
+ * barrier.  Pass the handle as tvr_dist.nccl_comm of every rank.  Not a performance path. */
+int tvr_local_comm_create(void** comm_out, int world);
+int tvr_local_comm_destroy(void* comm);
 
 /* ---- NCCL bootstrap (z-slab mode) ---- */
 int tvr_nccl_unique_id_size(void);

@@ -1,15 +1,25 @@
-// Distribution over NCCL.  Both modes: one-slice halo exchange with each
-// z-neighbour (ncclSend/ncclRecv inside one group) and a rank-ordered fp64 scalar sum
-// (ncclAllGather of the partial scalars, then a fixed-order sum on the host, so every rank
-// sees bitwise-identical scalars and takes the same line-search / BT branch).
-// Trial and momentum points never need a halo exchange: their halo planes are recomputed
-// from the halo planes of their inputs with the stencil's own functors (bitwise equal to the
-// neighbour's stored values); only gradients are exchanged.
+// Distribution.  Both modes: one-slice halo exchange with each
+// z-neighbour and a rank-ordered fp64 scalar sum (all-gather of the partial scalars, then a
+// fixed-order sum on the host, so every rank sees bitwise-identical scalars and takes the same
+// line-search / BT branch).  Trial and momentum points never need a halo exchange: their halo
+// planes are recomputed from the halo planes of their inputs with the stencil's own functors
+// (bitwise equal to the neighbour's stored values); only gradients are exchanged.
 // VIEWS mode (P2, non-separable geometry) adds an all-gather of the point before every A pass
 // and a reduce-scatter of the full-volume A_p^T r_p after every A^T pass.
+//
+// Two communicator backends behind one handle (tvr_dist.nccl_comm):
+//  * NCCL (tvr_nccl_comm_init): one process per GPU over NVLink / NVSwitch, the product path;
+//  * an in-process thread communicator (tvr_local_comm_create): ranks are host threads of one
+//    process, possibly sharing one GPU; every collective is host barrier -> device-to-device
+//    copies from the peers' buffers -> host barrier.  No kernel ever waits on another rank, so
+//    ranks on one GPU cannot deadlock.  It exists to run the multi-rank library logic (halo
+//    planes, P2 gather / reduce-scatter, rank-ordered sums, distributed solvers) on the one-GPU
+//    boxes of this build; it is not a performance path.
 #include <nccl.h>
 
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -26,9 +36,94 @@ namespace tvr {
     }                                                                                   \
   } while (0)
 
+constexpr uint32_t kNcclMagic = 0x4e43434cu;   // "NCCL"
+constexpr uint32_t kLocalMagic = 0x4c4f434cu;  // "LOCL"
+
+struct CommBase {
+  uint32_t magic;
+};
+struct NcclComm : CommBase {
+  ncclComm_t c;
+};
+struct LocalComm : CommBase {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t generation = 0;
+  std::vector<const void*> ptr;   // per rank: published device pointer
+  std::vector<int64_t> val;       // per rank: published integers
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int64_t gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+
+__global__ void add_inplace_kernel(int64_t n, const float* __restrict__ a, float* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] += a[i];
+}
+static cudaError_t launch_add_inplace(int64_t n, const float* a, float* y, cudaStream_t st) {
+  add_inplace_kernel<<<592, 256, 0, st>>>(n, a, y);
+  return cudaGetLastError();
+}
+
+static ncclComm_t nccl_of(const tvr_problem* p) { return static_cast<NcclComm*>(p->comm)->c; }
+static LocalComm* local_of(const tvr_problem* p) {
+  auto* b = static_cast<CommBase*>(p->comm);
+  return (b && b->magic == kLocalMagic) ? static_cast<LocalComm*>(b) : nullptr;
+}
+
+bool valid_comm(const void* comm) {
+  if (!comm) return false;
+  const uint32_t m = static_cast<const CommBase*>(comm)->magic;
+  return m == kNcclMagic || m == kLocalMagic;
+}
+
+// Local backend: publish this rank's pointer, wait for all, run copy(peer pointers), wait again
+// (so no rank overwrites a published buffer before every peer has read it).
+template <class F>
+static int local_collective(tvr_problem* p, const void* mine, F&& copy) {
+  LocalComm* L = local_of(p);
+  TVR_CUDA(cudaStreamSynchronize(p->stream));  // this rank's data is complete
+  L->ptr[p->rank] = mine;
+  L->barrier();
+  const int st = copy(L->ptr);
+  cudaError_t e = cudaStreamSynchronize(p->stream);
+  L->barrier();
+  if (st < 0) return st;
+  if (e != cudaSuccess) { set_error(std::string("local collective: ") + cudaGetErrorString(e)); return TVR_E_CUDA; }
+  return TVR_OK;
+}
+
 int halo_exchange(tvr_problem* p, float* v) {
   if (p->world <= 1) return TVR_OK;
-  ncclComm_t comm = (ncclComm_t)p->comm;
+  const size_t bytes = sizeof(float) * (size_t)p->plane;
+  if (LocalComm* L = local_of(p)) {
+    (void)L;
+    return local_collective(p, v, [&](const std::vector<const void*>& peer) -> int {
+      if (p->rank > 0) {  // lower halo = last owned plane of rank - 1
+        const float* src = static_cast<const float*>(peer[p->rank - 1]);
+        const int nzl_lo = (int)p->peer_nzl[p->rank - 1];
+        TVR_CUDA(cudaMemcpyAsync(v - p->plane, src + (int64_t)(nzl_lo - 1) * p->plane, bytes,
+                                 cudaMemcpyDeviceToDevice, p->stream));
+      }
+      if (p->rank < p->world - 1) {  // upper halo = first owned plane of rank + 1
+        TVR_CUDA(cudaMemcpyAsync(v + (int64_t)p->nzl * p->plane, peer[p->rank + 1], bytes,
+                                 cudaMemcpyDeviceToDevice, p->stream));
+      }
+      return TVR_OK;
+    });
+  }
+  ncclComm_t comm = nccl_of(p);
   const size_t cnt = (size_t)p->plane;
   TVR_NCCL(ncclGroupStart());
   if (p->rank > 0) {
@@ -60,8 +155,16 @@ int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double 
 }
 
 int dist_sum_scalars(tvr_problem* p, double* vals, int n) {
-  ncclComm_t comm = (ncclComm_t)p->comm;
-  TVR_NCCL(ncclAllGather(p->dscal, p->dgather, (size_t)n, ncclDouble, comm, p->stream));
+  if (local_of(p)) {
+    TVR_TRY(local_collective(p, p->dscal, [&](const std::vector<const void*>& peer) -> int {
+      for (int r = 0; r < p->world; ++r)
+        TVR_CUDA(cudaMemcpyAsync(p->dgather + (size_t)r * n, peer[r], sizeof(double) * n,
+                                 cudaMemcpyDeviceToDevice, p->stream));
+      return TVR_OK;
+    }));
+  } else {
+    TVR_NCCL(ncclAllGather(p->dscal, p->dgather, (size_t)n, ncclDouble, nccl_of(p), p->stream));
+  }
   double* all = p->hscal + 64;  // world x n staging after the first 64 slots
   TVR_CUDA(cudaMemcpyAsync(all, p->dgather, sizeof(double) * n * p->world, cudaMemcpyDeviceToHost,
                            p->stream));
@@ -75,6 +178,48 @@ int dist_sum_scalars(tvr_problem* p, double* vals, int n) {
   return TVR_OK;
 }
 
+// Every rank's slab [z0, z1), gathered once at create time (the halo exchange of the local
+// backend needs the lower neighbour's plane count; VIEWS mode needs every slab).
+int slab_table(tvr_problem* p) {
+  std::vector<int64_t> all(2 * p->world);
+  if (LocalComm* L = local_of(p)) {
+    L->val[2 * p->rank] = p->z0;
+    L->val[2 * p->rank + 1] = p->z1;
+    L->barrier();
+    for (int i = 0; i < 2 * p->world; ++i) all[i] = L->val[i];
+    L->barrier();
+  } else {
+    int64_t* d = nullptr;
+    TVR_CUDA(cudaMalloc(&d, sizeof(int64_t) * 2 * (p->world + 1)));
+    std::vector<int64_t> mine = {p->z0, p->z1};
+    cudaError_t e = cudaMemcpyAsync(d, mine.data(), sizeof(int64_t) * 2, cudaMemcpyHostToDevice,
+                                    p->stream);
+    ncclResult_t nr = ncclSuccess;
+    if (e == cudaSuccess) nr = ncclAllGather(d, d + 2, 2, ncclInt64, nccl_of(p), p->stream);
+    if (e == cudaSuccess && nr == ncclSuccess)
+      e = cudaMemcpyAsync(all.data(), d + 2, sizeof(int64_t) * 2 * p->world, cudaMemcpyDeviceToHost,
+                          p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    cudaFree(d);
+    if (nr != ncclSuccess) { set_error(std::string("slab table: ") + ncclGetErrorString(nr)); return TVR_E_NCCL; }
+    if (e != cudaSuccess) { set_error(std::string("slab table: ") + cudaGetErrorString(e)); return TVR_E_CUDA; }
+  }
+  p->slab_off.assign(p->world, 0);
+  p->slab_cnt.assign(p->world, 0);
+  p->peer_nzl.assign(p->world, 0);
+  for (int r = 0; r < p->world; ++r) {
+    const int64_t z0 = all[2 * r], z1 = all[2 * r + 1];
+    if (z0 != (r == 0 ? 0 : all[2 * r - 1]) || z1 <= z0 || (r == p->world - 1 && z1 != p->nz)) {
+      set_error("tvr_create: the ranks' slabs must tile [0, nz) in rank order");
+      return TVR_E_ARG;
+    }
+    p->slab_off[r] = z0 * p->plane;
+    p->slab_cnt[r] = (z1 - z0) * p->plane;
+    p->peer_nzl[r] = z1 - z0;
+  }
+  return TVR_OK;
+}
+
 // ---- VIEWS mode: rows split by projection views, volume vectors by z-slabs.
 bool views_dist(const tvr_problem* p) { return p->mode == TVR_SHARD_VIEWS && p->world > 1; }
 
@@ -84,54 +229,29 @@ static bool uniform_slabs(const tvr_problem* p) {
   return true;
 }
 
-// Every rank's slab [z0, z1), all-gathered once at create time; the slabs must tile [0, nz).
-int views_slab_table(tvr_problem* p) {
-  int64_t* d = nullptr;
-  TVR_CUDA(cudaMalloc(&d, sizeof(int64_t) * 2 * (p->world + 1)));
-  std::vector<int64_t> mine = {p->z0, p->z1}, all(2 * p->world);
-  cudaError_t e = cudaMemcpyAsync(d, mine.data(), sizeof(int64_t) * 2, cudaMemcpyHostToDevice,
-                                  p->stream);
-  ncclResult_t nr = ncclSuccess;
-  if (e == cudaSuccess)
-    nr = ncclAllGather(d, d + 2, 2, ncclInt64, (ncclComm_t)p->comm, p->stream);
-  if (e == cudaSuccess && nr == ncclSuccess)
-    e = cudaMemcpyAsync(all.data(), d + 2, sizeof(int64_t) * 2 * p->world, cudaMemcpyDeviceToHost,
-                        p->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
-  cudaFree(d);
-  if (nr != ncclSuccess) { set_error(std::string("slab table: ") + ncclGetErrorString(nr)); return TVR_E_NCCL; }
-  if (e != cudaSuccess) { set_error(std::string("slab table: ") + cudaGetErrorString(e)); return TVR_E_CUDA; }
-  p->slab_off.assign(p->world, 0);
-  p->slab_cnt.assign(p->world, 0);
-  for (int r = 0; r < p->world; ++r) {
-    const int64_t z0 = all[2 * r], z1 = all[2 * r + 1];
-    if (z0 != (r == 0 ? 0 : all[2 * r - 1]) || z1 <= z0 || (r == p->world - 1 && z1 != p->nz)) {
-      set_error("tvr_create: VIEWS slabs must tile [0, nz) in rank order");
-      return TVR_E_ARG;
-    }
-    p->slab_off[r] = z0 * p->plane;
-    p->slab_cnt[r] = (z1 - z0) * p->plane;
-  }
-  return TVR_OK;
-}
-
 // x_full[off_r : off_r + cnt_r] = slab of rank r, on every rank (the A pass needs the whole
-// point: a tilted ray crosses every slab).  Equal slabs: one ncclAllGather; ragged slabs: one
-// broadcast per rank inside a group.
+// point: a tilted ray crosses every slab).  NCCL: equal slabs one ncclAllGather, ragged slabs
+// one broadcast per rank inside a group.
 int gather_volume(tvr_problem* p, const float* slab, const float** full) {
   if (!views_dist(p)) {
     *full = slab;
     return TVR_OK;
   }
-  ncclComm_t comm = (ncclComm_t)p->comm;
-  if (uniform_slabs(p)) {
-    TVR_NCCL(ncclAllGather(slab, p->xfull, (size_t)p->slab_cnt[0], ncclFloat, comm, p->stream));
+  if (local_of(p)) {
+    TVR_TRY(local_collective(p, slab, [&](const std::vector<const void*>& peer) -> int {
+      for (int r = 0; r < p->world; ++r)
+        TVR_CUDA(cudaMemcpyAsync(p->xfull + p->slab_off[r], peer[r], sizeof(float) * p->slab_cnt[r],
+                                 cudaMemcpyDeviceToDevice, p->stream));
+      return TVR_OK;
+    }));
+  } else if (uniform_slabs(p)) {
+    TVR_NCCL(ncclAllGather(slab, p->xfull, (size_t)p->slab_cnt[0], ncclFloat, nccl_of(p), p->stream));
   } else {
     TVR_NCCL(ncclGroupStart());
     for (int r = 0; r < p->world; ++r) {
       float* dst = p->xfull + p->slab_off[r];
       TVR_NCCL(ncclBroadcast(r == p->rank ? (const void*)slab : (const void*)dst, dst,
-                             (size_t)p->slab_cnt[r], ncclFloat, r, comm, p->stream));
+                             (size_t)p->slab_cnt[r], ncclFloat, r, nccl_of(p), p->stream));
     }
     TVR_NCCL(ncclGroupEnd());
   }
@@ -139,19 +259,29 @@ int gather_volume(tvr_problem* p, const float* slab, const float** full) {
   return TVR_OK;
 }
 
-// slab = sum over ranks of full[off_rank : off_rank + cnt_rank] (fp32 sum inside NCCL; each
-// rank's partial A_p^T r_p already carries fp64-accumulated rows rounded once to fp32).
+// slab = sum over ranks of full[off_rank : off_rank + cnt_rank] (fp32 sums; each rank's partial
+// A_p^T r_p already carries fp64-accumulated rows rounded once to fp32).  NCCL: equal slabs one
+// ncclReduceScatter, ragged slabs one ncclReduce per rank; local backend: rank-order sum.
 int reduce_scatter_volume(tvr_problem* p, const float* full, float* slab) {
-  ncclComm_t comm = (ncclComm_t)p->comm;
+  if (local_of(p)) {
+    const int64_t cnt = p->slab_cnt[p->rank], off = p->slab_off[p->rank];
+    return local_collective(p, full, [&](const std::vector<const void*>& peer) -> int {
+      TVR_CUDA(cudaMemcpyAsync(slab, static_cast<const float*>(peer[0]) + off, sizeof(float) * cnt,
+                               cudaMemcpyDeviceToDevice, p->stream));
+      for (int r = 1; r < p->world; ++r)
+        TVR_CUDA(launch_add_inplace(cnt, static_cast<const float*>(peer[r]) + off, slab, p->stream));
+      return TVR_OK;
+    });
+  }
   if (uniform_slabs(p)) {
-    TVR_NCCL(ncclReduceScatter(full, slab, (size_t)p->slab_cnt[0], ncclFloat, ncclSum, comm,
+    TVR_NCCL(ncclReduceScatter(full, slab, (size_t)p->slab_cnt[0], ncclFloat, ncclSum, nccl_of(p),
                                p->stream));
   } else {
     TVR_NCCL(ncclGroupStart());
     for (int r = 0; r < p->world; ++r) {
       const float* src = full + p->slab_off[r];
       TVR_NCCL(ncclReduce(src, r == p->rank ? (void*)slab : (void*)src, (size_t)p->slab_cnt[r],
-                          ncclFloat, ncclSum, r, comm, p->stream));
+                          ncclFloat, ncclSum, r, nccl_of(p), p->stream));
     }
     TVR_NCCL(ncclGroupEnd());
   }
@@ -184,13 +314,41 @@ int tvr_nccl_comm_init(void** comm_out, const void* id, int world, int rank, int
   std::memcpy(&uid, id, sizeof(uid));
   ncclComm_t comm;
   TVR_NCCL(ncclCommInitRank(&comm, world, uid, rank));
-  *comm_out = (void*)comm;
+  auto* h = new NcclComm();
+  h->magic = kNcclMagic;
+  h->c = comm;
+  *comm_out = h;
   return TVR_OK;
 }
 
 int tvr_nccl_comm_destroy(void* comm) {
   if (!comm) return TVR_OK;
-  TVR_NCCL(ncclCommDestroy((ncclComm_t)comm));
+  auto* h = static_cast<NcclComm*>(comm);
+  if (h->magic != kNcclMagic) { set_error("tvr_nccl_comm_destroy: not an NCCL communicator"); return TVR_E_ARG; }
+  const ncclResult_t r = ncclCommDestroy(h->c);
+  h->magic = 0;
+  delete h;
+  if (r != ncclSuccess) { set_error(std::string("ncclCommDestroy: ") + ncclGetErrorString(r)); return TVR_E_NCCL; }
+  return TVR_OK;
+}
+
+int tvr_local_comm_create(void** comm_out, int world) {
+  if (!comm_out || world < 1) { set_error("tvr_local_comm_create: bad argument"); return TVR_E_ARG; }
+  auto* L = new LocalComm();
+  L->magic = kLocalMagic;
+  L->world = world;
+  L->ptr.assign(world, nullptr);
+  L->val.assign(2 * world, 0);
+  *comm_out = L;
+  return TVR_OK;
+}
+
+int tvr_local_comm_destroy(void* comm) {
+  if (!comm) return TVR_OK;
+  auto* L = static_cast<LocalComm*>(comm);
+  if (L->magic != kLocalMagic) { set_error("tvr_local_comm_destroy: not a local communicator"); return TVR_E_ARG; }
+  L->magic = 0;
+  delete L;
   return TVR_OK;
 }
 

@@ -730,8 +730,9 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
       set_error("tvr_create: unknown shard mode");
       return TVR_E_ARG;
     }
-    if (p->world > 1 && (p->mode == TVR_SHARD_NONE || !p->comm)) {
-      set_error("tvr_create: world > 1 needs ZSLAB or VIEWS mode and an NCCL communicator");
+    if (p->world > 1 && (p->mode == TVR_SHARD_NONE || !valid_comm(p->comm))) {
+      set_error("tvr_create: world > 1 needs ZSLAB or VIEWS mode and a communicator "
+                "(tvr_nccl_comm_init or tvr_local_comm_create)");
       return TVR_E_ARG;
     }
     if (p->rank < 0 || p->rank >= p->world) { set_error("tvr_create: bad rank"); return TVR_E_ARG; }
@@ -809,6 +810,8 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     TVR_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     p->own_stream = true;
   }
+  // every rank's slab bounds (the slabs must tile [0, nz) in rank order); collective
+  if (p->world > 1) TVR_TRY(slab_table(p));
 
   // ---- device copies (columns made slab-local) ----
   // Padding: 16-byte chunk loads and TMA bulk copies of whole 16-byte units may read up to 3
@@ -963,11 +966,8 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     p->dat.push_back(q);
   }
   if (views_dist(p)) {
-    // every rank's slab bounds, all-gathered from the callers' tvr_dist (the slabs must tile
-    // [0, nz) in rank order)
     TVR_TRY(dev_alloc(p, (void**)&p->xfull, sizeof(float) * p->ncol));
     TVR_TRY(dev_alloc(p, (void**)&p->wfull, sizeof(float) * p->ncol));
-    TVR_TRY(views_slab_table(p));
   }
   tv_set_grid(p->num_sms);
   const int64_t maxgrid = std::max<int64_t>({(int64_t)p->planA.grid, (int64_t)p->planT.grid,

@@ -156,7 +156,7 @@ struct tvr_problem {
   // A_p^T r_p before the reduce-scatter; per-rank slab offsets / sizes (elements)
   float* xfull = nullptr;
   float* wfull = nullptr;
-  std::vector<int64_t> slab_off, slab_cnt;
+  std::vector<int64_t> slab_off, slab_cnt, peer_nzl;  // every rank's slab (world > 1)
 
   // e2e pipeline of tvr_objective_grad_host (created on first use)
   cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -215,7 +215,8 @@ int dist_sum_scalars(tvr_problem* p, double* vals, int n);
 // VIEWS mode: the A pass's source (slab -> full volume, all-gathered) and the A^T pass's
 // target (full-volume partial -> slab, reduce-scattered); identity on one rank
 bool views_dist(const tvr_problem* p);
-int views_slab_table(tvr_problem* p);
+bool valid_comm(const void* comm);  // an NCCL or in-process thread communicator handle
+int slab_table(tvr_problem* p);     // every rank's slab, gathered at create time (collective)
 int gather_volume(tvr_problem* p, const float* slab, const float** full);
 int reduce_scatter_volume(tvr_problem* p, const float* full, float* slab);
 void resolve_pending_timings(tvr_problem* p);

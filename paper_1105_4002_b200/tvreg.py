@@ -137,6 +137,8 @@ SIGNATURES = {
     "tvr_nccl_comm_init": (ctypes.c_int, [ctypes.POINTER(c_vp), c_vp, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int]),
     "tvr_nccl_comm_destroy": (ctypes.c_int, [c_vp]),
+    "tvr_local_comm_create": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.c_int]),
+    "tvr_local_comm_destroy": (ctypes.c_int, [c_vp]),
     "tvr_set_allocator": (ctypes.c_int, [ALLOC_FN, FREE_FN, c_vp]),
     "tvr_last_error": (ctypes.c_char_p, []),
     "tvr_abi_version": (ctypes.c_int, []),
@@ -229,6 +231,18 @@ def nccl_comm_init(uid: bytes, world: int, rank: int, device: int) -> int:
 
 def nccl_comm_destroy(comm: int):
     _check(lib().tvr_nccl_comm_destroy(comm), "tvr_nccl_comm_destroy")
+
+
+def local_comm_create(world: int) -> int:
+    """In-process thread communicator: ranks are threads of this process (tests of the
+    multi-rank paths on one GPU; see include/libtvreg.h)."""
+    comm = c_vp()
+    _check(lib().tvr_local_comm_create(ctypes.byref(comm), world), "tvr_local_comm_create")
+    return comm.value
+
+
+def local_comm_destroy(comm: int):
+    _check(lib().tvr_local_comm_destroy(comm), "tvr_local_comm_destroy")
 
 
 # ----------------------------------------------------------------------- problem

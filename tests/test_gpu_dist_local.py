@@ -1,0 +1,140 @@
+"""Multi-rank library paths on one GPU: ranks are host threads sharing the
+in-process thread communicator (tvr_local_comm_create), each with its own tvr_problem on the
+same device.  Exercises the z-slab halo exchange, halo recomputation of trial / momentum points,
+the rank-ordered scalar sum, the VIEWS all-gather / reduce-scatter and the distributed solvers
+through the C ABI, against the one-rank problem."""
+import math
+import threading
+
+import numpy as np
+import pytest
+
+import harness
+from paper_1105_4002_b200.dist import local_slab, local_views
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tvreg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1105_4002_b200 import tvreg as T
+    return T
+
+
+def _run_ranks(world, fn):
+    """fn(rank) in `world` threads; re-raises the first failure."""
+    out, err = [None] * world, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    if err:
+        raise err[0]
+    return out
+
+
+def _separable():
+    return harness.separable_workload("t", (20, 18, 12), 9, 29, 3, alpha=0.02, tau=1e-2)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_zslab_gradient_equals_one_rank(tvreg, world):
+    w = _separable()
+    plane = w.grid[0] * w.grid[1]
+    x = harness.random_x(w.N)
+    P1 = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi)
+    g1 = torch.empty(w.N, device="cuda")
+    f1, _ = P1.objective_grad(torch.from_numpy(x).cuda(), g1)
+    comm = tvreg.local_comm_create(world)
+
+    def rank_fn(r):
+        sl = local_slab(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, world, r)
+        P = tvreg.Problem(sl.row_ptr, sl.col, sl.val, sl.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
+                          n_cols=w.N, world=world, rank=r, z0=sl.z0, z1=sl.z1, nccl_comm=comm)
+        xl = torch.from_numpy(np.ascontiguousarray(x[sl.z0 * plane:sl.z1 * plane])).cuda()
+        g = torch.empty(P.n, device="cuda")
+        f, _ = P.objective_grad(xl, g)
+        return sl.z0, f, g.cpu()
+
+    res = _run_ranks(world, rank_fn)
+    tvreg.local_comm_destroy(comm)
+    fs = [r[1] for r in res]
+    assert all(f == fs[0] for f in fs)                # every rank sees the same f
+    assert abs(fs[0] - f1) <= 1e-13 * abs(f1)         # rank-ordered partial sums
+    g = torch.cat([r[2] for r in sorted(res, key=lambda t: t[0])])
+    assert torch.equal(g, g1.cpu())                   # per-voxel results are the one-rank ones
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_views_gradient_matches_one_rank(tvreg, world):
+    grid, views = (14, 12, 10), 9
+    A = harness.siddon_tilted(*grid, views, 7, 17, 10.0)
+    b = harness.simulate_data(A, harness.phantom(*grid, 3))
+    x = harness.random_x(A.n_cols)
+    plane = grid[0] * grid[1]
+    P1 = tvreg.Problem(A.row_ptr, A.col, A.val, b, grid, 0.01, 1e-3)
+    g1 = torch.empty(A.n_cols, device="cuda")
+    f1, _ = P1.objective_grad(torch.from_numpy(x).cuda(), g1)
+    comm = tvreg.local_comm_create(world)
+
+    def rank_fn(r):
+        lv = local_views(A.row_ptr, A.col, A.val, b, grid, views, world, r)
+        P = tvreg.Problem(lv.row_ptr, lv.col, lv.val, lv.b, grid, 0.01, 1e-3, world=world, rank=r,
+                          z0=lv.z0, z1=lv.z1, nccl_comm=comm, shard="views")
+        xl = torch.from_numpy(np.ascontiguousarray(x[lv.z0 * plane:lv.z1 * plane])).cuda()
+        g = torch.empty(P.n, device="cuda")
+        f, _ = P.objective_grad(xl, g)
+        return lv.z0, f, g.cpu()
+
+    res = _run_ranks(world, rank_fn)
+    tvreg.local_comm_destroy(comm)
+    fs = [r[1] for r in res]
+    assert all(f == fs[0] for f in fs)
+    assert abs(fs[0] - f1) <= 1e-12 * abs(f1)
+    g = torch.cat([r[2] for r in sorted(res, key=lambda t: t[0])]).double()
+    # A^T r is summed over ranks in fp32: agreement to fp32 rounding
+    assert (g - g1.cpu().double()).norm() <= 1e-6 * g1.cpu().double().norm()
+
+
+@pytest.mark.parametrize("solver", ["gpbb", "upn"])
+def test_zslab_solvers_match_one_rank(tvreg, solver):
+    """The distributed solvers (host control, rank-ordered scalars) against the one-rank solve:
+    every rank takes the same branches; the objective and iterate agree to the scalar sums'
+    rounding (which can shift a line-search decision late in the run)."""
+    world = 2
+    w = _separable()
+    plane = w.grid[0] * w.grid[1]
+    P1 = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi)
+    x1 = torch.zeros(w.N, device="cuda")
+    r1 = getattr(P1, f"solve_{solver}")(x1, max_iters=5000, eps=1e-5)
+    comm = tvreg.local_comm_create(world)
+
+    def rank_fn(r):
+        sl = local_slab(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, world, r)
+        P = tvreg.Problem(sl.row_ptr, sl.col, sl.val, sl.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
+                          n_cols=w.N, world=world, rank=r, z0=sl.z0, z1=sl.z1, nccl_comm=comm)
+        x = torch.zeros(P.n, device="cuda")
+        res = getattr(P, f"solve_{solver}")(x, max_iters=5000, eps=1e-5)
+        return sl.z0, res, x.cpu()
+
+    out = _run_ranks(world, rank_fn)
+    tvreg.local_comm_destroy(comm)
+    its = [o[1].iters for o in out]
+    assert all(i == its[0] for i in its) and all(o[1].converged for o in out)
+    f = out[0][1].f
+    assert abs(f - r1.f) <= 1e-6 * abs(r1.f)
+    x = torch.cat([o[2] for o in sorted(out, key=lambda t: t[0])]).double()
+    assert (x - x1.cpu().double()).norm() <= 1e-3 * x1.cpu().double().norm()
+    assert 0.8 * r1.iters <= its[0] <= 1.25 * r1.iters
