@@ -730,12 +730,12 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
       set_error("tvr_create: unknown shard mode");
       return TVR_E_ARG;
     }
+    if (p->rank < 0 || p->rank >= p->world) { set_error("tvr_create: bad rank"); return TVR_E_ARG; }
     if (p->world > 1 && (p->mode == TVR_SHARD_NONE || !valid_comm(p->comm))) {
       set_error("tvr_create: world > 1 needs ZSLAB or VIEWS mode and a communicator "
                 "(tvr_nccl_comm_init or tvr_local_comm_create)");
       return TVR_E_ARG;
     }
-    if (p->rank < 0 || p->rank >= p->world) { set_error("tvr_create: bad rank"); return TVR_E_ARG; }
     if (p->world == 1 && (p->z0 != 0 || p->z1 != grid.nz) && p->mode == TVR_SHARD_VIEWS) {
       set_error("tvr_create: VIEWS mode on one rank owns every slice");
       return TVR_E_ARG;
