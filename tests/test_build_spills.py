@@ -1,0 +1,57 @@
+"""Register-spill guard for the hot kernels (build-level regression test, no GPU): the stencil and
+SpMV instantiations the passes launch must compile for sm_100a without spills (a spilling stencil
+ran 29 -> 37 us at c2 once, from a launch-bounds slip)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CSRC = os.path.join(ROOT, "paper_1105_4002_b200", "csrc")
+
+# (mangled-name pattern, spill bytes allowed)
+HOT = {
+    "tv.cu": [
+        (r"tv_kernelINS_8SrcPlainELi0ELi5EiE", 0),       # tvr_objective_grad: W1 | G
+        (r"tv_kernelINS_8SrcPlainELi0ELi69EiE", 16),     # solver gradient + stop test (12 B today)
+        (r"tv_kernelINS_8SrcPlainELi0ELi65EiE", 0),      # UPN stop test at x_{k+1}
+        (r"tv_kernelINS_11SrcMomentumELi0ELi15EiE", 0),  # UPN momentum point
+        (r"tv_kernelINS_8SrcTrialELi1ELi0EiE", 0),       # trial points
+        (r"tv_kernelINS_8SrcTrialELi1ELi32EiE", 0),
+        (r"tv_kernelINS_8SrcTrialELi1ELi64EiE", 0),
+    ],
+    "spmv.cu": [
+        (r"spmv16p_kernelILi8ELi3ELb1E", 0),   # c2 A pass
+        (r"spmv16p_kernelILi4ELi3ELb1E", 0),   # c2 A^T pass
+        (r"spmv16p_kernelILi8ELi2ELb0E", 0),   # c3 A pass (global gather)
+        (r"spmv32p_kernelILi4ELi2E", 0),       # non-separable
+        (r"spmv32p_kernelILi8ELi2E", 0),
+    ],
+}
+
+
+def _spills(src):
+    out = subprocess.run(
+        ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xptxas", "-v",
+         "-c", os.path.join(CSRC, src), "-o", os.devnull],
+        capture_output=True, text=True, check=True).stderr
+    res, cur = {}, None
+    for line in out.splitlines():
+        m = re.search(r"Compiling entry function '([^']+)'", line)
+        if m:
+            cur = m.group(1)
+        m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", line)
+        if m and cur:
+            res[cur] = int(m.group(1)) + int(m.group(2))
+    return res
+
+
+@pytest.mark.parametrize("src", sorted(HOT))
+def test_hot_kernels_do_not_spill(src):
+    sp = _spills(src)
+    for pat, allowed in HOT[src]:
+        hits = [k for k in sp if re.search(pat, k)]
+        assert hits, f"{pat} not compiled"
+        for k in hits:
+            assert sp[k] <= allowed, f"{k} spills {sp[k]} bytes"
