@@ -14,8 +14,8 @@ CSRC = os.path.join(ROOT, "paper_1105_4002_b200", "csrc")
 HOT = {
     "tv.cu": [
         (r"tv_kernelINS_8SrcPlainELi0ELi5EiE", 0),       # tvr_objective_grad: W1 | G
-        (r"tv_kernelINS_8SrcPlainELi0ELi69EiE", 16),     # solver gradient + stop test (12 B today)
-        (r"tv_kernelINS_8SrcPlainELi0ELi65EiE", 16),     # UPN stop test at x_{k+1} (12 B today)
+        (r"tv_kernelINS_8SrcPlainELi0ELi69EiE", 0),      # solver gradient + stop test
+        (r"tv_kernelINS_8SrcPlainELi0ELi65EiE", 0),      # UPN stop test at x_{k+1}
         (r"tv_kernelINS_11SrcMomentumELi0ELi15EiE", 0),  # UPN momentum point
         (r"tv_kernelINS_8SrcTrialELi1ELi0EiE", 0),       # trial points
         (r"tv_kernelINS_8SrcTrialELi1ELi32EiE", 0),
