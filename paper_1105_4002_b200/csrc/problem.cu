@@ -1110,7 +1110,19 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
   auto ev_in = [&](int c) { return p->pipe_ev[2 + c]; };
   auto ev_g = [&](int c) { return p->pipe_ev[2 + 16 + c]; };
   std::vector<int> z(C + 1);
-  for (int c = 0; c <= C; ++c) z[c] = (int)((int64_t)nz * c / C);
+  // tapered chunks: the first chunk's upload and the last chunk's download are the exposed
+  // transfers, so the end chunks get half the weight of the middle ones (TVR_E2E_TAPER=0: equal)
+  {
+    const bool taper = env_int("TVR_E2E_TAPER", 1) != 0 && C > 2;
+    const double total = taper ? C - 1.0 : (double)C;
+    double acc = 0.0;
+    z[0] = 0;
+    for (int c = 0; c < C; ++c) {
+      acc += (taper && (c == 0 || c == C - 1)) ? 0.5 : 1.0;
+      z[c + 1] = std::max(z[c] + 1, (int)std::lround(nz * acc / total));
+    }
+    z[C] = nz;
+  }
   constexpr int SA = 16, ST = 24;  // scalar slots: A chunk c at SA + c, stencil chunk c at ST + 6 c
   TVR_CUDA(cudaEventRecord(ev_start, p->stream));
   TVR_CUDA(cudaStreamWaitEvent(p->s_in, ev_start, 0));
@@ -1175,7 +1187,7 @@ int tvr_objective_grad_host(tvr_problem* p, const float* x_host, double* f_out, 
                             tvr_fparts* parts) {
   if (!p || !x_host) { set_error("tvr_objective_grad_host: NULL"); return TVR_E_ARG; }
   TVR_CUDA(cudaSetDevice(p->device));
-  const int C = std::min(env_int("TVR_E2E_CHUNKS", 2), std::min(6, p->nzl));  // 6: dscal slots
+  const int C = std::min(env_int("TVR_E2E_CHUNKS", 3), std::min(6, p->nzl));  // 6: dscal slots
   if (C > 1 && p->world == 1 && p->separable && !p->planA.tma.on && !p->planT.tma.on &&
       !p->planA.flat.on && !p->planT.flat.on && !p->planA.v.parts && !p->planT.v.parts &&
       pinned(x_host) && (!g_host || pinned(g_host)))
