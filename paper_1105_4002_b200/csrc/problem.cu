@@ -934,6 +934,16 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
       TVR_CUDA(cudaMemsetAsync(pl.col16p, 0, sizeof(uint16_t) * cap, p->stream));
       TVR_CUDA(launch_pad_rows(rows, which ? p->rpT : p->rp, pl.rpp, which ? p->colT16 : p->col16,
                                which ? p->valT : p->val, pl.col16p, pl.valp, p->stream));
+      // a staged window that fits one 512-thread CTA per SM only: one 1024-thread CTA instead
+      if (pl.staged && pl.block == 512 && spmv16p_occupancy(pl.v, 512, pl.smem) == 1 &&
+          env_int("TVR_SPMV_WIDE", 1)) {
+        SpmvVariant w = pl.v;
+        w.unroll = 2;
+        if (spmv16p_occupancy(w, 1024, pl.smem) >= 1 && (w.lpr == 4 || w.lpr == 8 || w.lpr == 16)) {
+          pl.v = w;
+          pl.block = 1024;
+        }
+      }
       pl.pad_grid = std::min<int64_t>((int64_t)p->num_sms * spmv16p_occupancy(pl.v, pl.block, pl.smem),
                                       std::max<int64_t>(1, pl.nitems));
     } else {

@@ -331,8 +331,8 @@ __device__ __forceinline__ double chunk8_sum(const int4 c, const float4 v0, cons
   return ((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
 }
 
-template <int LPR, int UNR, bool STAGED>
-__global__ void __launch_bounds__(512, 2) spmv16p_kernel(SpmvArgs a) {
+template <int LPR, int UNR, bool STAGED, int NT = 512>
+__global__ void __launch_bounds__(NT, 1024 / NT) spmv16p_kernel(SpmvArgs a) {
   extern __shared__ float stage[];
   const int lane = threadIdx.x & (LPR - 1);
   const int grp = threadIdx.x / LPR;
@@ -455,8 +455,17 @@ cudaError_t launch_pad_rows(int64_t m, const int64_t* rp, const int64_t* rpp, co
   return cudaGetLastError();
 }
 
+// block 512 (default), or 1024 for a staged plan whose window leaves room for one CTA per SM
+// only (c3 A^T: 131 KB), so 32 warps instead of 16 share the one window.
 template <class F>
-static cudaError_t dispatch16p(const SpmvVariant& v, F&& f) {
+static cudaError_t dispatch16p(const SpmvVariant& v, int block, F&& f) {
+  if (block == 1024) {
+    if (!v.staged) return cudaErrorInvalidValue;
+    if (v.lpr == 4 && v.unroll == 2) return f(spmv16p_kernel<4, 2, true, 1024>);
+    if (v.lpr == 8 && v.unroll == 2) return f(spmv16p_kernel<8, 2, true, 1024>);
+    if (v.lpr == 16 && v.unroll == 2) return f(spmv16p_kernel<16, 2, true, 1024>);
+    return cudaErrorInvalidValue;
+  }
 #define TVR_VP(L, U)                                                                   \
   if (v.lpr == L && v.unroll == U)                                                     \
     return v.staged ? f(spmv16p_kernel<L, U, true>) : f(spmv16p_kernel<L, U, false>);
@@ -467,7 +476,7 @@ static cudaError_t dispatch16p(const SpmvVariant& v, F&& f) {
 
 cudaError_t launch_spmv16p(const SpmvArgs& a, const SpmvVariant& v, int grid, int block,
                            size_t smem, cudaStream_t st) {
-  return dispatch16p(v, [&](auto k) -> cudaError_t {
+  return dispatch16p(v, block, [&](auto k) -> cudaError_t {
     cudaError_t e = ensure_smem_attr((const void*)k, smem);
     if (e != cudaSuccess) return e;
     k<<<grid, block, smem, st>>>(a);
@@ -477,7 +486,7 @@ cudaError_t launch_spmv16p(const SpmvArgs& a, const SpmvVariant& v, int grid, in
 
 int spmv16p_occupancy(const SpmvVariant& v, int block, size_t smem) {
   int occ = 0;
-  dispatch16p(v, [&](auto k) -> cudaError_t {
+  dispatch16p(v, block, [&](auto k) -> cudaError_t {
     ensure_smem_attr((const void*)k, smem);
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, block, smem);
   });
