@@ -36,6 +36,7 @@ struct SpmvVariant {
   int minb = 1;      // __launch_bounds__ min blocks per SM
   bool idx16 = false;  // 16-bit column offsets inside the staged slice window (6 B per entry)
   bool parts = false;  // (idx16, staged) window cut into parts: spmv16_parts_kernel
+  bool half = false;   // padded 16-bit kernel with the window's first part_len entries staged
 };
 cudaError_t launch_compress_cols(const SpmvArgs& a, const int32_t* col, uint16_t* col16, bool expand,
                                  int32_t* col_out, cudaStream_t st);

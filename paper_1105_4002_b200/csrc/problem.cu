@@ -565,6 +565,7 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
   pl.part_len = 0;
   int32_t maxlen = 0;
   for (int32_t l : win_len) maxlen = std::max(maxlen, l);
+  pl.max_win = maxlen;
   const bool want16 = separable && maxlen <= 65536 && env_int("TVR_IDX16", 1) != 0 &&
                       env_int("TVR_SPMV_TMA", 0) == 0;
   if (staged) {
@@ -934,6 +935,24 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
       TVR_CUDA(cudaMemsetAsync(pl.col16p, 0, sizeof(uint16_t) * cap, p->stream));
       TVR_CUDA(launch_pad_rows(rows, which ? p->rpT : p->rp, pl.rpp, which ? p->colT16 : p->col16,
                                which ? p->valT : p->val, pl.col16p, pl.valp, p->stream));
+      // a window too large for shared memory: stage its first part (leaving >= 80 KB of L1 for
+      // the streaming loads and the rest of the gathers), one 1024-thread CTA per SM
+      if (!pl.staged && env_int("TVR_SPMV_HALF", 1)) {
+        const int32_t maxlen = pl.max_win;
+        const int budget = env_int("TVR_SPMV_HALF_KB", 148) * 1024;
+        const int h = std::min<int>(maxlen, (int)((budget / 4) * 32 / 33) / 32 * 32);
+        SpmvVariant w = pl.v;
+        w.half = true;
+        w.unroll = 2;
+        const size_t sm = sizeof(float) * ((size_t)h + (size_t)h / 32 + 1);
+        if (h > 0 && maxlen > h && p->separable && (w.lpr == 4 || w.lpr == 8 || w.lpr == 16) &&
+            spmv16p_occupancy(w, 1024, sm) >= 1) {
+          pl.v = w;
+          pl.block = 1024;
+          pl.smem = sm;
+          pl.part_len = h;
+        }
+      }
       // a staged window that fits one 512-thread CTA per SM only: one 1024-thread CTA instead
       if (pl.staged && pl.block == 512 && spmv16p_occupancy(pl.v, 512, pl.smem) == 1 &&
           env_int("TVR_SPMV_WIDE", 1)) {

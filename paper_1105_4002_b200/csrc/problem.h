@@ -79,6 +79,7 @@ struct SpmvPlan {
   // padded-row copy for spmv16p_kernel (rows on 8-entry boundaries, zero pads)
   bool pad = false;
   int pad_grid = 0;
+  int32_t max_win = 0;  // largest slice window (entries)
   int64_t* rpp = nullptr;
   uint16_t* col16p = nullptr;  // 16-bit plans
   int32_t* col32p = nullptr;   // int32 global-gather plans

@@ -331,7 +331,25 @@ __device__ __forceinline__ double chunk8_sum(const int4 c, const float4 v0, cons
   return ((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
 }
 
-template <int LPR, int UNR, bool STAGED, int NT = 512>
+// Partly staged window (HALF): offsets below h come from shared memory, the rest from global
+// memory (L1) — for windows larger than shared memory (c3's 256 KB x-slice), so that part of the
+// gathers leaves the L1 tag / data pipe that global gathers saturate.
+__device__ __forceinline__ double chunk8_sum_part(const int4 c, const float4 v0, const float4 v1,
+                                                  const float* __restrict__ sm,
+                                                  const float* __restrict__ gbase, int h) {
+  const uint32_t cw[4] = {(uint32_t)c.x, (uint32_t)c.y, (uint32_t)c.z, (uint32_t)c.w};
+  const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+  double pr[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int cidx = (int)((cw[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+    const float xv = cidx < h ? sm[swz(cidx)] : __ldg(gbase + cidx);
+    pr[q] = (double)vv[q] * (double)xv;  // exact
+  }
+  return ((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
+}
+
+template <int LPR, int UNR, bool STAGED, int NT = 512, bool HALF = false>
 __global__ void __launch_bounds__(NT, 1024 / NT) spmv16p_kernel(SpmvArgs a) {
   extern __shared__ float stage[];
   const int lane = threadIdx.x & (LPR - 1);
@@ -352,7 +370,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16p_kernel(SpmvArgs a) {
       gbase = a.src + a.win_lo[z];
       if constexpr (STAGED) {
         __syncthreads();
-        const int len = a.win_len[z];
+        const int len = HALF ? min(a.win_len[z], a.part_len) : a.win_len[z];
         stage_window(stage, gbase, len);
         __syncthreads();
       }
@@ -397,7 +415,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16p_kernel(SpmvArgs a) {
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-          const double t = chunk8_sum<STAGED>(c[u], va[u], vb[u], stage, gbase);
+          const double t = HALF ? chunk8_sum_part(c[u], va[u], vb[u], stage, gbase, a.part_len)
+                                : chunk8_sum<STAGED>(c[u], va[u], vb[u], stage, gbase);
           acc[u] += ((ch + u) * 8 * LPR < lim) ? t : 0.0;
         }
       }
@@ -405,7 +424,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16p_kernel(SpmvArgs a) {
         const int4 c0 = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + ch * 8 * LPR));
         const float4 va0 = ld_stream_f4(vp + ch * 8 * LPR);
         const float4 vb0 = ld_stream_f4(vp + ch * 8 * LPR + 4);
-        const double t = chunk8_sum<STAGED>(c0, va0, vb0, stage, gbase);
+        const double t = HALF ? chunk8_sum_part(c0, va0, vb0, stage, gbase, a.part_len)
+                              : chunk8_sum<STAGED>(c0, va0, vb0, stage, gbase);
         acc[0] += (ch * 8 * LPR < lim) ? t : 0.0;
       }
 #pragma unroll
@@ -459,6 +479,12 @@ cudaError_t launch_pad_rows(int64_t m, const int64_t* rp, const int64_t* rpp, co
 // only (c3 A^T: 131 KB), so 32 warps instead of 16 share the one window.
 template <class F>
 static cudaError_t dispatch16p(const SpmvVariant& v, int block, F&& f) {
+  if (v.half) {  // partly staged window, one 1024-thread CTA per SM
+    if (v.lpr == 4) return f(spmv16p_kernel<4, 2, true, 1024, true>);
+    if (v.lpr == 8) return f(spmv16p_kernel<8, 2, true, 1024, true>);
+    if (v.lpr == 16) return f(spmv16p_kernel<16, 2, true, 1024, true>);
+    return cudaErrorInvalidValue;
+  }
   if (block == 1024) {
     if (!v.staged) return cudaErrorInvalidValue;
     if (v.lpr == 4 && v.unroll == 2) return f(spmv16p_kernel<4, 2, true, 1024>);

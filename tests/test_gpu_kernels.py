@@ -427,3 +427,34 @@ def test_objective_grad_host_pipeline(tvreg, c1, chunks, monkeypatch):
         assert abs(fh - f) <= 1e-13 * abs(f) and abs(tvh - tv) <= 1e-13 * abs(tv)
     fv, _ = P.objective_grad_host(xh.numpy(), None)  # value only
     assert abs(fv - f) <= 1e-13 * abs(f)
+
+
+@pytest.mark.parametrize("kb", ["4", "6"])
+def test_partly_staged_window_matches_staged(tvreg, kb, monkeypatch):
+    """Windows larger than shared memory stage their first part and gather the rest from global
+    memory (the c3 A pass); forced here on a small slice: results bitwise equal to the fully
+    staged kernel (same summation order) and to the oracle on dyadic data."""
+    grid = (48, 40, 5)
+    A = _dyadic_separable(*grid, 10, 61)
+    rng = np.random.default_rng(5)
+    x = rng.integers(0, 9, A.n_cols).astype(np.float32)
+    b = rng.integers(0, 9, A.n_rows).astype(np.float32)
+    outs = {}
+    for mode in ("staged", "half"):
+        monkeypatch.delenv("TVR_SPMV_STAGE", raising=False)
+        monkeypatch.delenv("TVR_SPMV_HALF_KB", raising=False)
+        if mode == "half":
+            monkeypatch.setenv("TVR_SPMV_STAGE", "0")
+            monkeypatch.setenv("TVR_SPMV_HALF_KB", kb)
+        P = make(tvreg, A, b, grid)
+        r = torch.empty(A.n_rows, device="cuda")
+        fid = P.residual(dev(x), r)
+        w = torch.empty(A.n_cols, device="cuda")
+        P.apply_AT(dev(b), w)
+        outs[mode] = (host(r).copy(), fid, host(w).copy())
+        P.close()
+    assert np.array_equal(outs["half"][0], outs["staged"][0])
+    assert np.array_equal(outs["half"][2], outs["staged"][2])
+    r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x.astype(np.float64)) - b
+    assert np.array_equal(outs["half"][0].astype(np.float64), r_ora)
+    assert outs["half"][1] == 0.5 * float(r_ora @ r_ora)
