@@ -458,3 +458,59 @@ def test_partly_staged_window_matches_staged(tvreg, kb, monkeypatch):
     r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x.astype(np.float64)) - b
     assert np.array_equal(outs["half"][0].astype(np.float64), r_ora)
     assert outs["half"][1] == 0.5 * float(r_ora @ r_ora)
+
+
+def test_objective_grad_c3_sampled(tvreg):
+    """BJ:9 workload (256^3, 1.9e9 entries) at full size in the bench's launch configuration
+    (padded 16-bit A with a partly staged window, A^T on one 1024-thread CTA per SM): sampled
+    outputs computed one by one in fp64 — rows of r = A x - b from A's rows, voxels of A^T r from
+    the slice matrix (A is block-diagonal by slice, C4), and the TV gradient from the oracle on a
+    5x5x5 neighbourhood (the 13-point stencil is local)."""
+    w = harness.preset("c3")
+    nx, ny, nz = w.grid
+    plane = nx * ny
+    x = harness.random_x(w.N)
+    P = make(tvreg, w.A, w.b, w.grid, w.alpha, w.tau)
+    g = torch.empty(w.N, device="cuda")
+    f, (fid, tv) = P.objective_grad(dev(x), g)
+    r = torch.empty(w.A.n_rows, device="cuda")
+    fid2 = P.residual(dev(x), r)
+    rh, gh = host(r), host(g)
+    rng = np.random.default_rng(9)
+    rp, col, val = w.A.row_ptr, w.A.col, w.A.val
+    xd = x.astype(np.float64)
+
+    def r_row(i):
+        s, e = rp[i], rp[i + 1]
+        return float(val[s:e].astype(np.float64) @ xd[col[s:e]]) - float(w.b[i])
+
+    for i in rng.integers(0, w.A.n_rows, 2000):
+        ri = r_row(i)
+        assert abs(rh[i] - ri) <= 1e-6 * (abs(ri) + 1e-3 * np.sqrt(2 * fid / w.A.n_rows))
+    # A^T r and the full gradient at sampled voxels: slice matrix S (rows v*bins + b) of slice z
+    S = harness.siddon_slice(nx, ny, w.geometry["views"], w.geometry["bins"]).to_scipy().tocsc()
+    ms = S.shape[0]
+    n_ok = 0
+    for j in rng.integers(0, w.N, 60):
+        z, jj = divmod(int(j), plane)
+        rows = S.indices[S.indptr[jj]:S.indptr[jj + 1]]
+        vals = S.data[S.indptr[jj]:S.indptr[jj + 1]].astype(np.float64)
+        wj = float(sum(v * r_row(z * ms + i) for v, i in zip(vals, rows)))
+        iz, iy, ix = z, jj // nx, jj % nx
+        lo = [max(0, c - 2) for c in (ix, iy, iz)]
+        hi = [min(n, c + 3) for c, n in zip((ix, iy, iz), (nx, ny, nz))]
+        sub = x.reshape(nz, ny, nx)[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
+        # the stencil at the centre reads u at the centre and one voxel below on each axis, i.e.
+        # x within +-1: a 5^3 crop reproduces it unless the centre sits on a cropped (not real)
+        # last face, where the oracle would apply the Neumann rule of C3
+        _, gsub = oracle.tv((sub.shape[2], sub.shape[1], sub.shape[0]), sub.ravel().astype(np.float64), w.tau)
+        c = (iz - lo[2], iy - lo[1], ix - lo[0])
+        gtv = gsub.reshape(sub.shape)[c]
+        ok = all((ci >= 1 or l == 0) and (s - 1 - ci >= 1 or h == n)
+                 for ci, l, h, s, n in zip(c[::-1], lo, hi, sub.shape[::-1], (nx, ny, nz)))
+        ref = wj + w.alpha * gtv
+        if ok:
+            assert abs(gh[j] - ref) <= 1e-5 * (abs(ref) + 1e-3), (j, gh[j], ref)
+            n_ok += 1
+    assert n_ok >= 50
+    assert abs(fid2 - fid) <= 1e-12 * fid
