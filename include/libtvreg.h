@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TVR_ABI_VERSION 2
+#define TVR_ABI_VERSION 3
 
 typedef enum {
   TVR_OK = 0,
@@ -108,6 +108,10 @@ typedef struct {
   int64_t device_bytes;                /* device memory held by the problem */
   int64_t n_cols_local;                /* columns of the local A (= rows of its A^T): N_local,
                                           or N in VIEWS mode */
+  int32_t views_fused_rs;              /* VIEWS mode: 1 if the A^T pass stores into the owners'
+                                          inboxes over peer memory (fused reduce-scatter), 0 if
+                                          it uses the collective reduce-scatter */
+  int32_t _pad0;
 } tvr_info;
 int tvr_get_info(const tvr_problem* p, tvr_info* info);
 

@@ -17,6 +17,7 @@
 //    boxes of this build; it is not a performance path.
 #include <nccl.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -286,6 +287,104 @@ int reduce_scatter_volume(tvr_problem* p, const float* full, float* slab) {
     TVR_NCCL(ncclGroupEnd());
   }
   return TVR_OK;
+}
+
+// Stream-ordered barrier: on return every rank's work enqueued before the barrier is complete
+// (NCCL: a one-int all-reduce on the stream; local: stream sync + host barrier).
+int dist_barrier(tvr_problem* p) {
+  if (p->world <= 1) return TVR_OK;
+  if (LocalComm* L = local_of(p)) {
+    TVR_CUDA(cudaStreamSynchronize(p->stream));
+    L->barrier();
+    return TVR_OK;
+  }
+  TVR_NCCL(ncclAllReduce(p->barrier_dev, p->barrier_dev, 1, ncclInt, ncclSum, nccl_of(p), p->stream));
+  return TVR_OK;
+}
+
+// Fused reduce-scatter of the VIEWS A^T pass: every rank owns an inbox with
+// one slot per rank; the A^T kernel of rank q stores row i (global voxel) into slot q of the
+// inbox of i's owner, directly through peer memory (NVLink), so the transfer happens inside the
+// kernel, row by row; the owner then sums its slots in rank order.  Pointers: local backend
+// from the shared process; NCCL backend via CUDA IPC handles all-gathered over NCCL.
+int setup_fused_rs(tvr_problem* p) {
+  const int W = p->world;
+  int64_t stride = 0;
+  for (int r = 0; r < W; ++r) stride = std::max(stride, p->slab_cnt[r]);
+  p->inbox_stride = stride;
+  TVR_TRY(dev_alloc(p, (void**)&p->inbox, sizeof(float) * (size_t)stride * W));
+  TVR_TRY(dev_alloc(p, (void**)&p->barrier_dev, 64));
+  TVR_CUDA(cudaMemsetAsync(p->barrier_dev, 0, 64, p->stream));
+  std::vector<float*> base(W, nullptr);
+  if (LocalComm* L = local_of(p)) {
+    TVR_CUDA(cudaStreamSynchronize(p->stream));
+    L->ptr[p->rank] = p->inbox;
+    L->barrier();
+    for (int r = 0; r < W; ++r) base[r] = (float*)L->ptr[r];
+    L->barrier();
+  } else {
+    cudaIpcMemHandle_t mine;
+    TVR_CUDA(cudaIpcGetMemHandle(&mine, p->inbox));
+    char* d = nullptr;
+    TVR_CUDA(cudaMalloc(&d, sizeof(cudaIpcMemHandle_t) * (W + 1)));
+    std::vector<cudaIpcMemHandle_t> all(W);
+    cudaError_t e = cudaMemcpyAsync(d, &mine, sizeof(mine), cudaMemcpyHostToDevice, p->stream);
+    ncclResult_t nr = ncclSuccess;
+    if (e == cudaSuccess)
+      nr = ncclAllGather(d, d + sizeof(mine), sizeof(mine), ncclChar, nccl_of(p), p->stream);
+    if (e == cudaSuccess && nr == ncclSuccess)
+      e = cudaMemcpyAsync(all.data(), d + sizeof(mine), sizeof(mine) * W, cudaMemcpyDeviceToHost,
+                          p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    cudaFree(d);
+    if (nr != ncclSuccess) { set_error(std::string("fused RS: ") + ncclGetErrorString(nr)); return TVR_E_NCCL; }
+    if (e != cudaSuccess) { set_error(std::string("fused RS: ") + cudaGetErrorString(e)); return TVR_E_CUDA; }
+    int ok = 1;
+    for (int r = 0; r < W && ok; ++r) {
+      if (r == p->rank) { base[r] = p->inbox; continue; }
+      void* q = nullptr;
+      if (cudaIpcOpenMemHandle(&q, all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+        break;
+      }
+      p->ipc_opened.push_back(q);
+      base[r] = (float*)q;
+    }
+    // every rank must take the same path: the fused mode only if all ranks mapped all peers
+    int* flag = p->barrier_dev + 1;
+    TVR_CUDA(cudaMemcpyAsync(flag, &ok, sizeof(int), cudaMemcpyHostToDevice, p->stream));
+    TVR_NCCL(ncclAllReduce(flag, flag, 1, ncclInt, ncclMin, nccl_of(p), p->stream));
+    TVR_CUDA(cudaMemcpyAsync(&ok, flag, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    TVR_CUDA(cudaStreamSynchronize(p->stream));
+    if (!ok) {  // no peer mapping somewhere: keep the NCCL reduce-scatter
+      dist_release(p);
+      return TVR_OK;
+    }
+  }
+  // store target for owner o: slot `rank` of o's inbox, shifted so the global row indexes it
+  std::vector<float*> tgt(W);
+  std::vector<int64_t> bounds(W + 1);
+  for (int o = 0; o < W; ++o) {
+    tgt[o] = base[o] + (int64_t)p->rank * stride - p->slab_off[o];
+    bounds[o] = p->slab_off[o];
+  }
+  bounds[W] = p->slab_off[W - 1] + p->slab_cnt[W - 1];
+  TVR_TRY(dev_alloc(p, (void**)&p->out_peer_dev, sizeof(float*) * W));
+  TVR_TRY(dev_alloc(p, (void**)&p->out_bounds_dev, sizeof(int64_t) * (W + 1)));
+  TVR_CUDA(cudaMemcpyAsync(p->out_peer_dev, tgt.data(), sizeof(float*) * W, cudaMemcpyHostToDevice,
+                           p->stream));
+  TVR_CUDA(cudaMemcpyAsync(p->out_bounds_dev, bounds.data(), sizeof(int64_t) * (W + 1),
+                           cudaMemcpyHostToDevice, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  p->fused_rs = true;
+  return TVR_OK;
+}
+
+void dist_release(tvr_problem* p) {
+  for (void* q : p->ipc_opened) cudaIpcCloseMemHandle(q);
+  p->ipc_opened.clear();
+  p->fused_rs = false;
 }
 
 }  // namespace tvr

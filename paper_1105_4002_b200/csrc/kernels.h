@@ -27,6 +27,12 @@ struct SpmvArgs {
   double* partials;
   unsigned* counter;
   double* scal;  // non-null: write 1/2-less sum r^2 to scal[0]
+  // fused reduce-scatter (VIEWS mode A^T pass, spmv32p_kernel): row i of the output goes to
+  // out_peer[o][i] for the owner o of i (out_bounds[o] <= i < out_bounds[o+1]); out_peer[o] is
+  // the owner's inbox slot of this rank, offset so that it is indexed by the global row
+  float* const* out_peer;
+  const int64_t* out_bounds;
+  int n_out;
 };
 
 struct SpmvVariant {
@@ -54,6 +60,8 @@ int spmv16p_occupancy(const SpmvVariant& v, int block, size_t smem);
 cudaError_t launch_spmv32p(const SpmvArgs& a, const SpmvVariant& v, int grid, int block,
                            cudaStream_t st);
 int spmv32p_occupancy(const SpmvVariant& v, int block);
+cudaError_t launch_inbox_sum(int64_t n, const float* inbox, int64_t stride, int world, float* out,
+                             cudaStream_t st);
 cudaError_t launch_pad_rows32(int64_t m, const int64_t* rp, const int64_t* rpp, const int32_t* col,
                               const float* val, int32_t* colp, float* valp, cudaStream_t st);
 cudaError_t launch_pad_rows(int64_t m, const int64_t* rp, const int64_t* rpp, const uint16_t* col16,

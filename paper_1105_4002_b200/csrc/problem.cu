@@ -120,6 +120,9 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
                           const float* b, float* out, double* scal) {
   SpmvArgs a;
   a.out_lo = nullptr;
+  a.out_peer = nullptr;
+  a.out_bounds = nullptr;
+  a.n_out = 0;
   a.rp = transposed ? p->rpT : p->rp;
   a.col = transposed ? p->colT : p->col;
   a.col16 = transposed ? p->colT16 : p->col16;
@@ -224,6 +227,11 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
   }
   SpmvArgs a = spmv_args(p, pl, transposed, src, b, out, scal);
   a.out_lo = out_lo;
+  if (transposed && p->fused_rs) {  // VIEWS A^T: rows stored into their owners' inboxes
+    a.out_peer = p->out_peer_dev;
+    a.out_bounds = p->out_bounds_dev;
+    a.n_out = p->world;
+  }
   if (pl.pad) {
     a.rp = pl.rpp;
     a.col16 = pl.col16p;
@@ -251,13 +259,23 @@ int pass_residual(tvr_problem* p, const float* x, float* r, int slot, float* r_l
 
 // w: a slab volume vector.  VIEWS mode computes the full-volume partial A_p^T r_p and
 // reduce-scatters it to the slabs.
+// w: a slab volume vector.  VIEWS mode computes the full-volume partial A_p^T r_p and
+// reduce-scatters it to the slabs: fused (the A^T kernel stores every row straight into its
+// owner's inbox over peer memory, the owner sums the inboxes in rank order) or through NCCL.
 int pass_AT(tvr_problem* p, const float* r, float* w) {
   float* dst = views_dist(p) ? p->wfull : w;
   const double bytes =
       entry_bytes(p->planT) * p->nnz + 8.0 * (p->ncol + 1) + 4.0 * p->m + 4.0 * p->ncol;
+  if (p->fused_rs) TVR_TRY(dist_barrier(p));  // every owner has consumed the previous inbox
   TVR_TRY(launch(p, K_SPMV_AT, bytes, [&] {
     return run_spmv(p, p->planT, true, r, nullptr, dst, nullptr, nullptr);
   }));
+  if (p->fused_rs) {
+    TVR_TRY(dist_barrier(p));  // every rank's stores into this rank's inbox are complete
+    TVR_CUDA(launch_inbox_sum(p->slab_cnt[p->rank], p->inbox, p->inbox_stride, p->world, w,
+                              p->stream));
+    return TVR_OK;
+  }
   if (views_dist(p)) TVR_TRY(reduce_scatter_volume(p, dst, w));
   return TVR_OK;
 }
@@ -997,6 +1015,9 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   if (views_dist(p)) {
     TVR_TRY(dev_alloc(p, (void**)&p->xfull, sizeof(float) * p->ncol));
     TVR_TRY(dev_alloc(p, (void**)&p->wfull, sizeof(float) * p->ncol));
+    // fused reduce-scatter: needs the padded int32 A^T kernel and peer-mapped inboxes
+    if (env_int("TVR_FUSED_RS", 1) && p->planT.pad && !p->planT.v.idx16)
+      TVR_TRY(setup_fused_rs(p));
   }
   tv_set_grid(p->num_sms);
   const int64_t maxgrid = std::max<int64_t>({(int64_t)p->planA.grid, (int64_t)p->planT.grid,
@@ -1020,6 +1041,7 @@ void tvr_destroy(tvr_problem* p) {
     cudaSetDevice(p->device);
     cudaStreamSynchronize(p->stream);
   }
+  dist_release(p);
   dev_free_all(p);
   for (auto e : p->pipe_ev) cudaEventDestroy(e);
   if (p->s_in) cudaStreamDestroy(p->s_in);
@@ -1063,6 +1085,8 @@ int tvr_get_info(const tvr_problem* p, tvr_info* info) {
   info->slab_staged_AT = p->planT.tma.on ? 2 : (p->planT.staged ? 1 : 0);
   info->device_bytes = p->device_bytes;
   info->n_cols_local = p->ncol;
+  info->views_fused_rs = p->fused_rs ? 1 : 0;
+  info->_pad0 = 0;
   return TVR_OK;
 }
 

@@ -158,6 +158,15 @@ struct tvr_problem {
   float* xfull = nullptr;
   float* wfull = nullptr;
   std::vector<int64_t> slab_off, slab_cnt, peer_nzl;  // every rank's slab (world > 1)
+  // fused reduce-scatter of the VIEWS A^T pass: this rank's inbox (world slots of inbox_stride
+  // floats), per-owner store targets (device array) and the owners' row bounds
+  bool fused_rs = false;
+  float* inbox = nullptr;
+  int64_t inbox_stride = 0;
+  float** out_peer_dev = nullptr;
+  int64_t* out_bounds_dev = nullptr;
+  std::vector<void*> ipc_opened;  // peer inboxes mapped with cudaIpcOpenMemHandle
+  int* barrier_dev = nullptr;
 
   // e2e pipeline of tvr_objective_grad_host (created on first use)
   cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -218,6 +227,9 @@ int dist_sum_scalars(tvr_problem* p, double* vals, int n);
 bool views_dist(const tvr_problem* p);
 bool valid_comm(const void* comm);  // an NCCL or in-process thread communicator handle
 int slab_table(tvr_problem* p);     // every rank's slab, gathered at create time (collective)
+int setup_fused_rs(tvr_problem* p); // VIEWS: inboxes mapped on every peer (collective)
+int dist_barrier(tvr_problem* p);   // stream-ordered barrier over the ranks (collective)
+void dist_release(tvr_problem* p);  // unmap peer memory
 int gather_volume(tvr_problem* p, const float* slab, const float** full);
 int reduce_scatter_volume(tvr_problem* p, const float* full, float* slab);
 void resolve_pending_timings(tvr_problem* p);

@@ -590,6 +590,11 @@ __global__ void __launch_bounds__(512, 2) spmv32p_kernel(SpmvArgs a) {
         a.out[row] = rh;
         if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
         sq += r * r;
+      } else if (a.out_peer) {
+        // fused reduce-scatter: store straight into the owner's inbox (NVLink peer memory)
+        int o = 0;
+        while (o + 1 < a.n_out && row >= a.out_bounds[o + 1]) ++o;
+        a.out_peer[o][row] = (float)accr;
       } else {
         a.out[row] = (float)accr;
       }
@@ -600,6 +605,24 @@ __global__ void __launch_bounds__(512, 2) spmv32p_kernel(SpmvArgs a) {
     double v[1] = {sq};
     reduce_to_scalars<1>(v, a.partials, a.counter, a.scal);
   }
+}
+
+// Owner side of the fused reduce-scatter: out[i] = sum over ranks r (in rank order) of
+// inbox[r stride + i].
+__global__ void inbox_sum_kernel(int64_t n, const float* __restrict__ inbox, int64_t stride, int world,
+                                 float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = inbox[i];
+    for (int r = 1; r < world; ++r) acc += inbox[(int64_t)r * stride + i];
+    out[i] = acc;
+  }
+}
+
+cudaError_t launch_inbox_sum(int64_t n, const float* inbox, int64_t stride, int world, float* out,
+                             cudaStream_t st) {
+  inbox_sum_kernel<<<592, 256, 0, st>>>(n, inbox, stride, world, out);
+  return cudaGetLastError();
 }
 
 __global__ void pad_rows32_kernel(int64_t m, const int64_t* rp, const int64_t* rpp, const int32_t* col,

@@ -60,7 +60,8 @@ class tvr_dist(ctypes.Structure):
 class tvr_info(ctypes.Structure):
     _fields_ = [("m_local", c_i64), ("n_local", c_i64), ("nnz_local", c_i64), ("z0", c_i32),
                 ("z1", c_i32), ("slab_staged_A", c_i32), ("slab_staged_AT", c_i32),
-                ("device_bytes", c_i64), ("n_cols_local", c_i64)]
+                ("device_bytes", c_i64), ("n_cols_local", c_i64), ("views_fused_rs", c_i32),
+                ("_pad0", c_i32)]
 
 
 class tvr_fparts(ctypes.Structure):

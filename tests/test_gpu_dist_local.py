@@ -138,3 +138,35 @@ def test_zslab_solvers_match_one_rank(tvreg, solver):
     x = torch.cat([o[2] for o in sorted(out, key=lambda t: t[0])]).double()
     assert (x - x1.cpu().double()).norm() <= 1e-3 * x1.cpu().double().norm()
     assert 0.8 * r1.iters <= its[0] <= 1.25 * r1.iters
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_views_fused_reduce_scatter_matches_collective(tvreg, world, monkeypatch):
+    """VIEWS A^T with the fused reduce-scatter (the kernel stores each row into its owner's
+    inbox, the owner sums the inboxes in rank order) equals the collective reduce-scatter
+    bitwise (same fp32 sums in rank order), and the distributed gradient matches one rank."""
+    grid, views = (14, 12, 10), 9
+    A = harness.siddon_tilted(*grid, views, 7, 17, 10.0)
+    b = harness.simulate_data(A, harness.phantom(*grid, 3))
+    x = harness.random_x(A.n_cols)
+    plane = grid[0] * grid[1]
+    outs = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("TVR_FUSED_RS", fused)
+        comm = tvreg.local_comm_create(world)
+
+        def rank_fn(r):
+            lv = local_views(A.row_ptr, A.col, A.val, b, grid, views, world, r)
+            P = tvreg.Problem(lv.row_ptr, lv.col, lv.val, lv.b, grid, 0.01, 1e-3, world=world,
+                              rank=r, z0=lv.z0, z1=lv.z1, nccl_comm=comm, shard="views")
+            assert P.info.views_fused_rs == int(fused)
+            xl = torch.from_numpy(np.ascontiguousarray(x[lv.z0 * plane:lv.z1 * plane])).cuda()
+            g = torch.empty(P.n, device="cuda")
+            vals = [P.objective_grad(xl, g)[0] for _ in range(3)]  # repeated passes reuse inboxes
+            return lv.z0, vals, g.cpu()
+
+        res = _run_ranks(world, rank_fn)
+        tvreg.local_comm_destroy(comm)
+        outs[fused] = (res[0][1], torch.cat([r[2] for r in sorted(res, key=lambda t: t[0])]))
+    assert outs["1"][0] == outs["0"][0]
+    assert torch.equal(outs["1"][1], outs["0"][1])
