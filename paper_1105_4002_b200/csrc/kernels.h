@@ -68,6 +68,40 @@ cudaError_t launch_pad_rows(int64_t m, const int64_t* rp, const int64_t* rpp, co
                             const float* val, uint16_t* col16p, float* valp, cudaStream_t st);
 int spmv_occupancy(const SpmvVariant& v, int block, size_t smem);
 
+// Sliced-ELL SpMV over 16-bit window offsets (spmv.cu spmv16s_kernel): blocks of 32 rows sorted
+// by length inside a slice, chunk-interleaved, one row per lane.
+struct SellArgs {
+  const int64_t* blk_off;   // per block: first chunk step (a step = 32 lanes x 8 entries)
+  const int32_t* blk_k;     // per block: chunk steps (its longest row's chunks)
+  const int32_t* blk_slice; // per block: slice (window)
+  const int64_t* cum;       // nblk+1 prefix of per-block work (steps + 2)
+  const int32_t* perm;      // 32 per block: row of each lane, -1 for an empty lane
+  const uint16_t* col16;    // [step][lane][8] window offsets (zero pads)
+  const float* val;         // [step][lane][8] values (zero pads)
+  const float* src;
+  const float* b;           // non-null: out = A src - b, sum r^2
+  float* out;
+  float* out_lo;
+  int64_t blk_lo, blk_hi;   // blocks [blk_lo, blk_hi)
+  const int64_t* win_lo;
+  const int32_t* win_len;
+  int part_len;             // half: window entries staged
+  double* partials;
+  unsigned* counter;
+  double* scal;
+};
+struct SellVariant {
+  bool staged = true;
+  bool half = false;
+  int block = 512;
+};
+cudaError_t launch_spmv16s(const SellArgs& a, const SellVariant& v, int grid, size_t smem,
+                           cudaStream_t st);
+int spmv16s_occupancy(const SellVariant& v, size_t smem);
+cudaError_t launch_sell_fill(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
+                             const int64_t* rp, const uint16_t* col16, const float* val,
+                             uint16_t* col16s, float* vals, cudaStream_t st);
+
 // Row-agnostic SpMV (spmv_flat.cu): warps stream items as tiles of 32 x 8 entries with a
 // head-mask segmented reduction.
 struct FlatArgs {

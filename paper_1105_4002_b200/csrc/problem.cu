@@ -152,6 +152,32 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
 static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed, const float* src,
                             const float* b, float* out, float* out_lo, double* scal,
                             int64_t it_lo = 0, int64_t it_hi = -1) {
+  if (pl.sell) {  // blocks [it_lo, it_hi) (the e2e pipeline's chunks) or all
+    SellArgs s;
+    s.blk_off = pl.sell_off;
+    s.blk_k = pl.sell_k;
+    s.blk_slice = pl.sell_slice;
+    s.cum = pl.sell_cum;
+    s.perm = pl.sell_perm;
+    s.col16 = pl.col16p;
+    s.val = pl.valp;
+    s.src = src;
+    s.b = b;
+    s.out = out;
+    s.out_lo = out_lo;
+    s.blk_lo = it_hi >= 0 ? it_lo : 0;
+    s.blk_hi = it_hi >= 0 ? it_hi : pl.sell_nblk;
+    s.win_lo = pl.win_lo;
+    s.win_len = pl.win_len;
+    s.part_len = pl.part_len;
+    s.partials = p->partials;
+    s.counter = p->counter;
+    s.scal = scal;
+    if (s.blk_hi <= s.blk_lo && scal)  // nothing to sum: the pass still defines its scalar
+      return cudaMemsetAsync(scal, 0, sizeof(double), p->stream);
+    const int g = (int)std::min<int64_t>(pl.pad_grid, std::max<int64_t>(1, s.blk_hi - s.blk_lo));
+    return launch_spmv16s(s, pl.sv, g, pl.smem, p->stream);
+  }
   if (it_hi >= 0) {  // items [it_lo, it_hi) only (per-row kernels; the e2e pipeline's chunks)
     SpmvArgs a = spmv_args(p, pl, transposed, src, b, out, scal);
     a.out_lo = out_lo;
@@ -561,6 +587,91 @@ static int make_flat_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_
   return TVR_OK;
 }
 
+// Sliced-ELL copy (spmv16s_kernel, TVR_SPMV_SELL): per slice, rows stably sorted by 8-entry chunk
+// count (descending) in blocks of 32; replaces the padded copy.  Returns TVR_OK with pl.sell
+// unset when not applicable (no slice windows, too many rows, not enough device memory).
+static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::vector<int64_t>& rph,
+                     int64_t rows) {
+  pl.sell = false;
+  if (!pl.v.idx16 || rows >= ((int64_t)1 << 31) || pl.nitems == 0) return TVR_OK;
+  std::vector<int64_t> prow(pl.nitems + 1);
+  std::vector<int32_t> psl(pl.nitems);
+  TVR_CUDA(cudaMemcpy(prow.data(), pl.item_row, sizeof(int64_t) * (pl.nitems + 1), cudaMemcpyDeviceToHost));
+  TVR_CUDA(cudaMemcpy(psl.data(), pl.item_slice, sizeof(int32_t) * pl.nitems, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> off, cum(1, 0), zend(pl.h_slice_item_end.size(), 0);
+  std::vector<int32_t> kk, sl, perm, idx;
+  int64_t steps = 0;
+  for (int64_t i = 0; i < pl.nitems;) {
+    int64_t e = i + 1;
+    while (e < pl.nitems && psl[e] == psl[i]) ++e;
+    const int64_t R0 = prow[i], R1 = prow[e];
+    idx.resize(R1 - R0);
+    for (int64_t r = R0; r < R1; ++r) idx[r - R0] = (int32_t)r;
+    auto nch = [&](int32_t r) { return (rph[r + 1] - rph[r] + 7) / 8; };
+    std::stable_sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) { return nch(x) > nch(y); });
+    for (size_t j = 0; j < idx.size(); j += 32) {
+      const int64_t K = nch(idx[j]);
+      off.push_back(steps);
+      kk.push_back((int32_t)K);
+      sl.push_back(psl[i]);
+      cum.push_back(cum.back() + K + 2);
+      for (size_t l = 0; l < 32; ++l) perm.push_back(j + l < idx.size() ? idx[j + l] : -1);
+      steps += K;
+    }
+    if ((size_t)psl[i] < zend.size()) zend[psl[i]] = (int64_t)kk.size();
+    i = e;
+  }
+  for (size_t z = 1; z < zend.size(); ++z) zend[z] = std::max(zend[z], zend[z - 1]);
+  const int64_t nblk = (int64_t)kk.size();
+  const size_t cap = (size_t)steps * 256 + 8;
+  const size_t need = cap * 6 + (size_t)nblk * (8 + 4 + 4 + 8 + 128);
+  size_t fr = 0, tot = 0;
+  TVR_CUDA(cudaMemGetInfo(&fr, &tot));
+  if (need + ((size_t)1 << 30) > fr) return TVR_OK;  // keep 1 GB of headroom
+  TVR_TRY(upload(p, (void**)&pl.sell_off, off.data(), sizeof(int64_t) * off.size()));
+  TVR_TRY(upload(p, (void**)&pl.sell_k, kk.data(), sizeof(int32_t) * kk.size()));
+  TVR_TRY(upload(p, (void**)&pl.sell_slice, sl.data(), sizeof(int32_t) * sl.size()));
+  TVR_TRY(upload(p, (void**)&pl.sell_cum, cum.data(), sizeof(int64_t) * cum.size()));
+  TVR_TRY(upload(p, (void**)&pl.sell_perm, perm.data(), sizeof(int32_t) * perm.size()));
+  TVR_TRY(dev_alloc(p, (void**)&pl.valp, sizeof(float) * cap));
+  TVR_CUDA(cudaMemsetAsync(pl.valp, 0, sizeof(float) * cap, p->stream));
+  TVR_TRY(dev_alloc(p, (void**)&pl.col16p, sizeof(uint16_t) * cap));
+  TVR_CUDA(cudaMemsetAsync(pl.col16p, 0, sizeof(uint16_t) * cap, p->stream));
+  TVR_CUDA(launch_sell_fill(nblk * 32, pl.sell_perm, pl.sell_off, transposed ? p->rpT : p->rp,
+                            transposed ? p->colT16 : p->col16, transposed ? p->valT : p->val,
+                            pl.col16p, pl.valp, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));  // host vectors die here
+  pl.sell_nblk = nblk;
+  pl.h_slice_item_end = zend;
+  // variant: staged window; a window too large for shared memory: its first part staged
+  // (as the padded kernel's HALF); a staged window that fits one 512-thread CTA: 1024 threads
+  SellVariant v;
+  v.staged = pl.staged;
+  v.block = 512;
+  size_t smem = pl.staged ? pl.smem : 0;
+  if (!pl.staged && env_int("TVR_SPMV_HALF", 1)) {
+    const int budget = env_int("TVR_SPMV_HALF_KB", 148) * 1024;
+    const int h = std::min<int>(pl.max_win, (int)((budget / 4) * 32 / 33) / 32 * 32);
+    if (h > 0 && pl.max_win > h) {
+      v.staged = v.half = true;
+      v.block = 1024;
+      smem = sizeof(float) * ((size_t)h + (size_t)h / 32 + 1);
+      pl.part_len = h;
+    }
+  }
+  if (v.staged && !v.half && spmv16s_occupancy(v, smem) == 1 && env_int("TVR_SPMV_WIDE", 1)) {
+    SellVariant w = v;
+    w.block = 1024;
+    if (spmv16s_occupancy(w, smem) >= 1) v = w;
+  }
+  pl.sv = v;
+  pl.smem = smem;
+  pl.pad_grid = (int)std::min<int64_t>((int64_t)p->num_sms * spmv16s_occupancy(v, smem),
+                                       std::max<int64_t>(1, nblk));
+  pl.sell = true;
+  return TVR_OK;
+}
+
 // rp: host row pointer of the operator (n_rows+1); slices: n_slices+1 row boundaries when
 // separable; windows: per slice gather window (lo, len); pitch padding for the A pass.
 static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& rp, int64_t n_rows,
@@ -938,6 +1049,10 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     TVR_CUDA(cudaMemcpyAsync(rph.data(), which ? p->rpT : p->rp, sizeof(int64_t) * (rows + 1),
                              cudaMemcpyDeviceToHost, p->stream));
     TVR_CUDA(cudaStreamSynchronize(p->stream));
+    if (p16 && p->separable && env_int("TVR_SPMV_SELL", 1)) {
+      TVR_TRY(make_sell(p, pl, which == 1, rph, rows));
+      if (pl.sell) continue;
+    }
     rpp[0] = 0;
     for (int64_t r = 0; r < rows; ++r) rpp[r + 1] = rpp[r] + (rph[r + 1] - rph[r] + q - 1) / q * q;
     const size_t cap = (size_t)rpp[rows] + (size_t)q * 32 * 4 + 8;  // slack: chunks read past the last row

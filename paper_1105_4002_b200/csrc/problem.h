@@ -80,6 +80,15 @@ struct SpmvPlan {
   bool pad = false;
   int pad_grid = 0;
   int32_t max_win = 0;  // largest slice window (entries)
+  // sliced-ELL copy (spmv16s_kernel; replaces the padded copy when built): col16p / valp hold it
+  bool sell = false;
+  SellVariant sv;
+  int64_t sell_nblk = 0;
+  int64_t* sell_off = nullptr;
+  int32_t* sell_k = nullptr;
+  int32_t* sell_slice = nullptr;
+  int64_t* sell_cum = nullptr;
+  int32_t* sell_perm = nullptr;
   int64_t* rpp = nullptr;
   uint16_t* col16p = nullptr;  // 16-bit plans
   int32_t* col32p = nullptr;   // int32 global-gather plans

@@ -519,6 +519,147 @@ int spmv16p_occupancy(const SpmvVariant& v, int block, size_t smem) {
   return occ > 0 ? occ : 1;
 }
 
+// Sliced-ELL kernel (SELL-32-sigma, sigma = one slice): inside each slice the rows are sorted by
+// chunk count (descending, stable) and cut into blocks of 32 rows, one row per lane; a block's rows
+// are padded with zero chunks to its longest row and stored chunk-interleaved
+// ([block step][lane][8 entries]), so every warp load is 512 contiguous bytes, every lane walks
+// its own row with no masking and no cross-lane reduction, and the sorted order keeps the zero
+// padding to the rows that share a block with a longer one.  CTAs split the block range by
+// work (a prefix sum of steps + 2 per block); warps take blocks round-robin.
+__device__ __forceinline__ int64_t lower_bound_i64(const int64_t* __restrict__ a, int64_t lo,
+                                                   int64_t hi, int64_t key) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+template <int UNR, bool STAGED, int NT = 512, bool HALF = false>
+__global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
+  extern __shared__ float stage[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
+  const int64_t w0 = a.cum[a.blk_lo], W = a.cum[a.blk_hi] - w0;
+  const int64_t t0 = w0 + W * blockIdx.x / gridDim.x, t1 = w0 + W * (blockIdx.x + 1) / gridDim.x;
+  const int64_t b0 = lower_bound_i64(a.cum, a.blk_lo, a.blk_hi, t0);
+  const int64_t b1 = blockIdx.x + 1 == gridDim.x ? a.blk_hi : lower_bound_i64(a.cum, a.blk_lo, a.blk_hi, t1);
+  double sq = 0.0;
+  for (int64_t it = b0; it < b1;) {
+    const int z = a.blk_slice[it];
+    int64_t it_end = it + 1;
+    while (it_end < b1 && a.blk_slice[it_end] == z) ++it_end;
+    const float* gbase = a.src + a.win_lo[z];
+    if constexpr (STAGED) {
+      __syncthreads();
+      stage_window(stage, gbase, HALF ? min(a.win_len[z], a.part_len) : a.win_len[z]);
+      __syncthreads();
+    }
+    for (int64_t k = it + warp; k < it_end; k += nwarps) {
+      const int64_t off = a.blk_off[k];
+      const int K = a.blk_k[k];
+      const int row = a.perm[k * 32 + lane];
+      const uint16_t* cp = a.col16 + (off * 32 + lane) * 8;
+      const float* vp = a.val + (off * 32 + lane) * 8;
+      double acc = 0.0;
+      int s = 0;
+      for (; s + UNR <= K; s += UNR) {
+        int4 c[UNR];
+        float4 va[UNR], vb[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          c[u] = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + (s + u) * 256));
+          va[u] = ld_stream_f4(vp + (s + u) * 256);
+          vb[u] = ld_stream_f4(vp + (s + u) * 256 + 4);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          acc += HALF ? chunk8_sum_part(c[u], va[u], vb[u], stage, gbase, a.part_len)
+                      : chunk8_sum<STAGED>(c[u], va[u], vb[u], stage, gbase);
+      }
+      for (; s < K; ++s) {
+        const int4 c0 = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + s * 256));
+        const float4 va0 = ld_stream_f4(vp + s * 256);
+        const float4 vb0 = ld_stream_f4(vp + s * 256 + 4);
+        acc += HALF ? chunk8_sum_part(c0, va0, vb0, stage, gbase, a.part_len)
+                    : chunk8_sum<STAGED>(c0, va0, vb0, stage, gbase);
+      }
+      if (row >= 0) {
+        if (a.b) {
+          const double r = acc - (double)__ldg(a.b + row);
+          const float rh = (float)r;
+          a.out[row] = rh;
+          if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
+          sq += r * r;
+        } else {
+          a.out[row] = (float)acc;
+        }
+      }
+    }
+    it = it_end;
+  }
+  if (a.scal) {
+    double v[1] = {sq};
+    reduce_to_scalars<1>(v, a.partials, a.counter, a.scal);
+  }
+}
+
+template <class F>
+static cudaError_t dispatch16s(const SellVariant& v, F&& f) {
+  if (v.half) return v.block == 1024 ? f(spmv16s_kernel<2, true, 1024, true>)
+                                     : f(spmv16s_kernel<2, true, 512, true>);
+  if (v.staged) return v.block == 1024 ? f(spmv16s_kernel<2, true, 1024>)
+                                       : f(spmv16s_kernel<2, true, 512>);
+  return v.block == 1024 ? f(spmv16s_kernel<2, false, 1024>) : f(spmv16s_kernel<2, false, 512>);
+}
+
+cudaError_t launch_spmv16s(const SellArgs& a, const SellVariant& v, int grid, size_t smem,
+                           cudaStream_t st) {
+  if (a.blk_hi <= a.blk_lo) return cudaSuccess;
+  return dispatch16s(v, [&](auto k) -> cudaError_t {
+    cudaError_t e = ensure_smem_attr((const void*)k, smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, v.block, smem, st>>>(a);
+    return cudaGetLastError();
+  });
+}
+
+int spmv16s_occupancy(const SellVariant& v, size_t smem) {
+  int occ = 0;
+  dispatch16s(v, [&](auto k) -> cudaError_t {
+    ensure_smem_attr((const void*)k, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, v.block, smem);
+  });
+  return occ > 0 ? occ : 1;
+}
+
+// Sliced-ELL copy: lane l of block j holds row perm[32 j + l]; its entry e goes to chunk step
+// off_j + e / 8, lane l, position e % 8.  One thread per (block, lane); zero pads by memset.
+__global__ void sell_fill_kernel(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
+                                 const int64_t* rp, const uint16_t* col16, const float* val,
+                                 uint16_t* col16s, float* vals) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nslots) return;
+  const int row = perm[t];
+  if (row < 0) return;
+  const int64_t j = t >> 5, l = t & 31, s = rp[row], len = rp[row + 1] - s;
+  const int64_t base = blk_off[j];
+  for (int64_t e = 0; e < len; ++e) {
+    const int64_t d = ((base + (e >> 3)) * 32 + l) * 8 + (e & 7);
+    col16s[d] = col16[s + e];
+    vals[d] = val[s + e];
+  }
+}
+
+cudaError_t launch_sell_fill(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
+                             const int64_t* rp, const uint16_t* col16, const float* val,
+                             uint16_t* col16s, float* vals, cudaStream_t st) {
+  if (nslots <= 0) return cudaSuccess;
+  sell_fill_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(nslots, perm, blk_off, rp,
+                                                                    col16, val, col16s, vals);
+  return cudaGetLastError();
+}
+
 // Padded-row int32 kernel (global columns: non-separable geometry or TVR_IDX16=0): rows start on
 // 4-entry boundaries, zero-padded, one select per 4-entry chunk (as spmv16p_kernel); gathers
 // from global memory (L1).

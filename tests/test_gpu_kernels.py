@@ -323,6 +323,71 @@ def test_flat_spmv_variants(tvreg, cfg, c1, monkeypatch):
         assert np.array_equal(outs["flat"][0][empty], -b[empty])
 
 
+def _separable_zoo(nx, ny, nz, seed):
+    """Slice-major rows, each inside one z slice, of 0, 1, 2, 3, 7, 8, 9, 31, 255 and nx*ny
+    entries (capped at the slice), dyadic values: row-length mixes for the sliced-ELL blocks
+    (empty rows, partial last blocks, rows padded to a longer block neighbour)."""
+    rng = np.random.default_rng(seed)
+    plane = nx * ny
+    rp, cols, vals = [0], [], []
+    for z in range(nz):
+        lens = rng.permutation(np.repeat([0, 1, 2, 3, 7, 8, 9, 31, min(255, plane), plane], 5))
+        for L in lens:
+            c = z * plane + np.sort(rng.choice(plane, size=L, replace=False))
+            cols.extend(c.tolist())
+            vals.extend((rng.integers(1, 2049, size=L) / 1024.0).tolist())
+            rp.append(rp[-1] + L)
+    return SmallCSR(rp, cols, vals, plane * nz)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "ragged", "zoo", "zoo_global", "zoo_half"])
+def test_sell_spmv(tvreg, cfg, c1, monkeypatch):
+    """The sliced-ELL kernel (spmv16s_kernel; the default for slice-structured matrices) against
+    the oracle, for both passes: exact on dyadic data (every row length class, empty rows, partial
+    blocks; staged, global-gather and partly staged windows), fp32 rounding otherwise; and
+    against the padded per-row kernel (TVR_SPMV_SELL=0)."""
+    rng = np.random.default_rng(12)
+    if cfg == "c1":
+        A, grid = c1.A, c1.grid
+        x = harness.random_x(A.n_cols)
+        b = c1.b
+    elif cfg == "ragged":
+        A, grid = harness.siddon_separable(37, 29, 11, 13, 47), (37, 29, 11)
+        x = harness.random_x(A.n_cols)
+        b = rng.random(A.n_rows).astype(np.float32)
+    else:
+        grid = (16, 16, 4)
+        A = _separable_zoo(16, 16, 4, 5)
+        x = rng.integers(0, 9, A.n_cols).astype(np.float32)
+        b = rng.integers(0, 9, A.n_rows).astype(np.float32)
+    if cfg == "zoo_global":
+        monkeypatch.setenv("TVR_SPMV_STAGE", "0")
+        monkeypatch.setenv("TVR_SPMV_HALF", "0")
+    if cfg == "zoo_half":  # 1 KB budget: offsets >= 224 of the 256-entry window from global memory
+        monkeypatch.setenv("TVR_SPMV_STAGE", "0")
+        monkeypatch.setenv("TVR_SPMV_HALF_KB", "1")
+    r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x.astype(np.float64)) - b
+    w_ora = oracle.rmatvec(A.row_ptr, A.col, A.val, b.astype(np.float64), A.n_cols)
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("TVR_SPMV_SELL", mode)
+        P = make(tvreg, A, b, grid)
+        r = torch.empty(A.n_rows, device="cuda")
+        fid = P.residual(dev(x), r)
+        w = torch.empty(A.n_cols, device="cuda")
+        P.apply_AT(dev(b), w)
+        outs[mode] = (host(r).astype(np.float64), fid, host(w).astype(np.float64))
+        P.close()
+    r, fid, w = outs["1"]
+    if cfg.startswith("zoo"):
+        assert np.array_equal(r, r_ora) and np.array_equal(w, w_ora)
+        assert fid == 0.5 * float(r_ora @ r_ora)
+    else:
+        assert rel(r, r_ora) <= 1e-6 and rel(w, w_ora) <= 1e-6
+        assert abs(fid - 0.5 * float(r_ora @ r_ora)) <= 1e-6 * fid
+    assert rel(r, outs["0"][0]) <= 1e-7 and rel(w, outs["0"][2]) <= 1e-7
+
+
 @pytest.mark.parametrize("cap", [1024, 300, 128])
 def test_window_parts_match_oracle(tvreg, c1, cap, monkeypatch):
     """Slice windows cut into parts (the c3 A pass path): rows' entries split at part boundaries,
