@@ -74,8 +74,10 @@ struct SellArgs {
   const int64_t* blk_off;   // per block: first chunk step (a step = 32 lanes x 8 entries)
   const int32_t* blk_k;     // per block: chunk steps (its longest row's chunks)
   const int32_t* blk_slice; // per block: slice (window)
+  const int64_t* zend;      // per slice: one past its last block
   const int64_t* cum;       // nblk+1 prefix of per-block work (steps + 2)
   const int32_t* perm;      // 32 per block: row of each lane, -1 for an empty lane
+  double* blk_sq;           // per block: sum of its rows' r^2 (scratch, when scal)
   const uint16_t* col16;    // [step][lane][8] window offsets (zero pads)
   const float* val;         // [step][lane][8] values (zero pads)
   const float* src;
@@ -93,6 +95,8 @@ struct SellArgs {
 struct SellVariant {
   bool staged = true;
   bool half = false;
+  bool dyn = true;    // warps take blocks from a shared counter (else round-robin)
+  int unroll = 2;     // steps of loads in flight per lane
   int block = 512;
 };
 cudaError_t launch_spmv16s(const SellArgs& a, const SellVariant& v, int grid, size_t smem,

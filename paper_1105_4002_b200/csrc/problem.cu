@@ -157,6 +157,8 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     s.blk_off = pl.sell_off;
     s.blk_k = pl.sell_k;
     s.blk_slice = pl.sell_slice;
+    s.zend = pl.sell_zend;
+    s.blk_sq = pl.sell_sq;
     s.cum = pl.sell_cum;
     s.perm = pl.sell_perm;
     s.col16 = pl.col16p;
@@ -624,6 +626,9 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
   for (size_t z = 1; z < zend.size(); ++z) zend[z] = std::max(zend[z], zend[z - 1]);
   const int64_t nblk = (int64_t)kk.size();
   const size_t cap = (size_t)steps * 256 + 8;
+  const int64_t wcost = env_int("TVR_SELL_BLKCOST", 2);
+  if (wcost != 2)
+    for (int64_t j = 0; j < nblk; ++j) cum[j + 1] = cum[j] + kk[j] + wcost;
   const size_t need = cap * 6 + (size_t)nblk * (8 + 4 + 4 + 8 + 128);
   size_t fr = 0, tot = 0;
   TVR_CUDA(cudaMemGetInfo(&fr, &tot));
@@ -632,6 +637,8 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
   TVR_TRY(upload(p, (void**)&pl.sell_k, kk.data(), sizeof(int32_t) * kk.size()));
   TVR_TRY(upload(p, (void**)&pl.sell_slice, sl.data(), sizeof(int32_t) * sl.size()));
   TVR_TRY(upload(p, (void**)&pl.sell_cum, cum.data(), sizeof(int64_t) * cum.size()));
+  TVR_TRY(upload(p, (void**)&pl.sell_zend, zend.data(), sizeof(int64_t) * zend.size()));
+  TVR_TRY(dev_alloc(p, (void**)&pl.sell_sq, sizeof(double) * std::max<int64_t>(1, nblk)));
   TVR_TRY(upload(p, (void**)&pl.sell_perm, perm.data(), sizeof(int32_t) * perm.size()));
   TVR_TRY(dev_alloc(p, (void**)&pl.valp, sizeof(float) * cap));
   TVR_CUDA(cudaMemsetAsync(pl.valp, 0, sizeof(float) * cap, p->stream));
@@ -647,14 +654,17 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
   // (as the padded kernel's HALF); a staged window that fits one 512-thread CTA: 1024 threads
   SellVariant v;
   v.staged = pl.staged;
-  v.block = 512;
+  v.block = env_int("TVR_SELL_BLOCK", 512);
+  v.dyn = env_int("TVR_SELL_DYN", 1) != 0;
+  v.unroll = env_int("TVR_SELL_UNROLL", 2);
   size_t smem = pl.staged ? pl.smem : 0;
   if (!pl.staged && env_int("TVR_SPMV_HALF", 1)) {
     const int budget = env_int("TVR_SPMV_HALF_KB", 148) * 1024;
     const int h = std::min<int>(pl.max_win, (int)((budget / 4) * 32 / 33) / 32 * 32);
     if (h > 0 && pl.max_win > h) {
       v.staged = v.half = true;
-      v.block = 1024;
+      v.unroll = env_int("TVR_SELL_HALF_UNROLL", 2);
+      v.block = v.unroll == 3 ? 1024 : env_int("TVR_SELL_HALF_BLOCK", 1024);
       smem = sizeof(float) * ((size_t)h + (size_t)h / 32 + 1);
       pl.part_len = h;
     }

@@ -87,6 +87,8 @@ struct SpmvPlan {
   int64_t* sell_off = nullptr;
   int32_t* sell_k = nullptr;
   int32_t* sell_slice = nullptr;
+  int64_t* sell_zend = nullptr;
+  double* sell_sq = nullptr;
   int64_t* sell_cum = nullptr;
   int32_t* sell_perm = nullptr;
   int64_t* rpp = nullptr;

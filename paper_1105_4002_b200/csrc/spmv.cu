@@ -536,29 +536,51 @@ __device__ __forceinline__ int64_t lower_bound_i64(const int64_t* __restrict__ a
   return lo;
 }
 
-template <int UNR, bool STAGED, int NT = 512, bool HALF = false>
+template <int UNR, bool STAGED, int NT = 512, bool HALF = false, bool DYN = true>
 __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
   extern __shared__ float stage[];
+  __shared__ int s_next;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
   const int64_t w0 = a.cum[a.blk_lo], W = a.cum[a.blk_hi] - w0;
   const int64_t t0 = w0 + W * blockIdx.x / gridDim.x, t1 = w0 + W * (blockIdx.x + 1) / gridDim.x;
   const int64_t b0 = lower_bound_i64(a.cum, a.blk_lo, a.blk_hi, t0);
   const int64_t b1 = blockIdx.x + 1 == gridDim.x ? a.blk_hi : lower_bound_i64(a.cum, a.blk_lo, a.blk_hi, t1);
-  double sq = 0.0;
+  double sq = 0.0;  // static assignment: this thread's rows; DYN: the CTA's total (thread 0)
   for (int64_t it = b0; it < b1;) {
     const int z = a.blk_slice[it];
-    int64_t it_end = it + 1;
-    while (it_end < b1 && a.blk_slice[it_end] == z) ++it_end;
+    const int64_t it_end = min(b1, a.zend[z]);
     const float* gbase = a.src + a.win_lo[z];
-    if constexpr (STAGED) {
-      __syncthreads();
-      stage_window(stage, gbase, HALF ? min(a.win_len[z], a.part_len) : a.win_len[z]);
-      __syncthreads();
+    if (STAGED || DYN) __syncthreads();  // previous segment done: window and counter reusable
+    if (DYN && threadIdx.x == 0) s_next = nwarps;
+    if constexpr (STAGED) stage_window(stage, gbase, HALF ? min(a.win_len[z], a.part_len) : a.win_len[z]);
+    if (STAGED || DYN) __syncthreads();
+    // DYN: warps take the segment's blocks from a shared counter (blocks are sorted by length
+    // inside a slice, so this is longest-first list scheduling); the next block's descriptors are
+    // loaded while the current block streams
+    int64_t k = it + warp;
+    int64_t off = 0;
+    int K = 0, row = -1;
+    if (k < it_end) {
+      off = a.blk_off[k];
+      K = a.blk_k[k];
+      row = a.perm[k * 32 + lane];
     }
-    for (int64_t k = it + warp; k < it_end; k += nwarps) {
-      const int64_t off = a.blk_off[k];
-      const int K = a.blk_k[k];
-      const int row = a.perm[k * 32 + lane];
+    while (k < it_end) {
+      int64_t kn;
+      if constexpr (DYN) {
+        int nx = 0;
+        if (lane == 0) nx = atomicAdd(&s_next, 1);
+        kn = it + __shfl_sync(0xffffffffu, nx, 0);
+      } else {
+        kn = k + nwarps;
+      }
+      int64_t off_n = 0;
+      int K_n = 0, row_n = -1;
+      if (kn < it_end) {
+        off_n = a.blk_off[kn];
+        K_n = a.blk_k[kn];
+        row_n = a.perm[kn * 32 + lane];
+      }
       const uint16_t* cp = a.col16 + (off * 32 + lane) * 8;
       const float* vp = a.val + (off * 32 + lane) * 8;
       double acc = 0.0;
@@ -584,21 +606,45 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
         acc += HALF ? chunk8_sum_part(c0, va0, vb0, stage, gbase, a.part_len)
                     : chunk8_sum<STAGED>(c0, va0, vb0, stage, gbase);
       }
+      double q = 0.0;
       if (row >= 0) {
         if (a.b) {
           const double r = acc - (double)__ldg(a.b + row);
           const float rh = (float)r;
           a.out[row] = rh;
           if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
-          sq += r * r;
+          q = r * r;
         } else {
           a.out[row] = (float)acc;
         }
       }
+      if (a.scal) {
+        if constexpr (DYN) {  // per-block sum in a fixed lane order, summed in block order below
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) q += __shfl_xor_sync(0xffffffffu, q, d);
+          if (lane == 0) a.blk_sq[k] = q;
+        } else {
+          sq += q;
+        }
+      }
+      k = kn;
+      off = off_n;
+      K = K_n;
+      row = row_n;
     }
     it = it_end;
   }
   if (a.scal) {
+    if constexpr (DYN) {  // the CTA's blocks in block order: deterministic whatever warp ran them
+      __syncthreads();
+      if (warp == 0) {
+        double t = 0.0;
+        for (int64_t k = b0 + lane; k < b1; k += 32) t += a.blk_sq[k];
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+        if (lane == 0) sq = t;
+      }
+    }
     double v[1] = {sq};
     reduce_to_scalars<1>(v, a.partials, a.counter, a.scal);
   }
@@ -606,6 +652,18 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
 
 template <class F>
 static cudaError_t dispatch16s(const SellVariant& v, F&& f) {
+  if (!v.dyn) {
+    if (v.half) return f(spmv16s_kernel<2, true, 1024, true, false>);
+    if (v.staged) return v.block == 1024 ? f(spmv16s_kernel<3, true, 1024, false, false>)
+                                         : f(spmv16s_kernel<3, true, 512, false, false>);
+    return f(spmv16s_kernel<3, false, 512, false, false>);
+  }
+  if (v.unroll == 3) {
+    if (v.half) return f(spmv16s_kernel<3, true, 1024, true>);
+    if (v.staged) return v.block == 1024 ? f(spmv16s_kernel<3, true, 1024>)
+                                         : f(spmv16s_kernel<3, true, 512>);
+    return v.block == 1024 ? f(spmv16s_kernel<3, false, 1024>) : f(spmv16s_kernel<3, false, 512>);
+  }
   if (v.half) return v.block == 1024 ? f(spmv16s_kernel<2, true, 1024, true>)
                                      : f(spmv16s_kernel<2, true, 512, true>);
   if (v.staged) return v.block == 1024 ? f(spmv16s_kernel<2, true, 1024>)

@@ -22,7 +22,10 @@ HOT = {
         (r"tv_kernelINS_8SrcTrialELi1ELi64EiE", 0),
     ],
     "spmv.cu": [
-        (r"spmv16p_kernelILi8ELi3ELb1E", 0),   # c2 A pass
+        (r"spmv16s_kernelILi2ELb1ELi512ELb0ELb1E", 0),   # sliced ELL: c2 A and A^T passes
+        (r"spmv16s_kernelILi2ELb1ELi1024ELb0ELb1E", 0),  # c3 A^T pass (wide CTA)
+        (r"spmv16s_kernelILi2ELb1ELi1024ELb1ELb1E", 0),  # c3 A pass (partly staged window)
+        (r"spmv16p_kernelILi8ELi3ELb1E", 0),   # padded per-row kernel (TVR_SPMV_SELL=0)
         (r"spmv16p_kernelILi4ELi3ELb1E", 0),   # c2 A^T pass
         (r"spmv16p_kernelILi8ELi2ELb0E", 0),   # c3 A pass (global gather)
         (r"spmv32p_kernelILi4ELi2E", 0),       # non-separable
