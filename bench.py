@@ -300,6 +300,7 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_solve:
         out["solvers"] = solver_timings(tvreg, torch)
         out["c3_gradient"] = large_config_line(tvreg, torch)
+        out["sliced"] = sliced_lines(tvreg, torch)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(w)
     P.close()
@@ -364,6 +365,49 @@ def large_config_line(tvreg, torch, cfg="c3", steps=10):
                ms_per_step=ms, steps=steps, kernels=kt)
     P.close()
     return res
+
+
+def sliced_lines(tvreg, torch, configs=("c2", "c3"), steps=20):
+    """f4: the slice-shared operator (tvr_create_sliced: one slice's matrix applied
+    to every slice) on the same c2 / c3 problems; gradient evaluations per second, the device
+    memory it needs against the stored operator's, and a UPN time-to-eps at c2.  Context beside
+    the headline, which stays the stored-CSR contract (BJ:5)."""
+    import harness
+    out = {}
+    stream = torch.cuda.current_stream()
+    for cfg in configs:
+        w = harness.sliced_preset(cfg)
+        P = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
+                          stream=stream.cuda_stream, sliced=True)
+        x = torch.from_numpy(harness.random_x(int(np.prod(w.grid)))).cuda()
+        g = torch.empty_like(x)
+        for _ in range(3):
+            P.objective_grad(x, g)
+        P.profile(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(steps):
+            P.objective_grad(x, g)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        st = P.kernel_stats()
+        rec = dict(workload=f"{cfg} slice-shared: {w.grid[0]}^3, slice matrix {w.A.n_rows} x "
+                            f"{w.A.n_cols}, nnz {w.A.nnz} (operator nnz {w.A.nnz * w.grid[2]})",
+                   value=1e3 / ms, unit=UNIT, ms_per_step=ms, steps=steps,
+                   device_bytes=int(P.info.device_bytes),
+                   kernels={k: dict(ms_per_launch=v["ms"] / v["launches"])
+                            for k, v in st.items() if v["launches"]})
+        if cfg == "c2":
+            P.profile(False)
+            x0 = torch.zeros_like(x)
+            r = P.solve_upn(x0, eps=1e-6, max_iters=20000)
+            rec["upn"] = dict(converged=r.converged, iters=r.iters, seconds=r.seconds, f=r.f)
+        out[cfg] = rec
+        P.close()
+        del w
+    return out
 
 
 # ------------------------------------------------------------ reference arm

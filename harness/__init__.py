@@ -279,3 +279,28 @@ def preset(name: str, **over) -> Workload:
     return separable_workload(name, p["grid"], p["views"], p["bins"], p["n_ell"],
                               p.get("alpha", 0.01), p.get("tau", 1e-4), p.get("lo", 0.0),
                               p.get("hi", float("inf")))
+
+
+def sliced_preset(name: str, **over) -> Workload:
+    """A slice-separable preset (c1-c4) with ONE slice's matrix in `A` (nx*ny columns) for the
+    slice-shared operator (tvr_create_sliced): the operator is I_nz (x) A.  b and x_true
+    are those of preset(name) (the projections are simulated slice by slice, same rows, same
+    noise), without building the nz-times larger CSR."""
+    p = dict(PRESETS[name])
+    p.update(over)
+    if p.get("sphere") or "det" in p:
+        raise ValueError(f"{name}: not slice-separable")
+    nx, ny, nz = p["grid"]
+    As = siddon_slice(nx, ny, p["views"], p["bins"])
+    xt = np.ascontiguousarray(phantom(nx, ny, nz, p["n_ell"]), np.float32)
+    plane, ms = nx * ny, As.n_rows
+    y = np.empty(ms * nz, np.float64)
+    for z in range(nz):
+        lib().hx_simulate_projections(ms, _p(As.row_ptr), _p(As.col), _p(As.val),
+                                      _p(np.ascontiguousarray(xt[z * plane:(z + 1) * plane])),
+                                      _p(y[z * ms:(z + 1) * ms]))
+    sigma = 0.01 * np.linalg.norm(y) / np.sqrt(len(y))
+    b = (y + sigma * normal(len(y), SEED_NOISE)).astype(np.float32)
+    return Workload(name, (nx, ny, nz), As, b, xt, p.get("alpha", 0.01), p.get("tau", 1e-4),
+                    p.get("lo", 0.0), p.get("hi", float("inf")),
+                    dict(kind="sliced", views=p["views"], bins=p["bins"]))

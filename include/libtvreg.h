@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TVR_ABI_VERSION 3
+#define TVR_ABI_VERSION 4
 
 typedef enum {
   TVR_OK = 0,
@@ -98,6 +98,25 @@ typedef struct {
  * b_host: m_local fp32 values (host).  alpha >= 0, tau > 0, lo < hi (+-INFINITY allowed). */
 int tvr_create(tvr_problem** out, const tvr_csr* A_local, const float* b_host, tvr_grid grid,
                double alpha, double tau, double lo, double hi, const tvr_dist* dist);
+
+/* Slice-shared operator (structure-exploiting projector; BJ:5, BJ:7).
+ * For slice-invariant geometry (parallel beam, rays inside z-slices, the same 2D geometry in
+ * every slice: configs c1-c4) the system matrix is block diagonal with one repeated block,
+ * A = I_nz (x) A_slice (Eq.(1); the ray model of P:238-245 restricted to one slice):
+ *   row z*m_s + i of A has the entries of row i of A_slice on the columns z*nx*ny + c.
+ * A_slice: m_s rows, n_cols = nx*ny, HOST CSR with the same rules as tvr_create (columns are
+ *   in-slice voxel indices y*nx + x); read only during the call.
+ * b_host: m_s * nz_local fp32 (host), slice-major (the rows of slice z0 first).
+ * The device stores only A_slice and its transpose (c2: 7.5 MB instead of 1.9 GB) and applies
+ * them to every slice; every other call behaves as for tvr_create on the expanded matrix
+ * (results equal to fp32 rounding, the same fp64 reductions).  tvr_get_AT returns the
+ * transpose of A_slice (nx*ny rows).
+ * dist: NULL / NONE or ZSLAB (each rank passes the same A_slice and its slab's rows of b);
+ * VIEWS -> TVR_E_ARG.  Needs nx*ny <= 65536 and m_s <= 65536 (16-bit window offsets),
+ * else TVR_E_ARG; TVR_E_OOM if the sliced-ELL copy does not fit. */
+int tvr_create_sliced(tvr_problem** out, const tvr_csr* A_slice, const float* b_host,
+                      tvr_grid grid, double alpha, double tau, double lo, double hi,
+                      const tvr_dist* dist);
 void tvr_destroy(tvr_problem* p);
 
 typedef struct {
@@ -111,7 +130,8 @@ typedef struct {
   int32_t views_fused_rs;              /* VIEWS mode: 1 if the A^T pass stores into the owners'
                                           inboxes over peer memory (fused reduce-scatter), 0 if
                                           it uses the collective reduce-scatter */
-  int32_t _pad0;
+  int32_t slice_shared;                /* tvr_create_sliced: slices sharing the stored slice
+                                          matrix (the slab's nz); 0 for tvr_create */
 } tvr_info;
 int tvr_get_info(const tvr_problem* p, tvr_info* info);
 
@@ -206,7 +226,9 @@ int tvr_tv(tvr_problem* p, const float* x_dev, double* tv_out, float* grad_dev);
 /* ||G_nu(x)||_2 with G_nu(x) = nu (x - P_Q(x - grad f(x)/nu)) (Eq. (10)); G_dev nullable. */
 int tvr_gradient_map(tvr_problem* p, const float* x_dev, double nu, double* norm_out, float* G_dev);
 /* Copy the device transposed CSR to host arrays of n_cols_local+1 / nnz_local entries
- * (n_cols_local = N_local, or N in VIEWS mode, where A^T of the local rows spans the volume). */
+ * (n_cols_local = N_local, or N in VIEWS mode, where A^T of the local rows spans the volume).
+ * Slice-shared problems (tvr_create_sliced): the transpose of A_slice, nx*ny+1 / nnz_local /
+ * slice_shared entries. */
 int tvr_get_AT(tvr_problem* p, int64_t* row_ptr_host, int32_t* col_host, float* val_host);
 
 /* ---- per-kernel timing (CUDA events on the problem's stream) ---- */

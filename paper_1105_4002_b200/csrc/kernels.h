@@ -73,18 +73,25 @@ int spmv_occupancy(const SpmvVariant& v, int block, size_t smem);
 struct SellArgs {
   const int64_t* blk_off;   // per block: first chunk step (a step = 32 lanes x 8 entries)
   const int32_t* blk_k;     // per block: chunk steps (its longest row's chunks)
+                            // (per-block arrays are indexed by stored block k % nb)
   const int32_t* blk_slice; // per block: slice (window)
   const int64_t* zend;      // per slice: one past its last block
   const int64_t* cum;       // nblk+1 prefix of per-block work (steps + 2)
   const int32_t* perm;      // 32 per block: row of each lane, -1 for an empty lane
-  double* blk_sq;           // per block: sum of its rows' r^2 (scratch, when scal)
+  double* blk_sq;           // per virtual block: sum of its rows' r^2 (scratch, when scal)
   const uint16_t* col16;    // [step][lane][8] window offsets (zero pads)
   const float* val;         // [step][lane][8] values (zero pads)
   const float* src;
   const float* b;           // non-null: out = A src - b, sum r^2
   float* out;
   float* out_lo;
-  int64_t blk_lo, blk_hi;   // blocks [blk_lo, blk_hi)
+  int64_t blk_lo, blk_hi;   // virtual blocks [blk_lo, blk_hi): block k % nb of repetition k / nb
+  int64_t nb;               // stored blocks
+  int32_t rep;              // repetitions (slice-shared operator: slices; else 1)
+  int64_t rep_rows;         // output row offset per repetition
+  int64_t rep_win;          // gather-window offset per repetition
+  int64_t rep_total;        // slice groups (spmv16z_kernel): slices in all groups
+  int32_t wstride;          // slice groups: shared-memory floats between staged windows
   const int64_t* win_lo;
   const int32_t* win_len;
   int part_len;             // half: window entries staged
@@ -96,6 +103,7 @@ struct SellVariant {
   bool staged = true;
   bool half = false;
   bool dyn = true;    // warps take blocks from a shared counter (else round-robin)
+  int zgroup = 1;     // slice-shared operator: slices per pass (spmv16z_kernel when > 1)
   int unroll = 2;     // steps of loads in flight per lane
   int block = 512;
 };

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <numeric>
 #include <vector>
 
 #include "problem.h"
@@ -168,7 +169,13 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     s.out = out;
     s.out_lo = out_lo;
     s.blk_lo = it_hi >= 0 ? it_lo : 0;
-    s.blk_hi = it_hi >= 0 ? it_hi : pl.sell_nblk;
+    s.blk_hi = it_hi >= 0 ? it_hi : pl.sell_nblk * pl.rep;
+    s.nb = pl.sell_nblk;
+    s.rep = pl.rep;
+    s.rep_rows = pl.rep_rows;
+    s.rep_win = pl.rep_win;
+    s.rep_total = pl.rep_total;
+    s.wstride = pl.wstride;
     s.win_lo = pl.win_lo;
     s.win_len = pl.win_len;
     s.part_len = pl.part_len;
@@ -278,7 +285,10 @@ static double entry_bytes(const SpmvPlan& pl) { return pl.v.idx16 ? 6.0 : 8.0; }
 int pass_residual(tvr_problem* p, const float* x, float* r, int slot, float* r_lo) {
   const float* src = x;
   TVR_TRY(gather_volume(p, x, &src));
-  const double bytes = entry_bytes(p->planA) * p->nnz + 8.0 * (p->m + 1) + 4.0 * p->ncol +
+  // slice-shared operator: the one stored slice matrix is read from HBM once (L2 after that)
+  const double nnz_hbm = p->sliced ? (double)p->nnz_s : (double)p->nnz;
+  const double rows_hbm = p->sliced ? (double)p->m_s : (double)p->m;
+  const double bytes = entry_bytes(p->planA) * nnz_hbm + 8.0 * (rows_hbm + 1) + 4.0 * p->ncol +
                        8.0 * p->m + (r_lo ? 4.0 * p->m : 0.0);
   return launch(p, K_SPMV_A, bytes, [&] {
     return run_spmv(p, p->planA, false, src, p->b, r, r_lo, p->dscal + slot);
@@ -292,8 +302,9 @@ int pass_residual(tvr_problem* p, const float* x, float* r, int slot, float* r_l
 // owner's inbox over peer memory, the owner sums the inboxes in rank order) or through NCCL.
 int pass_AT(tvr_problem* p, const float* r, float* w) {
   float* dst = views_dist(p) ? p->wfull : w;
-  const double bytes =
-      entry_bytes(p->planT) * p->nnz + 8.0 * (p->ncol + 1) + 4.0 * p->m + 4.0 * p->ncol;
+  const double bytes = entry_bytes(p->planT) * (p->sliced ? (double)p->nnz_s : (double)p->nnz) +
+                       8.0 * ((p->sliced ? (double)p->plane : (double)p->ncol) + 1) + 4.0 * p->m +
+                       4.0 * p->ncol;
   if (p->fused_rs) TVR_TRY(dist_barrier(p));  // every owner has consumed the previous inbox
   TVR_TRY(launch(p, K_SPMV_AT, bytes, [&] {
     return run_spmv(p, p->planT, true, r, nullptr, dst, nullptr, nullptr);
@@ -638,7 +649,7 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
   TVR_TRY(upload(p, (void**)&pl.sell_slice, sl.data(), sizeof(int32_t) * sl.size()));
   TVR_TRY(upload(p, (void**)&pl.sell_cum, cum.data(), sizeof(int64_t) * cum.size()));
   TVR_TRY(upload(p, (void**)&pl.sell_zend, zend.data(), sizeof(int64_t) * zend.size()));
-  TVR_TRY(dev_alloc(p, (void**)&pl.sell_sq, sizeof(double) * std::max<int64_t>(1, nblk)));
+  TVR_TRY(dev_alloc(p, (void**)&pl.sell_sq, sizeof(double) * std::max<int64_t>(1, nblk * pl.rep)));
   TVR_TRY(upload(p, (void**)&pl.sell_perm, perm.data(), sizeof(int32_t) * perm.size()));
   TVR_TRY(dev_alloc(p, (void**)&pl.valp, sizeof(float) * cap));
   TVR_CUDA(cudaMemsetAsync(pl.valp, 0, sizeof(float) * cap, p->stream));
@@ -674,10 +685,38 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
     w.block = 1024;
     if (spmv16s_occupancy(w, smem) >= 1) v = w;
   }
+  // slice-shared operator: Z consecutive slices per pass (spmv16z_kernel), as many staged
+  // windows as fit one 1024-thread CTA's shared memory (TVR_SLICE_Z caps Z; 1 disables)
+  pl.rep_total = pl.rep;
+  if (pl.rep > 1 && v.staged && !v.half) {
+    const int32_t ws = (int32_t)(((size_t)pl.max_win + pl.max_win / 32 + 1 + 3) / 4 * 4);
+    int maxsm = 0;
+    TVR_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device));
+    const int zcap = std::min(4, std::max(1, env_int("TVR_SLICE_Z", 2)));
+    for (int Z = zcap; Z >= 2; --Z) {
+      const size_t sz = sizeof(float) * (size_t)ws * Z;
+      if (Z > pl.rep || sz + 2048 > (size_t)maxsm) continue;
+      SellVariant w = v;
+      w.zgroup = Z;
+      w.block = 1024;
+      if (spmv16s_occupancy(w, sz) < 1) continue;
+      v = w;
+      smem = sz;
+      pl.wstride = ws;
+      pl.rep = (int32_t)((pl.rep_total + Z - 1) / Z);
+      break;
+    }
+  }
+  if (pl.rep_total > 1) {  // per slice: one past the last block of the groups ending by it
+    const int Z = v.zgroup;
+    pl.h_slice_item_end.resize(pl.rep_total);
+    for (int64_t z = 0; z < pl.rep_total; ++z)
+      pl.h_slice_item_end[z] = (z == pl.rep_total - 1 ? (int64_t)pl.rep : (z + 1) / Z) * nblk;
+  }
   pl.sv = v;
   pl.smem = smem;
   pl.pad_grid = (int)std::min<int64_t>((int64_t)p->num_sms * spmv16s_occupancy(v, smem),
-                                       std::max<int64_t>(1, nblk));
+                                       std::max<int64_t>(1, nblk * pl.rep));
   pl.sell = true;
   return TVR_OK;
 }
@@ -838,8 +877,10 @@ void tvr_upn_default(tvr_upn_opts* o) {
   o->bt_max = 200;
 }
 
+// sliced: A is one slice's matrix (n_cols = nx*ny) applied to every slice (tvr_create_sliced).
 static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tvr_grid grid,
-                       double alpha, double tau, double lo, double hi, const tvr_dist* dist) {
+                       double alpha, double tau, double lo, double hi, const tvr_dist* dist,
+                       bool sliced) {
   if (!A || !b_host) { set_error("tvr_create: NULL argument"); return TVR_E_ARG; }
   if (grid.nx <= 0 || grid.ny <= 0 || grid.nz <= 0) { set_error("tvr_create: bad grid"); return TVR_E_ARG; }
   if (!(tau > 0.0) || !std::isfinite(tau)) { set_error("tvr_create: tau must be > 0"); return TVR_E_ARG; }
@@ -847,8 +888,11 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   if (!(lo < hi) || std::isnan(lo) || std::isnan(hi)) { set_error("tvr_create: need lo < hi"); return TVR_E_ARG; }
   p->nx = grid.nx; p->ny = grid.ny; p->nz = grid.nz;
   p->plane = (int64_t)grid.nx * grid.ny;
-  const int64_t Nglob = p->plane * grid.nz;
-  if (A->n_cols != Nglob) { set_error("tvr_create: A.n_cols != nx*ny*nz"); return TVR_E_ARG; }
+  const int64_t Nglob = sliced ? p->plane : p->plane * grid.nz;  // column range of the given A
+  if (A->n_cols != Nglob) {
+    set_error(sliced ? "tvr_create_sliced: A_slice.n_cols != nx*ny" : "tvr_create: A.n_cols != nx*ny*nz");
+    return TVR_E_ARG;
+  }
   if (A->n_rows < 0 || A->nnz < 0 || (A->nnz > 0 && (!A->col_idx || !A->val)) || !A->row_ptr) {
     set_error("tvr_create: bad CSR sizes/pointers");
     return TVR_E_ARG;
@@ -883,14 +927,23 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   }
   p->nzl = p->z1 - p->z0;
   const bool views = p->mode == TVR_SHARD_VIEWS;
+  if (sliced && views) {
+    set_error("tvr_create_sliced: VIEWS mode is not supported (use ZSLAB)");
+    return TVR_E_ARG;
+  }
+  p->sliced = sliced;
   p->zA0 = views ? 0 : p->z0;
   p->nzA = views ? grid.nz : p->nzl;
 
   // ---- validate the CSR (host) ----
+  // m, nnz: rows and entries of the matrix stored on the device (the slice matrix when sliced);
+  // m_full: rows of the operator (and of b, r)
   const int64_t m = A->n_rows, nnz = A->nnz;
+  const int64_t m_full = sliced ? m * p->nzA : m;
   const int64_t* rp = A->row_ptr;
   if (rp[0] != 0 || rp[m] != nnz) { set_error("CSR: row_ptr[0] != 0 or row_ptr[m] != nnz"); return TVR_E_CSR; }
-  const int64_t colmin = p->zA0 * p->plane, colmax = (p->zA0 + p->nzA) * p->plane;
+  const int64_t colmin = sliced ? 0 : p->zA0 * p->plane;
+  const int64_t colmax = sliced ? p->plane : (p->zA0 + p->nzA) * p->plane;
   p->separable = true;
   std::vector<int32_t> row_slice(m, -1);
   for (int64_t i = 0; i < m; ++i) {
@@ -913,7 +966,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
       row_slice[i] = (int32_t)zf;
     }
   }
-  for (int64_t i = 0; i < m; ++i)
+  for (int64_t i = 0; i < m_full; ++i)
     if (!std::isfinite(b_host[i])) { set_error("b: non-finite entry"); return TVR_E_ARG; }
   // slice-major row order: assign empty rows to the slice of the previous non-empty row
   if (p->separable) {
@@ -924,7 +977,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
       cur = row_slice[i];
     }
   }
-  if (p->separable) {
+  if (p->separable && !sliced) {
     p->slice_row.assign(p->nzA + 1, m);
     p->slice_row[0] = 0;
     int64_t i = 0;
@@ -933,12 +986,18 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
       p->slice_row[z] = i;
     }
   }
+  if (sliced) {  // every row is inside the one stored slice; operator rows are z m_s + i
+    p->slice_row.resize(p->nzA + 1);
+    for (int z = 0; z <= p->nzA; ++z) p->slice_row[z] = (int64_t)z * m;
+    p->m_s = m;
+    p->nnz_s = nnz;
+  }
 
-  p->m = m;
+  p->m = m_full;
   p->n = p->plane * p->nzl;
   p->ncol = p->plane * p->nzA;
-  p->nnz = nnz;
-  const int64_t n = p->ncol;  // rows of the local A^T
+  p->nnz = sliced ? nnz * p->nzA : nnz;  // entries of the operator
+  const int64_t n = sliced ? p->plane : p->ncol;  // rows of the stored A^T
 
   // ---- device and stream (everything above is host-only validation) ----
   if (p->device < 0) TVR_CUDA(cudaGetDevice(&p->device));
@@ -973,9 +1032,9 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     TVR_CUDA(cudaStreamSynchronize(p->stream));
   }
   TVR_CUDA(cudaMemcpyAsync(p->val, A->val, sizeof(float) * nnz, cudaMemcpyHostToDevice, p->stream));
-  TVR_TRY(dev_alloc(p, (void**)&p->b, sizeof(float) * (m + 4)));
-  TVR_CUDA(cudaMemsetAsync(p->b, 0, sizeof(float) * (m + 4), p->stream));
-  TVR_CUDA(cudaMemcpyAsync(p->b, b_host, sizeof(float) * m, cudaMemcpyHostToDevice, p->stream));
+  TVR_TRY(dev_alloc(p, (void**)&p->b, sizeof(float) * (m_full + 4)));
+  TVR_CUDA(cudaMemsetAsync(p->b, 0, sizeof(float) * (m_full + 4), p->stream));
+  TVR_CUDA(cudaMemcpyAsync(p->b, b_host, sizeof(float) * m_full, cudaMemcpyHostToDevice, p->stream));
 
   // ---- transposed CSR on the device ----
   TVR_TRY(dev_alloc(p, (void**)&p->rpT, sizeof(int64_t) * (n + 3)));
@@ -1006,11 +1065,13 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     std::vector<int64_t> rpv(rp, rp + m + 1);
     std::vector<int64_t> wlo, sr;
     std::vector<int32_t> wlen;
+    const int nsl = sliced ? 1 : p->nzA;  // slices of the stored matrix
+    const std::vector<int64_t> srA = sliced ? std::vector<int64_t>{0, m} : p->slice_row;
     if (p->separable) {
-      for (int z = 0; z < p->nzA; ++z) { wlo.push_back((int64_t)z * p->plane); wlen.push_back((int32_t)p->plane); }
+      for (int z = 0; z < nsl; ++z) { wlo.push_back((int64_t)z * p->plane); wlen.push_back((int32_t)p->plane); }
     }
     const double mean_A = m > 0 ? (double)nnz / m : 0.0;
-    TVR_TRY(make_plan(p, p->planA, rpv, m, p->separable, p->slice_row, wlo, wlen,
+    TVR_TRY(make_plan(p, p->planA, rpv, m, p->separable, srA, wlo, wlen,
                       mean_A, "TVR_LPR_A", true));
     // A^T: rows are voxels; slice z owns voxel rows [z plane, (z+1) plane) and gathers r over
     // the slice's A rows.
@@ -1019,10 +1080,10 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     TVR_CUDA(cudaStreamSynchronize(p->stream));
     wlo.clear(); wlen.clear();
     if (p->separable) {
-      for (int z = 0; z <= p->nzA; ++z) sr.push_back((int64_t)z * p->plane);
-      for (int z = 0; z < p->nzA; ++z) {
-        wlo.push_back(p->slice_row[z]);
-        wlen.push_back((int32_t)(p->slice_row[z + 1] - p->slice_row[z]));
+      for (int z = 0; z <= nsl; ++z) sr.push_back((int64_t)z * p->plane);
+      for (int z = 0; z < nsl; ++z) {
+        wlo.push_back(srA[z]);
+        wlen.push_back((int32_t)(srA[z + 1] - srA[z]));
       }
     }
     const double mean_len = n > 0 ? (double)nnz / n : 0.0;
@@ -1047,6 +1108,17 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
                                p->stream));
   }
   TVR_CUDA(cudaStreamSynchronize(p->stream));
+  if (sliced) {  // the sliced-ELL blocks of the one stored slice repeat over the slab's slices
+    if (!p->planA.v.idx16 || !p->planT.v.idx16 || p->planA.v.parts || p->planT.v.parts) {
+      set_error("tvr_create_sliced: needs 16-bit slice windows (nx*ny and m_s <= 65536)");
+      return TVR_E_ARG;
+    }
+    p->planA.rep = p->planT.rep = p->nzA;
+    p->planA.rep_rows = m;          // A pass: slice z writes rows z m_s + i, gathers x's slice z
+    p->planA.rep_win = p->plane;
+    p->planT.rep_rows = p->plane;   // A^T pass: writes voxels of slice z, gathers r's rows of z
+    p->planT.rep_win = m;
+  }
   // ---- padded-row copies (TVR_SPMV_PAD=0 disables): 16-bit plans pad rows to 8 entries,
   // int32 global-gather plans to 4; skipped when the copy would not fit in free device memory
   for (int which = 0; which < 2; ++which) {
@@ -1059,9 +1131,13 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     TVR_CUDA(cudaMemcpyAsync(rph.data(), which ? p->rpT : p->rp, sizeof(int64_t) * (rows + 1),
                              cudaMemcpyDeviceToHost, p->stream));
     TVR_CUDA(cudaStreamSynchronize(p->stream));
-    if (p16 && p->separable && env_int("TVR_SPMV_SELL", 1)) {
+    if (p16 && p->separable && (env_int("TVR_SPMV_SELL", 1) || sliced)) {
       TVR_TRY(make_sell(p, pl, which == 1, rph, rows));
       if (pl.sell) continue;
+      if (sliced) {
+        set_error("tvr_create_sliced: sliced-ELL copy not built (device memory)");
+        return TVR_E_OOM;
+      }
     }
     rpp[0] = 0;
     for (int64_t r = 0; r < rows; ++r) rpp[r + 1] = rpp[r] + (rph[r + 1] - rph[r] + q - 1) / q * q;
@@ -1134,7 +1210,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   }
   for (int i = 0; i < NDAT; ++i) {
     float* q = nullptr;
-    TVR_TRY(dev_alloc(p, (void**)&q, sizeof(float) * std::max<int64_t>(m, 1)));
+    TVR_TRY(dev_alloc(p, (void**)&q, sizeof(float) * std::max<int64_t>(m_full, 1)));
     p->dat.push_back(q);
   }
   if (views_dist(p)) {
@@ -1186,9 +1262,31 @@ int tvr_create(tvr_problem** out, const tvr_csr* A, const float* b_host, tvr_gri
   if (!p) { set_error("host allocation failed"); return TVR_E_OOM; }
   int s;
   try {
-    s = create_impl(p, A, b_host, grid, alpha, tau, lo, hi, dist);
+    s = create_impl(p, A, b_host, grid, alpha, tau, lo, hi, dist, false);
   } catch (const std::exception& ex) {
     set_error(std::string("tvr_create: ") + ex.what());
+    s = TVR_E_OOM;
+  }
+  if (s != TVR_OK) {
+    tvr_destroy(p);
+    return s;
+  }
+  *out = p;
+  return TVR_OK;
+}
+
+int tvr_create_sliced(tvr_problem** out, const tvr_csr* A_slice, const float* b_host,
+                      tvr_grid grid, double alpha, double tau, double lo, double hi,
+                      const tvr_dist* dist) {
+  if (!out) { set_error("tvr_create_sliced: out is NULL"); return TVR_E_ARG; }
+  *out = nullptr;
+  tvr_problem* p = new (std::nothrow) tvr_problem();
+  if (!p) { set_error("host allocation failed"); return TVR_E_OOM; }
+  int s;
+  try {
+    s = create_impl(p, A_slice, b_host, grid, alpha, tau, lo, hi, dist, true);
+  } catch (const std::exception& ex) {
+    set_error(std::string("tvr_create_sliced: ") + ex.what());
     s = TVR_E_OOM;
   }
   if (s != TVR_OK) {
@@ -1211,7 +1309,7 @@ int tvr_get_info(const tvr_problem* p, tvr_info* info) {
   info->device_bytes = p->device_bytes;
   info->n_cols_local = p->ncol;
   info->views_fused_rs = p->fused_rs ? 1 : 0;
-  info->_pad0 = 0;
+  info->slice_shared = p->sliced ? p->nzA : 0;
   return TVR_OK;
 }
 
@@ -1300,6 +1398,23 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
       z[c + 1] = std::max(z[c] + 1, (int)std::lround(nz * acc / total));
     }
     z[C] = nz;
+  }
+  // slice-shared operator in groups of Z slices: chunk boundaries on group boundaries (a group's
+  // pass reads all its slices' inputs and writes all its rows)
+  {
+    auto grp = [](const SpmvPlan& pl) { return pl.sell ? pl.sv.zgroup : 1; };
+    const int ga = grp(p->planA), gt = grp(p->planT);
+    const int G = ga / std::gcd(ga, gt) * gt;
+    if (G > 1) {
+      std::vector<int> za(1, 0);
+      for (int c = 1; c < C; ++c) {
+        const int zr = (int)std::lround((double)z[c] / G) * G;
+        if (zr > za.back() && zr < nz) za.push_back(zr);
+      }
+      za.push_back(nz);
+      z = za;
+      C = (int)za.size() - 1;
+    }
   }
   constexpr int SA = 16, ST = 24;  // scalar slots: A chunk c at SA + c, stencil chunk c at ST + 6 c
   TVR_CUDA(cudaEventRecord(ev_start, p->stream));
@@ -1425,22 +1540,24 @@ int tvr_gradient_map(tvr_problem* p, const float* x_dev, double nu, double* norm
 int tvr_get_AT(tvr_problem* p, int64_t* rp_h, int32_t* col_h, float* val_h) {
   if (!p) { set_error("tvr_get_AT: NULL"); return TVR_E_ARG; }
   TVR_CUDA(cudaSetDevice(p->device));
-  if (rp_h) TVR_CUDA(cudaMemcpyAsync(rp_h, p->rpT, sizeof(int64_t) * (p->ncol + 1), cudaMemcpyDeviceToHost, p->stream));
+  // the stored transpose: of the slice matrix for a slice-shared problem
+  const int64_t rows = p->sliced ? p->plane : p->ncol, nnz = p->sliced ? p->nnz_s : p->nnz;
+  if (rp_h) TVR_CUDA(cudaMemcpyAsync(rp_h, p->rpT, sizeof(int64_t) * (rows + 1), cudaMemcpyDeviceToHost, p->stream));
   if (col_h && p->colT16) {
     // the device holds 16-bit window offsets: expand them back to the canonical int32 columns
     int32_t* tmp = nullptr;
-    TVR_CUDA(cudaMalloc(&tmp, sizeof(int32_t) * std::max<int64_t>(p->nnz, 1)));
+    TVR_CUDA(cudaMalloc(&tmp, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
     SpmvArgs a = spmv_args(p, p->planT, true, nullptr, nullptr, nullptr, nullptr);
     cudaError_t e = launch_parts_rows(a, true, nullptr, p->colT16, p->planT.part_off, tmp, p->stream);
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(col_h, tmp, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, p->stream);
+      e = cudaMemcpyAsync(col_h, tmp, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, p->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
     cudaFree(tmp);
     if (e != cudaSuccess) { set_error(std::string("tvr_get_AT: ") + cudaGetErrorString(e)); return TVR_E_CUDA; }
   } else if (col_h) {
-    TVR_CUDA(cudaMemcpyAsync(col_h, p->colT, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToHost, p->stream));
+    TVR_CUDA(cudaMemcpyAsync(col_h, p->colT, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, p->stream));
   }
-  if (val_h) TVR_CUDA(cudaMemcpyAsync(val_h, p->valT, sizeof(float) * p->nnz, cudaMemcpyDeviceToHost, p->stream));
+  if (val_h) TVR_CUDA(cudaMemcpyAsync(val_h, p->valT, sizeof(float) * nnz, cudaMemcpyDeviceToHost, p->stream));
   TVR_CUDA(cudaStreamSynchronize(p->stream));
   return TVR_OK;
 }

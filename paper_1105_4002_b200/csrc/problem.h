@@ -82,6 +82,10 @@ struct SpmvPlan {
   int32_t max_win = 0;  // largest slice window (entries)
   // sliced-ELL copy (spmv16s_kernel; replaces the padded copy when built): col16p / valp hold it
   bool sell = false;
+  int32_t rep = 1;                     // slice-shared operator: the blocks repeat per slice
+  int64_t rep_rows = 0, rep_win = 0;   // per repetition: output row / gather window offsets
+  int64_t rep_total = 0;               // slice groups (sv.zgroup > 1): slices; rep = groups
+  int32_t wstride = 0;                 // slice groups: floats between the staged windows
   SellVariant sv;
   int64_t sell_nblk = 0;
   int64_t* sell_off = nullptr;
@@ -148,6 +152,10 @@ struct tvr_problem {
   size_t nnz_pad = 0;
   float* b = nullptr;
   bool separable = false;
+  // slice-shared operator (tvr_create_sliced): the device holds one slice's
+  // matrix (m_s rows over the nx*ny voxels of a slice) and its transpose, applied to every slice
+  int64_t m_s = 0, nnz_s = 0;
+  bool sliced = false;
   std::vector<int64_t> slice_row;  // nzl+1 local row boundaries per slice (separable only)
   tvr::SpmvPlan planA, planT;
 

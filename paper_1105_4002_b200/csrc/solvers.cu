@@ -248,7 +248,8 @@ bool use_device_control(const tvr_problem* p) {
   if (p->world > 1) return false;
   const char* e = std::getenv("TVR_CONTROL");
   if (e && *e) return std::string(e) == "device";
-  if (p->control == TVR_CONTROL_AUTO) return p->nnz < ((int64_t)1 << 25);
+  if (p->control == TVR_CONTROL_AUTO)  // by the stored matrix (the slice's, when slice-shared)
+    return (p->sliced ? p->nnz_s : p->nnz) < ((int64_t)1 << 25);
   return p->control == TVR_CONTROL_DEVICE;
 }
 

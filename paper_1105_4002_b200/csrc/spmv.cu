@@ -536,20 +536,36 @@ __device__ __forceinline__ int64_t lower_bound_i64(const int64_t* __restrict__ a
   return lo;
 }
 
+// Work prefix of virtual block k (block k % nb of repetition k / nb; SellArgs) and the first
+// virtual block in [lo, hi] whose prefix reaches t.
+__device__ __forceinline__ int64_t sell_work(const SellArgs& a, int64_t k) {
+  const int64_t z = k / a.nb;
+  return z * a.cum[a.nb] + a.cum[k - z * a.nb];
+}
+__device__ __forceinline__ int64_t sell_lower(const SellArgs& a, int64_t lo, int64_t hi, int64_t t) {
+  const int64_t ws = a.cum[a.nb];
+  const int64_t z = ws > 0 ? t / ws : 0;
+  const int64_t k = z >= a.rep ? (int64_t)a.rep * a.nb
+                               : z * a.nb + lower_bound_i64(a.cum, 0, a.nb, t - z * ws);
+  return min(max(k, lo), hi);
+}
+
 template <int UNR, bool STAGED, int NT = 512, bool HALF = false, bool DYN = true>
 __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
   extern __shared__ float stage[];
   __shared__ int s_next;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
-  const int64_t w0 = a.cum[a.blk_lo], W = a.cum[a.blk_hi] - w0;
+  const int64_t w0 = sell_work(a, a.blk_lo), W = sell_work(a, a.blk_hi) - w0;
   const int64_t t0 = w0 + W * blockIdx.x / gridDim.x, t1 = w0 + W * (blockIdx.x + 1) / gridDim.x;
-  const int64_t b0 = lower_bound_i64(a.cum, a.blk_lo, a.blk_hi, t0);
-  const int64_t b1 = blockIdx.x + 1 == gridDim.x ? a.blk_hi : lower_bound_i64(a.cum, a.blk_lo, a.blk_hi, t1);
+  const int64_t b0 = sell_lower(a, a.blk_lo, a.blk_hi, t0);
+  const int64_t b1 = blockIdx.x + 1 == gridDim.x ? a.blk_hi : sell_lower(a, a.blk_lo, a.blk_hi, t1);
   double sq = 0.0;  // static assignment: this thread's rows; DYN: the CTA's total (thread 0)
   for (int64_t it = b0; it < b1;) {
-    const int z = a.blk_slice[it];
-    const int64_t it_end = min(b1, a.zend[z]);
-    const float* gbase = a.src + a.win_lo[z];
+    const int64_t rz = it / a.nb, zb = rz * a.nb;  // repetition (slice-shared operator) and base
+    const int z = a.blk_slice[it - zb];
+    const int64_t it_end = min(b1, zb + a.zend[z]);
+    const float* gbase = a.src + a.win_lo[z] + rz * a.rep_win;
+    const int64_t row_off = rz * a.rep_rows;
     if (STAGED || DYN) __syncthreads();  // previous segment done: window and counter reusable
     if (DYN && threadIdx.x == 0) s_next = nwarps;
     if constexpr (STAGED) stage_window(stage, gbase, HALF ? min(a.win_len[z], a.part_len) : a.win_len[z]);
@@ -561,9 +577,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
     int64_t off = 0;
     int K = 0, row = -1;
     if (k < it_end) {
-      off = a.blk_off[k];
-      K = a.blk_k[k];
-      row = a.perm[k * 32 + lane];
+      off = a.blk_off[k - zb];
+      K = a.blk_k[k - zb];
+      row = a.perm[(k - zb) * 32 + lane];
     }
     while (k < it_end) {
       int64_t kn;
@@ -577,9 +593,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
       int64_t off_n = 0;
       int K_n = 0, row_n = -1;
       if (kn < it_end) {
-        off_n = a.blk_off[kn];
-        K_n = a.blk_k[kn];
-        row_n = a.perm[kn * 32 + lane];
+        off_n = a.blk_off[kn - zb];
+        K_n = a.blk_k[kn - zb];
+        row_n = a.perm[(kn - zb) * 32 + lane];
       }
       const uint16_t* cp = a.col16 + (off * 32 + lane) * 8;
       const float* vp = a.val + (off * 32 + lane) * 8;
@@ -608,14 +624,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
       }
       double q = 0.0;
       if (row >= 0) {
+        const int64_t orow = row + row_off;
         if (a.b) {
-          const double r = acc - (double)__ldg(a.b + row);
+          const double r = acc - (double)__ldg(a.b + orow);
           const float rh = (float)r;
-          a.out[row] = rh;
-          if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
+          a.out[orow] = rh;
+          if (a.out_lo) a.out_lo[orow] = (float)(r - (double)rh);
           q = r * r;
         } else {
-          a.out[row] = (float)acc;
+          a.out[orow] = (float)acc;
         }
       }
       if (a.scal) {
@@ -650,8 +667,141 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
   }
 }
 
+// Slice-shared operator, Z slices per pass (the SpMM form of f4): a group of Z consecutive
+// slices applies the same stored blocks, so the CTA stages the Z slices' windows side by side
+// (a.wstride floats apart) and every lane loads each chunk of its row once and gathers it
+// against the Z windows, accumulating Z rows (slice zs0 + zz, row row + (zs0 + zz) rep_rows).
+// Per slice the chunk sums and their order are those of spmv16s_kernel (bitwise the same rows).
+// Virtual block k: stored block k % nb of slice group k / nb (a.rep groups of a.zgroup slices,
+// the last one possibly partial: a.rep_total slices).
+template <int Z, int UNR, int NT = 1024>
+__global__ void __launch_bounds__(NT, 1024 / NT) spmv16z_kernel(SellArgs a) {
+  extern __shared__ float stage[];
+  __shared__ int s_next;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
+  const int64_t w0 = sell_work(a, a.blk_lo), W = sell_work(a, a.blk_hi) - w0;
+  const int64_t t0 = w0 + W * blockIdx.x / gridDim.x, t1 = w0 + W * (blockIdx.x + 1) / gridDim.x;
+  const int64_t b0 = sell_lower(a, a.blk_lo, a.blk_hi, t0);
+  const int64_t b1 = blockIdx.x + 1 == gridDim.x ? a.blk_hi : sell_lower(a, a.blk_lo, a.blk_hi, t1);
+  for (int64_t it = b0; it < b1;) {
+    const int64_t rz = it / a.nb, zb = rz * a.nb;
+    const int z = a.blk_slice[it - zb];
+    const int64_t it_end = min(b1, zb + a.zend[z]);
+    const int64_t zs0 = rz * Z;  // first slice of the group
+    const int zc = (int)(a.rep_total - zs0 < Z ? a.rep_total - zs0 : Z);
+    __syncthreads();
+    if (threadIdx.x == 0) s_next = nwarps;
+    {
+      const int len = a.win_len[z];
+      for (int zz = 0; zz < zc; ++zz) {
+        const float* g = a.src + a.win_lo[z] + (zs0 + zz) * a.rep_win;
+        float* st = stage + zz * a.wstride;
+        for (int i = threadIdx.x; i < len; i += NT) {
+          const uint32_t dst = (uint32_t)__cvta_generic_to_shared(st + swz(i));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(g + i) : "memory");
+        }
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+    __syncthreads();
+    int64_t k = it + warp;
+    int64_t off = 0;
+    int K = 0, row = -1;
+    if (k < it_end) {
+      off = a.blk_off[k - zb];
+      K = a.blk_k[k - zb];
+      row = a.perm[(k - zb) * 32 + lane];
+    }
+    while (k < it_end) {
+      int nx = 0;
+      if (lane == 0) nx = atomicAdd(&s_next, 1);
+      const int64_t kn = it + __shfl_sync(0xffffffffu, nx, 0);
+      int64_t off_n = 0;
+      int K_n = 0, row_n = -1;
+      if (kn < it_end) {
+        off_n = a.blk_off[kn - zb];
+        K_n = a.blk_k[kn - zb];
+        row_n = a.perm[(kn - zb) * 32 + lane];
+      }
+      const uint16_t* cp = a.col16 + (off * 32 + lane) * 8;
+      const float* vp = a.val + (off * 32 + lane) * 8;
+      double acc[Z];
+#pragma unroll
+      for (int zz = 0; zz < Z; ++zz) acc[zz] = 0.0;
+      auto chunk = [&](const int4 c, const float4 v0, const float4 v1) {
+#pragma unroll
+        for (int zz = 0; zz < Z; ++zz)
+          if (zz < zc) acc[zz] += chunk8_sum<true>(c, v0, v1, stage + zz * a.wstride, nullptr);
+      };
+      int s = 0;
+      for (; s + UNR <= K; s += UNR) {
+        int4 c[UNR];
+        float4 va[UNR], vb[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          c[u] = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + (s + u) * 256));
+          va[u] = ld_stream_f4(vp + (s + u) * 256);
+          vb[u] = ld_stream_f4(vp + (s + u) * 256 + 4);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) chunk(c[u], va[u], vb[u]);
+      }
+      for (; s < K; ++s) {
+        const int4 c0 = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + s * 256));
+        const float4 va0 = ld_stream_f4(vp + s * 256);
+        const float4 vb0 = ld_stream_f4(vp + s * 256 + 4);
+        chunk(c0, va0, vb0);
+      }
+      double q = 0.0;
+      if (row >= 0) {
+#pragma unroll
+        for (int zz = 0; zz < Z; ++zz) {
+          if (zz < zc) {
+            const int64_t orow = row + (zs0 + zz) * a.rep_rows;
+            if (a.b) {
+              const double r = acc[zz] - (double)__ldg(a.b + orow);
+              const float rh = (float)r;
+              a.out[orow] = rh;
+              if (a.out_lo) a.out_lo[orow] = (float)(r - (double)rh);
+              q += r * r;
+            } else {
+              a.out[orow] = (float)acc[zz];
+            }
+          }
+        }
+      }
+      if (a.scal) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) q += __shfl_xor_sync(0xffffffffu, q, d);
+        if (lane == 0) a.blk_sq[k] = q;
+      }
+      k = kn;
+      off = off_n;
+      K = K_n;
+      row = row_n;
+    }
+    it = it_end;
+  }
+  if (a.scal) {
+    double sq = 0.0;
+    __syncthreads();
+    if (warp == 0) {
+      double t = 0.0;
+      for (int64_t k = b0 + lane; k < b1; k += 32) t += a.blk_sq[k];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+      if (lane == 0) sq = t;
+    }
+    double v[1] = {sq};
+    reduce_to_scalars<1>(v, a.partials, a.counter, a.scal);
+  }
+}
+
 template <class F>
 static cudaError_t dispatch16s(const SellVariant& v, F&& f) {
+  if (v.zgroup == 2) return f(spmv16z_kernel<2, 1>);
+  if (v.zgroup == 3) return f(spmv16z_kernel<3, 1>);
+  if (v.zgroup == 4) return f(spmv16z_kernel<4, 1>);
   if (!v.dyn) {
     if (v.half) return f(spmv16s_kernel<2, true, 1024, true, false>);
     if (v.staged) return v.block == 1024 ? f(spmv16s_kernel<3, true, 1024, false, false>)

@@ -61,7 +61,7 @@ class tvr_info(ctypes.Structure):
     _fields_ = [("m_local", c_i64), ("n_local", c_i64), ("nnz_local", c_i64), ("z0", c_i32),
                 ("z1", c_i32), ("slab_staged_A", c_i32), ("slab_staged_AT", c_i32),
                 ("device_bytes", c_i64), ("n_cols_local", c_i64), ("views_fused_rs", c_i32),
-                ("_pad0", c_i32)]
+                ("slice_shared", c_i32)]
 
 
 class tvr_fparts(ctypes.Structure):
@@ -108,6 +108,9 @@ FREE_FN = ctypes.CFUNCTYPE(None, c_vp, ctypes.c_int, c_vp, c_vp)
 SIGNATURES = {
     "tvr_create": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.POINTER(tvr_csr), c_vp, tvr_grid,
                                   c_f64, c_f64, c_f64, c_f64, ctypes.POINTER(tvr_dist)]),
+    "tvr_create_sliced": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.POINTER(tvr_csr), c_vp,
+                                         tvr_grid, c_f64, c_f64, c_f64, c_f64,
+                                         ctypes.POINTER(tvr_dist)]),
     "tvr_destroy": (None, [c_vp]),
     "tvr_get_info": (ctypes.c_int, [c_vp, ctypes.POINTER(tvr_info)]),
     "tvr_objective_grad": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(c_f64), c_vp,
@@ -271,17 +274,22 @@ class Problem:
     def __init__(self, row_ptr, col, val, b, grid, alpha: float, tau: float, lo: float = 0.0,
                  hi: float = math.inf, *, n_cols: int | None = None, world: int = 1, rank: int = 0,
                  z0: int | None = None, z1: int | None = None, nccl_comm: int | None = None,
-                 device: int = -1, stream: int | None = None, shard: str | None = None):
+                 device: int = -1, stream: int | None = None, shard: str | None = None,
+                 sliced: bool = False):
         """shard: None (ZSLAB when world > 1 or z0 is given, else NONE), "zslab" or "views"
-        (rows of any geometry, global columns; see tvr_dist in include/libtvreg.h)."""
+        (rows of any geometry, global columns; see tvr_dist in include/libtvreg.h).
+        sliced: the CSR is ONE slice's matrix (n_cols = nx*ny) applied to every slice of the
+        slab, b has m_s * slab-slices entries (tvr_create_sliced)."""
         L = lib()
         self._keep = [np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
                       np.ascontiguousarray(val, np.float32), np.ascontiguousarray(b, np.float32)]
         rp, cl, vl, bb = self._keep
         nx, ny, nz = grid
         self.grid = (nx, ny, nz)
-        csr = tvr_csr(len(rp) - 1, n_cols if n_cols is not None else nx * ny * nz, int(rp[-1]),
-                      rp.ctypes.data, cl.ctypes.data, vl.ctypes.data)
+        if n_cols is None:
+            n_cols = nx * ny if sliced else nx * ny * nz
+        csr = tvr_csr(len(rp) - 1, n_cols, int(rp[-1]), rp.ctypes.data, cl.ctypes.data,
+                      vl.ctypes.data)
         dist = None
         if shard is None:
             mode = TVR_SHARD_ZSLAB if (world > 1 or z0 is not None) else TVR_SHARD_NONE
@@ -292,9 +300,10 @@ class Problem:
                             0 if z0 is None else z0, nz if z1 is None else z1,
                             nccl_comm, device, stream)
         h = c_vp()
-        _check(L.tvr_create(ctypes.byref(h), ctypes.byref(csr), bb.ctypes.data,
-                            tvr_grid(nx, ny, nz), alpha, tau, lo, hi,
-                            ctypes.byref(dist) if dist is not None else None), "tvr_create")
+        create = L.tvr_create_sliced if sliced else L.tvr_create
+        _check(create(ctypes.byref(h), ctypes.byref(csr), bb.ctypes.data,
+                      tvr_grid(nx, ny, nz), alpha, tau, lo, hi,
+                      ctypes.byref(dist) if dist is not None else None), create.__name__)
         self._h = h
         self._keep = None  # host arrays are copied by tvr_create
         info = tvr_info()
@@ -355,9 +364,13 @@ class Problem:
         return v.value
 
     def get_AT(self):
-        rp = np.empty(self.info.n_cols_local + 1, np.int64)
-        cl = np.empty(self.nnz, np.int32)
-        vl = np.empty(self.nnz, np.float32)
+        """The stored transposed CSR (of the slice matrix for a slice-shared problem)."""
+        s = self.info.slice_shared
+        rows = self.grid[0] * self.grid[1] if s else self.info.n_cols_local
+        nnz = self.nnz // s if s else self.nnz
+        rp = np.empty(rows + 1, np.int64)
+        cl = np.empty(nnz, np.int32)
+        vl = np.empty(nnz, np.float32)
         _check(lib().tvr_get_AT(self._h, rp.ctypes.data, cl.ctypes.data, vl.ctypes.data), "tvr_get_AT")
         return rp, cl, vl
 

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(tvreg.SIGNATURES), set(names) ^ set(tvreg.SIGNATURES)
-    assert L.tvr_abi_version() == 3
+    assert L.tvr_abi_version() == 4
 
 
 def test_defaults_match_the_paper():
@@ -80,3 +80,22 @@ def test_create_views_mode_validation(kw):
     with pytest.raises(tvreg.TVRError) as e:
         _create([0, 2], [0, 5], [1, 1], [0], grid=(2, 2, 2), **kw)
     assert e.value.status == tvreg.TVR_E_ARG
+
+
+@pytest.mark.parametrize("case,status", [
+    (dict(n_cols=8), tvreg.TVR_E_ARG),                       # n_cols must be nx*ny (one slice)
+    (dict(shard="views", world=1, z0=0, z1=2), tvreg.TVR_E_ARG),  # VIEWS unsupported
+    (dict(col=[5]), tvreg.TVR_E_CSR),                        # column outside the slice
+    (dict(b=[0, 0, np.inf]), tvreg.TVR_E_ARG),               # b has m_s * nz entries, all finite
+])
+def test_create_sliced_validation(case, status):
+    """tvr_create_sliced (f4): host-side checks before any CUDA call; the slice matrix has
+    nx*ny columns and b one row block per slice."""
+    args = dict(rp=[0, 1], col=[1], val=[1.0], b=[0.0, 0.0], grid=(2, 2, 2))
+    kw = {k: v for k, v in case.items() if k not in args}
+    args.update({k: v for k, v in case.items() if k in args})
+    if "b" in case and len(case["b"]) == 3:
+        args["grid"] = (2, 2, 3)
+    with pytest.raises(tvreg.TVRError) as e:
+        _create(args["rp"], args["col"], args["val"], args["b"], grid=args["grid"], sliced=True, **kw)
+    assert e.value.status == status

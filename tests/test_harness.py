@@ -184,3 +184,21 @@ def test_f2_presets_match_the_paper_sizes():
         p = harness.PRESETS[name]
         assert p["grid"] == (64, 64, 64) and p["views"] == views and p["det"] == (91, 91)
     assert 55 * 91 * 91 == 455455 and 19 * 91 * 91 == 157339
+
+
+def test_sliced_preset_is_the_separable_preset():
+    """sliced_preset (f4 inputs): its slice matrix, replicated over the slices, is preset's CSR
+    entry for entry, and b / x_true are preset's bit for bit."""
+    w = harness.preset("c1")
+    s = harness.sliced_preset("c1")
+    nx, ny, nz = w.grid
+    plane, ms, k = nx * ny, s.A.n_rows, s.A.nnz
+    assert s.A.n_cols == plane and ms * nz == w.A.n_rows and k * nz == w.A.nnz
+    for z in (0, 1, nz - 1):
+        rows = w.A.row_ptr[z * ms:(z + 1) * ms + 1]
+        assert np.array_equal(rows - rows[0], s.A.row_ptr)
+        seg = slice(int(rows[0]), int(rows[-1]))
+        assert np.array_equal(w.A.col[seg] - z * plane, s.A.col)
+        assert np.array_equal(w.A.val[seg].view(np.uint32), s.A.val.view(np.uint32))
+    assert np.array_equal(w.b.view(np.uint32), s.b.view(np.uint32))
+    assert np.array_equal(np.asarray(w.x_true, np.float32), s.x_true)
