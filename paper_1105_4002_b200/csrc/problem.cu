@@ -2,6 +2,7 @@
 // entry points other than the solvers (solvers.cu) and NCCL plumbing (dist.cu).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -1390,11 +1391,12 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
   // transfers, so the end chunks get half the weight of the middle ones (TVR_E2E_TAPER=0: equal)
   {
     const bool taper = env_int("TVR_E2E_TAPER", 1) != 0 && C > 2;
-    const double total = taper ? C - 1.0 : (double)C;
+    const double tw = taper ? std::min(1.0, std::max(0.05, env_int("TVR_E2E_TAPER_PCT", 30) / 100.0)) : 1.0;
+    const double total = C - 2.0 + 2.0 * tw;
     double acc = 0.0;
     z[0] = 0;
     for (int c = 0; c < C; ++c) {
-      acc += (taper && (c == 0 || c == C - 1)) ? 0.5 : 1.0;
+      acc += (c == 0 || c == C - 1) ? tw : 1.0;
       z[c + 1] = std::max(z[c] + 1, (int)std::lround(nz * acc / total));
     }
     z[C] = nz;
@@ -1417,13 +1419,31 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
     }
   }
   constexpr int SA = 16, ST = 24;  // scalar slots: A chunk c at SA + c, stencil chunk c at ST + 6 c
+  // TVR_E2E_TRACE=1: timing events at every stage, printed to stderr (diagnostics)
+  const bool trace = env_int("TVR_E2E_TRACE", 0) != 0;
+  std::vector<std::pair<std::string, cudaEvent_t>> tr;
+  auto mark = [&](const std::string& name, cudaStream_t st) -> int {
+    if (!trace) return TVR_OK;
+    cudaEvent_t e;
+    TVR_CUDA(cudaEventCreate(&e));
+    TVR_CUDA(cudaEventRecord(e, st));
+    tr.emplace_back(name, e);
+    return TVR_OK;
+  };
+  TVR_TRY(mark("start", p->stream));
   TVR_CUDA(cudaEventRecord(ev_start, p->stream));
   TVR_CUDA(cudaStreamWaitEvent(p->s_in, ev_start, 0));
   TVR_CUDA(cudaStreamWaitEvent(p->s_out, ev_start, 0));
+  // TVR_E2E_UPFRONT=1: x goes up whole before any pass (an H2D copy running under the SpMV
+  // passes slows them by ~25 %, measured; D2H copies do not), only the downloads overlap
+  const bool upfront = env_int("TVR_E2E_UPFRONT", 0) != 0;
   for (int c = 0; c < C; ++c) {
     const size_t off = (size_t)z[c] * plane, cnt = (size_t)(z[c + 1] - z[c]) * plane;
-    TVR_CUDA(cudaMemcpyAsync(x + off, xh + off, sizeof(float) * cnt, cudaMemcpyHostToDevice, p->s_in));
+    if (!upfront || c == 0)
+      TVR_CUDA(cudaMemcpyAsync(x + off, xh + off, sizeof(float) * (upfront ? (size_t)nz * plane : cnt),
+                               cudaMemcpyHostToDevice, p->s_in));
     TVR_CUDA(cudaEventRecord(ev_in(c), p->s_in));
+    TVR_TRY(mark("in" + std::to_string(c), p->s_in));
   }
   auto items = [](const SpmvPlan& pl, int z0, int z1, int64_t& lo, int64_t& hi) {
     lo = z0 > 0 ? pl.h_slice_item_end[z0 - 1] : 0;
@@ -1432,16 +1452,19 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
   const double bytes_row = entry_bytes(p->planA) * (double)p->nnz / nz;  // per slice, for counters
   for (int c = 0; c < C; ++c) {
     TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_in(c), 0));
+    TVR_TRY(mark("A" + std::to_string(c) + ">", p->stream));
     int64_t lo, hi;
     items(p->planA, z[c], z[c + 1], lo, hi);
     TVR_TRY(launch(p, K_SPMV_A, bytes_row * (z[c + 1] - z[c]), [&] {
       return run_spmv(p, p->planA, false, x, p->b, r, nullptr, p->dscal + SA + c, lo, hi);
     }));
+    TVR_TRY(mark("A" + std::to_string(c) + "<", p->stream));
     if (gh) {
       items(p->planT, z[c], z[c + 1], lo, hi);
       TVR_TRY(launch(p, K_SPMV_AT, bytes_row * (z[c + 1] - z[c]), [&] {
         return run_spmv(p, p->planT, true, r, nullptr, w, nullptr, nullptr, lo, hi);
       }));
+      TVR_TRY(mark("AT" + std::to_string(c) + "<", p->stream));
     }
     if (c + 1 < C) TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_in(c + 1), 0));  // plane z[c+1]
     TVArgs a = tv_args(p, ST + 6 * c);
@@ -1451,18 +1474,33 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
     a.w1 = gh ? w + off : nullptr;
     a.g_out = gh ? g + off : nullptr;
     const double N = (double)a.nzl * plane;
+    TVR_TRY(mark("TV" + std::to_string(c) + ">", p->stream));
     TVR_TRY(launch(p, K_TV_GRAD, N * (gh ? 12.0 : 8.0),
                    [&] { return launch_tv_grad_plain(a, x + off, p->stream); }));
+    TVR_TRY(mark("TV" + std::to_string(c) + "<", p->stream));
     if (gh) {
       TVR_CUDA(cudaEventRecord(ev_g(c), p->stream));
       TVR_CUDA(cudaStreamWaitEvent(p->s_out, ev_g(c), 0));
       TVR_CUDA(cudaMemcpyAsync(gh + off, g + off, sizeof(float) * N, cudaMemcpyDeviceToHost, p->s_out));
+      TVR_TRY(mark("out" + std::to_string(c), p->s_out));
     }
   }
   TVR_CUDA(cudaEventRecord(ev_done, p->s_out));
   TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_done, 0));
   TVR_CUDA(cudaMemcpyAsync(p->hscal, p->dscal, sizeof(double) * 64, cudaMemcpyDeviceToHost, p->stream));
+  TVR_TRY(mark("end", p->stream));
   TVR_CUDA(cudaStreamSynchronize(p->stream));
+  if (trace) {
+    std::string line = "e2e trace (us):";
+    for (auto& t : tr) {
+      float ms = 0.f;
+      const cudaError_t e = cudaEventElapsedTime(&ms, tr[0].second, t.second);
+      line += " " + t.first + "=" +
+              (e == cudaSuccess ? std::to_string((int)std::lround(ms * 1e3)) : cudaGetErrorString(e));
+    }
+    for (auto& t : tr) cudaEventDestroy(t.second);
+    std::fprintf(stderr, "%s\n", line.c_str());
+  }
   resolve_pending_timings(p);
   double rsq = 0.0, tv = 0.0;
   for (int c = 0; c < C; ++c) {

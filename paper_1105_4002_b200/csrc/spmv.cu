@@ -30,11 +30,18 @@ __device__ __forceinline__ int swz(int c) { return c + (c >> 5); }
 // every copy is in flight at once and the CTA waits one memory latency, instead of one per
 // loop trip of a load -> store loop (the restage was ~10% of the A pass's stall samples).
 // The caller brackets it with __syncthreads().
+// The block size is a multiple of 32, so slot swz(i + blockDim) = swz(i) + blockDim * 33 / 32:
+// both addresses advance by a constant (a few instructions per copy instead of a recomputed
+// 64-bit address and swizzle).
 __device__ __forceinline__ void stage_window(float* stage, const float* __restrict__ g, int len) {
-  for (int i = threadIdx.x; i < len; i += blockDim.x) {
-    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + swz(i));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(g + i) : "memory");
-  }
+  const int step = blockDim.x;
+  uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + swz(threadIdx.x));
+  const uint32_t dstep = (uint32_t)(step + (step >> 5)) * 4u;
+  const float* src = g + threadIdx.x;
+  int n = len > (int)threadIdx.x ? (len - (int)threadIdx.x + step - 1) / step : 0;
+#pragma unroll 4
+  for (; n > 0; --n, dst += dstep, src += step)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
@@ -550,15 +557,27 @@ __device__ __forceinline__ int64_t sell_lower(const SellArgs& a, int64_t lo, int
   return min(max(k, lo), hi);
 }
 
+// The CTA's virtual block range [b0, b1): searched once by thread 0, broadcast in shared memory.
+__device__ __forceinline__ void sell_cta_range(const SellArgs& a, int64_t& b0, int64_t& b1) {
+  __shared__ int64_t s_rng[2];
+  if (threadIdx.x == 0) {
+    const int64_t w0 = sell_work(a, a.blk_lo), W = sell_work(a, a.blk_hi) - w0;
+    const int64_t t0 = w0 + W * blockIdx.x / gridDim.x, t1 = w0 + W * (blockIdx.x + 1) / gridDim.x;
+    s_rng[0] = sell_lower(a, a.blk_lo, a.blk_hi, t0);
+    s_rng[1] = blockIdx.x + 1 == gridDim.x ? a.blk_hi : sell_lower(a, a.blk_lo, a.blk_hi, t1);
+  }
+  __syncthreads();
+  b0 = s_rng[0];
+  b1 = s_rng[1];
+}
+
 template <int UNR, bool STAGED, int NT = 512, bool HALF = false, bool DYN = true>
 __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
   extern __shared__ float stage[];
   __shared__ int s_next;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
-  const int64_t w0 = sell_work(a, a.blk_lo), W = sell_work(a, a.blk_hi) - w0;
-  const int64_t t0 = w0 + W * blockIdx.x / gridDim.x, t1 = w0 + W * (blockIdx.x + 1) / gridDim.x;
-  const int64_t b0 = sell_lower(a, a.blk_lo, a.blk_hi, t0);
-  const int64_t b1 = blockIdx.x + 1 == gridDim.x ? a.blk_hi : sell_lower(a, a.blk_lo, a.blk_hi, t1);
+  int64_t b0, b1;
+  sell_cta_range(a, b0, b1);
   double sq = 0.0;  // static assignment: this thread's rows; DYN: the CTA's total (thread 0)
   for (int64_t it = b0; it < b1;) {
     const int64_t rz = it / a.nb, zb = rz * a.nb;  // repetition (slice-shared operator) and base
@@ -679,10 +698,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16z_kernel(SellArgs a) {
   extern __shared__ float stage[];
   __shared__ int s_next;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
-  const int64_t w0 = sell_work(a, a.blk_lo), W = sell_work(a, a.blk_hi) - w0;
-  const int64_t t0 = w0 + W * blockIdx.x / gridDim.x, t1 = w0 + W * (blockIdx.x + 1) / gridDim.x;
-  const int64_t b0 = sell_lower(a, a.blk_lo, a.blk_hi, t0);
-  const int64_t b1 = blockIdx.x + 1 == gridDim.x ? a.blk_hi : sell_lower(a, a.blk_lo, a.blk_hi, t1);
+  int64_t b0, b1;
+  sell_cta_range(a, b0, b1);
   for (int64_t it = b0; it < b1;) {
     const int64_t rz = it / a.nb, zb = rz * a.nb;
     const int z = a.blk_slice[it - zb];
@@ -693,13 +710,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16z_kernel(SellArgs a) {
     if (threadIdx.x == 0) s_next = nwarps;
     {
       const int len = a.win_len[z];
+      const uint32_t dstep = (uint32_t)(NT + NT / 32) * 4u;
       for (int zz = 0; zz < zc; ++zz) {
-        const float* g = a.src + a.win_lo[z] + (zs0 + zz) * a.rep_win;
-        float* st = stage + zz * a.wstride;
-        for (int i = threadIdx.x; i < len; i += NT) {
-          const uint32_t dst = (uint32_t)__cvta_generic_to_shared(st + swz(i));
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(g + i) : "memory");
-        }
+        const float* src = a.src + a.win_lo[z] + (zs0 + zz) * a.rep_win + threadIdx.x;
+        uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + zz * a.wstride + swz(threadIdx.x));
+        int n = len > (int)threadIdx.x ? (len - (int)threadIdx.x + NT - 1) / NT : 0;
+#pragma unroll 4
+        for (; n > 0; --n, dst += dstep, src += NT)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
     }
