@@ -79,6 +79,8 @@ struct SellArgs {
   const int64_t* cum;       // nblk+1 prefix of per-block work (steps + 2)
   const int32_t* perm;      // 32 per block: row of each lane, -1 for an empty lane
   double* blk_sq;           // per virtual block: sum of its rows' r^2 (scratch, when scal)
+  const double* acc_in;     // column parts after the first: each row starts from acc_in[row]
+  double* acc_out;          // column parts before the last: the row's fp64 sum goes here
   const uint16_t* col16;    // [step][lane][8] window offsets (zero pads)
   const float* val;         // [step][lane][8] values (zero pads)
   const float* src;
@@ -111,8 +113,12 @@ cudaError_t launch_spmv16s(const SellArgs& a, const SellVariant& v, int grid, si
                            cudaStream_t st);
 int spmv16s_occupancy(const SellVariant& v, size_t smem);
 cudaError_t launch_sell_fill(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
-                             const int64_t* rp, const uint16_t* col16, const float* val,
+                             const int64_t* rp, const int32_t* lo_off, const int32_t* hi_off,
+                             uint16_t coff, const uint16_t* col16, const float* val,
                              uint16_t* col16s, float* vals, cudaStream_t st);
+// per row: the first entry offset (from rp[r]) whose 16-bit column is >= h
+cudaError_t launch_sell_split(int64_t rows, const int64_t* rp, const uint16_t* col16, int h,
+                              int32_t* split, cudaStream_t st);
 
 // Row-agnostic SpMV (spmv_flat.cu): warps stream items as tiles of 32 x 8 entries with a
 // head-mask segmented reduction.

@@ -153,40 +153,58 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
 // register-streaming kernel.
 static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed, const float* src,
                             const float* b, float* out, float* out_lo, double* scal,
-                            int64_t it_lo = 0, int64_t it_hi = -1) {
-  if (pl.sell) {  // blocks [it_lo, it_hi) (the e2e pipeline's chunks) or all
-    SellArgs s;
-    s.blk_off = pl.sell_off;
-    s.blk_k = pl.sell_k;
-    s.blk_slice = pl.sell_slice;
-    s.zend = pl.sell_zend;
-    s.blk_sq = pl.sell_sq;
-    s.cum = pl.sell_cum;
-    s.perm = pl.sell_perm;
-    s.col16 = pl.col16p;
-    s.val = pl.valp;
-    s.src = src;
-    s.b = b;
-    s.out = out;
-    s.out_lo = out_lo;
-    s.blk_lo = it_hi >= 0 ? it_lo : 0;
-    s.blk_hi = it_hi >= 0 ? it_hi : pl.sell_nblk * pl.rep;
-    s.nb = pl.sell_nblk;
-    s.rep = pl.rep;
-    s.rep_rows = pl.rep_rows;
-    s.rep_win = pl.rep_win;
-    s.rep_total = pl.rep_total;
-    s.wstride = pl.wstride;
-    s.win_lo = pl.win_lo;
-    s.win_len = pl.win_len;
-    s.part_len = pl.part_len;
-    s.partials = p->partials;
-    s.counter = p->counter;
-    s.scal = scal;
-    if (s.blk_hi <= s.blk_lo && scal)  // nothing to sum: the pass still defines its scalar
-      return cudaMemsetAsync(scal, 0, sizeof(double), p->stream);
-    const int g = (int)std::min<int64_t>(pl.pad_grid, std::max<int64_t>(1, s.blk_hi - s.blk_lo));
-    return launch_spmv16s(s, pl.sv, g, pl.smem, p->stream);
+                            int z_lo = 0, int z_hi = -1) {
+  if (pl.sell) {  // slices [z_lo, z_hi) (the e2e pipeline's chunks) or all; column parts in order
+    const int P = (int)pl.sd.size();
+    for (int q = 0; q < P; ++q) {
+      const SellData& d = pl.sd[q];
+      SellArgs s;
+      s.blk_off = d.off;
+      s.blk_k = d.k;
+      s.blk_slice = d.slice;
+      s.zend = d.zend;
+      s.blk_sq = d.sq;
+      s.cum = d.cum;
+      s.perm = d.perm;
+      s.col16 = d.col16;
+      s.val = d.val;
+      s.src = src;
+      s.b = q == P - 1 ? b : nullptr;
+      s.out = out;
+      s.out_lo = q == P - 1 ? out_lo : nullptr;
+      s.acc_in = q > 0 ? pl.sell_acc : nullptr;
+      s.acc_out = q < P - 1 ? pl.sell_acc : nullptr;
+      s.blk_lo = z_hi >= 0 ? (z_lo > 0 ? d.h_slice_end[z_lo - 1] : 0) : 0;
+      s.blk_hi = z_hi >= 0 ? d.h_slice_end[z_hi - 1] : d.nblk * pl.rep;
+      s.nb = d.nblk;
+      s.rep = pl.rep;
+      s.rep_rows = pl.rep_rows;
+      s.rep_win = pl.rep_win;
+      s.rep_total = pl.rep_total;
+      s.wstride = pl.wstride;
+      s.win_lo = d.win_lo;
+      s.win_len = d.win_len;
+      s.part_len = pl.part_len;
+      s.partials = p->partials;
+      s.counter = p->counter;
+      s.scal = q == P - 1 ? scal : nullptr;
+      if (s.blk_hi <= s.blk_lo) {
+        if (s.scal) {  // nothing to sum: the pass still defines its scalar
+          cudaError_t e = cudaMemsetAsync(s.scal, 0, sizeof(double), p->stream);
+          if (e != cudaSuccess) return e;
+        }
+        continue;
+      }
+      const int g = (int)std::min<int64_t>(pl.pad_grid, std::max<int64_t>(1, s.blk_hi - s.blk_lo));
+      cudaError_t e = launch_spmv16s(s, pl.sv, g, pl.smem, p->stream);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  int64_t it_lo = 0, it_hi = -1;  // per-row kernels: the items of slices [z_lo, z_hi)
+  if (z_hi >= 0) {
+    it_lo = z_lo > 0 ? pl.h_slice_item_end[z_lo - 1] : 0;
+    it_hi = pl.h_slice_item_end[z_hi - 1];
   }
   if (it_hi >= 0) {  // items [it_lo, it_hi) only (per-row kernels; the e2e pipeline's chunks)
     SpmvArgs a = spmv_args(p, pl, transposed, src, b, out, scal);
@@ -601,34 +619,36 @@ static int make_flat_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_
   return TVR_OK;
 }
 
-// Sliced-ELL copy (spmv16s_kernel, TVR_SPMV_SELL): per slice, rows stably sorted by 8-entry chunk
-// count (descending) in blocks of 32; replaces the padded copy.  Returns TVR_OK with pl.sell
-// unset when not applicable (no slice windows, too many rows, not enough device memory).
-static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::vector<int64_t>& rph,
-                     int64_t rows) {
-  pl.sell = false;
-  if (!pl.v.idx16 || rows >= ((int64_t)1 << 31) || pl.nitems == 0) return TVR_OK;
-  std::vector<int64_t> prow(pl.nitems + 1);
-  std::vector<int32_t> psl(pl.nitems);
-  TVR_CUDA(cudaMemcpy(prow.data(), pl.item_row, sizeof(int64_t) * (pl.nitems + 1), cudaMemcpyDeviceToHost));
-  TVR_CUDA(cudaMemcpy(psl.data(), pl.item_slice, sizeof(int32_t) * pl.nitems, cudaMemcpyDeviceToHost));
+// One sliced-ELL structure: per slice (prow / psl: the per-row plan's items), rows stably sorted
+// by 8-entry chunk count of `lens` (descending) in blocks of 32; entries [lo_off, hi_off) of each
+// row with coff subtracted from the offsets; the windows shifted by coff and clipped to part_h
+// (0: whole).  ok = false when it does not fit in free device memory.
+static int build_sell_data(tvr_problem* p, SpmvPlan& pl, bool transposed,
+                           const std::vector<int64_t>& prow, const std::vector<int32_t>& psl,
+                           const std::vector<int64_t>& lens, const int32_t* lo_off,
+                           const int32_t* hi_off, int coff, int part_h,
+                           const std::vector<int64_t>& wlo, const std::vector<int32_t>& wlen,
+                           SellData& d, bool& ok) {
+  ok = false;
+  const int64_t nitems = (int64_t)psl.size();
   std::vector<int64_t> off, cum(1, 0), zend(pl.h_slice_item_end.size(), 0);
   std::vector<int32_t> kk, sl, perm, idx;
   int64_t steps = 0;
-  for (int64_t i = 0; i < pl.nitems;) {
+  const int64_t wcost = env_int("TVR_SELL_BLKCOST", 2);
+  for (int64_t i = 0; i < nitems;) {
     int64_t e = i + 1;
-    while (e < pl.nitems && psl[e] == psl[i]) ++e;
+    while (e < nitems && psl[e] == psl[i]) ++e;
     const int64_t R0 = prow[i], R1 = prow[e];
     idx.resize(R1 - R0);
     for (int64_t r = R0; r < R1; ++r) idx[r - R0] = (int32_t)r;
-    auto nch = [&](int32_t r) { return (rph[r + 1] - rph[r] + 7) / 8; };
+    auto nch = [&](int32_t r) { return (lens[r] + 7) / 8; };
     std::stable_sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) { return nch(x) > nch(y); });
     for (size_t j = 0; j < idx.size(); j += 32) {
       const int64_t K = nch(idx[j]);
       off.push_back(steps);
       kk.push_back((int32_t)K);
       sl.push_back(psl[i]);
-      cum.push_back(cum.back() + K + 2);
+      cum.push_back(cum.back() + K + wcost);
       for (size_t l = 0; l < 32; ++l) perm.push_back(j + l < idx.size() ? idx[j + l] : -1);
       steps += K;
     }
@@ -638,58 +658,134 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
   for (size_t z = 1; z < zend.size(); ++z) zend[z] = std::max(zend[z], zend[z - 1]);
   const int64_t nblk = (int64_t)kk.size();
   const size_t cap = (size_t)steps * 256 + 8;
-  const int64_t wcost = env_int("TVR_SELL_BLKCOST", 2);
-  if (wcost != 2)
-    for (int64_t j = 0; j < nblk; ++j) cum[j + 1] = cum[j] + kk[j] + wcost;
   const size_t need = cap * 6 + (size_t)nblk * (8 + 4 + 4 + 8 + 128);
   size_t fr = 0, tot = 0;
   TVR_CUDA(cudaMemGetInfo(&fr, &tot));
   if (need + ((size_t)1 << 30) > fr) return TVR_OK;  // keep 1 GB of headroom
-  TVR_TRY(upload(p, (void**)&pl.sell_off, off.data(), sizeof(int64_t) * off.size()));
-  TVR_TRY(upload(p, (void**)&pl.sell_k, kk.data(), sizeof(int32_t) * kk.size()));
-  TVR_TRY(upload(p, (void**)&pl.sell_slice, sl.data(), sizeof(int32_t) * sl.size()));
-  TVR_TRY(upload(p, (void**)&pl.sell_cum, cum.data(), sizeof(int64_t) * cum.size()));
-  TVR_TRY(upload(p, (void**)&pl.sell_zend, zend.data(), sizeof(int64_t) * zend.size()));
-  TVR_TRY(dev_alloc(p, (void**)&pl.sell_sq, sizeof(double) * std::max<int64_t>(1, nblk * pl.rep)));
-  TVR_TRY(upload(p, (void**)&pl.sell_perm, perm.data(), sizeof(int32_t) * perm.size()));
-  TVR_TRY(dev_alloc(p, (void**)&pl.valp, sizeof(float) * cap));
-  TVR_CUDA(cudaMemsetAsync(pl.valp, 0, sizeof(float) * cap, p->stream));
-  TVR_TRY(dev_alloc(p, (void**)&pl.col16p, sizeof(uint16_t) * cap));
-  TVR_CUDA(cudaMemsetAsync(pl.col16p, 0, sizeof(uint16_t) * cap, p->stream));
-  TVR_CUDA(launch_sell_fill(nblk * 32, pl.sell_perm, pl.sell_off, transposed ? p->rpT : p->rp,
-                            transposed ? p->colT16 : p->col16, transposed ? p->valT : p->val,
-                            pl.col16p, pl.valp, p->stream));
+  std::vector<int64_t> wl(wlo.size());
+  std::vector<int32_t> wn(wlen.size());
+  for (size_t z = 0; z < wlo.size(); ++z) {
+    wl[z] = wlo[z] + coff;
+    const int32_t rest = std::max<int32_t>(0, wlen[z] - coff);
+    wn[z] = part_h > 0 ? std::min<int32_t>(rest, part_h) : rest;
+  }
+  TVR_TRY(upload(p, (void**)&d.off, off.data(), sizeof(int64_t) * off.size()));
+  TVR_TRY(upload(p, (void**)&d.k, kk.data(), sizeof(int32_t) * kk.size()));
+  TVR_TRY(upload(p, (void**)&d.slice, sl.data(), sizeof(int32_t) * sl.size()));
+  TVR_TRY(upload(p, (void**)&d.cum, cum.data(), sizeof(int64_t) * cum.size()));
+  TVR_TRY(upload(p, (void**)&d.zend, zend.data(), sizeof(int64_t) * zend.size()));
+  TVR_TRY(upload(p, (void**)&d.win_lo, wl.data(), sizeof(int64_t) * wl.size()));
+  TVR_TRY(upload(p, (void**)&d.win_len, wn.data(), sizeof(int32_t) * wn.size()));
+  TVR_TRY(dev_alloc(p, (void**)&d.sq, sizeof(double) * std::max<int64_t>(1, nblk * pl.rep)));
+  TVR_TRY(upload(p, (void**)&d.perm, perm.data(), sizeof(int32_t) * perm.size()));
+  TVR_TRY(dev_alloc(p, (void**)&d.val, sizeof(float) * cap));
+  TVR_CUDA(cudaMemsetAsync(d.val, 0, sizeof(float) * cap, p->stream));
+  TVR_TRY(dev_alloc(p, (void**)&d.col16, sizeof(uint16_t) * cap));
+  TVR_CUDA(cudaMemsetAsync(d.col16, 0, sizeof(uint16_t) * cap, p->stream));
+  TVR_CUDA(launch_sell_fill(nblk * 32, d.perm, d.off, transposed ? p->rpT : p->rp, lo_off, hi_off,
+                            (uint16_t)coff, transposed ? p->colT16 : p->col16,
+                            transposed ? p->valT : p->val, d.col16, d.val, p->stream));
   TVR_CUDA(cudaStreamSynchronize(p->stream));  // host vectors die here
-  pl.sell_nblk = nblk;
-  pl.h_slice_item_end = zend;
-  // variant: staged window; a window too large for shared memory: its first part staged
-  // (as the padded kernel's HALF); a staged window that fits one 512-thread CTA: 1024 threads
+  d.nblk = nblk;
+  d.h_slice_end = zend;
+  ok = true;
+  return TVR_OK;
+}
+
+// Sliced-ELL copy (spmv16s_kernel, TVR_SPMV_SELL): replaces the padded copy.  A slice window too
+// large for shared memory is cut into P column parts of h entries (TVR_SELL_PARTS=1, default),
+// each staged whole in its own pass; else its first part is staged and the rest gathered from
+// global memory (HALF).  Returns TVR_OK with pl.sell unset when not applicable (no slice
+// windows, too many rows, not enough device memory).
+static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::vector<int64_t>& rph,
+                     int64_t rows) {
+  pl.sell = false;
+  if (!pl.v.idx16 || rows >= ((int64_t)1 << 31) || pl.nitems == 0) return TVR_OK;
+  std::vector<int64_t> prow(pl.nitems + 1);
+  std::vector<int32_t> psl(pl.nitems);
+  TVR_CUDA(cudaMemcpy(prow.data(), pl.item_row, sizeof(int64_t) * (pl.nitems + 1), cudaMemcpyDeviceToHost));
+  TVR_CUDA(cudaMemcpy(psl.data(), pl.item_slice, sizeof(int32_t) * pl.nitems, cudaMemcpyDeviceToHost));
+  const size_t nsl = pl.h_slice_item_end.size();
+  std::vector<int64_t> wlo(nsl);
+  std::vector<int32_t> wlen(nsl);
+  TVR_CUDA(cudaMemcpy(wlo.data(), pl.win_lo, sizeof(int64_t) * nsl, cudaMemcpyDeviceToHost));
+  TVR_CUDA(cudaMemcpy(wlen.data(), pl.win_len, sizeof(int32_t) * nsl, cudaMemcpyDeviceToHost));
   SellVariant v;
   v.staged = pl.staged;
   v.block = env_int("TVR_SELL_BLOCK", 512);
   v.dyn = env_int("TVR_SELL_DYN", 1) != 0;
   v.unroll = env_int("TVR_SELL_UNROLL", 2);
   size_t smem = pl.staged ? pl.smem : 0;
-  if (!pl.staged && env_int("TVR_SPMV_HALF", 1)) {
+  // column parts for windows larger than shared memory
+  int P = 1, h = 0;
+  if (!pl.staged && p->separable && env_int("TVR_SELL_PARTS", 1)) {
+    int maxsm = 0;
+    TVR_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device));
+    int capf = (int)(((size_t)(maxsm - 4096) / 4) * 32 / 33) / 32 * 32;  // floats per part
+    capf = std::min(capf, std::max(32, env_int("TVR_SELL_PART_FLOATS", capf)));  // tests
+    if (capf > 0) {
+      P = (pl.max_win + capf - 1) / capf;
+      h = ((pl.max_win + P - 1) / P + 31) / 32 * 32;
+    }
+    if (P < 2) P = 1;
+  }
+  std::vector<int32_t> split_h;  // P = 2: per row, the first entry of part 1
+  int32_t* split_d = nullptr;
+  if (P > 1) {
+    // (P - 1) split arrays, one per inner part boundary
+    TVR_TRY(dev_alloc(p, (void**)&split_d, sizeof(int32_t) * (size_t)rows * (P - 1)));
+    for (int q = 1; q < P; ++q)
+      TVR_CUDA(launch_sell_split(rows, transposed ? p->rpT : p->rp, transposed ? p->colT16 : p->col16,
+                                 q * h, split_d + (size_t)rows * (q - 1), p->stream));
+    split_h.resize((size_t)rows * (P - 1));
+    TVR_CUDA(cudaMemcpyAsync(split_h.data(), split_d, sizeof(int32_t) * split_h.size(),
+                             cudaMemcpyDeviceToHost, p->stream));
+    TVR_CUDA(cudaStreamSynchronize(p->stream));
+  }
+  pl.sd.assign(P, SellData());
+  for (int q = 0; q < P; ++q) {
+    std::vector<int64_t> lens(rows);
+    for (int64_t r = 0; r < rows; ++r) {
+      const int64_t len = rph[r + 1] - rph[r];
+      const int64_t e0 = q == 0 ? 0 : split_h[(size_t)rows * (q - 1) + r];
+      const int64_t e1 = q == P - 1 ? len : split_h[(size_t)rows * q + r];
+      lens[r] = e1 - e0;
+    }
+    bool ok = false;
+    TVR_TRY(build_sell_data(p, pl, transposed, prow, psl, lens,
+                            q == 0 ? nullptr : split_d + (size_t)rows * (q - 1),
+                            q == P - 1 ? nullptr : split_d + (size_t)rows * q, q * h,
+                            P > 1 ? h : 0, wlo, wlen, pl.sd[q], ok));
+    if (!ok) { pl.sd.clear(); return TVR_OK; }
+  }
+  if (P > 1) {
+    TVR_TRY(dev_alloc(p, (void**)&pl.sell_acc, sizeof(double) * std::max<int64_t>(1, rows * pl.rep)));
+    v.staged = true;
+    smem = sizeof(float) * ((size_t)h + (size_t)h / 32 + 1);
+  } else if (!pl.staged && env_int("TVR_SPMV_HALF", 1)) {
+    // a window too large for shared memory: its first part staged, the rest from global memory
     const int budget = env_int("TVR_SPMV_HALF_KB", 148) * 1024;
-    const int h = std::min<int>(pl.max_win, (int)((budget / 4) * 32 / 33) / 32 * 32);
-    if (h > 0 && pl.max_win > h) {
+    const int hh = std::min<int>(pl.max_win, (int)((budget / 4) * 32 / 33) / 32 * 32);
+    if (hh > 0 && pl.max_win > hh) {
       v.staged = v.half = true;
       v.unroll = env_int("TVR_SELL_HALF_UNROLL", 2);
       v.block = v.unroll == 3 ? 1024 : env_int("TVR_SELL_HALF_BLOCK", 1024);
-      smem = sizeof(float) * ((size_t)h + (size_t)h / 32 + 1);
-      pl.part_len = h;
+      smem = sizeof(float) * ((size_t)hh + (size_t)hh / 32 + 1);
+      pl.part_len = hh;
     }
   }
+  // a staged window that fits one 512-thread CTA per SM: one 1024-thread CTA instead
   if (v.staged && !v.half && spmv16s_occupancy(v, smem) == 1 && env_int("TVR_SPMV_WIDE", 1)) {
     SellVariant w = v;
     w.block = 1024;
     if (spmv16s_occupancy(w, smem) >= 1) v = w;
   }
+  const int64_t nblk = pl.sd[0].nblk;
+  pl.h_slice_item_end = pl.sd[0].h_slice_end;
   // slice-shared operator: Z consecutive slices per pass (spmv16z_kernel), as many staged
   // windows as fit one 1024-thread CTA's shared memory (TVR_SLICE_Z caps Z; 1 disables)
   pl.rep_total = pl.rep;
-  if (pl.rep > 1 && v.staged && !v.half) {
+  if (pl.rep > 1 && v.staged && !v.half && P == 1) {
     const int32_t ws = (int32_t)(((size_t)pl.max_win + pl.max_win / 32 + 1 + 3) / 4 * 4);
     int maxsm = 0;
     TVR_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device));
@@ -710,9 +806,12 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
   }
   if (pl.rep_total > 1) {  // per slice: one past the last block of the groups ending by it
     const int Z = v.zgroup;
-    pl.h_slice_item_end.resize(pl.rep_total);
-    for (int64_t z = 0; z < pl.rep_total; ++z)
-      pl.h_slice_item_end[z] = (z == pl.rep_total - 1 ? (int64_t)pl.rep : (z + 1) / Z) * nblk;
+    for (auto& d : pl.sd) {
+      d.h_slice_end.resize(pl.rep_total);
+      for (int64_t z = 0; z < pl.rep_total; ++z)
+        d.h_slice_end[z] = (z == pl.rep_total - 1 ? (int64_t)pl.rep : (z + 1) / Z) * d.nblk;
+    }
+    pl.h_slice_item_end = pl.sd[0].h_slice_end;
   }
   pl.sv = v;
   pl.smem = smem;
@@ -1445,24 +1544,17 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
     TVR_CUDA(cudaEventRecord(ev_in(c), p->s_in));
     TVR_TRY(mark("in" + std::to_string(c), p->s_in));
   }
-  auto items = [](const SpmvPlan& pl, int z0, int z1, int64_t& lo, int64_t& hi) {
-    lo = z0 > 0 ? pl.h_slice_item_end[z0 - 1] : 0;
-    hi = pl.h_slice_item_end[z1 - 1];
-  };
   const double bytes_row = entry_bytes(p->planA) * (double)p->nnz / nz;  // per slice, for counters
   for (int c = 0; c < C; ++c) {
     TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_in(c), 0));
     TVR_TRY(mark("A" + std::to_string(c) + ">", p->stream));
-    int64_t lo, hi;
-    items(p->planA, z[c], z[c + 1], lo, hi);
     TVR_TRY(launch(p, K_SPMV_A, bytes_row * (z[c + 1] - z[c]), [&] {
-      return run_spmv(p, p->planA, false, x, p->b, r, nullptr, p->dscal + SA + c, lo, hi);
+      return run_spmv(p, p->planA, false, x, p->b, r, nullptr, p->dscal + SA + c, z[c], z[c + 1]);
     }));
     TVR_TRY(mark("A" + std::to_string(c) + "<", p->stream));
     if (gh) {
-      items(p->planT, z[c], z[c + 1], lo, hi);
       TVR_TRY(launch(p, K_SPMV_AT, bytes_row * (z[c + 1] - z[c]), [&] {
-        return run_spmv(p, p->planT, true, r, nullptr, w, nullptr, nullptr, lo, hi);
+        return run_spmv(p, p->planT, true, r, nullptr, w, nullptr, nullptr, z[c], z[c + 1]);
       }));
       TVR_TRY(mark("AT" + std::to_string(c) + "<", p->stream));
     }

@@ -73,6 +73,25 @@ struct FlatPlan {
   int64_t n_empty = 0;
 };
 
+// One sliced-ELL structure (spmv16s_kernel): blocks of 32 rows of one slice each.  A window too
+// large for shared memory is cut into column parts, one structure per part (the part's entries
+// of every row, offsets relative to the part's window).
+struct SellData {
+  int64_t nblk = 0;
+  int64_t* off = nullptr;
+  int32_t* k = nullptr;
+  int32_t* slice = nullptr;
+  int64_t* zend = nullptr;
+  double* sq = nullptr;
+  int64_t* cum = nullptr;
+  int32_t* perm = nullptr;
+  uint16_t* col16 = nullptr;
+  float* val = nullptr;
+  int64_t* win_lo = nullptr;   // the plan's windows, shifted to the part
+  int32_t* win_len = nullptr;
+  std::vector<int64_t> h_slice_end;  // per slice: one past its last block
+};
+
 struct SpmvPlan {
   TmaPlan tma;
   FlatPlan flat;
@@ -87,14 +106,8 @@ struct SpmvPlan {
   int64_t rep_total = 0;               // slice groups (sv.zgroup > 1): slices; rep = groups
   int32_t wstride = 0;                 // slice groups: floats between the staged windows
   SellVariant sv;
-  int64_t sell_nblk = 0;
-  int64_t* sell_off = nullptr;
-  int32_t* sell_k = nullptr;
-  int32_t* sell_slice = nullptr;
-  int64_t* sell_zend = nullptr;
-  double* sell_sq = nullptr;
-  int64_t* sell_cum = nullptr;
-  int32_t* sell_perm = nullptr;
+  std::vector<SellData> sd;            // one structure, or one per column part (sell_parts)
+  double* sell_acc = nullptr;          // column parts: per-row fp64 partial sums between parts
   int64_t* rpp = nullptr;
   uint16_t* col16p = nullptr;  // 16-bit plans
   int32_t* col32p = nullptr;   // int32 global-gather plans

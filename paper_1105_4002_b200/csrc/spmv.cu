@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
       }
       const uint16_t* cp = a.col16 + (off * 32 + lane) * 8;
       const float* vp = a.val + (off * 32 + lane) * 8;
-      double acc = 0.0;
+      double acc = (a.acc_in && row >= 0) ? a.acc_in[row + row_off] : 0.0;
       int s = 0;
       for (; s + UNR <= K; s += UNR) {
         int4 c[UNR];
@@ -642,7 +642,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
                     : chunk8_sum<STAGED>(c0, va0, vb0, stage, gbase);
       }
       double q = 0.0;
-      if (row >= 0) {
+      if (row >= 0 && a.acc_out) {
+        a.acc_out[row + row_off] = acc;
+      } else if (row >= 0) {
         const int64_t orow = row + row_off;
         if (a.b) {
           const double r = acc - (double)__ldg(a.b + orow);
@@ -861,28 +863,56 @@ int spmv16s_occupancy(const SellVariant& v, size_t smem) {
 
 // Sliced-ELL copy: lane l of block j holds row perm[32 j + l]; its entry e goes to chunk step
 // off_j + e / 8, lane l, position e % 8.  One thread per (block, lane); zero pads by memset.
+// Column parts: lane l's row contributes its entries [lo_off[row], hi_off[row]) (null: 0 / the
+// row's length) with the part's window start coff subtracted from the 16-bit offsets.
 __global__ void sell_fill_kernel(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
-                                 const int64_t* rp, const uint16_t* col16, const float* val,
+                                 const int64_t* rp, const int32_t* lo_off, const int32_t* hi_off,
+                                 uint16_t coff, const uint16_t* col16, const float* val,
                                  uint16_t* col16s, float* vals) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= nslots) return;
   const int row = perm[t];
   if (row < 0) return;
-  const int64_t j = t >> 5, l = t & 31, s = rp[row], len = rp[row + 1] - s;
+  const int64_t j = t >> 5, l = t & 31;
+  const int64_t e0 = lo_off ? lo_off[row] : 0;
+  const int64_t e1 = hi_off ? hi_off[row] : rp[row + 1] - rp[row];
+  const int64_t s = rp[row] + e0, len = e1 - e0;
   const int64_t base = blk_off[j];
   for (int64_t e = 0; e < len; ++e) {
     const int64_t d = ((base + (e >> 3)) * 32 + l) * 8 + (e & 7);
-    col16s[d] = col16[s + e];
+    col16s[d] = (uint16_t)(col16[s + e] - coff);
     vals[d] = val[s + e];
   }
 }
 
 cudaError_t launch_sell_fill(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
-                             const int64_t* rp, const uint16_t* col16, const float* val,
+                             const int64_t* rp, const int32_t* lo_off, const int32_t* hi_off,
+                             uint16_t coff, const uint16_t* col16, const float* val,
                              uint16_t* col16s, float* vals, cudaStream_t st) {
   if (nslots <= 0) return cudaSuccess;
-  sell_fill_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(nslots, perm, blk_off, rp,
-                                                                    col16, val, col16s, vals);
+  sell_fill_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(
+      nslots, perm, blk_off, rp, lo_off, hi_off, coff, col16, val, col16s, vals);
+  return cudaGetLastError();
+}
+
+__global__ void sell_split_kernel(int64_t rows, const int64_t* rp, const uint16_t* col16, int h,
+                                  int32_t* split) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  int64_t lo = rp[r], hi = rp[r + 1];
+  const int64_t s = lo;
+  while (lo < hi) {  // columns ascend within a row
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int)col16[mid] < h) lo = mid + 1;
+    else hi = mid;
+  }
+  split[r] = (int32_t)(lo - s);
+}
+
+cudaError_t launch_sell_split(int64_t rows, const int64_t* rp, const uint16_t* col16, int h,
+                              int32_t* split, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  sell_split_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(rows, rp, col16, h, split);
   return cudaGetLastError();
 }
 

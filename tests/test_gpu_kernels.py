@@ -388,6 +388,48 @@ def test_sell_spmv(tvreg, cfg, c1, monkeypatch):
     assert rel(r, outs["0"][0]) <= 1e-7 and rel(w, outs["0"][2]) <= 1e-7
 
 
+@pytest.mark.parametrize("cfg,floats", [("zoo", "96"), ("zoo", "128"), ("c1", "300"), ("c1", "512")])
+def test_sell_column_parts(tvreg, cfg, floats, c1, monkeypatch):
+    """Windows larger than shared memory cut into column parts (the c3 A pass): each row's
+    entries split at the part boundaries, one sliced-ELL pass per part with the fp64 row sum
+    carried between passes; forced here on small windows (TVR_SELL_PART_FLOATS).  Exact on dyadic
+    data (rows spanning every part, empty parts), fp32 rounding otherwise, and the e2e pipeline's
+    gradient equals the device one."""
+    monkeypatch.setenv("TVR_SPMV_STAGE", "0")
+    monkeypatch.setenv("TVR_SELL_PART_FLOATS", floats)
+    rng = np.random.default_rng(13)
+    if cfg == "zoo":
+        grid = (16, 16, 4)
+        A = _separable_zoo(16, 16, 4, 6)
+        x = rng.integers(0, 9, A.n_cols).astype(np.float32)
+        b = rng.integers(0, 9, A.n_rows).astype(np.float32)
+    else:
+        A, grid = c1.A, c1.grid
+        x = harness.random_x(A.n_cols)
+        b = c1.b
+    P = make(tvreg, A, b, grid)
+    r = torch.empty(A.n_rows, device="cuda")
+    fid = P.residual(dev(x), r)
+    w = torch.empty(A.n_cols, device="cuda")
+    P.apply_AT(dev(b), w)
+    r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x.astype(np.float64)) - b
+    w_ora = oracle.rmatvec(A.row_ptr, A.col, A.val, b.astype(np.float64), A.n_cols)
+    rr, ww = host(r).astype(np.float64), host(w).astype(np.float64)
+    if cfg == "zoo":
+        assert np.array_equal(rr, r_ora) and np.array_equal(ww, w_ora)
+        assert fid == 0.5 * float(r_ora @ r_ora)
+    else:
+        assert rel(rr, r_ora) <= 1e-6 and rel(ww, w_ora) <= 1e-6
+        assert abs(fid - 0.5 * float(r_ora @ r_ora)) <= 1e-6 * fid
+    g = torch.empty(A.n_cols, device="cuda")
+    f, _ = P.objective_grad(dev(x), g)
+    xh = torch.from_numpy(np.ascontiguousarray(x, np.float32)).pin_memory()
+    gh = torch.empty(A.n_cols, dtype=torch.float32).pin_memory()
+    fh, _ = P.objective_grad_host(xh.numpy(), gh.numpy())
+    assert torch.equal(gh, g.cpu()) and abs(fh - f) <= 1e-13 * abs(f)
+    P.close()
+
+
 @pytest.mark.parametrize("cap", [1024, 300, 128])
 def test_window_parts_match_oracle(tvreg, c1, cap, monkeypatch):
     """Slice windows cut into parts (the c3 A pass path): rows' entries split at part boundaries,
