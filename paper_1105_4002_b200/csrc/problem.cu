@@ -1344,6 +1344,7 @@ void tvr_destroy(tvr_problem* p) {
   }
   dist_release(p);
   dev_free_all(p);
+  if (p->e2e_exec) cudaGraphExecDestroy(p->e2e_exec);
   for (auto e : p->pipe_ev) cudaEventDestroy(e);
   if (p->s_in) cudaStreamDestroy(p->s_in);
   if (p->s_out) cudaStreamDestroy(p->s_out);
@@ -1529,58 +1530,92 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
     tr.emplace_back(name, e);
     return TVR_OK;
   };
-  TVR_TRY(mark("start", p->stream));
-  TVR_CUDA(cudaEventRecord(ev_start, p->stream));
-  TVR_CUDA(cudaStreamWaitEvent(p->s_in, ev_start, 0));
-  TVR_CUDA(cudaStreamWaitEvent(p->s_out, ev_start, 0));
-  // TVR_E2E_UPFRONT=1: x goes up whole before any pass (an H2D copy running under the SpMV
-  // passes slows them by ~25 %, measured; D2H copies do not), only the downloads overlap
-  const bool upfront = env_int("TVR_E2E_UPFRONT", 0) != 0;
-  for (int c = 0; c < C; ++c) {
-    const size_t off = (size_t)z[c] * plane, cnt = (size_t)(z[c + 1] - z[c]) * plane;
-    if (!upfront || c == 0)
-      TVR_CUDA(cudaMemcpyAsync(x + off, xh + off, sizeof(float) * (upfront ? (size_t)nz * plane : cnt),
-                               cudaMemcpyHostToDevice, p->s_in));
-    TVR_CUDA(cudaEventRecord(ev_in(c), p->s_in));
-    TVR_TRY(mark("in" + std::to_string(c), p->s_in));
-  }
-  const double bytes_row = entry_bytes(p->planA) * (double)p->nnz / nz;  // per slice, for counters
-  for (int c = 0; c < C; ++c) {
-    TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_in(c), 0));
-    TVR_TRY(mark("A" + std::to_string(c) + ">", p->stream));
-    TVR_TRY(launch(p, K_SPMV_A, bytes_row * (z[c + 1] - z[c]), [&] {
-      return run_spmv(p, p->planA, false, x, p->b, r, nullptr, p->dscal + SA + c, z[c], z[c + 1]);
-    }));
-    TVR_TRY(mark("A" + std::to_string(c) + "<", p->stream));
-    if (gh) {
-      TVR_TRY(launch(p, K_SPMV_AT, bytes_row * (z[c + 1] - z[c]), [&] {
-        return run_spmv(p, p->planT, true, r, nullptr, w, nullptr, nullptr, z[c], z[c + 1]);
+  // The whole pipeline (copies, events, passes on three streams) as one enqueue; replayed as a
+  // CUDA graph while the host buffers and chunking stay the same (TVR_E2E_GRAPH=0: eager)
+  auto enqueue = [&]() -> int {
+    TVR_TRY(mark("start", p->stream));
+    TVR_CUDA(cudaEventRecord(ev_start, p->stream));
+    TVR_CUDA(cudaStreamWaitEvent(p->s_in, ev_start, 0));
+    TVR_CUDA(cudaStreamWaitEvent(p->s_out, ev_start, 0));
+    // TVR_E2E_UPFRONT=1: x goes up whole before any pass (an H2D copy running under the SpMV
+    // passes slows them by ~25 %, measured; D2H copies do not), only the downloads overlap
+    const bool upfront = env_int("TVR_E2E_UPFRONT", 0) != 0;
+    for (int c = 0; c < C; ++c) {
+      const size_t off = (size_t)z[c] * plane, cnt = (size_t)(z[c + 1] - z[c]) * plane;
+      if (!upfront || c == 0)
+        TVR_CUDA(cudaMemcpyAsync(x + off, xh + off, sizeof(float) * (upfront ? (size_t)nz * plane : cnt),
+                                 cudaMemcpyHostToDevice, p->s_in));
+      TVR_CUDA(cudaEventRecord(ev_in(c), p->s_in));
+      TVR_TRY(mark("in" + std::to_string(c), p->s_in));
+    }
+    const double bytes_row = entry_bytes(p->planA) * (double)p->nnz / nz;  // per slice, for counters
+    for (int c = 0; c < C; ++c) {
+      TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_in(c), 0));
+      TVR_TRY(mark("A" + std::to_string(c) + ">", p->stream));
+      TVR_TRY(launch(p, K_SPMV_A, bytes_row * (z[c + 1] - z[c]), [&] {
+        return run_spmv(p, p->planA, false, x, p->b, r, nullptr, p->dscal + SA + c, z[c], z[c + 1]);
       }));
-      TVR_TRY(mark("AT" + std::to_string(c) + "<", p->stream));
+      TVR_TRY(mark("A" + std::to_string(c) + "<", p->stream));
+      if (gh) {
+        TVR_TRY(launch(p, K_SPMV_AT, bytes_row * (z[c + 1] - z[c]), [&] {
+          return run_spmv(p, p->planT, true, r, nullptr, w, nullptr, nullptr, z[c], z[c + 1]);
+        }));
+        TVR_TRY(mark("AT" + std::to_string(c) + "<", p->stream));
+      }
+      if (c + 1 < C) TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_in(c + 1), 0));  // plane z[c+1]
+      TVArgs a = tv_args(p, ST + 6 * c);
+      const int64_t off = (int64_t)z[c] * plane;
+      a.zg0 = p->z0 + z[c];
+      a.nzl = z[c + 1] - z[c];
+      a.w1 = gh ? w + off : nullptr;
+      a.g_out = gh ? g + off : nullptr;
+      const double N = (double)a.nzl * plane;
+      TVR_TRY(mark("TV" + std::to_string(c) + ">", p->stream));
+      TVR_TRY(launch(p, K_TV_GRAD, N * (gh ? 12.0 : 8.0),
+                     [&] { return launch_tv_grad_plain(a, x + off, p->stream); }));
+      TVR_TRY(mark("TV" + std::to_string(c) + "<", p->stream));
+      if (gh) {
+        TVR_CUDA(cudaEventRecord(ev_g(c), p->stream));
+        TVR_CUDA(cudaStreamWaitEvent(p->s_out, ev_g(c), 0));
+        TVR_CUDA(cudaMemcpyAsync(gh + off, g + off, sizeof(float) * N, cudaMemcpyDeviceToHost, p->s_out));
+        TVR_TRY(mark("out" + std::to_string(c), p->s_out));
+      }
     }
-    if (c + 1 < C) TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_in(c + 1), 0));  // plane z[c+1]
-    TVArgs a = tv_args(p, ST + 6 * c);
-    const int64_t off = (int64_t)z[c] * plane;
-    a.zg0 = p->z0 + z[c];
-    a.nzl = z[c + 1] - z[c];
-    a.w1 = gh ? w + off : nullptr;
-    a.g_out = gh ? g + off : nullptr;
-    const double N = (double)a.nzl * plane;
-    TVR_TRY(mark("TV" + std::to_string(c) + ">", p->stream));
-    TVR_TRY(launch(p, K_TV_GRAD, N * (gh ? 12.0 : 8.0),
-                   [&] { return launch_tv_grad_plain(a, x + off, p->stream); }));
-    TVR_TRY(mark("TV" + std::to_string(c) + "<", p->stream));
-    if (gh) {
-      TVR_CUDA(cudaEventRecord(ev_g(c), p->stream));
-      TVR_CUDA(cudaStreamWaitEvent(p->s_out, ev_g(c), 0));
-      TVR_CUDA(cudaMemcpyAsync(gh + off, g + off, sizeof(float) * N, cudaMemcpyDeviceToHost, p->s_out));
-      TVR_TRY(mark("out" + std::to_string(c), p->s_out));
+    TVR_CUDA(cudaEventRecord(ev_done, p->s_out));
+    TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_done, 0));
+    TVR_CUDA(cudaMemcpyAsync(p->hscal, p->dscal, sizeof(double) * 64, cudaMemcpyDeviceToHost, p->stream));
+    TVR_TRY(mark("end", p->stream));
+    return TVR_OK;
+  };
+  const bool graph = !trace && !p->prof && env_int("TVR_E2E_GRAPH", 1) != 0;
+  if (graph) {
+    if (!p->e2e_exec || p->e2e_xh != xh || p->e2e_gh != gh || p->e2e_z != z) {
+      if (p->e2e_exec) { cudaGraphExecDestroy(p->e2e_exec); p->e2e_exec = nullptr; }
+      const int64_t l0 = p->launches;
+      const double b0 = p->bytes_total;
+      TVR_CUDA(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeRelaxed));
+      const int st = enqueue();
+      cudaGraph_t gr = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(p->stream, &gr);
+      p->e2e_launches = p->launches - l0;
+      p->e2e_bytes = p->bytes_total - b0;
+      p->launches = l0;
+      p->bytes_total = b0;
+      if (st < 0) { if (gr) cudaGraphDestroy(gr); return st; }
+      TVR_CUDA(e);
+      const cudaError_t ei = cudaGraphInstantiate(&p->e2e_exec, gr, 0);
+      cudaGraphDestroy(gr);
+      TVR_CUDA(ei);
+      p->e2e_xh = xh;
+      p->e2e_gh = gh;
+      p->e2e_z = z;
     }
+    TVR_CUDA(cudaGraphLaunch(p->e2e_exec, p->stream));
+    p->launches += p->e2e_launches;
+    p->bytes_total += p->e2e_bytes;
+  } else {
+    TVR_TRY(enqueue());
   }
-  TVR_CUDA(cudaEventRecord(ev_done, p->s_out));
-  TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_done, 0));
-  TVR_CUDA(cudaMemcpyAsync(p->hscal, p->dscal, sizeof(double) * 64, cudaMemcpyDeviceToHost, p->stream));
-  TVR_TRY(mark("end", p->stream));
   TVR_CUDA(cudaStreamSynchronize(p->stream));
   if (trace) {
     std::string line = "e2e trace (us):";

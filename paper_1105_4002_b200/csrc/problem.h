@@ -202,6 +202,13 @@ struct tvr_problem {
 
   // e2e pipeline of tvr_objective_grad_host (created on first use)
   cudaStream_t s_in = nullptr, s_out = nullptr;
+  // host-buffer pipeline as a CUDA graph, for these host buffers and chunk boundaries
+  cudaGraphExec_t e2e_exec = nullptr;
+  const float* e2e_xh = nullptr;
+  const float* e2e_gh = nullptr;
+  std::vector<int> e2e_z;
+  int64_t e2e_launches = 0;
+  double e2e_bytes = 0.0;
   std::vector<cudaEvent_t> pipe_ev;
 
   // profiling
