@@ -154,6 +154,32 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
 static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed, const float* src,
                             const float* b, float* out, float* out_lo, double* scal,
                             int z_lo = 0, int z_hi = -1) {
+  if (pl.sell32) {  // int32 sliced ELL (non-separable: no slice ranges)
+    const SellData& d = pl.sd[0];
+    SellArgs s{};
+    s.blk_off = d.off;
+    s.blk_k = d.k;
+    s.blk_slice = d.slice;
+    s.zend = d.zend;
+    s.blk_sq = d.sq;
+    s.cum = d.cum;
+    s.perm = d.perm;
+    s.col32 = d.col32;
+    s.val = d.val;
+    s.src = src;
+    s.b = b;
+    s.out = out;
+    s.out_lo = out_lo;
+    s.blk_lo = 0;
+    s.blk_hi = d.nblk;
+    s.nb = d.nblk;
+    s.rep = 1;
+    s.partials = p->partials;
+    s.counter = p->counter;
+    s.scal = scal;
+    if (d.nblk == 0) return scal ? cudaMemsetAsync(scal, 0, sizeof(double), p->stream) : cudaSuccess;
+    return launch_spmv32s(s, pl.sv.unroll, (int)std::min<int64_t>(pl.pad_grid, d.nblk), p->stream);
+  }
   if (pl.sell) {  // slices [z_lo, z_hi) (the e2e pipeline's chunks) or all; column parts in order
     const int P = (int)pl.sd.size();
     for (int q = 0; q < P; ++q) {
@@ -821,6 +847,64 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
   return TVR_OK;
 }
 
+// Int32 sliced ELL (spmv32s_kernel, TVR_SPMV_SELL32, non-separable plans): blocks of 32
+// consecutive rows padded to their longest row in 4-entry chunks; replaces the padded copy.
+static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::vector<int64_t>& rph,
+                       int64_t rows) {
+  pl.sell32 = false;
+  if (rows >= ((int64_t)1 << 31) || rows == 0) return TVR_OK;
+  const int64_t nblk = (rows + 31) / 32;
+  std::vector<int64_t> off(nblk), cum(nblk + 1, 0);
+  std::vector<int32_t> kk(nblk), sl(nblk, 0), perm((size_t)nblk * 32);
+  int64_t steps = 0;
+  for (int64_t j = 0; j < nblk; ++j) {
+    int64_t K = 0;
+    for (int64_t l = 0; l < 32; ++l) {
+      const int64_t r = j * 32 + l;
+      perm[(size_t)j * 32 + l] = r < rows ? (int32_t)r : -1;
+      if (r < rows) K = std::max<int64_t>(K, (rph[r + 1] - rph[r] + 3) / 4);
+    }
+    off[j] = steps;
+    kk[j] = (int32_t)K;
+    cum[j + 1] = cum[j] + K + 2;
+    steps += K;
+  }
+  const size_t cap = (size_t)steps * 128 + 8;
+  const size_t need = cap * 8 + (size_t)nblk * (8 + 4 + 4 + 8 + 128 + 8);
+  size_t fr = 0, tot = 0;
+  TVR_CUDA(cudaMemGetInfo(&fr, &tot));
+  if (need + ((size_t)1 << 30) > fr) return TVR_OK;  // keep 1 GB of headroom
+  SellData d;
+  std::vector<int64_t> zend(1, nblk), wl(1, 0);
+  std::vector<int32_t> wn(1, 0);
+  TVR_TRY(upload(p, (void**)&d.off, off.data(), sizeof(int64_t) * off.size()));
+  TVR_TRY(upload(p, (void**)&d.k, kk.data(), sizeof(int32_t) * kk.size()));
+  TVR_TRY(upload(p, (void**)&d.slice, sl.data(), sizeof(int32_t) * sl.size()));
+  TVR_TRY(upload(p, (void**)&d.cum, cum.data(), sizeof(int64_t) * cum.size()));
+  TVR_TRY(upload(p, (void**)&d.zend, zend.data(), sizeof(int64_t)));
+  TVR_TRY(upload(p, (void**)&d.win_lo, wl.data(), sizeof(int64_t)));
+  TVR_TRY(upload(p, (void**)&d.win_len, wn.data(), sizeof(int32_t)));
+  TVR_TRY(dev_alloc(p, (void**)&d.sq, sizeof(double) * std::max<int64_t>(1, nblk)));
+  TVR_TRY(upload(p, (void**)&d.perm, perm.data(), sizeof(int32_t) * perm.size()));
+  TVR_TRY(dev_alloc(p, (void**)&d.val, sizeof(float) * cap));
+  TVR_CUDA(cudaMemsetAsync(d.val, 0, sizeof(float) * cap, p->stream));
+  TVR_TRY(dev_alloc(p, (void**)&d.col32, sizeof(int32_t) * cap));
+  TVR_CUDA(cudaMemsetAsync(d.col32, 0, sizeof(int32_t) * cap, p->stream));
+  TVR_CUDA(launch_sell_fill32(nblk * 32, d.perm, d.off, transposed ? p->rpT : p->rp,
+                              transposed ? p->colT : p->col, transposed ? p->valT : p->val,
+                              d.col32, d.val, p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));  // host vectors die here
+  d.nblk = nblk;
+  d.h_slice_end = zend;
+  pl.sd.assign(1, d);
+  pl.sv = SellVariant();
+  pl.sv.unroll = env_int("TVR_SELL32_UNROLL", 2);
+  pl.pad_grid = (int)std::min<int64_t>((int64_t)p->num_sms * spmv32s_occupancy(pl.sv.unroll),
+                                       std::max<int64_t>(1, nblk));
+  pl.sell32 = true;
+  return TVR_OK;
+}
+
 // rp: host row pointer of the operator (n_rows+1); slices: n_slices+1 row boundaries when
 // separable; windows: per slice gather window (lo, len); pitch padding for the A pass.
 static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& rp, int64_t n_rows,
@@ -1231,6 +1315,14 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     TVR_CUDA(cudaMemcpyAsync(rph.data(), which ? p->rpT : p->rp, sizeof(int64_t) * (rows + 1),
                              cudaMemcpyDeviceToHost, p->stream));
     TVR_CUDA(cudaStreamSynchronize(p->stream));
+    // int32 sliced ELL for the A^T pass (voxel rows: a block's lanes gather neighbouring ray ids,
+    // c5 A^T 5.62 -> 3.69 ms); the A pass keeps the per-row kernel (parallel rays in one block
+    // gather unrelated lines: c5 A 6.20 -> 6.99 ms), TVR_SPMV_SELL32 = 0 none / 1 A^T / 2 both
+    const int s32 = env_int("TVR_SPMV_SELL32", 1);
+    if (p32 && (s32 == 2 || (s32 == 1 && which == 1)) && !(which == 1 && views_dist(p))) {
+      TVR_TRY(make_sell32(p, pl, which == 1, rph, rows));
+      if (pl.sell32) continue;
+    }
     if (p16 && p->separable && (env_int("TVR_SPMV_SELL", 1) || sliced)) {
       TVR_TRY(make_sell(p, pl, which == 1, rph, rows));
       if (pl.sell) continue;

@@ -817,6 +817,141 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16z_kernel(SellArgs a) {
   }
 }
 
+// Sliced ELL over int32 global columns (non-separable geometry; spmv32s_kernel): blocks of 32
+// consecutive rows (no sorting: neighbouring rays / voxels share a block, so at each step the
+// lanes gather neighbouring entries of x or r, and the lengths of neighbours are close), each
+// padded with zero 4-entry chunks to its longest row, stored [block step][lane][4 entries].
+// The gathers go through L1 (__ldg); warps take blocks from a shared counter; per-block sums
+// as spmv16s_kernel (deterministic).
+template <int UNR>
+__global__ void __launch_bounds__(512, 2) spmv32s_kernel(SellArgs a) {
+  __shared__ int s_next;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 512 >> 5;
+  int64_t b0, b1;
+  sell_cta_range(a, b0, b1);
+  if (threadIdx.x == 0) s_next = nwarps;
+  __syncthreads();
+  int64_t k = b0 + warp;
+  int64_t off = 0;
+  int K = 0, row = -1;
+  if (k < b1) {
+    off = a.blk_off[k];
+    K = a.blk_k[k];
+    row = a.perm[k * 32 + lane];
+  }
+  while (k < b1) {
+    int nx = 0;
+    if (lane == 0) nx = atomicAdd(&s_next, 1);
+    const int64_t kn = b0 + __shfl_sync(0xffffffffu, nx, 0);
+    int64_t off_n = 0;
+    int K_n = 0, row_n = -1;
+    if (kn < b1) {
+      off_n = a.blk_off[kn];
+      K_n = a.blk_k[kn];
+      row_n = a.perm[kn * 32 + lane];
+    }
+    const int32_t* cp = a.col32 + (off * 32 + lane) * 4;
+    const float* vp = a.val + (off * 32 + lane) * 4;
+    double acc = 0.0;
+    auto chunk = [&](const int4 c, const float4 v) {
+      const double p0 = (double)v.x * (double)__ldg(a.src + c.x);
+      const double p1 = (double)v.y * (double)__ldg(a.src + c.y);
+      const double p2 = (double)v.z * (double)__ldg(a.src + c.z);
+      const double p3 = (double)v.w * (double)__ldg(a.src + c.w);
+      return (p0 + p1) + (p2 + p3);
+    };
+    int s = 0;
+    for (; s + UNR <= K; s += UNR) {
+      int4 c[UNR];
+      float4 v[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        c[u] = ld_stream_i4(cp + (s + u) * 128);
+        v[u] = ld_stream_f4(vp + (s + u) * 128);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) acc += chunk(c[u], v[u]);
+    }
+    for (; s < K; ++s) acc += chunk(ld_stream_i4(cp + s * 128), ld_stream_f4(vp + s * 128));
+    double q = 0.0;
+    if (row >= 0) {
+      if (a.b) {
+        const double r = acc - (double)__ldg(a.b + row);
+        const float rh = (float)r;
+        a.out[row] = rh;
+        if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
+        q = r * r;
+      } else {
+        a.out[row] = (float)acc;
+      }
+    }
+    if (a.scal) {
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) q += __shfl_xor_sync(0xffffffffu, q, d);
+      if (lane == 0) a.blk_sq[k] = q;
+    }
+    k = kn;
+    off = off_n;
+    K = K_n;
+    row = row_n;
+  }
+  if (a.scal) {
+    double sq = 0.0;
+    __syncthreads();
+    if (warp == 0) {
+      double t = 0.0;
+      for (int64_t kk = b0 + lane; kk < b1; kk += 32) t += a.blk_sq[kk];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+      if (lane == 0) sq = t;
+    }
+    double v[1] = {sq};
+    reduce_to_scalars<1>(v, a.partials, a.counter, a.scal);
+  }
+}
+
+cudaError_t launch_spmv32s(const SellArgs& a, int unroll, int grid, cudaStream_t st) {
+  if (a.blk_hi <= a.blk_lo) return cudaSuccess;
+  if (unroll >= 3) spmv32s_kernel<3><<<grid, 512, 0, st>>>(a);
+  else if (unroll == 2) spmv32s_kernel<2><<<grid, 512, 0, st>>>(a);
+  else spmv32s_kernel<1><<<grid, 512, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+int spmv32s_occupancy(int unroll) {
+  int occ = 0;
+  const void* k = unroll >= 3 ? (const void*)spmv32s_kernel<3>
+                              : unroll == 2 ? (const void*)spmv32s_kernel<2> : (const void*)spmv32s_kernel<1>;
+  ensure_smem_attr(k, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 512, 0);
+  return occ > 0 ? occ : 1;
+}
+
+__global__ void sell_fill32_kernel(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
+                                   const int64_t* rp, const int32_t* col, const float* val,
+                                   int32_t* cols, float* vals) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nslots) return;
+  const int row = perm[t];
+  if (row < 0) return;
+  const int64_t j = t >> 5, l = t & 31, s = rp[row], len = rp[row + 1] - s;
+  const int64_t base = blk_off[j];
+  for (int64_t e = 0; e < len; ++e) {
+    const int64_t d = ((base + (e >> 2)) * 32 + l) * 4 + (e & 3);
+    cols[d] = col[s + e];
+    vals[d] = val[s + e];
+  }
+}
+
+cudaError_t launch_sell_fill32(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
+                               const int64_t* rp, const int32_t* col, const float* val,
+                               int32_t* cols, float* vals, cudaStream_t st) {
+  if (nslots <= 0) return cudaSuccess;
+  sell_fill32_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(nslots, perm, blk_off, rp,
+                                                                      col, val, cols, vals);
+  return cudaGetLastError();
+}
+
 template <class F>
 static cudaError_t dispatch16s(const SellVariant& v, F&& f) {
   if (v.zgroup == 2) return f(spmv16z_kernel<2, 1>);

@@ -430,6 +430,41 @@ def test_sell_column_parts(tvreg, cfg, floats, c1, monkeypatch):
     P.close()
 
 
+@pytest.mark.parametrize("cfg", ["zoo", "sphere"])
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+def test_sell32_spmv(tvreg, cfg, mode, monkeypatch):
+    """Int32 sliced ELL for non-separable matrices (spmv32s_kernel; TVR_SPMV_SELL32 = 0 none,
+    1 the A^T pass, 2 both): exact on dyadic data with rows of every length class, the oracle to
+    fp32 rounding on the paper's sphere geometry."""
+    monkeypatch.setenv("TVR_SPMV_SELL32", mode)
+    rng = np.random.default_rng(21)
+    if cfg == "zoo":
+        grid = (16, 16, 4)
+        A = _row_length_zoo(16 * 16 * 4, 9)
+        x = rng.integers(0, 9, A.n_cols).astype(np.float32)
+        b = rng.integers(0, 9, A.n_rows).astype(np.float32)
+    else:
+        grid = (24, 24, 24)
+        A = harness.siddon_sphere(24, 24, 24, 7, 33, 33)
+        x = harness.random_x(A.n_cols)
+        b = rng.random(A.n_rows).astype(np.float32)
+    P = make(tvreg, A, b, grid)
+    r = torch.empty(A.n_rows, device="cuda")
+    fid = P.residual(dev(x), r)
+    w = torch.empty(A.n_cols, device="cuda")
+    P.apply_AT(dev(b), w)
+    P.close()
+    r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x.astype(np.float64)) - b
+    w_ora = oracle.rmatvec(A.row_ptr, A.col, A.val, b.astype(np.float64), A.n_cols)
+    rr, ww = host(r).astype(np.float64), host(w).astype(np.float64)
+    if cfg == "zoo":
+        assert np.array_equal(rr, r_ora) and np.array_equal(ww, w_ora)
+        assert fid == 0.5 * float(r_ora @ r_ora)
+    else:
+        assert rel(rr, r_ora) <= 1e-6 and rel(ww, w_ora) <= 1e-6
+        assert abs(fid - 0.5 * float(r_ora @ r_ora)) <= 1e-6 * fid
+
+
 @pytest.mark.parametrize("cap", [1024, 300, 128])
 def test_window_parts_match_oracle(tvreg, c1, cap, monkeypatch):
     """Slice windows cut into parts (the c3 A pass path): rows' entries split at part boundaries,
