@@ -82,7 +82,9 @@ struct SellArgs {
   const double* acc_in;     // column parts after the first: each row starts from acc_in[row]
   double* acc_out;          // column parts before the last: the row's fp64 sum goes here
   const uint16_t* col16;    // [step][lane][8] window offsets (zero pads)
-  const int32_t* col32;     // spmv32s_kernel: [step][lane][4] int32 global columns
+  const int32_t* col32;     // spmv32s_kernel: int32 global columns in 4-entry chunks
+  const int64_t* row_start; // spmv32s_kernel row-mode blocks: per slot, row start (chunks)
+  const int64_t* rp;        // spmv32s_kernel row-mode blocks: the CSR row pointer (lengths)
   const float* val;         // [step][lane][8] values (zero pads)
   const float* src;
   const float* b;           // non-null: out = A src - b, sum r^2
@@ -120,8 +122,11 @@ cudaError_t launch_sell_fill(int64_t nslots, const int32_t* perm, const int64_t*
 cudaError_t launch_spmv32s(const SellArgs& a, int unroll, int grid, cudaStream_t st);
 int spmv32s_occupancy(int unroll);
 cudaError_t launch_sell_fill32(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
-                               const int64_t* rp, const int32_t* col, const float* val,
-                               int32_t* cols, float* vals, cudaStream_t st);
+                               const int32_t* blk_k, const int64_t* row_start, const int64_t* rp,
+                               const int32_t* col, const float* val, int32_t* cols, float* vals,
+                               cudaStream_t st);
+cudaError_t launch_sell32_mode(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,
+                               uint8_t* mode, cudaStream_t st);
 // per row: the first entry offset (from rp[r]) whose 16-bit column is >= h
 cudaError_t launch_sell_split(int64_t rows, const int64_t* rp, const uint16_t* col16, int h,
                               int32_t* split, cudaStream_t st);

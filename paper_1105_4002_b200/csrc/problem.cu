@@ -165,6 +165,8 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     s.cum = d.cum;
     s.perm = d.perm;
     s.col32 = d.col32;
+    s.row_start = d.row_start;
+    s.rp = transposed ? p->rpT : p->rp;
     s.val = d.val;
     s.src = src;
     s.b = b;
@@ -848,31 +850,54 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
 }
 
 // Int32 sliced ELL (spmv32s_kernel, TVR_SPMV_SELL32, non-separable plans): blocks of 32
-// consecutive rows padded to their longest row in 4-entry chunks; replaces the padded copy.
+// consecutive rows; per block lane mode (padded to the longest row, one row per lane) or, with
+// `modes`, row mode (rows back to back, 8 lanes per row) when its gathers change cache lines less
+// often.  Replaces the padded copy.
 static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::vector<int64_t>& rph,
-                       int64_t rows) {
+                       int64_t rows, bool modes) {
   pl.sell32 = false;
   if (rows >= ((int64_t)1 << 31) || rows == 0) return TVR_OK;
   const int64_t nblk = (rows + 31) / 32;
-  std::vector<int64_t> off(nblk), cum(nblk + 1, 0);
+  std::vector<uint8_t> mode(nblk, 0);
+  if (modes) {
+    uint8_t* md = nullptr;
+    TVR_CUDA(cudaMalloc(&md, nblk));
+    cudaError_t e = launch_sell32_mode(nblk, rows, transposed ? p->rpT : p->rp,
+                                       transposed ? p->colT : p->col, md, p->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(mode.data(), md, nblk, cudaMemcpyDeviceToHost, p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    cudaFree(md);
+    TVR_CUDA(e);
+  }
+  std::vector<int64_t> off(nblk), cum(nblk + 1, 0), rstart((size_t)nblk * 32, 0);
   std::vector<int32_t> kk(nblk), sl(nblk, 0), perm((size_t)nblk * 32);
-  int64_t steps = 0;
+  int64_t chunks = 0, n_row_mode = 0;
   for (int64_t j = 0; j < nblk; ++j) {
-    int64_t K = 0;
+    int64_t K = 0, tot = 0;
     for (int64_t l = 0; l < 32; ++l) {
       const int64_t r = j * 32 + l;
       perm[(size_t)j * 32 + l] = r < rows ? (int32_t)r : -1;
-      if (r < rows) K = std::max<int64_t>(K, (rph[r + 1] - rph[r] + 3) / 4);
+      const int64_t n = r < rows ? (rph[r + 1] - rph[r] + 3) / 4 : 0;
+      rstart[(size_t)j * 32 + l] = tot;
+      tot += n;
+      K = std::max(K, n);
     }
-    off[j] = steps;
-    kk[j] = (int32_t)K;
-    cum[j + 1] = cum[j] + K + 2;
-    steps += K;
+    off[j] = chunks;
+    if (mode[j]) {
+      kk[j] = (int32_t)-tot;
+      chunks += tot;
+      cum[j + 1] = cum[j] + (tot + 31) / 32 + 2;
+      ++n_row_mode;
+    } else {
+      kk[j] = (int32_t)K;
+      chunks += K * 32;
+      cum[j + 1] = cum[j] + K + 2;
+    }
   }
-  const size_t cap = (size_t)steps * 128 + 8;
-  const size_t need = cap * 8 + (size_t)nblk * (8 + 4 + 4 + 8 + 128 + 8);
-  size_t fr = 0, tot = 0;
-  TVR_CUDA(cudaMemGetInfo(&fr, &tot));
+  const size_t cap = (size_t)chunks * 4 + 8;
+  const size_t need = cap * 8 + (size_t)nblk * (8 + 4 + 4 + 8 + 128 + 8 + 256);
+  size_t fr = 0, tot_mem = 0;
+  TVR_CUDA(cudaMemGetInfo(&fr, &tot_mem));
   if (need + ((size_t)1 << 30) > fr) return TVR_OK;  // keep 1 GB of headroom
   SellData d;
   std::vector<int64_t> zend(1, nblk), wl(1, 0);
@@ -884,15 +909,16 @@ static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std:
   TVR_TRY(upload(p, (void**)&d.zend, zend.data(), sizeof(int64_t)));
   TVR_TRY(upload(p, (void**)&d.win_lo, wl.data(), sizeof(int64_t)));
   TVR_TRY(upload(p, (void**)&d.win_len, wn.data(), sizeof(int32_t)));
+  TVR_TRY(upload(p, (void**)&d.row_start, rstart.data(), sizeof(int64_t) * rstart.size()));
   TVR_TRY(dev_alloc(p, (void**)&d.sq, sizeof(double) * std::max<int64_t>(1, nblk)));
   TVR_TRY(upload(p, (void**)&d.perm, perm.data(), sizeof(int32_t) * perm.size()));
   TVR_TRY(dev_alloc(p, (void**)&d.val, sizeof(float) * cap));
   TVR_CUDA(cudaMemsetAsync(d.val, 0, sizeof(float) * cap, p->stream));
   TVR_TRY(dev_alloc(p, (void**)&d.col32, sizeof(int32_t) * cap));
   TVR_CUDA(cudaMemsetAsync(d.col32, 0, sizeof(int32_t) * cap, p->stream));
-  TVR_CUDA(launch_sell_fill32(nblk * 32, d.perm, d.off, transposed ? p->rpT : p->rp,
-                              transposed ? p->colT : p->col, transposed ? p->valT : p->val,
-                              d.col32, d.val, p->stream));
+  TVR_CUDA(launch_sell_fill32(nblk * 32, d.perm, d.off, d.k, d.row_start,
+                              transposed ? p->rpT : p->rp, transposed ? p->colT : p->col,
+                              transposed ? p->valT : p->val, d.col32, d.val, p->stream));
   TVR_CUDA(cudaStreamSynchronize(p->stream));  // host vectors die here
   d.nblk = nblk;
   d.h_slice_end = zend;
@@ -902,6 +928,7 @@ static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std:
   pl.pad_grid = (int)std::min<int64_t>((int64_t)p->num_sms * spmv32s_occupancy(pl.sv.unroll),
                                        std::max<int64_t>(1, nblk));
   pl.sell32 = true;
+  pl.sell32_row_blocks = n_row_mode;
   return TVR_OK;
 }
 
@@ -1318,9 +1345,12 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     // int32 sliced ELL for the A^T pass (voxel rows: a block's lanes gather neighbouring ray ids,
     // c5 A^T 5.62 -> 3.69 ms); the A pass keeps the per-row kernel (parallel rays in one block
     // gather unrelated lines: c5 A 6.20 -> 6.99 ms), TVR_SPMV_SELL32 = 0 none / 1 A^T / 2 both
-    const int s32 = env_int("TVR_SPMV_SELL32", 1);
-    if (p32 && (s32 == 2 || (s32 == 1 && which == 1)) && !(which == 1 && views_dist(p))) {
-      TVR_TRY(make_sell32(p, pl, which == 1, rph, rows));
+    // TVR_SPMV_SELL32 = 3: the A pass too, with per-block lane / row modes (default when the
+    // gathered volume is larger than 32 MB, so that its gathers miss L1 / L2: c5 A 6.18 -> 5.21
+    // ms; on f2's 1 MB volume the per-row kernel stays ahead, 91 vs 95 us)
+    const int s32 = env_int("TVR_SPMV_SELL32", (double)p->ncol * 4.0 > 32.0 * (1 << 20) ? 3 : 1);
+    if (p32 && (s32 >= 2 || (s32 == 1 && which == 1)) && !(which == 1 && views_dist(p))) {
+      TVR_TRY(make_sell32(p, pl, which == 1, rph, rows, which == 0 && s32 == 3));
       if (pl.sell32) continue;
     }
     if (p16 && p->separable && (env_int("TVR_SPMV_SELL", 1) || sliced)) {

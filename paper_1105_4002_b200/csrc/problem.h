@@ -87,6 +87,7 @@ struct SellData {
   int32_t* perm = nullptr;
   uint16_t* col16 = nullptr;
   int32_t* col32 = nullptr;    // spmv32s (int32 global columns)
+  int64_t* row_start = nullptr;  // spmv32s row-mode blocks: per slot, row start in chunks
   float* val = nullptr;
   int64_t* win_lo = nullptr;   // the plan's windows, shifted to the part
   int32_t* win_len = nullptr;
@@ -103,6 +104,7 @@ struct SpmvPlan {
   // sliced-ELL copy (spmv16s_kernel; replaces the padded copy when built): col16p / valp hold it
   bool sell = false;
   bool sell32 = false;                 // int32 sliced ELL (spmv32s_kernel): sd[0], no windows
+  int64_t sell32_row_blocks = 0;       // of its blocks, those in row mode
   int32_t rep = 1;                     // slice-shared operator: the blocks repeat per slice
   int64_t rep_rows = 0, rep_win = 0;   // per repetition: output row / gather window offsets
   int64_t rep_total = 0;               // slice groups (sv.zgroup > 1): slices; rep = groups

@@ -818,11 +818,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16z_kernel(SellArgs a) {
 }
 
 // Sliced ELL over int32 global columns (non-separable geometry; spmv32s_kernel): blocks of 32
-// consecutive rows (no sorting: neighbouring rays / voxels share a block, so at each step the
-// lanes gather neighbouring entries of x or r, and the lengths of neighbours are close), each
-// padded with zero 4-entry chunks to its longest row, stored [block step][lane][4 entries].
-// The gathers go through L1 (__ldg); warps take blocks from a shared counter; per-block sums
-// as spmv16s_kernel (deterministic).
+// consecutive rows (no sorting), two block modes chosen per block at create time by which
+// gather order touches fewer cache lines:
+//  * lane mode (blk_k >= 0): one row per lane, rows padded with zero 4-entry chunks to the
+//    block's longest, stored [step][lane][4]: at each step the 32 lanes gather the s-th entries of
+//    32 neighbouring rows (A^T: neighbouring voxels' rays, i.e. neighbouring ray ids; A: parallel
+//    rays whose neighbours are along x);
+//  * row mode (blk_k < 0, -blk_k chunks): the block's rows back to back (row starts in
+//    a.row_start, in chunks), 8 lanes per row and 4 rows at a time, as the per-row kernel (rays
+//    running along x: consecutive entries are neighbouring voxels).
+// Offsets are in 4-entry chunks.  The gathers go through L1 (__ldg); warps take blocks from a
+// shared counter; per-block sums as spmv16s_kernel (deterministic).
 template <int UNR>
 __global__ void __launch_bounds__(512, 2) spmv32s_kernel(SellArgs a) {
   __shared__ int s_next;
@@ -831,6 +837,24 @@ __global__ void __launch_bounds__(512, 2) spmv32s_kernel(SellArgs a) {
   sell_cta_range(a, b0, b1);
   if (threadIdx.x == 0) s_next = nwarps;
   __syncthreads();
+  auto gather4 = [&](const int4 c, const float4 v) {
+    const double p0 = (double)v.x * (double)__ldg(a.src + c.x);
+    const double p1 = (double)v.y * (double)__ldg(a.src + c.y);
+    const double p2 = (double)v.z * (double)__ldg(a.src + c.z);
+    const double p3 = (double)v.w * (double)__ldg(a.src + c.w);
+    return (p0 + p1) + (p2 + p3);
+  };
+  auto emit = [&](int64_t row, double acc) -> double {
+    if (a.b) {
+      const double r = acc - (double)__ldg(a.b + row);
+      const float rh = (float)r;
+      a.out[row] = rh;
+      if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
+      return r * r;
+    }
+    a.out[row] = (float)acc;
+    return 0.0;
+  };
   int64_t k = b0 + warp;
   int64_t off = 0;
   int K = 0, row = -1;
@@ -850,39 +874,46 @@ __global__ void __launch_bounds__(512, 2) spmv32s_kernel(SellArgs a) {
       K_n = a.blk_k[kn];
       row_n = a.perm[kn * 32 + lane];
     }
-    const int32_t* cp = a.col32 + (off * 32 + lane) * 4;
-    const float* vp = a.val + (off * 32 + lane) * 4;
-    double acc = 0.0;
-    auto chunk = [&](const int4 c, const float4 v) {
-      const double p0 = (double)v.x * (double)__ldg(a.src + c.x);
-      const double p1 = (double)v.y * (double)__ldg(a.src + c.y);
-      const double p2 = (double)v.z * (double)__ldg(a.src + c.z);
-      const double p3 = (double)v.w * (double)__ldg(a.src + c.w);
-      return (p0 + p1) + (p2 + p3);
-    };
-    int s = 0;
-    for (; s + UNR <= K; s += UNR) {
-      int4 c[UNR];
-      float4 v[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        c[u] = ld_stream_i4(cp + (s + u) * 128);
-        v[u] = ld_stream_f4(vp + (s + u) * 128);
-      }
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) acc += chunk(c[u], v[u]);
-    }
-    for (; s < K; ++s) acc += chunk(ld_stream_i4(cp + s * 128), ld_stream_f4(vp + s * 128));
     double q = 0.0;
-    if (row >= 0) {
-      if (a.b) {
-        const double r = acc - (double)__ldg(a.b + row);
-        const float rh = (float)r;
-        a.out[row] = rh;
-        if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
-        q = r * r;
-      } else {
-        a.out[row] = (float)acc;
+    if (K >= 0) {  // lane mode
+      const int32_t* cp = a.col32 + (off + lane) * 4;
+      const float* vp = a.val + (off + lane) * 4;
+      double acc = 0.0;
+      int s = 0;
+      for (; s + UNR <= K; s += UNR) {
+        int4 c[UNR];
+        float4 v[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          c[u] = ld_stream_i4(cp + (s + u) * 128);
+          v[u] = ld_stream_f4(vp + (s + u) * 128);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) acc += gather4(c[u], v[u]);
+      }
+      for (; s < K; ++s) acc += gather4(ld_stream_i4(cp + s * 128), ld_stream_f4(vp + s * 128));
+      if (row >= 0) q = emit(row, acc);
+    } else {  // row mode: 8 lanes per row, 4 rows at a time
+      const int grp = lane >> 3, gl = lane & 7;
+      const int64_t my_start = a.row_start[k * 32 + lane];  // chunks from the block start
+      const int my_n = row >= 0 ? (int)((a.rp[row + 1] - a.rp[row] + 3) >> 2) : 0;
+      for (int i0 = 0; i0 < 32; i0 += 4) {
+        const int ri = __shfl_sync(0xffffffffu, row, i0 + grp);
+        const int64_t si = off + __shfl_sync(0xffffffffu, my_start, i0 + grp);
+        const int ni = __shfl_sync(0xffffffffu, my_n, i0 + grp);
+        double acc = 0.0;
+        int c = gl;
+        for (; c + 8 < ni; c += 16) {
+          const int4 c0 = ld_stream_i4(a.col32 + (si + c) * 4);
+          const float4 v0 = ld_stream_f4(a.val + (si + c) * 4);
+          const int4 c1 = ld_stream_i4(a.col32 + (si + c + 8) * 4);
+          const float4 v1 = ld_stream_f4(a.val + (si + c + 8) * 4);
+          acc += gather4(c0, v0);
+          acc += gather4(c1, v1);
+        }
+        if (c < ni) acc += gather4(ld_stream_i4(a.col32 + (si + c) * 4), ld_stream_f4(a.val + (si + c) * 4));
+        acc = group_sum<8>(acc);
+        if (gl == 0 && ri >= 0) q += emit(ri, acc);
       }
     }
     if (a.scal) {
@@ -910,6 +941,43 @@ __global__ void __launch_bounds__(512, 2) spmv32s_kernel(SellArgs a) {
   }
 }
 
+// Block modes (one warp per block, lane = row): cache-line changes between the gathers a warp
+// issues together, in lane mode (lane l vs l-1 at the same entry) and in row mode (entry e vs
+// e-1 of one row); 1 = row mode when it changes lines less often.
+__global__ void sell32_mode_kernel(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,
+                                   uint8_t* mode) {
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= nblk) return;
+  const int64_t r = j * 32 + lane;
+  const int64_t s = r < rows ? rp[r] : 0, len = r < rows ? rp[r + 1] - s : 0;
+  int64_t mn = len;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+  int lane_chg = 0, row_chg = 0;
+  int prev = mn > 0 ? (col[s] >> 5) : 0;
+  for (int64_t e = 0; e < mn; ++e) {
+    const int line = col[s + e] >> 5;  // 128-byte line of the gathered fp32 value
+    const int up = __shfl_up_sync(0xffffffffu, line, 1);
+    if (lane > 0 && up != line) ++lane_chg;
+    if (e > 0 && line != prev) ++row_chg;
+    prev = line;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    lane_chg += __shfl_xor_sync(0xffffffffu, lane_chg, d);
+    row_chg += __shfl_xor_sync(0xffffffffu, row_chg, d);
+  }
+  if (lane == 0) mode[j] = (uint8_t)(row_chg < lane_chg ? 1 : 0);
+}
+
+cudaError_t launch_sell32_mode(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,
+                               uint8_t* mode, cudaStream_t st) {
+  if (nblk <= 0) return cudaSuccess;
+  sell32_mode_kernel<<<(unsigned)((nblk * 32 + 255) / 256), 256, 0, st>>>(nblk, rows, rp, col, mode);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spmv32s(const SellArgs& a, int unroll, int grid, cudaStream_t st) {
   if (a.blk_hi <= a.blk_lo) return cudaSuccess;
   if (unroll >= 3) spmv32s_kernel<3><<<grid, 512, 0, st>>>(a);
@@ -928,6 +996,7 @@ int spmv32s_occupancy(int unroll) {
 }
 
 __global__ void sell_fill32_kernel(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
+                                   const int32_t* blk_k, const int64_t* row_start,
                                    const int64_t* rp, const int32_t* col, const float* val,
                                    int32_t* cols, float* vals) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -936,19 +1005,22 @@ __global__ void sell_fill32_kernel(int64_t nslots, const int32_t* perm, const in
   if (row < 0) return;
   const int64_t j = t >> 5, l = t & 31, s = rp[row], len = rp[row + 1] - s;
   const int64_t base = blk_off[j];
+  const bool lane_mode = blk_k[j] >= 0;
   for (int64_t e = 0; e < len; ++e) {
-    const int64_t d = ((base + (e >> 2)) * 32 + l) * 4 + (e & 3);
+    const int64_t d = lane_mode ? (base + (e >> 2) * 32 + l) * 4 + (e & 3)
+                                : (base + row_start[t]) * 4 + e;
     cols[d] = col[s + e];
     vals[d] = val[s + e];
   }
 }
 
 cudaError_t launch_sell_fill32(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
-                               const int64_t* rp, const int32_t* col, const float* val,
-                               int32_t* cols, float* vals, cudaStream_t st) {
+                               const int32_t* blk_k, const int64_t* row_start, const int64_t* rp,
+                               const int32_t* col, const float* val, int32_t* cols, float* vals,
+                               cudaStream_t st) {
   if (nslots <= 0) return cudaSuccess;
-  sell_fill32_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(nslots, perm, blk_off, rp,
-                                                                      col, val, cols, vals);
+  sell_fill32_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(
+      nslots, perm, blk_off, blk_k, row_start, rp, col, val, cols, vals);
   return cudaGetLastError();
 }
 

@@ -430,12 +430,13 @@ def test_sell_column_parts(tvreg, cfg, floats, c1, monkeypatch):
     P.close()
 
 
-@pytest.mark.parametrize("cfg", ["zoo", "sphere"])
-@pytest.mark.parametrize("mode", ["0", "1", "2"])
+@pytest.mark.parametrize("cfg", ["zoo", "sphere", "tilted"])
+@pytest.mark.parametrize("mode", ["0", "1", "2", "3"])
 def test_sell32_spmv(tvreg, cfg, mode, monkeypatch):
     """Int32 sliced ELL for non-separable matrices (spmv32s_kernel; TVR_SPMV_SELL32 = 0 none,
-    1 the A^T pass, 2 both): exact on dyadic data with rows of every length class, the oracle to
-    fp32 rounding on the paper's sphere geometry."""
+    1 the A^T pass, 2 both in lane mode, 3 the A pass with per-block lane / row modes): exact on
+    dyadic data with rows of every length class, the oracle to fp32 rounding on the paper's
+    sphere geometry and on tilted rays (c5's geometry)."""
     monkeypatch.setenv("TVR_SPMV_SELL32", mode)
     rng = np.random.default_rng(21)
     if cfg == "zoo":
@@ -443,9 +444,14 @@ def test_sell32_spmv(tvreg, cfg, mode, monkeypatch):
         A = _row_length_zoo(16 * 16 * 4, 9)
         x = rng.integers(0, 9, A.n_cols).astype(np.float32)
         b = rng.integers(0, 9, A.n_rows).astype(np.float32)
-    else:
+    elif cfg == "sphere":
         grid = (24, 24, 24)
         A = harness.siddon_sphere(24, 24, 24, 7, 33, 33)
+        x = harness.random_x(A.n_cols)
+        b = rng.random(A.n_rows).astype(np.float32)
+    else:
+        grid = (20, 20, 20)
+        A = harness.siddon_tilted(20, 20, 20, 9, 20, 29, 10.0)
         x = harness.random_x(A.n_cols)
         b = rng.random(A.n_rows).astype(np.float32)
     P = make(tvreg, A, b, grid)
