@@ -300,6 +300,7 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_solve:
         out["solvers"] = solver_timings(tvreg, torch)
         out["c3_gradient"] = large_config_line(tvreg, torch)
+        out["c5_gradient"] = large_config_line(tvreg, torch, cfg="c5")
         out["sliced"] = sliced_lines(tvreg, torch)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(w)
@@ -337,7 +338,8 @@ def solver_timings(tvreg, torch, configs=("c1", "c2", "f2few", "f2many")):
 
 
 def large_config_line(tvreg, torch, cfg="c3", steps=10):
-    """Gradient evaluations on the 256^3 workload (BJ:9), for context beside the c2 headline."""
+    """Gradient evaluations on a 256^3 workload (c3: BJ configs[2], separable; c5: configs[4],
+    non-separable), for context beside the c2 headline."""
     import harness
     w = harness.preset(cfg)
     stream = torch.cuda.current_stream()

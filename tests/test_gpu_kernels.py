@@ -662,3 +662,54 @@ def test_objective_grad_c3_sampled(tvreg):
             n_ok += 1
     assert n_ok >= 50
     assert abs(fid2 - fid) <= 1e-12 * fid
+
+
+def test_objective_grad_c5_sampled(tvreg):
+    """BJ configs[4] (non-separable 256^3, rays tilted up to 10 deg, 2.67e9 entries) at full size
+    in the bench's launch configuration (int32 sliced ELL: A with per-block lane / row modes,
+    A^T in lane mode): sampled rows of r = A x - b from A's rows, sampled voxels of the gradient
+    from the entries of A's column j (found in one pass over the CSR) and the oracle TV on a
+    5x5x5 neighbourhood, all in fp64."""
+    w = harness.preset("c5")
+    nx, ny, nz = w.grid
+    x = harness.random_x(w.N)
+    P = make(tvreg, w.A, w.b, w.grid, w.alpha, w.tau)
+    g = torch.empty(w.N, device="cuda")
+    f, (fid, tv) = P.objective_grad(dev(x), g)
+    r = torch.empty(w.A.n_rows, device="cuda")
+    fid2 = P.residual(dev(x), r)
+    rh, gh = host(r), host(g)
+    P.close()
+    rng = np.random.default_rng(10)
+    rp, col, val = w.A.row_ptr, w.A.col, w.A.val
+    xd = x.astype(np.float64)
+
+    def r_row(i):
+        s, e = rp[i], rp[i + 1]
+        return float(val[s:e].astype(np.float64) @ xd[col[s:e]]) - float(w.b[i])
+
+    for i in rng.integers(0, w.A.n_rows, 2000):
+        ri = r_row(i)
+        assert abs(rh[i] - ri) <= 1e-6 * (abs(ri) + 1e-3 * np.sqrt(2 * fid / w.A.n_rows))
+    js = np.unique(rng.integers(0, w.N, 40))
+    hit = np.nonzero(np.isin(col, js, kind="table"))[0]
+    hit_rows = np.searchsorted(rp, hit, side="right") - 1
+    n_ok = 0
+    for j in js:
+        sel = col[hit] == j
+        wj = float(sum(float(val[k]) * r_row(int(i)) for k, i in zip(hit[sel], hit_rows[sel])))
+        iz, rem = divmod(int(j), nx * ny)
+        iy, ix = divmod(rem, nx)
+        lo = [max(0, c - 2) for c in (ix, iy, iz)]
+        hi = [min(n, c + 3) for c, n in zip((ix, iy, iz), (nx, ny, nz))]
+        sub = x.reshape(nz, ny, nx)[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
+        _, gsub = oracle.tv((sub.shape[2], sub.shape[1], sub.shape[0]), sub.ravel().astype(np.float64), w.tau)
+        c = (iz - lo[2], iy - lo[1], ix - lo[0])
+        ok = all((ci >= 1 or l == 0) and (s - 1 - ci >= 1 or h == n)
+                 for ci, l, h, s, n in zip(c[::-1], lo, hi, sub.shape[::-1], (nx, ny, nz)))
+        ref = wj + w.alpha * gsub.reshape(sub.shape)[c]
+        if ok:
+            assert abs(gh[j] - ref) <= 1e-5 * (abs(ref) + 1e-3), (j, gh[j], ref)
+            n_ok += 1
+    assert n_ok >= 30
+    assert abs(fid2 - fid) <= 1e-12 * fid
