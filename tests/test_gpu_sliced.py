@@ -234,3 +234,28 @@ def test_sliced_zslab_two_ranks(tvreg, zg, monkeypatch):
     g = torch.cat([t[2] for t in sorted(res, key=lambda t: t[0])])
     assert torch.equal(g, g1.cpu())
     P1.close()
+
+
+@pytest.mark.parametrize("floats", ["96", "128"])
+def test_sliced_column_parts(tvreg, floats, monkeypatch):
+    """Slice-shared operator whose slice window is cut into column parts (the c3 x-slice case),
+    forced on a 256-voxel slice: exact on dyadic data for both passes and the fidelity."""
+    monkeypatch.setenv("TVR_SPMV_STAGE", "0")
+    monkeypatch.setenv("TVR_SELL_PART_FLOATS", floats)
+    grid = (16, 16, 5)
+    As = dyadic_slice(16, 16, 7)
+    A = expand(As, grid[2])
+    rng = np.random.default_rng(8)
+    x = rng.integers(0, 9, A.n_cols).astype(np.float32)
+    b = rng.integers(0, 9, A.n_rows).astype(np.float32)
+    P = tvreg.Problem(As.row_ptr, As.col, As.val, b, grid, 0.01, 1e-4, sliced=True)
+    r = torch.empty(A.n_rows, device="cuda")
+    fid = P.residual(dev(x), r)
+    w = torch.empty(A.n_cols, device="cuda")
+    P.apply_AT(dev(b), w)
+    P.close()
+    r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x.astype(np.float64)) - b
+    w_ora = oracle.rmatvec(A.row_ptr, A.col, A.val, b.astype(np.float64), A.n_cols)
+    assert np.array_equal(r.cpu().numpy().astype(np.float64), r_ora)
+    assert np.array_equal(w.cpu().numpy().astype(np.float64), w_ora)
+    assert fid == 0.5 * float(r_ora @ r_ora)
