@@ -79,6 +79,9 @@ struct SellArgs {
   const int64_t* cum;       // nblk+1 prefix of per-block work (steps + 2)
   const int32_t* perm;      // 32 per block: row of each lane, -1 for an empty lane
   double* blk_sq;           // per virtual block: sum of its rows' r^2 (scratch, when scal)
+  float* const* out_peer;   // spmv32s_kernel, VIEWS A^T: per owner rank, its inbox (row-indexed)
+  const int64_t* out_bounds;
+  int n_out;
   const double* acc_in;     // column parts after the first: each row starts from acc_in[row]
   double* acc_out;          // column parts before the last: the row's fp64 sum goes here
   const uint16_t* col16;    // [step][lane][8] window offsets (zero pads)

@@ -179,6 +179,11 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     s.partials = p->partials;
     s.counter = p->counter;
     s.scal = scal;
+    if (transposed && p->fused_rs) {  // VIEWS A^T: rows stored into their owners' inboxes
+      s.out_peer = p->out_peer_dev;
+      s.out_bounds = p->out_bounds_dev;
+      s.n_out = p->world;
+    }
     if (d.nblk == 0) return scal ? cudaMemsetAsync(scal, 0, sizeof(double), p->stream) : cudaSuccess;
     return launch_spmv32s(s, pl.sv.unroll, (int)std::min<int64_t>(pl.pad_grid, d.nblk), p->stream);
   }
@@ -1350,7 +1355,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     // gathered volume is larger than 32 MB, so that its gathers miss L1 / L2: c5 A 6.18 -> 5.21
     // ms; on f2's 1 MB volume the per-row kernel stays ahead, 91 vs 95 us)
     const int s32 = env_int("TVR_SPMV_SELL32", (double)p->ncol * 4.0 > 32.0 * (1 << 20) ? 3 : 1);
-    if (p32 && (s32 >= 2 || (s32 == 1 && which == 1)) && !(which == 1 && views_dist(p))) {
+    if (p32 && (s32 >= 2 || (s32 == 1 && which == 1))) {
       TVR_TRY(make_sell32(p, pl, which == 1, rph, rows, which == 0 && s32 == 3));
       if (pl.sell32) continue;
     }
@@ -1440,7 +1445,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     TVR_TRY(dev_alloc(p, (void**)&p->xfull, sizeof(float) * p->ncol));
     TVR_TRY(dev_alloc(p, (void**)&p->wfull, sizeof(float) * p->ncol));
     // fused reduce-scatter: needs the padded int32 A^T kernel and peer-mapped inboxes
-    if (env_int("TVR_FUSED_RS", 1) && p->planT.pad && !p->planT.v.idx16)
+    if (env_int("TVR_FUSED_RS", 1) && (p->planT.pad || p->planT.sell32) && !p->planT.v.idx16)
       TVR_TRY(setup_fused_rs(p));
   }
   tv_set_grid(p->num_sms);

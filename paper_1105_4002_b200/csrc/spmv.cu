@@ -852,6 +852,12 @@ __global__ void __launch_bounds__(512, 2) spmv32s_kernel(SellArgs a) {
       if (a.out_lo) a.out_lo[row] = (float)(r - (double)rh);
       return r * r;
     }
+    if (a.out_peer) {  // fused reduce-scatter: straight into the owner's inbox (peer memory)
+      int o = 0;
+      while (o + 1 < a.n_out && row >= a.out_bounds[o + 1]) ++o;
+      a.out_peer[o][row] = (float)acc;
+      return 0.0;
+    }
     a.out[row] = (float)acc;
     return 0.0;
   };
