@@ -1476,6 +1476,7 @@ void tvr_destroy(tvr_problem* p) {
   for (auto e : p->pipe_ev) cudaEventDestroy(e);
   if (p->s_in) cudaStreamDestroy(p->s_in);
   if (p->s_out) cudaStreamDestroy(p->s_out);
+  if (p->s_a) cudaStreamDestroy(p->s_a);
   for (auto& t : p->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
   for (auto e : p->event_pool) cudaEventDestroy(e);
   if (p->hscal) cudaFreeHost(p->hscal);
@@ -1608,9 +1609,17 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
   if (!p->s_in) {
     TVR_CUDA(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
     TVR_CUDA(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
-    p->pipe_ev.resize(2 * 16 + 2);
+    TVR_CUDA(cudaStreamCreateWithFlags(&p->s_a, cudaStreamNonBlocking));
+    p->pipe_ev.resize(3 * 16 + 2);
     for (auto& e : p->pipe_ev) TVR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    TVR_TRY(dev_alloc(p, (void**)&p->partials2, sizeof(double) * p->partials_cap));
+    TVR_TRY(dev_alloc(p, (void**)&p->counter2, 64));
+    TVR_CUDA(cudaMemsetAsync(p->counter2, 0, 64, p->stream));
   }
+  // TVR_E2E_ASTREAM=1: the A passes run on their own stream (with their own reduction scratch),
+  // so chunk c+1's A pass can start while chunk c's A^T pass and stencil finish
+  const bool astream = env_int("TVR_E2E_ASTREAM", 1) != 0;
+  auto ev_a = [&](int c) { return p->pipe_ev[2 + 32 + c]; };
   cudaEvent_t ev_start = p->pipe_ev[0], ev_done = p->pipe_ev[1];
   auto ev_in = [&](int c) { return p->pipe_ev[2 + c]; };
   auto ev_g = [&](int c) { return p->pipe_ev[2 + 16 + c]; };
@@ -1619,7 +1628,7 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
   // transfers, so the end chunks get half the weight of the middle ones (TVR_E2E_TAPER=0: equal)
   {
     const bool taper = env_int("TVR_E2E_TAPER", 1) != 0 && C > 2;
-    const double tw = taper ? std::min(1.0, std::max(0.05, env_int("TVR_E2E_TAPER_PCT", 30) / 100.0)) : 1.0;
+    const double tw = taper ? std::min(1.0, std::max(0.05, env_int("TVR_E2E_TAPER_PCT", 60) / 100.0)) : 1.0;
     const double total = C - 2.0 + 2.0 * tw;
     double acc = 0.0;
     z[0] = 0;
@@ -1678,12 +1687,29 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
     }
     const double bytes_row = entry_bytes(p->planA) * (double)p->nnz / nz;  // per slice, for counters
     for (int c = 0; c < C; ++c) {
-      TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_in(c), 0));
-      TVR_TRY(mark("A" + std::to_string(c) + ">", p->stream));
-      TVR_TRY(launch(p, K_SPMV_A, bytes_row * (z[c + 1] - z[c]), [&] {
-        return run_spmv(p, p->planA, false, x, p->b, r, nullptr, p->dscal + SA + c, z[c], z[c + 1]);
-      }));
-      TVR_TRY(mark("A" + std::to_string(c) + "<", p->stream));
+      if (astream) {
+        TVR_CUDA(cudaStreamWaitEvent(p->s_a, ev_in(c), 0));
+        // run the A pass on s_a with the second reduction scratch
+        std::swap(p->stream, p->s_a);
+        std::swap(p->partials, p->partials2);
+        std::swap(p->counter, p->counter2);
+        const int st = launch(p, K_SPMV_A, bytes_row * (z[c + 1] - z[c]), [&] {
+          return run_spmv(p, p->planA, false, x, p->b, r, nullptr, p->dscal + SA + c, z[c], z[c + 1]);
+        });
+        std::swap(p->stream, p->s_a);
+        std::swap(p->partials, p->partials2);
+        std::swap(p->counter, p->counter2);
+        TVR_TRY(st);
+        TVR_CUDA(cudaEventRecord(ev_a(c), p->s_a));
+        TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_a(c), 0));
+      } else {
+        TVR_CUDA(cudaStreamWaitEvent(p->stream, ev_in(c), 0));
+        TVR_TRY(mark("A" + std::to_string(c) + ">", p->stream));
+        TVR_TRY(launch(p, K_SPMV_A, bytes_row * (z[c + 1] - z[c]), [&] {
+          return run_spmv(p, p->planA, false, x, p->b, r, nullptr, p->dscal + SA + c, z[c], z[c + 1]);
+        }));
+        TVR_TRY(mark("A" + std::to_string(c) + "<", p->stream));
+      }
       if (gh) {
         TVR_TRY(launch(p, K_SPMV_AT, bytes_row * (z[c + 1] - z[c]), [&] {
           return run_spmv(p, p->planT, true, r, nullptr, w, nullptr, nullptr, z[c], z[c + 1]);

@@ -205,7 +205,9 @@ struct tvr_problem {
   int* barrier_dev = nullptr;
 
   // e2e pipeline of tvr_objective_grad_host (created on first use)
-  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaStream_t s_in = nullptr, s_out = nullptr, s_a = nullptr;
+  double* partials2 = nullptr;   // second reduction scratch (the pipeline's A stream)
+  unsigned* counter2 = nullptr;
   // host-buffer pipeline as a CUDA graph, for these host buffers and chunk boundaries
   cudaGraphExec_t e2e_exec = nullptr;
   const float* e2e_xh = nullptr;
