@@ -122,8 +122,8 @@ cudaError_t launch_sell_fill(int64_t nslots, const int32_t* perm, const int64_t*
                              const int64_t* rp, const int32_t* lo_off, const int32_t* hi_off,
                              uint16_t coff, const uint16_t* col16, const float* val,
                              uint16_t* col16s, float* vals, cudaStream_t st);
-cudaError_t launch_spmv32s(const SellArgs& a, int unroll, int grid, cudaStream_t st);
-int spmv32s_occupancy(int unroll);
+cudaError_t launch_spmv32s(const SellArgs& a, int unroll, int grid, cudaStream_t st, int block = 512);
+int spmv32s_occupancy(int unroll, int block = 512);
 cudaError_t launch_sell_fill32(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
                                const int32_t* blk_k, const int64_t* row_start, const int64_t* rp,
                                const int32_t* col, const float* val, int32_t* cols, float* vals,

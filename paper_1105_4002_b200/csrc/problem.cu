@@ -185,7 +185,8 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
       s.n_out = p->world;
     }
     if (d.nblk == 0) return scal ? cudaMemsetAsync(scal, 0, sizeof(double), p->stream) : cudaSuccess;
-    return launch_spmv32s(s, pl.sv.unroll, (int)std::min<int64_t>(pl.pad_grid, d.nblk), p->stream);
+    return launch_spmv32s(s, pl.sv.unroll, (int)std::min<int64_t>(pl.pad_grid, d.nblk), p->stream,
+                          pl.sv.block);
   }
   if (pl.sell) {  // slices [z_lo, z_hi) (the e2e pipeline's chunks) or all; column parts in order
     const int P = (int)pl.sd.size();
@@ -931,7 +932,8 @@ static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std:
   pl.sv = SellVariant();
   // steps in flight: 3 for A^T (c5 3.85 -> 3.69 ms), 2 for A (3: 5.21 -> 5.29 ms)
   pl.sv.unroll = env_int("TVR_SELL32_UNROLL", transposed ? 3 : 2);
-  pl.pad_grid = (int)std::min<int64_t>((int64_t)p->num_sms * spmv32s_occupancy(pl.sv.unroll),
+  pl.sv.block = env_int("TVR_SELL32_BLOCK", 512);
+  pl.pad_grid = (int)std::min<int64_t>((int64_t)p->num_sms * spmv32s_occupancy(pl.sv.unroll, pl.sv.block),
                                        std::max<int64_t>(1, nblk));
   pl.sell32 = true;
   pl.sell32_row_blocks = n_row_mode;

@@ -829,10 +829,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16z_kernel(SellArgs a) {
 //    running along x: consecutive entries are neighbouring voxels).
 // Offsets are in 4-entry chunks.  The gathers go through L1 (__ldg); warps take blocks from a
 // shared counter; per-block sums as spmv16s_kernel (deterministic).
-template <int UNR>
-__global__ void __launch_bounds__(512, 2) spmv32s_kernel(SellArgs a) {
+template <int UNR, int NT = 512>
+__global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
   __shared__ int s_next;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = 512 >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
   int64_t b0, b1;
   sell_cta_range(a, b0, b1);
   if (threadIdx.x == 0) s_next = nwarps;
@@ -984,20 +984,26 @@ cudaError_t launch_sell32_mode(int64_t nblk, int64_t rows, const int64_t* rp, co
   return cudaGetLastError();
 }
 
-cudaError_t launch_spmv32s(const SellArgs& a, int unroll, int grid, cudaStream_t st) {
-  if (a.blk_hi <= a.blk_lo) return cudaSuccess;
-  if (unroll >= 3) spmv32s_kernel<3><<<grid, 512, 0, st>>>(a);
-  else if (unroll == 2) spmv32s_kernel<2><<<grid, 512, 0, st>>>(a);
-  else spmv32s_kernel<1><<<grid, 512, 0, st>>>(a);
-  return cudaGetLastError();
+static const void* spmv32s_ptr(int unroll, int block) {
+  if (block == 1024)
+    return unroll >= 3 ? (const void*)spmv32s_kernel<3, 1024>
+                       : unroll == 2 ? (const void*)spmv32s_kernel<2, 1024> : (const void*)spmv32s_kernel<1, 1024>;
+  return unroll >= 3 ? (const void*)spmv32s_kernel<3>
+                     : unroll == 2 ? (const void*)spmv32s_kernel<2> : (const void*)spmv32s_kernel<1>;
 }
 
-int spmv32s_occupancy(int unroll) {
+cudaError_t launch_spmv32s(const SellArgs& a, int unroll, int grid, cudaStream_t st, int block) {
+  if (a.blk_hi <= a.blk_lo) return cudaSuccess;
+  void* args[] = {const_cast<SellArgs*>(&a)};
+  return cudaLaunchKernel(spmv32s_ptr(unroll, block), dim3(grid), dim3(block == 1024 ? 1024 : 512),
+                          args, 0, st);
+}
+
+int spmv32s_occupancy(int unroll, int block) {
   int occ = 0;
-  const void* k = unroll >= 3 ? (const void*)spmv32s_kernel<3>
-                              : unroll == 2 ? (const void*)spmv32s_kernel<2> : (const void*)spmv32s_kernel<1>;
+  const void* k = spmv32s_ptr(unroll, block);
   ensure_smem_attr(k, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 512, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, block == 1024 ? 1024 : 512, 0);
   return occ > 0 ? occ : 1;
 }
 
