@@ -120,7 +120,7 @@ static int elem_grid(tvr_problem* p, int64_t n) {
 // ----------------------------------------------------------------- passes
 static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, const float* src,
                           const float* b, float* out, double* scal) {
-  SpmvArgs a;
+  SpmvArgs a{};
   a.out_lo = nullptr;
   a.out_peer = nullptr;
   a.out_bounds = nullptr;
@@ -192,7 +192,7 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     const int P = (int)pl.sd.size();
     for (int q = 0; q < P; ++q) {
       const SellData& d = pl.sd[q];
-      SellArgs s;
+      SellArgs s{};
       s.blk_off = d.off;
       s.blk_k = d.k;
       s.blk_slice = d.slice;
@@ -259,7 +259,7 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
                        pl.block, pl.smem, p->stream);
   }
   if (pl.tma.on) {
-    TmaSpmvArgs t;
+    TmaSpmvArgs t{};
     t.rp = transposed ? p->rpT : p->rp;
     t.col = transposed ? p->colT : p->col;
     t.val = transposed ? p->valT : p->val;
@@ -288,7 +288,7 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
   }
   if (pl.flat.on) {
     const FlatPlan& f = pl.flat;
-    FlatArgs a;
+    FlatArgs a{};
     a.rp = transposed ? p->rpT : p->rp;
     a.col = transposed ? p->colT : p->col;
     a.col16 = transposed ? p->colT16 : p->col16;
