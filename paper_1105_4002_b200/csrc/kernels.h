@@ -129,7 +129,7 @@ cudaError_t launch_sell_fill32(int64_t nslots, const int32_t* perm, const int64_
                                const int32_t* col, const float* val, int32_t* cols, float* vals,
                                cudaStream_t st);
 cudaError_t launch_sell32_mode(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,
-                               uint8_t* mode, cudaStream_t st);
+                               uint8_t* mode, cudaStream_t st, int bias_pct = 100);
 // per row: the first entry offset (from rp[r]) whose 16-bit column is >= h
 cudaError_t launch_sell_split(int64_t rows, const int64_t* rp, const uint16_t* col16, int h,
                               int32_t* split, cudaStream_t st);

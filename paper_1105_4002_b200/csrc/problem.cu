@@ -869,7 +869,8 @@ static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std:
     uint8_t* md = nullptr;
     TVR_CUDA(cudaMalloc(&md, nblk));
     cudaError_t e = launch_sell32_mode(nblk, rows, transposed ? p->rpT : p->rp,
-                                       transposed ? p->colT : p->col, md, p->stream);
+                                       transposed ? p->colT : p->col, md, p->stream,
+                                       env_int("TVR_SELL32_BIAS", 40));
     if (e == cudaSuccess) e = cudaMemcpyAsync(mode.data(), md, nblk, cudaMemcpyDeviceToHost, p->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
     cudaFree(md);

@@ -951,7 +951,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
 // issues together, in lane mode (lane l vs l-1 at the same entry) and in row mode (entry e vs
 // e-1 of one row); 1 = row mode when it changes lines less often.
 __global__ void sell32_mode_kernel(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,
-                                   uint8_t* mode) {
+                                   uint8_t* mode, int bias_pct) {
   const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (j >= nblk) return;
@@ -974,13 +974,14 @@ __global__ void sell32_mode_kernel(int64_t nblk, int64_t rows, const int64_t* rp
     lane_chg += __shfl_xor_sync(0xffffffffu, lane_chg, d);
     row_chg += __shfl_xor_sync(0xffffffffu, row_chg, d);
   }
-  if (lane == 0) mode[j] = (uint8_t)(row_chg < lane_chg ? 1 : 0);
+  if (lane == 0) mode[j] = (uint8_t)((int64_t)row_chg * 100 < (int64_t)lane_chg * bias_pct ? 1 : 0);
 }
 
 cudaError_t launch_sell32_mode(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,
-                               uint8_t* mode, cudaStream_t st) {
+                               uint8_t* mode, cudaStream_t st, int bias_pct) {
   if (nblk <= 0) return cudaSuccess;
-  sell32_mode_kernel<<<(unsigned)((nblk * 32 + 255) / 256), 256, 0, st>>>(nblk, rows, rp, col, mode);
+  sell32_mode_kernel<<<(unsigned)((nblk * 32 + 255) / 256), 256, 0, st>>>(nblk, rows, rp, col, mode,
+                                                                         bias_pct);
   return cudaGetLastError();
 }
 
