@@ -377,7 +377,7 @@ class Problem:
     # ---- solvers
     def set_control(self, mode: str):
         """Solver control: "device" (one CUDA graph per solve), "host", or "auto" (default: device
-        below 2^25 matrix entries); SURVEY f3."""
+        below 2^28 matrix entries); SURVEY f3."""
         _check(lib().tvr_set_control(self._h, {"host": TVR_CONTROL_HOST, "device": TVR_CONTROL_DEVICE,
                                                "auto": TVR_CONTROL_AUTO}[mode]), "tvr_set_control")
 
