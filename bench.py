@@ -310,18 +310,19 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
-def solver_timings(tvreg, torch, configs=("c1", "c2", "f2few", "f2many")):
+def solver_timings(tvreg, torch, configs=("c1", "c2", "f2few", "f2many", "c3")):
     """Time-to-eps of GPBB and UPN (BJ:7: gradient map 1e-6 relative to ||G_1(x_0)||, x_0 = 0),
     and GP capped at 2000 iterations (GP does not reach the accuracy); f2few / f2many
-    are the paper's own experiment shape (64^3, sphere geometry, 19 / 55 views of 91^2),
-    with the algorithmic HBM GB/s of the whole solve (bytes of every pass / wall time)."""
+    are the paper's own experiment shape (64^3, sphere geometry, 19 / 55 views of 91^2), c3 the
+    256^3 full solve of BJ configs[2] (one GPU), with the algorithmic HBM GB/s of the whole solve
+    (bytes of every pass / wall time)."""
     import harness
     out = {}
     for cfg in configs:
         w = harness.preset(cfg)
         P = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
                           stream=torch.cuda.current_stream().cuda_stream)
-        for solver in ("gpbb", "upn") + (("gp",) if cfg != "c2" else ()):
+        for solver in ("gpbb", "upn") + (("gp",) if cfg not in ("c2", "c3") else ()):
             x = torch.zeros(w.N, device="cuda")
             # GP (the paper's comparator, f1) does not reach 1e-6 in any reasonable count: capped
             # at the paper's 2000 iterations (P:260)
