@@ -312,7 +312,20 @@ int setup_fused_rs(tvr_problem* p) {
   int64_t stride = 0;
   for (int r = 0; r < W; ++r) stride = std::max(stride, p->slab_cnt[r]);
   p->inbox_stride = stride;
-  TVR_TRY(dev_alloc(p, (void**)&p->inbox, sizeof(float) * (size_t)stride * W));
+  const size_t inbox_bytes = sizeof(float) * (size_t)stride * W;
+  if (local_of(p)) {
+    TVR_TRY(dev_alloc(p, (void**)&p->inbox, inbox_bytes));
+  } else {
+    // CUDA IPC maps a whole allocation and returns its base address, so the inbox must be an
+    // allocation of its own (never a sub-block of a caching-allocator segment): raw cudaMalloc
+    if (cudaMalloc((void**)&p->inbox, inbox_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      p->inbox = nullptr;
+      set_error("fused RS: inbox allocation failed");
+      return TVR_E_OOM;
+    }
+    p->inbox_raw = true;
+  }
   TVR_TRY(dev_alloc(p, (void**)&p->barrier_dev, 64));
   TVR_CUDA(cudaMemsetAsync(p->barrier_dev, 0, 64, p->stream));
   std::vector<float*> base(W, nullptr);
@@ -384,6 +397,9 @@ int setup_fused_rs(tvr_problem* p) {
 void dist_release(tvr_problem* p) {
   for (void* q : p->ipc_opened) cudaIpcCloseMemHandle(q);
   p->ipc_opened.clear();
+  if (p->inbox_raw && p->inbox) cudaFree(p->inbox);
+  if (p->inbox_raw) p->inbox = nullptr;
+  p->inbox_raw = false;
   p->fused_rs = false;
 }
 

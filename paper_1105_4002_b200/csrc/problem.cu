@@ -1140,8 +1140,9 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
                 "(tvr_nccl_comm_init or tvr_local_comm_create)");
       return TVR_E_ARG;
     }
-    if (p->world == 1 && (p->z0 != 0 || p->z1 != grid.nz) && p->mode == TVR_SHARD_VIEWS) {
-      set_error("tvr_create: VIEWS mode on one rank owns every slice");
+    if (p->world == 1 && (p->z0 != 0 || p->z1 != grid.nz)) {
+      // one rank owns every slice: no neighbour would fill the halo planes of a partial slab
+      set_error("tvr_create: a single rank (world == 1) must own every slice (z0 = 0, z1 = nz)");
       return TVR_E_ARG;
     }
   }
@@ -1226,7 +1227,9 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   if (user_stream) {
     p->stream = user_stream;
   } else {
-    TVR_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    // a BLOCKING stream: it orders after work on the legacy default stream (torch's default
+    // stream producing x_dev, e.g. torch.zeros), so inputs are complete before the passes read them
+    TVR_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamDefault));
     p->own_stream = true;
   }
   // every rank's slab bounds (the slabs must tile [0, nz) in rank order); collective

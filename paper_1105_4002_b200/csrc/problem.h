@@ -198,6 +198,7 @@ struct tvr_problem {
   // floats), per-owner store targets (device array) and the owners' row bounds
   bool fused_rs = false;
   float* inbox = nullptr;
+  bool inbox_raw = false;            // NCCL backend: inbox from cudaMalloc (IPC-mappable), freed by dist_release
   int64_t inbox_stride = 0;
   float** out_peer_dev = nullptr;
   int64_t* out_bounds_dev = nullptr;

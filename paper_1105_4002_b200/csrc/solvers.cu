@@ -164,7 +164,7 @@ static int gpbb_impl(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_re
     ++n_g;
     f = f_bar;
     fhist.push_back(f);
-    if (fhist.size() > 64) fhist.pop_front();
+    if (fhist.size() > (size_t)o.K + 1) fhist.pop_front();  // f_hat window: last K+1
     ++k;
   }
   TVR_CUDA(cudaMemcpyAsync(x_io, x_cur, sizeof(float) * p->n, cudaMemcpyDeviceToDevice, p->stream));

@@ -63,10 +63,25 @@ def test_create_validation_statuses(case, status):
 
 
 def test_create_slab_rejects_rows_outside_the_slab():
-    # 2x2x2 grid, rank owns slice z=1 (voxels 4..7); a row touching voxel 0 is not separable
+    # 2x2x2 grid, rank 1 of 2 owns slice z=1 (voxels 4..7); a row touching voxel 0 is not
+    # separable.  The CSR check runs on the host before any collective or CUDA call.
+    comm = tvreg.local_comm_create(2)
+    try:
+        with pytest.raises(tvreg.TVRError) as e:
+            _create([0, 2], [0, 5], [1, 1], [0], grid=(2, 2, 2), world=2, rank=1, z0=1, z1=2,
+                    nccl_comm=comm)
+        assert e.value.status == tvreg.TVR_E_NOT_SEPARABLE
+    finally:
+        tvreg.local_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("shard", ["zslab", "views"])
+def test_create_single_rank_must_own_every_slice(shard):
+    """world == 1 with a partial slab: no neighbour fills the TV halo planes, so
+    tvr_create rejects it in every shard mode."""
     with pytest.raises(tvreg.TVRError) as e:
-        _create([0, 2], [0, 5], [1, 1], [0], grid=(2, 2, 2), z0=1, z1=2)
-    assert e.value.status == tvreg.TVR_E_NOT_SEPARABLE
+        _create([0, 1], [5], [1], [0], grid=(2, 2, 2), shard=shard, z0=1, z1=2)
+    assert e.value.status == tvreg.TVR_E_ARG
 
 
 @pytest.mark.parametrize("kw", [

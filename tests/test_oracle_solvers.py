@@ -248,3 +248,135 @@ def test_gp_converges_and_is_slower_than_upn():
     g = oracle.gp(P, np.zeros(P.N), eps=1e-4, max_iters=20000)
     u = oracle.upn(P, np.zeros(P.N), eps=1e-4, max_iters=20000)
     assert g.converged and u.converged and u.iters < g.iters
+
+
+# ----------------------------------------------------------------------- GP
+def test_gp_exact_step_spec_example():
+    """f(x) = 1/2 (x - 1)^2, Q = R_+, x0 = 0, L known = 1 -> x1 = 1 exactly, converged in
+    one step (Eq.(6), with BT of Alg. 2 accepting its first trial)."""
+    P = _prob(identity_csr(1), [1.0], (1, 1, 1), 0.0, 1e-3)
+    res = oracle.gp(P, np.zeros(1), eps=1e-12, max_iters=10, L_bar=1.0)
+    assert res.converged and res.iters == 1
+    assert res.x[0] == 1.0 and res.f == 0.0
+    assert res.history[0]["L"] == 1.0 and res.history[0]["trials"] == 1
+
+
+def _diag_quadratic(n=40, q=1e-2, seed=31):
+    """f(x) = 1/2 ||D x - b||^2 with eigenvalues lam = d^2 in [q, 1] (fp32 d, exact lam)."""
+
+    # one isolated smallest eigenvalue, so the slowest mode dominates after ~100 iterations
+    d = np.sqrt(np.concatenate([[q], np.geomspace(5 * q, 1.0, n - 1)])).astype(np.float32)
+    lam = d.astype(np.float64) ** 2
+    b = np.random.default_rng(seed).uniform(-1, 1, n).astype(np.float32)
+    xs = b.astype(np.float64) / d.astype(np.float64)
+    return d, lam, b, xs
+
+
+def test_gp_closed_form_trajectory_and_rate_envelope():
+    """Unconstrained quadratic with L_bar = L = max lam: BT accepts its first trial every
+    iteration (the bound of P:180 holds for L~ >= lam_max), so Eq.(6) gives the closed form
+    x_k - x* = (1 - lam/L)^k (x_0 - x*) componentwise and
+    f_k - f* = 1/2 sum lam (1 - lam/L)^(2k) e0^2.  The history must follow it, stay under the
+    Eq.(7) envelope (1 - mu/L)^k C_GP and decay at the sharp slope 2 log(1 - mu/L)."""
+    d, lam, b, xs = _diag_quadratic()
+    P = _prob(diag_csr(d), b, (4, 5, 2), 0.0, 1e-3, lo=-math.inf)
+    L, mu = lam.max(), lam.min()
+    res = oracle.gp(P, np.zeros(len(d)), eps=1e-30, max_iters=600, L_bar=L)
+    assert [h["trials"] for h in res.history] == [1] * len(res.history)
+    assert all(h["L"] == L for h in res.history)
+    e0 = -xs
+    ks = np.array([h["iter"] for h in res.history])
+    exact = np.array([0.5 * np.sum(lam * (1 - lam / L) ** (2 * k) * e0 ** 2) for k in ks])
+    gaps = np.array([h["f"] for h in res.history]) - P.f(xs)
+    ok = exact > 1e-9 * exact[0]
+    assert np.allclose(gaps[ok], exact[ok], rtol=1e-6, atol=0)
+    C = gaps[0] / (1 - mu / L)
+    assert np.all(gaps[ok] <= C * (1 - mu / L) ** ks[ok] * (1 + 1e-9))
+    sel = ok & (ks > 100)
+    slope = np.polyfit(ks[sel], np.log(gaps[sel]), 1)[0]
+    assert abs(slope / (2 * math.log(1 - mu / L)) - 1) <= 0.05
+
+
+def test_gp_keeps_L_between_iterations():
+    """Isotropic quadratic with Hessian L0 I and L_bar < L0: the first BT call takes
+    ceil(log_rho(L0/L_bar)) + 1 trials (S:292-293), and because BT is seeded with L_{k-1}
+    (P:213 for UPN) every later iteration accepts its first trial.  Resetting L to
+    L_bar each iteration would repeat the long search."""
+    n, L0, rho = 30, 10.0, 1.3
+    s = np.float32(math.sqrt(L0))
+    lam = float(s) ** 2
+    b = np.random.default_rng(32).uniform(-1, 1, n).astype(np.float32)
+    P = _prob(diag_csr(np.full(n, s)), b, (5, 3, 2), 0.0, 1e-3, lo=-math.inf)
+    res = oracle.gp(P, np.zeros(n), eps=1e-12, max_iters=50, L_bar=1.0, rho=rho)
+    m = math.ceil(math.log(lam / 1.0, rho) - 1e-12)
+    assert res.history[0]["trials"] == m + 1
+    assert all(h["trials"] == 1 for h in res.history[1:])
+    Lt = rho ** m
+    assert all(h["L"] == pytest.approx(Lt, rel=1e-12) for h in res.history)
+    # each iteration contracts the error by exactly (1 - lam / L~)
+    xs = b.astype(np.float64) / float(s)
+    gap0 = P.f(np.zeros(n)) - P.f(xs)
+    for h in res.history[:5]:
+        assert h["f"] - P.f(xs) == pytest.approx(gap0 * (1 - lam / Lt) ** (2 * h["iter"]),
+                                                 rel=1e-9, abs=1e-300)
+
+
+def test_gp_monotone_on_ct_problem():
+    """GP with BT decreases f at every iteration (S:317 'objective strictly nonincreasing'),
+    and L_k never decreases (seeded with L_{k-1})."""
+    A = harness.siddon_separable(10, 10, 4, 6, 15)
+    b = harness.simulate_data(A, harness.phantom(10, 10, 4, 3))
+    P = _prob(A, b, (10, 10, 4), 0.01, 1e-2)
+    res = oracle.gp(P, np.zeros(P.N), eps=1e-5, max_iters=3000)
+    f = np.array([h["f"] for h in res.history])
+    assert np.all(np.diff(f) <= 1e-12 * np.abs(f[1:]))
+    Ls = np.array([h["L"] for h in res.history])
+    assert np.all(np.diff(Ls) >= 0)
+
+
+def test_gp_stop_uses_nu_equal_L():
+    """C11: the stop test of GP (as UPN) evaluates G_nu at x_{k+1} with nu = L_k (Eq.(10),
+    P:225-228).  On a box-constrained CT problem the recorded map equals ||G_{L_k}(x)|| at the
+    returned x, which differs from ||G_1(x)||, and the decision flips exactly at exit."""
+    A = harness.siddon_separable(10, 10, 4, 6, 15)
+    b = harness.simulate_data(A, harness.phantom(10, 10, 4, 3))
+    P = _prob(A, b, (10, 10, 4), 0.01, 1e-2, lo=0.0, hi=0.6)
+    eps = 1e-3
+    res = oracle.gp(P, np.zeros(P.N), eps=eps, max_iters=20000)
+    assert res.converged
+    L = res.history[-1]["L"]
+    g = P.grad(res.x)
+    gL = float(np.linalg.norm(L * (res.x - P.proj(res.x - g / L))))
+    g1 = float(np.linalg.norm(res.x - P.proj(res.x - g)))
+    assert res.gmap == pytest.approx(gL, rel=1e-12)
+    assert abs(gL - g1) > 1e-3 * gL
+    assert res.history[-1]["gmap"] <= eps * res.gmap_ref < res.history[-2]["gmap"]
+
+
+# ------------------------------------------------------------ stop scaling
+def test_stop_abs_per_n_divides_by_N():
+    """stop when ||G_nu(x^(k))||_2 / N <= eps (N, not sqrt N; C12)."""
+    assert oracle._stop(0.5, 1.0, 100, 0.01, "abs_per_n")          # 0.005 <= 0.01
+    assert not oracle._stop(2.0, 1.0, 100, 0.01, "abs_per_n")      # 0.02 > 0.01
+    # with sqrt(N) this would not stop: 0.5 / 10 = 0.05 > 0.01
+    assert not (0.5 / math.sqrt(100) <= 0.01)
+    assert oracle._stop(0.5, 100.0, 100, 0.005, "rel") and not oracle._stop(0.6, 100.0, 100, 0.005, "rel")
+
+
+def test_gp_abs_per_n_stop_iteration_closed_form():
+    """On the closed-form quadratic of test_gp_closed_form_trajectory_and_rate_envelope (no
+    active bounds, so G_L = grad f = lam e_k), the first k with ||lam (1 - lam/L)^k e0|| / N <= eps
+    is known exactly; the solver must stop there, where dividing by sqrt(N) stops later."""
+    d, lam, b, xs = _diag_quadratic()
+    n = len(d)
+    P = _prob(diag_csr(d), b, (4, 5, 2), 0.0, 1e-3, lo=-math.inf)
+    L = lam.max()
+    e0 = -xs
+    gk = lambda k: float(np.linalg.norm(lam * (1 - lam / L) ** k * e0))
+    eps = 1e-5
+    k_n = next(k for k in range(1, 10000) if gk(k) / n <= eps)
+    k_sqrt = next(k for k in range(1, 10000) if gk(k) / math.sqrt(n) <= eps)
+    assert k_sqrt > k_n + 10
+    res = oracle.gp(P, np.zeros(n), eps=eps, stop_mode="abs_per_n", max_iters=10000, L_bar=L)
+    assert res.converged and res.iters == k_n
+    assert res.gmap / n <= eps
