@@ -287,35 +287,45 @@ def run_ours(args, rank, world, local_rank):
                ms_per_step_instrumented=ms_total_prof / args.steps,
                scaling="weak", vs_baseline=None, dtype="f64",
                storage_dtype="f32", data="synthetic",
-               config=(dict(workload_desc(args.config, w),
-                            parallelism=f"zslab{world}" if world > 1 else "single",
-                            **({"weak_scaling": f"one {args.config} slab per GPU: volume "
-                                f"{w.grid[0]}x{w.grid[1]}x{w.grid[2] * world}, value = {args.config} "
-                                "gradient evaluations per second summed over GPUs"} if world > 1 else {}))
-                       if w is not None else {}),
+               # config: the workload only, identical to the reference arm's (same_config)
+               config=workload_desc(args.config, w) if w is not None else {},
+               parallelism=f"zslab{world}" if world > 1 else "single",
+               **({"weak_scaling": f"one {args.config} slab per GPU: volume {w.grid[0]}x"
+                   f"{w.grid[1]}x{w.grid[2] * world}, value = {args.config} gradient evaluations "
+                   "per second summed over GPUs"} if world > 1 and w is not None else {}),
                roofline=roofline, e2e=e2e, gpu_launches=int(launches), clocks=clk,
                kernels=ktab, step_hbm_gbs=step_bytes / (ms_step / 1e3) / 1e9,
                step_frac=step_bytes / (ms_step / 1e3) / 1e9 / peak)
 
     if rank == 0 and world == 1 and not args.no_solve:
         out["solvers"] = solver_timings(tvreg, torch)
-        out["c3_gradient"] = large_config_line(tvreg, torch)
+        out["c3_gradient"] = large_config_line(tvreg, torch, solve=("gpbb", "upn"))
         out["c5_gradient"] = large_config_line(tvreg, torch, cfg="c5")
         out["sliced"] = sliced_lines(tvreg, torch)
+    if world > 1 and not args.no_solve:
+        # strong scaling of the 256^3 workloads (every rank takes part; rank 0 reports)
+        P.close()
+        P = None
+        torch.cuda.empty_cache()
+        out["c3_gradient"] = large_config_line(tvreg, torch, "c3", 10, world, rank, local_rank,
+                                               solve=("gpbb",))
+        torch.cuda.empty_cache()
+        out["c5_gradient"] = large_config_line(tvreg, torch, "c5", 10, world, rank, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(w)
-    P.close()
+    if P is not None:
+        P.close()
     if comm:
         tvreg.nccl_comm_destroy(comm)
     return out
 
 
-def solver_timings(tvreg, torch, configs=("c1", "c2", "f2few", "f2many", "c3")):
+def solver_timings(tvreg, torch, configs=("c1", "c2", "f2few", "f2many")):
     """Time-to-eps of GPBB and UPN (BJ:7: gradient map 1e-6 relative to ||G_1(x_0)||, x_0 = 0),
     and GP capped at 2000 iterations (GP does not reach the accuracy); f2few / f2many
-    are the paper's own experiment shape (64^3, sphere geometry, 19 / 55 views of 91^2), c3 the
-    256^3 full solve of BJ configs[2] (one GPU), with the algorithmic HBM GB/s of the whole solve
-    (bytes of every pass / wall time)."""
+    are the paper's own experiment shape (64^3, sphere geometry, 19 / 55 views of 91^2), with the
+    algorithmic HBM GB/s of the whole solve (bytes of every pass / wall time).  The 256^3 full
+    solves of BJ configs[2] are in the c3_gradient line (any N)."""
     import harness
     out = {}
     for cfg in configs:
@@ -338,35 +348,108 @@ def solver_timings(tvreg, torch, configs=("c1", "c2", "f2few", "f2many", "c3")):
     return out
 
 
-def large_config_line(tvreg, torch, cfg="c3", steps=10):
+def large_config_line(tvreg, torch, cfg="c3", steps=10, world=1, rank=0, local_rank=0, solve=None):
     """Gradient evaluations on a 256^3 workload (c3: BJ configs[2], separable; c5: configs[4],
-    non-separable), for context beside the c2 headline."""
+    non-separable) at N = world GPUs, STRONG scaling (the whole 256^3 problem split over the ranks,
+    the north star's "80 % parallel efficiency at 8 GPUs on the 256^3 workloads"):
+      c3: z-slabs (P1): each rank builds only its slices' rows (harness.strong_slab), one TV halo
+          exchange per evaluation and the rank-ordered scalar all-gather over NCCL;
+      c5: views (P2): each rank traces only its views' rays (harness.views_block), the point is
+          all-gathered before the A pass and A^T r reduce-scattered to the slabs.
+    value = whole-problem gradient evaluations per second (device time, max over ranks), so the
+    parallel efficiency at N is value(N) / (N value(1)).  solve: optional solver names timed to
+    REL 1e-6 from x0 = 0 on the same (sharded) problem (c3: configs[2]'s GPBB full solve)."""
     import harness
-    w = harness.preset(cfg)
     stream = torch.cuda.current_stream()
-    P = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
-                      stream=stream.cuda_stream)
-    x = torch.from_numpy(harness.random_x(w.N)).cuda()
-    g = torch.empty(w.N, device="cuda")
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        from paper_1105_4002_b200.dist import nccl_comm_from_process_group
+        comm = nccl_comm_from_process_group(world, rank, local_rank)
+        if cfg == "c5":
+            vb = harness.views_block(cfg, world, rank)
+            s2 = torch.tensor([float(vb.y @ vb.y)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(s2)  # sigma of the noise needs ||A x_true|| over every view
+            b = vb.data(float(s2.item()))
+            A, grid, z0, z1 = vb.A, vb.grid, vb.z0, vb.z1
+            P = tvreg.Problem(A.row_ptr, A.col, A.val, b, grid, vb.alpha, vb.tau, vb.lo, vb.hi,
+                              world=world, rank=rank, z0=z0, z1=z1, nccl_comm=comm,
+                              device=local_rank, stream=stream.cuda_stream, shard="views")
+            nnz_loc = A.nnz
+            del A, vb
+        else:
+            sl = harness.strong_slab(cfg, world, rank)
+            grid, z0, z1 = sl.grid, sl.z0, sl.z1
+            P = tvreg.Problem(sl.row_ptr, sl.col, sl.val, sl.b, grid, sl.alpha, sl.tau, sl.lo,
+                              sl.hi, n_cols=grid[0] * grid[1] * grid[2], world=world, rank=rank,
+                              z0=z0, z1=z1, nccl_comm=comm, device=local_rank,
+                              stream=stream.cuda_stream)
+            nnz_loc = int(sl.row_ptr[-1])
+            del sl
+        plane = grid[0] * grid[1]
+        x_full = harness.random_x(grid[0] * grid[1] * grid[2])
+        x = torch.from_numpy(np.ascontiguousarray(x_full[z0 * plane:z1 * plane])).cuda()
+        nnz_tot = torch.tensor([nnz_loc], dtype=torch.int64, device="cuda")
+        dist.all_reduce(nnz_tot)
+        nnz_tot = int(nnz_tot.item())
+    else:
+        w = harness.preset(cfg)
+        grid = w.grid
+        P = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
+                          stream=stream.cuda_stream)
+        nnz_tot = w.A.nnz
+        x = torch.from_numpy(harness.random_x(w.N)).cuda()
+        del w
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def maxrank(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    g = torch.empty(P.n, device="cuda")
     for _ in range(3):
         P.objective_grad(x, g)
-    P.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
     torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(steps):
         P.objective_grad(x, g)
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
+    barrier()
+    ms = maxrank(e0.elapsed_time(e1)) / steps
+    P.profile(True)
+    for _ in range(steps):
+        P.objective_grad(x, g)
+    torch.cuda.synchronize()
     st = P.kernel_stats()
+    P.profile(False)
     peak, _ = peaks()
     kt = {k: dict(ms_per_launch=v["ms"] / v["launches"],
                   achieved_gbs=v["bytes"] / v["ms"] / 1e6, frac=v["bytes"] / v["ms"] / 1e6 / peak)
           for k, v in st.items() if v["launches"]}
-    res = dict(workload=f"{cfg}: {w.grid[0]}^3, nnz {w.A.nnz}", value=1e3 / ms, unit=UNIT,
-               ms_per_step=ms, steps=steps, kernels=kt)
+    par = "single" if world == 1 else (f"views{world}" if cfg == "c5" else f"zslab{world}")
+    res = dict(workload=f"{cfg}: {grid[0]}^3, nnz {nnz_tot}", n_gpus=world, parallelism=par,
+               scaling="strong" if world > 1 else "single", value=1e3 / ms, unit=UNIT,
+               ms_per_step=ms, steps=steps, kernels_rank0=kt)
+    for solver in solve or ():
+        x0 = torch.zeros(P.n, device="cuda")
+        barrier()
+        r = getattr(P, f"solve_{solver}")(x0, max_iters=20000, eps=1e-6)
+        res[solver] = dict(converged=r.converged, iters=r.iters, n_f=r.n_f, n_grad=r.n_grad,
+                           seconds=maxrank(r.seconds), f=r.f, gmap_rel=r.gmap_rel,
+                           ms_per_iter=1e3 * maxrank(r.seconds) / max(1, r.iters))
     P.close()
+    if comm:
+        barrier()
+        tvreg.nccl_comm_destroy(comm)
     return res
 
 

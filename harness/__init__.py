@@ -52,6 +52,8 @@ def lib():
         L.hx_siddon2d.argtypes = [i32, i32, i32, i32, vp, vp, vp]
         L.hx_siddon3d.restype = i64
         L.hx_siddon3d.argtypes = [i32, i32, i32, i32, i32, i32, f64, vp, vp, vp]
+        L.hx_siddon3d_views.restype = i64
+        L.hx_siddon3d_views.argtypes = [i32, i32, i32, i32, i32, i32, f64, i32, i32, vp, vp, vp]
         L.hx_siddon_sphere.restype = i64
         L.hx_siddon_sphere.argtypes = [i32, i32, i32, i32, i32, i32, vp, vp, vp]
         L.hx_replicate_slices.restype = None
@@ -127,6 +129,22 @@ def siddon_tilted(nx: int, ny: int, nz: int, views: int, det_rows: int, det_cols
     col = np.empty(nnz, np.int32)
     val = np.empty(nnz, np.float32)
     L.hx_siddon3d(nx, ny, nz, views, det_rows, det_cols, phimax_deg, _p(rp), _p(col), _p(val))
+    return CSR(m, nx * ny * nz, rp, col, val)
+
+
+def siddon_tilted_views(nx: int, ny: int, nz: int, views: int, det_rows: int, det_cols: int,
+                        phimax_deg: float, v0: int, v1: int) -> CSR:
+    """Rows of views [v0, v1) of siddon_tilted (a contiguous block of its view-major rows,
+    bit-identical to that block of the full matrix): one rank's part of a view-sharded run."""
+    L = lib()
+    m = (v1 - v0) * det_rows * det_cols
+    rp = np.zeros(m + 1, np.int64)
+    nnz = L.hx_siddon3d_views(nx, ny, nz, views, det_rows, det_cols, phimax_deg, v0, v1, _p(rp),
+                              None, None)
+    col = np.empty(nnz, np.int32)
+    val = np.empty(nnz, np.float32)
+    L.hx_siddon3d_views(nx, ny, nz, views, det_rows, det_cols, phimax_deg, v0, v1, _p(rp), _p(col),
+                        _p(val))
     return CSR(m, nx * ny * nz, rp, col, val)
 
 
@@ -255,6 +273,87 @@ def weak_slab(name: str, world: int, rank: int) -> SlabWorkload:
     return SlabWorkload((nx, ny, nz * world), z0, z1, A.row_ptr, col, A.val, b,
                         p.get("alpha", 0.01), p.get("tau", 1e-4), p.get("lo", 0.0),
                         p.get("hi", float("inf")))
+
+
+def _balanced(n: int, world: int, rank: int):
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def strong_slab(name: str, world: int, rank: int) -> SlabWorkload:
+    """Rank `rank`'s part of preset `name` (slice-separable) split over `world` ranks by z-slabs
+    (strong scaling): slices [z0, z1) (balanced) and exactly the rows of
+    preset(name) that touch them, with global columns, and the same b (the projections are
+    simulated slice by slice with the same per-row sums, so sigma and every row of b equal the
+    single-process workload's).  Only the rank's rows of A are built."""
+    p = dict(PRESETS[name])
+    nx, ny, nz = p["grid"]
+    As = siddon_slice(nx, ny, p["views"], p["bins"])
+    z0, z1 = _balanced(nz, world, rank)
+    plane, ms = nx * ny, As.n_rows
+    xt = np.ascontiguousarray(phantom(nx, ny, nz, p["n_ell"]), np.float32)
+    y = np.empty(ms * nz, np.float64)
+    for z in range(nz):
+        lib().hx_simulate_projections(ms, _p(As.row_ptr), _p(As.col), _p(As.val),
+                                      _p(np.ascontiguousarray(xt[z * plane:(z + 1) * plane])),
+                                      _p(y[z * ms:(z + 1) * ms]))
+    sigma = 0.01 * np.linalg.norm(y) / np.sqrt(len(y))
+    e = normal(len(y), SEED_NOISE)
+    b = (y[z0 * ms:z1 * ms] + sigma * e[z0 * ms:z1 * ms]).astype(np.float32)
+    nzl = z1 - z0
+    rp = np.empty(ms * nzl + 1, np.int64)
+    col = np.empty(As.nnz * nzl, np.int32)
+    val = np.empty(As.nnz * nzl, np.float32)
+    lib().hx_replicate_slices(ms, As.nnz, _p(As.row_ptr), _p(As.col), _p(As.val), plane, nzl,
+                              _p(rp), _p(col), _p(val))
+    col += np.int32(z0 * plane)
+    return SlabWorkload((nx, ny, nz), z0, z1, rp, col, val, b, p.get("alpha", 0.01),
+                        p.get("tau", 1e-4), p.get("lo", 0.0), p.get("hi", float("inf")))
+
+
+@dataclass
+class ViewBlock:
+    """One rank's part of a view-sharded (P2) workload: views [v0, v1), their rows (global
+    columns), the noise-free projections y of those rows, and the rank's z-slab [z0, z1)."""
+    grid: tuple
+    v0: int
+    v1: int
+    z0: int
+    z1: int
+    row0: int
+    m_total: int
+    A: CSR
+    y: np.ndarray
+    alpha: float
+    tau: float
+    lo: float
+    hi: float
+
+    def data(self, sum_y2: float, noise_rel: float = 0.01, seed: int = SEED_NOISE) -> np.ndarray:
+        """b of the rank's rows given sum_i y_i^2 over ALL rows (e.g. an all-reduce of the ranks'
+        partial sums): sigma = noise_rel sqrt(sum y^2 / m), the noise stream of all m rows (C16)."""
+        sigma = noise_rel * np.sqrt(sum_y2) / np.sqrt(self.m_total)
+        e = normal(self.m_total, seed)[self.row0:self.row0 + self.A.n_rows]
+        return (self.y + sigma * e).astype(np.float32)
+
+
+def views_block(name: str, world: int, rank: int) -> ViewBlock:
+    """Rank `rank`'s views of a tilted preset (c5) split over `world` ranks (balanced view ranges,
+    slabs balanced like strong_slab); only its rows are traced."""
+    p = dict(PRESETS[name])
+    nx, ny, nz = p["grid"]
+    V, (R, C) = p["views"], p["det"]
+    v0, v1 = _balanced(V, world, rank)
+    z0, z1 = _balanced(nz, world, rank)
+    A = siddon_tilted_views(nx, ny, nz, V, R, C, p["tilt"], v0, v1)
+    xt = phantom(nx, ny, nz, p["n_ell"])
+    y = np.empty(A.n_rows, np.float64)
+    lib().hx_simulate_projections(A.n_rows, _p(A.row_ptr), _p(A.col), _p(A.val),
+                                  _p(np.ascontiguousarray(xt, np.float32)), _p(y))
+    return ViewBlock((nx, ny, nz), v0, v1, z0, z1, v0 * R * C, V * R * C, A, y,
+                     p.get("alpha", 0.01), p.get("tau", 1e-4), p.get("lo", 0.0),
+                     p.get("hi", float("inf")))
 
 
 def preset(name: str, **over) -> Workload:

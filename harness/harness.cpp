@@ -164,17 +164,29 @@ void hx_replicate_slices(int64_t m_s, int64_t nnz_s, const int64_t* rp_s, const 
 // d = (cos phi cos th, cos phi sin th, sin phi), u = (-sin th, cos th, 0),
 // w = d x u; pixel (r, c) centre (c-(C-1)/2) u + (r-(R-1)/2) w.  Rows are
 // view-major i = (v*R + r)*C + c (C4).  Columns (iz*ny + iy)*nx + ix.
+int64_t hx_siddon3d_views(int nx, int ny, int nz, int V, int R, int C, double phimax_deg,
+                          int v0, int v1, int64_t* row_ptr, int32_t* col, float* val);
 int64_t hx_siddon3d(int nx, int ny, int nz, int V, int R, int C, double phimax_deg,
                     int64_t* row_ptr, int32_t* col, float* val) {
+  return hx_siddon3d_views(nx, ny, nz, V, R, C, phimax_deg, 0, V, row_ptr, col, val);
+}
+
+// The rows of views [v0, v1) only (a contiguous block of the view-major rows, for one rank of a
+// view-sharded run): row_ptr has (v1 - v0) R C + 1 entries starting at 0; the rays are those of
+// the full geometry (the tilt and angle of view v depend on V, not on the block).
+int64_t hx_siddon3d_views(int nx, int ny, int nz, int V, int R, int C, double phimax_deg,
+                          int v0, int v1, int64_t* row_ptr, int32_t* col, float* val) {
   const int n[3] = {nx, ny, nz};
-  const int64_t m = (int64_t)V * R * C;
+  const int64_t m = (int64_t)(v1 - v0) * R * C;
+  const int64_t i0 = (int64_t)v0 * R * C;
   std::vector<int64_t> cnt(col && val ? 0 : m, 0);
 #pragma omp parallel
   {
     std::vector<double> ts;
     std::vector<Seg> segs;
 #pragma omp for schedule(dynamic, 64)
-    for (int64_t i = 0; i < m; ++i) {
+    for (int64_t il = 0; il < m; ++il) {
+      const int64_t i = i0 + il;
       const int v = (int)(i / ((int64_t)R * C));
       const int r = (int)((i / C) % R), cc = (int)(i % C);
       double ct, st;
@@ -189,13 +201,13 @@ int64_t hx_siddon3d(int nx, int ny, int nz, int V, int R, int C, double phimax_d
       const double p0[3] = {a * u[0] + bb * w[0], a * u[1] + bb * w[1], a * u[2] + bb * w[2]};
       trace_ray(p0, d, n, 3, ts, segs);
       if (col && val) {
-        int64_t off = row_ptr[i];
+        int64_t off = row_ptr[il];
         for (size_t k = 0; k < segs.size(); ++k) {
           col[off + k] = (int32_t)segs[k].col;
           val[off + k] = (float)segs[k].len;
         }
       } else {
-        cnt[i] = (int64_t)segs.size();
+        cnt[il] = (int64_t)segs.size();
       }
     }
   }

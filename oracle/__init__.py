@@ -64,6 +64,8 @@ def lib():
         L.ora_rmatvec_scatter.argtypes = [i64, i64, vp, vp, vp, vp, vp]
         L.ora_transpose.restype = None
         L.ora_transpose.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp]
+        L.ora_transpose_range.restype = None
+        L.ora_transpose_range.argtypes = [i64, i64, vp, vp, vp, i64, i64, vp, vp, vp]
         L.ora_tv.restype = f64
         L.ora_tv.argtypes = [i32, i32, i32, vp, f64, vp]
         _lib = L
@@ -106,6 +108,20 @@ def transpose(row_ptr, col, val, n: int):
     vT = np.empty(nnz, np.float32)
     lib().ora_transpose(m, n, _p(row_ptr), _p(col), _p(val), _p(rT), _p(cT), _p(vT))
     return rT, cT, vT
+
+
+def transpose_range(row_ptr, col, val, n: int, j0: int, j1: int):
+    """(rowT in full, colT[rowT[j0]:rowT[j1]], valT[rowT[j0]:rowT[j1]]) of the canonical A^T
+    (same stable counting sort as transpose(); for matrices too large to transpose twice)."""
+    m = len(row_ptr) - 1
+    rT = np.empty(n + 1, np.int64)
+    # sizes of the part come from the histogram, computed first by the same routine
+    lib().ora_transpose_range(m, n, _p(row_ptr), _p(col), _p(val), 0, 0, _p(rT), None, None)
+    cnt = int(rT[j1] - rT[j0])
+    cT = np.empty(max(cnt, 1), np.int32)
+    vT = np.empty(max(cnt, 1), np.float32)
+    lib().ora_transpose_range(m, n, _p(row_ptr), _p(col), _p(val), j0, j1, _p(rT), _p(cT), _p(vT))
+    return rT, cT[:cnt], vT[:cnt]
 
 
 def tv(grid, x, tau: float, want_grad: bool = True):

@@ -88,3 +88,29 @@ double ora_tv(int nx, int ny, int nz, const double *x, double tau, double *grad)
       }
   return tv;
 }
+
+/* The canonical transposed CSR of ora_transpose restricted to the rows j0 <= j < j1 of A^T
+ * (columns of A): rowT[0..n] in full (histogram of the columns + exclusive scan, as above) and
+ * the entries of rows j0..j1-1, i.e. positions rowT[j0] .. rowT[j1]-1 of colT / valT, written to
+ * colT_part / valT_part at offset p - rowT[j0].  Same stable counting sort (rows of A visited in
+ * ascending i), so the part is bit-identical to the slice of the full transpose; it lets a test
+ * check a matrix whose full transpose does not fit in host memory twice (c5, > 2^31 entries). */
+void ora_transpose_range(int64_t m, int64_t n, const int64_t *row_ptr, const int32_t *col,
+                         const float *val, int64_t j0, int64_t j1, int64_t *rowT,
+                         int32_t *colT_part, float *valT_part) {
+  for (int64_t j = 0; j <= n; ++j) rowT[j] = 0;
+  for (int64_t k = 0; k < row_ptr[m]; ++k) rowT[col[k] + 1] += 1;
+  for (int64_t j = 0; j < n; ++j) rowT[j + 1] += rowT[j];
+  const int64_t base = rowT[j0];
+  int64_t *next = (int64_t *)malloc(sizeof(int64_t) * (size_t)(j1 > j0 ? j1 - j0 : 1));
+  for (int64_t j = j0; j < j1; ++j) next[j - j0] = rowT[j];
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+      const int64_t c = col[k];
+      if (c < j0 || c >= j1) continue;
+      int64_t p = next[c - j0]++;
+      colT_part[p - base] = (int32_t)i;
+      valT_part[p - base] = val[k];
+    }
+  free(next);
+}

@@ -155,6 +155,24 @@ int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double 
   return TVR_OK;
 }
 
+int halo_fill_trial_x(tvr_problem* p, const float* x, const float* x_lo, const float* g, double s,
+                      float* v, float* v_lo) {
+  if (p->world <= 1) return TVR_OK;
+  TVR_CUDA(launch_halo_fill_trial_x(x, x_lo, g, s, p->lo, p->hi, p->plane, p->nzl, p->z0 > 0,
+                                    p->z1 < p->nz, v, v_lo, p->stream));
+  p->launches++;
+  return TVR_OK;
+}
+
+int halo_fill_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, const float* x0,
+                         const float* x0_lo, double beta, float* y, float* y_lo) {
+  if (p->world <= 1) return TVR_OK;
+  TVR_CUDA(launch_halo_fill_momentum_x(x1, x1_lo, x0, x0_lo, beta, p->plane, p->nzl, p->z0 > 0,
+                                       p->z1 < p->nz, y, y_lo, p->stream));
+  p->launches++;
+  return TVR_OK;
+}
+
 int dist_sum_scalars(tvr_problem* p, double* vals, int n) {
   if (local_of(p)) {
     TVR_TRY(local_collective(p, p->dscal, [&](const std::vector<const void*>& peer) -> int {

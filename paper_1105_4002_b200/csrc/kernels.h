@@ -103,6 +103,10 @@ struct SellArgs {
   const int64_t* win_lo;
   const int32_t* win_len;
   int part_len;             // half: window entries staged
+  int32_t ilv;              // spmv32s_kernel: > 0 = CTA c walks the block chunks c, c + G,
+                            // c + 2G, ... of ilv blocks each (the grid sweeps the block order
+                            // together: z-ordered blocks keep the gathered sub-volume in L2);
+                            // 0 = one contiguous work-balanced range per CTA
   double* partials;
   unsigned* counter;
   double* scal;
@@ -130,6 +134,10 @@ cudaError_t launch_sell_fill32(int64_t nslots, const int32_t* perm, const int64_
                                cudaStream_t st);
 cudaError_t launch_sell32_mode(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,
                                uint8_t* mode, cudaStream_t st, int bias_pct = 100);
+// per block of 32 consecutive rows: the z (column / plane) of the middle entry of its middle
+// nonempty row, -1 for an empty block (the key of the z-ordered block layout)
+cudaError_t launch_sell32_zkey(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,
+                               int64_t plane, int32_t* key, cudaStream_t st);
 // per row: the first entry offset (from rp[r]) whose 16-bit column is >= h
 cudaError_t launch_sell_split(int64_t rows, const int64_t* rp, const uint16_t* col16, int h,
                               int32_t* split, cudaStream_t st);
@@ -229,6 +237,8 @@ struct TVArgs {
   const float* tx;
   const float* tg;
   const float* xo;  // mu_k reductions
+  const float* xo_lo;  // extended iterates (SrcTrialX): lo part of xo
+  float* v_lo_out;     // extended iterates: lo part of the written state
   double* partials;
   unsigned* counter;
   double* scal;     // 6 doubles
@@ -244,6 +254,20 @@ cudaError_t launch_tv_grad_momentum(const TVArgs& a, const float* x1, const floa
                                     cudaStream_t st);
 cudaError_t launch_tv_trial(const TVArgs& a, const float* x, const float* g, double s,
                             cudaStream_t st);
+// extended-precision iterates (hi + lo pairs; tv.cu SrcTrialX / SrcMomentumX): a.v_lo_out (and
+// a.xo_lo with a.xo) required
+cudaError_t launch_tv_trial_x(const TVArgs& a, const float* x, const float* x_lo, const float* g,
+                              double s, cudaStream_t st);
+cudaError_t launch_tv_grad_momentum_x(const TVArgs& a, const float* x1, const float* x1_lo,
+                                      const float* x0, const float* x0_lo, double beta,
+                                      cudaStream_t st);
+cudaError_t launch_halo_fill_trial_x(const float* x, const float* x_lo, const float* g, double s,
+                                     double lo, double hi, int64_t plane, int nzl, int has_lo,
+                                     int has_hi, float* v, float* v_lo, cudaStream_t st);
+cudaError_t launch_halo_fill_momentum_x(const float* x1, const float* x1_lo, const float* x0,
+                                        const float* x0_lo, double beta, int64_t plane, int nzl,
+                                        int has_lo, int has_hi, float* v, float* v_lo,
+                                        cudaStream_t st);
 int tv_num_blocks(int nx, int ny, int nzl);
 int tv_set_grid(int num_sms);  // size the persistent stencil grid for the current device
 cudaError_t launch_halo_fill_trial(const float* x, const float* g, double s, double lo, double hi,

@@ -176,6 +176,7 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     s.blk_hi = d.nblk;
     s.nb = d.nblk;
     s.rep = 1;
+    s.ilv = pl.sell32_ilv;
     s.partials = p->partials;
     s.counter = p->counter;
     s.scal = scal;
@@ -432,6 +433,40 @@ int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, floa
   const double N = (double)n_local(p);
   const double bytes = N * (12.0 + (xo ? 4.0 : 0.0));
   return launch(p, K_TV_TRIAL, bytes, [&] { return launch_tv_trial(a, x, g, s, p->stream); });
+}
+
+int pass_tv_trial_x(tvr_problem* p, const float* x, const float* x_lo, const float* g, double s,
+                    float* v, float* v_lo, const float* xo, const float* xo_lo, int slot,
+                    const double* dparam) {
+  TVArgs a = tv_args(p, slot);
+  a.dparam = dparam;
+  a.v_out = v;
+  a.v_lo_out = v_lo;
+  a.tx = x;
+  a.tg = g;
+  a.xo = xo;
+  a.xo_lo = xo_lo;
+  a.stop_step = 0.0;
+  const double N = (double)n_local(p);
+  const double bytes = N * (20.0 + (xo ? 8.0 : 0.0));
+  return launch(p, K_TV_TRIAL, bytes, [&] { return launch_tv_trial_x(a, x, x_lo, g, s, p->stream); });
+}
+
+int pass_tv_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, const float* x0,
+                       const float* x0_lo, double beta, const float* w1, const float* w0,
+                       float* g, float* y, float* y_lo, int slot, const double* dparam) {
+  TVArgs a = tv_args(p, slot);
+  a.dparam = dparam;
+  a.w1 = w1;
+  a.w0 = w0;
+  a.wbeta = beta;
+  a.g_out = g;
+  a.v_out = y;
+  a.v_lo_out = y_lo;
+  const double N = (double)n_local(p);
+  return launch(p, K_TV_GRAD, N * 36.0, [&] {
+    return launch_tv_grad_momentum_x(a, x1, x1_lo, x0, x0_lo, beta, p->stream);
+  });
 }
 
 int pass_momentum(tvr_problem* p, const float* r1, const float* r1lo, const float* r0,
@@ -876,13 +911,33 @@ static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std:
     cudaFree(md);
     TVR_CUDA(e);
   }
+  // Block order.  The A pass of a large non-separable volume (c5: 67 MB of x, ~100 x refetched
+  // from DRAM when the grid works on rays spread over every view, profiles/r01m) stores its
+  // blocks in z order of the voxels they gather (the z of each block's middle entry; rays tilted
+  // by <= 10 deg span a band of ~60 slices) and the grid sweeps that order together (interleaved
+  // CTA chunks), so the x sub-volume in flight stays in L2.  TVR_SELL32_ZORDER=0: row order.
+  std::vector<int64_t> ord(nblk);
+  for (int64_t j = 0; j < nblk; ++j) ord[j] = j;
+  const bool zorder = !transposed && modes && env_int("TVR_SELL32_ZORDER", 1) != 0;
+  if (zorder) {
+    int32_t* kd = nullptr;
+    std::vector<int32_t> key(nblk);
+    TVR_CUDA(cudaMalloc(&kd, sizeof(int32_t) * nblk));
+    cudaError_t e = launch_sell32_zkey(nblk, rows, p->rp, p->col, p->plane, kd, p->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(key.data(), kd, sizeof(int32_t) * nblk, cudaMemcpyDeviceToHost, p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    cudaFree(kd);
+    TVR_CUDA(e);
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+  }
   std::vector<int64_t> off(nblk), cum(nblk + 1, 0), rstart((size_t)nblk * 32, 0);
   std::vector<int32_t> kk(nblk), sl(nblk, 0), perm((size_t)nblk * 32);
   int64_t chunks = 0, n_row_mode = 0;
   for (int64_t j = 0; j < nblk; ++j) {
     int64_t K = 0, tot = 0;
     for (int64_t l = 0; l < 32; ++l) {
-      const int64_t r = j * 32 + l;
+      const int64_t r = ord[j] * 32 + l;
       perm[(size_t)j * 32 + l] = r < rows ? (int32_t)r : -1;
       const int64_t n = r < rows ? (rph[r + 1] - rph[r] + 3) / 4 : 0;
       rstart[(size_t)j * 32 + l] = tot;
@@ -890,7 +945,7 @@ static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std:
       K = std::max(K, n);
     }
     off[j] = chunks;
-    if (mode[j]) {
+    if (mode[ord[j]]) {
       kk[j] = (int32_t)-tot;
       chunks += tot;
       cum[j + 1] = cum[j] + (tot + 31) / 32 + 2;
@@ -938,6 +993,9 @@ static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std:
                                        std::max<int64_t>(1, nblk));
   pl.sell32 = true;
   pl.sell32_row_blocks = n_row_mode;
+  pl.sell32_zorder = zorder;
+  // interleaved chunks of TVR_SELL32_ILV blocks (default 4 with the z order, else ranges)
+  pl.sell32_ilv = env_int("TVR_SELL32_ILV", zorder ? 4 : 0);
   return TVR_OK;
 }
 
@@ -1434,7 +1492,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   if (p->planT.v.idx16) { dev_free(p, p->colT); p->colT = nullptr; }
 
   // ---- work vectors ----
-  const int NVOL = 10, NDAT = 4;
+  const int NVOL = 13, NDAT = 4;  // 10-12: lo parts of the extended-precision solver iterates
   const size_t volbytes = sizeof(float) * (size_t)(p->plane * (p->nzl + 2));
   for (int i = 0; i < NVOL; ++i) {
     float* q = nullptr;

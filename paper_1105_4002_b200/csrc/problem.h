@@ -105,6 +105,8 @@ struct SpmvPlan {
   bool sell = false;
   bool sell32 = false;                 // int32 sliced ELL (spmv32s_kernel): sd[0], no windows
   int64_t sell32_row_blocks = 0;       // of its blocks, those in row mode
+  int32_t sell32_ilv = 0;              // interleaved CTA chunks of this many blocks (0: ranges)
+  bool sell32_zorder = false;          // blocks stored in z order of the voxels they gather
   int32_t rep = 1;                     // slice-shared operator: the blocks repeat per slice
   int64_t rep_rows = 0, rep_win = 0;   // per repetition: output row / gather window offsets
   int64_t rep_total = 0;               // slice groups (sv.zgroup > 1): slices; rep = groups
@@ -255,6 +257,17 @@ int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta, c
 int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, float* v,  // a5
                   double stop_step, const float* xo, int slot,
                   const double* dparam = nullptr);  // dparam: device-side (s, stop_step)
+// extended-precision iterates (hi + lo pairs, tv.cu SrcTrialX / SrcMomentumX): the trial from the
+// base state (x, x_lo) writes the state (v, v_lo) and evaluates at v; xo / xo_lo the mu_k
+// reference (nullable)
+int pass_tv_trial_x(tvr_problem* p, const float* x, const float* x_lo, const float* g, double s,
+                    float* v, float* v_lo, const float* xo, const float* xo_lo, int slot,
+                    const double* dparam = nullptr);
+// UPN point from (x1, x1_lo), (x0, x0_lo): gradient (w blend) at x1 + beta (x1 - x0) of the hi
+// parts, state y = (y, y_lo) from the full pairs
+int pass_tv_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, const float* x0,
+                       const float* x0_lo, double beta, const float* w1, const float* w0,
+                       float* g, float* y, float* y_lo, int slot, const double* dparam = nullptr);
 int pass_momentum(tvr_problem* p, const float* r1, const float* r1lo, const float* r0,  // a6
                   const float* r0lo, double beta, int slot, const double* dbeta = nullptr);
 int pass_project(tvr_problem* p, float* x);
@@ -267,6 +280,10 @@ int halo_exchange(tvr_problem* p, float* v);
 // recompute the halo planes of a trial / momentum point from its inputs' halo planes
 int halo_fill_trial(tvr_problem* p, const float* x, const float* g, double s, float* v);
 int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double beta, float* y);
+int halo_fill_trial_x(tvr_problem* p, const float* x, const float* x_lo, const float* g, double s,
+                      float* v, float* v_lo);
+int halo_fill_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, const float* x0,
+                         const float* x0_lo, double beta, float* y, float* y_lo);
 int dist_sum_scalars(tvr_problem* p, double* vals, int n);
 // VIEWS mode: the A pass's source (slab -> full volume, all-gathered) and the A^T pass's
 // target (full-volume partial -> slab, reduce-scattered); identity on one rank

@@ -59,6 +59,7 @@ static int gpbb_device(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_
 
 struct UpnState {
   float *xk, *xn, *ybuf, *gy, *wk, *wn, *rk, *rn, *rk_lo, *rn_lo;
+  float *xk_lo, *xn_lo, *y_lo;  // extended-precision iterates (lo parts of xk, xn, y)
   double L, mu, theta, fxk, fy, gn, gref;
   int64_t k, n_f, n_g, n_ls;
   bool conv;
@@ -378,8 +379,9 @@ static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnS
   }
   hd.rec = drec;
   const size_t vb = sizeof(float) * p->n, db = sizeof(float) * p->m;
-  // y_1 = x_1 lives in ybuf from here on
+  // y_1 = x_1 lives in ybuf (and y_lo) from here on
   TVR_CUDA(cudaMemcpyAsync(st.ybuf, st.xk, vb, cudaMemcpyDeviceToDevice, p->stream));
+  TVR_CUDA(cudaMemcpyAsync(st.y_lo, st.xk_lo, vb, cudaMemcpyDeviceToDevice, p->stream));
   TVR_CUDA(cudaMemcpyAsync(d, &hd, sizeof(hd), cudaMemcpyHostToDevice, p->stream));
   TVR_CUDA(cudaStreamSynchronize(p->stream));
 
@@ -407,7 +409,8 @@ static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnS
   }));
   // one BT trial: x = P_Q(y - g_y/L~), its TV and BT / mu reductions, r = A x - b
   TVR_TRY(capture_body(p, body_bt, &bytes_bt, [&]() -> int {
-    TVR_TRY(pass_tv_trial(p, st.ybuf, st.gy, 0.0, st.xn, 0.0, st.xk, S_TV, d->dp_trial));
+    TVR_TRY(pass_tv_trial_x(p, st.ybuf, st.y_lo, st.gy, 0.0, st.xn, st.xn_lo, st.xk, st.xk_lo,
+                            S_TV, d->dp_trial));
     TVR_TRY(pass_residual(p, st.xn, st.rn, S_RSQ, st.rn_lo));
     TVR_CUDA(launch_upn_bt(d, p->dscal, h, p->stream));
     return TVR_OK;
@@ -418,9 +421,10 @@ static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnS
     TVR_TRY(pass_tv_grad(p, st.xn, nullptr, 0.0, st.wn, nullptr, 0.0, nullptr, nullptr, nullptr,
                          nullptr, 1.0 /* 1/L_k on the device */, S_TV, p->alpha, d->dp_stop));
     TVR_TRY(pass_momentum(p, st.rn, st.rn_lo, st.rk, st.rk_lo, 0.0, S_MOM, d->dp_mom));
-    TVR_TRY(pass_tv_grad(p, st.xn, st.xk, 0.0, st.wn, st.wk, 0.0, st.gy, st.ybuf, nullptr, nullptr,
-                         0.0, S_TV2, p->alpha, d->dp_mom));
+    TVR_TRY(pass_tv_momentum_x(p, st.xn, st.xn_lo, st.xk, st.xk_lo, 0.0, st.wn, st.wk, st.gy,
+                               st.ybuf, st.y_lo, S_TV2, d->dp_mom));
     TVR_CUDA(cudaMemcpyAsync(st.xk, st.xn, vb, cudaMemcpyDeviceToDevice, p->stream));
+    TVR_CUDA(cudaMemcpyAsync(st.xk_lo, st.xn_lo, vb, cudaMemcpyDeviceToDevice, p->stream));
     TVR_CUDA(cudaMemcpyAsync(st.rk, st.rn, db, cudaMemcpyDeviceToDevice, p->stream));
     TVR_CUDA(cudaMemcpyAsync(st.rk_lo, st.rn_lo, db, cudaMemcpyDeviceToDevice, p->stream));
     TVR_CUDA(cudaMemcpyAsync(st.wk, st.wn, vb, cudaMemcpyDeviceToDevice, p->stream));
@@ -435,8 +439,8 @@ static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnS
     TVR_CUDA(cudaMemcpy(rec.hist + rec.n, drec, sizeof(tvr_record) * std::min(hd.n_rec, hd.rec_cap),
                         cudaMemcpyDeviceToHost));
   rec.n += hd.n_rec;
-  p->bytes_total += (double)hd.bt_execs * bytes_bt + (double)hd.n_g * (bytes_rest + 4.0 * vb + 4.0 * db);
-  p->launches += 2 * hd.bt_execs + 4 * hd.n_g;
+  p->bytes_total += (double)hd.bt_execs * bytes_bt + (double)hd.n_g * (bytes_rest + 6.0 * vb + 4.0 * db);
+  p->launches += 2 * hd.bt_execs + 5 * hd.n_g;
   st.L = hd.L; st.mu = hd.mu; st.theta = hd.theta; st.fxk = hd.fxk; st.fy = hd.fy; st.gn = hd.gn;
   st.k = hd.k; st.n_f += hd.n_f; st.n_g += hd.n_g; st.n_ls += hd.n_ls; st.conv = hd.conv != 0;
   if (hd.status == TVR_E_NONFINITE) { set_error("UPN: non-finite objective"); *status = TVR_E_NONFINITE; }
@@ -455,16 +459,21 @@ struct BTOut {
 }  // namespace
 
 // BT (Alg. 2): L~ = L_bar; x = P_Q(y - g_y/L~) until f(x) <= f(y) + g_y^T(x-y) + L~/2||x-y||^2.
-static int backtrack(tvr_problem* p, const float* y, const float* gy, double fy, double L_bar,
-                     const tvr_upn_opts& o, const float* xk_for_mu, float* x_out, float* r_out,
+// The iterates are extended-precision states (hi, lo) (tv.cu SrcTrialX): y + y_lo is the base,
+// the trial's state goes to (x_out, x_out_lo), f is evaluated at its hi part x_out.
+static int backtrack(tvr_problem* p, const float* y, const float* y_lo, const float* gy, double fy,
+                     double L_bar, const tvr_upn_opts& o, const float* xk_for_mu,
+                     const float* xk_lo_for_mu, float* x_out, float* x_out_lo, float* r_out,
                      float* r_out_lo, BTOut& out) {
   double L = L_bar;
   out.trials = 0;
   out.mu_gd = out.mu_dd = 0.0;
   for (;;) {
     const double s = 1.0 / L;
-    TVR_TRY(pass_tv_trial(p, y, gy, s, x_out, 0.0, out.trials == 0 ? xk_for_mu : nullptr, S_TV));
-    TVR_TRY(halo_fill_trial(p, y, gy, s, x_out));
+    const bool mu_red = out.trials == 0 && xk_for_mu;
+    TVR_TRY(pass_tv_trial_x(p, y, y_lo, gy, s, x_out, x_out_lo, mu_red ? xk_for_mu : nullptr,
+                            mu_red ? xk_lo_for_mu : nullptr, S_TV));
+    TVR_TRY(halo_fill_trial_x(p, y, y_lo, gy, s, x_out, x_out_lo));
     TVR_TRY(pass_residual(p, x_out, r_out, S_RSQ, r_out_lo));
     TVR_TRY(fetch_scalars(p, S_COUNT));
     const double fx = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
@@ -501,6 +510,11 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   float* rn = datvec(p, 1);
   float* rk_lo = datvec(p, 2);  // fp32 remainders: r = hi + lo to ~2^-48 (f(y) by linearity)
   float* rn_lo = datvec(p, 3);
+  // extended-precision iterates: lo parts of x_k, x_{k+1}, y_k
+  float* xk_lo = volvec(p, 10);
+  float* xn_lo = volvec(p, 11);
+  float* y_lo = volvec(p, 12);
+  TVR_CUDA(cudaMemsetAsync(xk_lo - p->plane, 0, sizeof(float) * p->plane * (p->nzl + 2), p->stream));
 
   TVR_TRY(copy_in(p, xk, x_io));
   TVR_TRY(pass_project(p, xk));
@@ -517,7 +531,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
 
   // [x_1, L_0] = BT(x_0, L_bar)
   BTOut bt;
-  TVR_TRY(backtrack(p, xk, gy, f0, o.L0, o, nullptr, xn, rn, rn_lo, bt));
+  TVR_TRY(backtrack(p, xk, xk_lo, gy, f0, o.L0, o, nullptr, nullptr, xn, xn_lo, rn, rn_lo, bt));
   n_f += bt.trials;
   n_ls += bt.trials;
   double L = bt.L;
@@ -525,6 +539,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   double theta = std::sqrt(mu / L);    // theta_1
   if (!(theta > 0.0 && theta <= 1.0)) { set_error("UPN: theta_1 outside (0,1]"); return TVR_E_THETA; }
   std::swap(xk, xn);  // x_1
+  std::swap(xk_lo, xn_lo);
   std::swap(rk, rn);
   std::swap(rk_lo, rn_lo);
   TVR_TRY(pass_AT(p, rk, wk));
@@ -536,6 +551,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   double fxk = bt.f, fy = bt.f;
   double gn = L * std::sqrt(p->hscal[S_TV + 3]);
   const float* y = xk;
+  const float* ylo = xk_lo;
   int64_t k = 1;
   bool conv = stop_test(gn, gref, Nglob, o.eps, o.stop_mode);
   {
@@ -546,15 +562,16 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   }
   int status = TVR_OK;
   if (!conv && k < o.max_iters && use_device_control(p)) {
-    UpnState us{xk, xn, ybuf, gy, wk, wn, rk, rn, rk_lo, rn_lo, L, mu, theta, fxk, fy, gn, gref,
-                k, n_f, n_g, n_ls, conv};
+    UpnState us{xk, xn, ybuf, gy, wk, wn, rk, rn, rk_lo, rn_lo, xk_lo, xn_lo, y_lo, L, mu, theta,
+                fxk, fy, gn, gref, k, n_f, n_g, n_ls, conv};
     TVR_TRY(upn_device(p, o, rec, us, &status));
     L = us.L; mu = us.mu; theta = us.theta; fxk = us.fxk; fy = us.fy; gn = us.gn;
     k = us.k; n_f = us.n_f; n_g = us.n_g; n_ls = us.n_ls; conv = us.conv;
   }
   while (!conv && k < o.max_iters && status == TVR_OK) {
     // [x_{k+1}, L_k] = BT(y_k, L_{k-1})
-    int s = backtrack(p, y, gy, fy, L, o, y == xk ? nullptr : xk, xn, rn, rn_lo, bt);
+    int s = backtrack(p, y, ylo, gy, fy, L, o, y == xk ? nullptr : xk, xk_lo, xn, xn_lo, rn, rn_lo,
+                      bt);
     if (s < 0) { status = s; break; }
     n_f += bt.trials;
     n_ls += bt.trials;
@@ -577,18 +594,20 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
     TVR_TRY(pass_tv_grad(p, xn, nullptr, 0.0, wn, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr,
                          1.0 / L, S_TV));
     TVR_TRY(pass_momentum(p, rn, rn_lo, rk, rk_lo, beta, S_MOM));
-    TVR_TRY(pass_tv_grad(p, xn, xk, beta, wn, wk, beta, gy, ybuf, nullptr, nullptr, 0.0, S_TV2));
-    TVR_TRY(halo_fill_momentum(p, xn, xk, beta, ybuf));
+    TVR_TRY(pass_tv_momentum_x(p, xn, xn_lo, xk, xk_lo, beta, wn, wk, gy, ybuf, y_lo, S_TV2));
+    TVR_TRY(halo_fill_momentum_x(p, xn, xn_lo, xk, xk_lo, beta, ybuf, y_lo));
     TVR_TRY(halo_exchange(p, gy));
     TVR_TRY(fetch_scalars(p, S_COUNT));
     ++n_g;
     gn = L * std::sqrt(p->hscal[S_TV + 3]);
     ++k;
     std::swap(xk, xn);
+    std::swap(xk_lo, xn_lo);
     std::swap(rk, rn);
     std::swap(rk_lo, rn_lo);
     std::swap(wk, wn);
     y = ybuf;
+    ylo = y_lo;
     fxk = bt.f;
     fy = 0.5 * p->hscal[S_MOM] + p->alpha * p->hscal[S_TV2];
     theta = theta_n;
@@ -629,6 +648,9 @@ static int gp_impl(tvr_problem* p, float* x_io, const tvr_gp_opts& o, tvr_result
   float* w = volvec(p, 5);
   float* rk = datvec(p, 0);
   float* rn = datvec(p, 1);
+  float* xk_lo = volvec(p, 10);  // extended-precision iterates (as UPN)
+  float* xn_lo = volvec(p, 11);
+  TVR_CUDA(cudaMemsetAsync(xk_lo - p->plane, 0, sizeof(float) * p->plane * (p->nzl + 2), p->stream));
 
   TVR_TRY(copy_in(p, xk, x_io));
   TVR_TRY(pass_project(p, xk));
@@ -651,13 +673,14 @@ static int gp_impl(tvr_problem* p, float* x_io, const tvr_gp_opts& o, tvr_result
   int status = TVR_OK;
   for (;;) {
     BTOut bt;
-    const int s = backtrack(p, xk, g, f, L, bo, nullptr, xn, rn, nullptr, bt);
+    const int s = backtrack(p, xk, xk_lo, g, f, L, bo, nullptr, nullptr, xn, xn_lo, rn, nullptr, bt);
     if (s < 0) { status = s; break; }
     n_f += bt.trials;
     n_ls += bt.trials;
     L = bt.L;
     ++k;
     std::swap(xk, xn);
+    std::swap(xk_lo, xn_lo);
     std::swap(rk, rn);
     f = bt.f;
     TVR_TRY(pass_AT(p, rk, w));

@@ -833,8 +833,23 @@ template <int UNR, int NT = 512>
 __global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
   __shared__ int s_next;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
+  // The CTA's blocks as a sequence j = 0, 1, ..: contiguous (ilv = 0: [b0, b1)) or interleaved
+  // (chunk q = blockIdx.x + (j / ilv) G of ilv blocks); blk(j) maps it to the stored block.
   int64_t b0, b1;
-  sell_cta_range(a, b0, b1);
+  const int64_t ilv = a.ilv;
+  if (ilv > 0) {
+    const int64_t nch = (a.blk_hi - a.blk_lo + ilv - 1) / ilv;  // chunks
+    const int64_t mine = nch > blockIdx.x ? (nch - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    b0 = 0;
+    b1 = mine * ilv;  // an upper bound: the last chunk may be short (blk() >= blk_hi: skipped)
+  } else {
+    sell_cta_range(a, b0, b1);
+  }
+  auto blk = [&](int64_t j) -> int64_t {
+    if (ilv <= 0) return j;
+    const int64_t q = blockIdx.x + (j / ilv) * (int64_t)gridDim.x;
+    return a.blk_lo + q * ilv + j % ilv;
+  };
   if (threadIdx.x == 0) s_next = nwarps;
   __syncthreads();
   auto gather4 = [&](const int4 c, const float4 v) {
@@ -861,24 +876,35 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
     a.out[row] = (float)acc;
     return 0.0;
   };
-  int64_t k = b0 + warp;
+  // j: position in the CTA's sequence; k = blk(j) the stored block (k >= blk_hi: past the end)
+  int64_t j = b0 + warp;
+  int64_t k = blk(j);
   int64_t off = 0;
   int K = 0, row = -1;
-  if (k < b1) {
+  if (j < b1 && k < a.blk_hi) {
     off = a.blk_off[k];
     K = a.blk_k[k];
     row = a.perm[k * 32 + lane];
   }
-  while (k < b1) {
+  while (j < b1) {
     int nx = 0;
     if (lane == 0) nx = atomicAdd(&s_next, 1);
-    const int64_t kn = b0 + __shfl_sync(0xffffffffu, nx, 0);
+    const int64_t jn = b0 + __shfl_sync(0xffffffffu, nx, 0);
+    const int64_t kn = blk(jn);
     int64_t off_n = 0;
     int K_n = 0, row_n = -1;
-    if (kn < b1) {
+    if (jn < b1 && kn < a.blk_hi) {
       off_n = a.blk_off[kn];
       K_n = a.blk_k[kn];
       row_n = a.perm[kn * 32 + lane];
+    }
+    if (k >= a.blk_hi) {  // past the last (short) chunk: nothing to do
+      j = jn;
+      k = kn;
+      off = off_n;
+      K = K_n;
+      row = row_n;
+      continue;
     }
     double q = 0.0;
     if (K >= 0) {  // lane mode
@@ -927,6 +953,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
       for (int d = 16; d > 0; d >>= 1) q += __shfl_xor_sync(0xffffffffu, q, d);
       if (lane == 0) a.blk_sq[k] = q;
     }
+    j = jn;
     k = kn;
     off = off_n;
     K = K_n;
@@ -935,9 +962,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
   if (a.scal) {
     double sq = 0.0;
     __syncthreads();
-    if (warp == 0) {
+    if (warp == 0) {  // the CTA's blocks in its sequence order: deterministic
       double t = 0.0;
-      for (int64_t kk = b0 + lane; kk < b1; kk += 32) t += a.blk_sq[kk];
+      for (int64_t jj = b0 + lane; jj < b1; jj += 32) {
+        const int64_t kk = blk(jj);
+        if (kk < a.blk_hi) t += a.blk_sq[kk];
+      }
 #pragma unroll
       for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
       if (lane == 0) sq = t;
@@ -975,6 +1005,31 @@ __global__ void sell32_mode_kernel(int64_t nblk, int64_t rows, const int64_t* rp
     row_chg += __shfl_xor_sync(0xffffffffu, row_chg, d);
   }
   if (lane == 0) mode[j] = (uint8_t)((int64_t)row_chg * 100 < (int64_t)lane_chg * bias_pct ? 1 : 0);
+}
+
+__global__ void sell32_zkey_kernel(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,
+                                   int64_t plane, int32_t* key) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= nblk) return;
+  int32_t z = -1;
+  const int64_t r_lo = j * 32, r_hi = min(rows, r_lo + 32);
+  // the middle row, else the nearest nonempty one
+  for (int64_t d = 0; d < 32 && z < 0; ++d) {
+    for (int sgn = 0; sgn < 2 && z < 0; ++sgn) {
+      const int64_t r = r_lo + 16 + (sgn ? -d - 1 : d);
+      if (r < r_lo || r >= r_hi) continue;
+      const int64_t s = rp[r], e = rp[r + 1];
+      if (e > s) z = (int32_t)(col[s + (e - s) / 2] / plane);
+    }
+  }
+  key[j] = z;
+}
+
+cudaError_t launch_sell32_zkey(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,
+                               int64_t plane, int32_t* key, cudaStream_t st) {
+  if (nblk <= 0) return cudaSuccess;
+  sell32_zkey_kernel<<<(unsigned)((nblk + 255) / 256), 256, 0, st>>>(nblk, rows, rp, col, plane, key);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_sell32_mode(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,

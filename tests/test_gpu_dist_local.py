@@ -2,7 +2,8 @@
 in-process thread communicator (tvr_local_comm_create), each with its own tvr_problem on the
 same device.  Exercises the z-slab halo exchange, halo recomputation of trial / momentum points,
 the rank-ordered scalar sum, the VIEWS all-gather / reduce-scatter and the distributed solvers
-through the C ABI, against the one-rank problem."""
+through the C ABI, against the one-rank problem and against the oracle (SURVEY §8(c).4 item 4:
+the P-rank run matches the 1-GPU run, and the same parity bars against the oracle hold)."""
 import math
 import threading
 
@@ -10,6 +11,7 @@ import numpy as np
 import pytest
 
 import harness
+import oracle
 from paper_1105_4002_b200.dist import local_slab, local_views
 
 torch = pytest.importorskip("torch")
@@ -45,6 +47,22 @@ def _run_ranks(world, fn):
     return out
 
 
+def _oracle(A, b, grid, alpha, tau, lo=0.0, hi=math.inf):
+    return oracle.Problem(A.row_ptr, A.col, A.val, b, grid, alpha, tau, lo, hi)
+
+
+def _solve_parity(Po, x_gpu, f_gpu, solver, eps):
+    """BJ:5 converged-reconstruction parity: the oracle's own solve to the same eps; both
+    objectives evaluated with the oracle's evaluator; gap <= 1e-5, image difference <= 1e-3."""
+    ref = getattr(oracle, solver)(Po, np.zeros(Po.N), eps=eps, max_iters=20000)
+    assert ref.converged
+    xg = x_gpu.double().numpy()
+    fg = Po.f(xg)
+    assert abs(fg - f_gpu) <= 1e-6 * abs(fg)            # the solver's f is the oracle's at its x
+    assert abs(fg - ref.f) <= 1e-5 * abs(ref.f)
+    assert np.linalg.norm(xg - ref.x) <= 1e-3 * np.linalg.norm(ref.x)
+
+
 def _separable():
     return harness.separable_workload("t", (20, 18, 12), 9, 29, 3, alpha=0.02, tau=1e-2)
 
@@ -75,6 +93,10 @@ def test_zslab_gradient_equals_one_rank(tvreg, world):
     assert abs(fs[0] - f1) <= 1e-13 * abs(f1)         # rank-ordered partial sums
     g = torch.cat([r[2] for r in sorted(res, key=lambda t: t[0])])
     assert torch.equal(g, g1.cpu())                   # per-voxel results are the one-rank ones
+    # and against the oracle (BJ:5: single gradient to relative L2 <= 1e-5)
+    fo, go = _oracle(w.A, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi).fg(x)
+    assert abs(fs[0] - fo) <= 1e-9 * abs(fo)
+    assert np.linalg.norm(g.double().numpy() - go) <= 1e-6 * np.linalg.norm(go)
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -106,6 +128,9 @@ def test_views_gradient_matches_one_rank(tvreg, world):
     g = torch.cat([r[2] for r in sorted(res, key=lambda t: t[0])]).double()
     # A^T r is summed over ranks in fp32: agreement to fp32 rounding
     assert (g - g1.cpu().double()).norm() <= 1e-6 * g1.cpu().double().norm()
+    fo, go = _oracle(A, b, grid, 0.01, 1e-3).fg(x)
+    assert abs(fs[0] - fo) <= 1e-9 * abs(fo)
+    assert np.linalg.norm(g.numpy() - go) <= 1e-6 * np.linalg.norm(go)
 
 
 @pytest.mark.parametrize("solver", ["gpbb", "upn"])
@@ -118,7 +143,7 @@ def test_zslab_solvers_match_one_rank(tvreg, solver):
     plane = w.grid[0] * w.grid[1]
     P1 = tvreg.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi)
     x1 = torch.zeros(w.N, device="cuda")
-    r1 = getattr(P1, f"solve_{solver}")(x1, max_iters=5000, eps=1e-5)
+    r1 = getattr(P1, f"solve_{solver}")(x1, max_iters=20000, eps=1e-6)
     comm = tvreg.local_comm_create(world)
 
     def rank_fn(r):
@@ -126,7 +151,7 @@ def test_zslab_solvers_match_one_rank(tvreg, solver):
         P = tvreg.Problem(sl.row_ptr, sl.col, sl.val, sl.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
                           n_cols=w.N, world=world, rank=r, z0=sl.z0, z1=sl.z1, nccl_comm=comm)
         x = torch.zeros(P.n, device="cuda")
-        res = getattr(P, f"solve_{solver}")(x, max_iters=5000, eps=1e-5)
+        res = getattr(P, f"solve_{solver}")(x, max_iters=20000, eps=1e-6)
         return sl.z0, res, x.cpu()
 
     out = _run_ranks(world, rank_fn)
@@ -138,6 +163,34 @@ def test_zslab_solvers_match_one_rank(tvreg, solver):
     x = torch.cat([o[2] for o in sorted(out, key=lambda t: t[0])]).double()
     assert (x - x1.cpu().double()).norm() <= 1e-3 * x1.cpu().double().norm()
     assert 0.8 * r1.iters <= its[0] <= 1.25 * r1.iters
+    _solve_parity(_oracle(w.A, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi), x, f, solver, 1e-6)
+
+
+@pytest.mark.parametrize("solver", ["gpbb", "upn"])
+def test_views_solvers_match_oracle(tvreg, solver):
+    """Distributed solve in VIEWS mode (P2: tilted rays, rows sharded by views, A^T r
+    reduce-scattered to slabs) against the oracle's solve of the whole problem."""
+    world = 2
+    grid, views = (14, 12, 10), 9
+    A = harness.siddon_tilted(*grid, views, 7, 17, 10.0)
+    b = harness.simulate_data(A, harness.phantom(*grid, 3))
+    alpha, tau = 0.01, 1e-2
+    comm = tvreg.local_comm_create(world)
+
+    def rank_fn(r):
+        lv = local_views(A.row_ptr, A.col, A.val, b, grid, views, world, r)
+        P = tvreg.Problem(lv.row_ptr, lv.col, lv.val, lv.b, grid, alpha, tau, world=world, rank=r,
+                          z0=lv.z0, z1=lv.z1, nccl_comm=comm, shard="views")
+        x = torch.zeros(P.n, device="cuda")
+        res = getattr(P, f"solve_{solver}")(x, max_iters=20000, eps=1e-6)
+        return lv.z0, res, x.cpu()
+
+    out = _run_ranks(world, rank_fn)
+    tvreg.local_comm_destroy(comm)
+    its = [o[1].iters for o in out]
+    assert all(i == its[0] for i in its) and all(o[1].converged for o in out)
+    x = torch.cat([o[2] for o in sorted(out, key=lambda t: t[0])])
+    _solve_parity(_oracle(A, b, grid, alpha, tau), x, out[0][1].f, solver, 1e-6)
 
 
 @pytest.mark.parametrize("world", [2, 3])

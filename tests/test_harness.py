@@ -202,3 +202,44 @@ def test_sliced_preset_is_the_separable_preset():
         assert np.array_equal(w.A.val[seg].view(np.uint32), s.A.val.view(np.uint32))
     assert np.array_equal(w.b.view(np.uint32), s.b.view(np.uint32))
     assert np.array_equal(np.asarray(w.x_true, np.float32), s.x_true)
+
+
+def test_strong_slab_is_the_presets_rows(monkeypatch):
+    """strong_slab (per-rank generator of a z-slab-sharded run) reproduces exactly the rows of
+    A and b of the single-process workload for its slices (rows (z V + v) bins + b, C4)."""
+    monkeypatch.setitem(harness.PRESETS, "tiny", dict(grid=(20, 18, 12), views=9, bins=29, n_ell=3))
+    full = harness.preset("tiny")
+    ms = 9 * 29
+    for world in (1, 2, 3, 5):
+        seen = 0
+        for r in range(world):
+            s = harness.strong_slab("tiny", world, r)
+            r0, r1 = s.z0 * ms, s.z1 * ms
+            e0, e1 = full.A.row_ptr[r0], full.A.row_ptr[r1]
+            assert np.array_equal(s.row_ptr, full.A.row_ptr[r0:r1 + 1] - e0)
+            assert np.array_equal(s.col, full.A.col[e0:e1])
+            assert np.array_equal(s.val.view(np.uint32), full.A.val[e0:e1].view(np.uint32))
+            assert np.array_equal(s.b.view(np.uint32), full.b[r0:r1].view(np.uint32))
+            seen += s.z1 - s.z0
+        assert seen == 12
+
+
+def test_views_block_is_the_presets_rows(monkeypatch):
+    """views_block traces only a rank's views; its rows equal that block of the full tilted
+    matrix, and b assembled from the ranks' partial sums of y^2 equals the preset's b."""
+    monkeypatch.setitem(harness.PRESETS, "tinyt",
+                        dict(grid=(14, 12, 10), views=9, det=(7, 17), tilt=10.0, n_ell=3))
+    full = harness.preset("tinyt")
+    for world in (1, 2, 3):
+        parts = [harness.views_block("tinyt", world, r) for r in range(world)]
+        rows = [(p.row0, p.row0 + p.A.n_rows) for p in parts]
+        assert rows[0][0] == 0 and rows[-1][1] == full.A.n_rows
+        assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+        for p, (r0, r1) in zip(parts, rows):
+            e0, e1 = full.A.row_ptr[r0], full.A.row_ptr[r1]
+            assert np.array_equal(p.A.row_ptr, full.A.row_ptr[r0:r1 + 1] - e0)
+            assert np.array_equal(p.A.col, full.A.col[e0:e1])
+            assert np.array_equal(p.A.val.view(np.uint32), full.A.val[e0:e1].view(np.uint32))
+        s2 = sum(float(p.y @ p.y) for p in parts)
+        b = np.concatenate([p.data(s2) for p in parts])
+        assert np.array_equal(b.view(np.uint32), full.b.view(np.uint32))

@@ -75,6 +75,21 @@ def test_transpose_is_canonical():
     assert np.array_equal(S.data.view(np.uint32), vT.view(np.uint32))
 
 
+@pytest.mark.parametrize("j0,j1", [(0, 90), (0, 1), (17, 61), (89, 90), (30, 30)])
+def test_transpose_range_is_a_slice_of_the_canonical_transpose(j0, j1):
+    """transpose_range (the column-range form used for c5's > 2^31-entry check) against scipy's
+    CSC conversion (a library routine): rowT in full, and exactly the entries of rows j0..j1-1."""
+    import scipy.sparse as sp
+    A = random_csr(120, 90, 0.08, seed=9, empty_rows=5)
+    rT, cT, vT = oracle.transpose_range(A.row_ptr, A.col, A.val, 90, j0, j1)
+    S = sp.csr_matrix((A.val, A.col, A.row_ptr), shape=(120, 90)).tocsc()
+    S.sort_indices()
+    assert np.array_equal(S.indptr, rT)
+    s, e = S.indptr[j0], S.indptr[j1]
+    assert np.array_equal(S.indices[s:e], cT)
+    assert np.array_equal(S.data[s:e].view(np.uint32), vT.view(np.uint32))
+
+
 def test_transpose_product_equals_scatter(c1):
     A = c1.A
     rT, cT, vT = oracle.transpose(A.row_ptr, A.col, A.val, A.n_cols)
