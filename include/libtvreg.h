@@ -20,7 +20,10 @@
  *  - "_dev" pointers are DEVICE pointers on the problem's device, caller-owned (e.g. torch
  *    tensors' data_ptr()); "_host" pointers are host memory (pinned is fastest).
  *  - Calls are ordered on the problem's CUDA stream and return once every host-side output
- *    they report is valid (device outputs are complete when the call returns).
+ *    they report is valid (device outputs are complete when the call returns).  A
+ *    library-created stream (tvr_dist NULL or cuda_stream NULL) is a BLOCKING stream: it waits
+ *    for work queued on the legacy default stream (e.g. torch's default stream producing x_dev).
+ *    With a caller stream, inputs must be produced on that stream or synchronised by the caller.
  *  - In distributed mode every call is collective: all ranks make it in the same order.
  *  - Arithmetic: fp32 storage; fp64 row accumulators, fp64 per-voxel TV math and fp64
  *    fixed-order reductions (deterministic run to run).
@@ -92,10 +95,16 @@ typedef struct {
   void* cuda_stream; /* cudaStream_t to order work on, or NULL for a library-created stream */
 } tvr_dist;
 
-/* Create a problem: validates A (TVR_E_CSR), copies A and b to device memory, builds the
- * canonical transposed CSR on the device (bit-exact: rows of A^T ascending by source row,
- * values moved bit for bit), and detects slice-separable structure for slab-staged SpMV.
- * b_host: m_local fp32 values (host).  alpha >= 0, tau > 0, lo < hi (+-INFINITY allowed). */
+/* Create a problem for phi_tau(x) = 1/2||Ax - b||^2 + alpha TV_tau(x), x in Q = [lo, hi]^N
+ * (Eq. (1)-(2); Q per P:77, a scalar box C22; b = A x_true + e of Eq. (11),
+ * P:243-245, supplied by the caller).  Validates A (TVR_E_CSR), copies A and b to device memory,
+ * builds the canonical transposed CSR on the device (bit-exact, rows of A^T ascending
+ * by source row, values moved bit for bit), and detects slice-separable structure for
+ * slab-staged SpMV.  A_local: host CSR (caller-owned, read only during the call).
+ * b_host: m_local fp32 values (host, caller-owned).  alpha >= 0 (alpha = 0 allowed, C24),
+ * tau > 0 (Huber smoothing, C1), lo < hi (+-INFINITY allowed).  *out receives a library-owned
+ * handle (tvr_destroy).  Errors: TVR_E_ARG, TVR_E_CSR, TVR_E_NOT_SEPARABLE, TVR_E_CUDA,
+ * TVR_E_NCCL, TVR_E_OOM; on error *out is NULL and nothing is leaked. */
 int tvr_create(tvr_problem** out, const tvr_csr* A_local, const float* b_host, tvr_grid grid,
                double alpha, double tau, double lo, double hi, const tvr_dist* dist);
 
@@ -140,9 +149,13 @@ typedef struct {
   double fidelity, tv, f;
 } tvr_fparts;
 
-/* f = phi_tau(x) and g = grad phi_tau(x) = A^T(Ax - b) + alpha grad TV_tau(x).
- * x_dev, g_dev: N_local fp32 device vectors (g_dev may be NULL: value only, no A^T pass).
- * parts may be NULL. */
+/* One gradient evaluation (the unit of BJ:2's metric): f = phi_tau(x) (Eq. (1)) and
+ * g = grad phi_tau(x) = A^T(Ax - b) + alpha grad TV_tau(x) (the gradient of Eq. (1)-(2); TV_tau's
+ * gradient sum_j D_j^T (D_j x / max(||D_j x||, tau)), C2), i.e. the A pass with the fused
+ * residual (a1), the A^T pass (a2) and the fused stencil (a4).  x_dev, g_dev: N_local fp32
+ * DEVICE vectors, caller-owned (g_dev may be NULL: value only, no A^T pass).  f_out: host, the
+ * fp64 value (identical on every rank).  parts may be NULL.  Collective in distributed mode.
+ * Errors: TVR_E_ARG (NULL x_dev / f_out), TVR_E_CUDA, TVR_E_NCCL. */
 int tvr_objective_grad(tvr_problem* p, const float* x_dev, double* f_out, float* g_dev,
                        tvr_fparts* parts);
 /* Same computation with HOST x and g (copied inside the call: the end-to-end API). */
@@ -203,9 +216,17 @@ typedef struct {
   double f, gmap_rel, gmap_abs_per_n, gmap_ref, seconds, bytes;
 } tvr_result;
 
-/* Solve from x_dev_inout (projected onto Q first); on return it holds the last iterate
- * tested by the stopping rule.  hist may be NULL; records beyond hist_cap are dropped.
- * Returns TVR_OK (converged), TVR_NOT_CONVERGED, or an error. */
+/* Solve min phi_tau over Q (Eq. (1)) from x_dev_inout (projected onto Q first, C13); on return
+ * it holds the last iterate tested by the stopping rule (Eq. (10); C14).
+ *   tvr_solve_gpbb: GPBB, Alg. 1: BB step, nonmonotone Armijo line
+ *     search over the last K+1 accepted values; readings C6, C11, C21.
+ *   tvr_solve_upn: UPN, Alg. 3 with BT, Alg. 2 and the mu_k estimate of
+ *     Eq. (9); readings C7-C10.  Its iterates are carried as fp32 hi + lo pairs (the
+ *     objective is evaluated at the hi part).
+ * x_dev_inout: N_local fp32 device vector, caller-owned.  hist may be NULL; records beyond
+ * hist_cap are counted but not stored.  Returns TVR_OK (converged), TVR_NOT_CONVERGED
+ * (max_iters; x and res still filled in), TVR_E_LINESEARCH, TVR_E_THETA, TVR_E_NONFINITE,
+ * TVR_E_ARG (invalid options), TVR_E_CUDA, TVR_E_NCCL. */
 int tvr_solve_gpbb(tvr_problem* p, float* x_dev_inout, const tvr_gpbb_opts* opts, tvr_result* res,
                    tvr_record* hist, int64_t hist_cap);
 int tvr_solve_upn(tvr_problem* p, float* x_dev_inout, const tvr_upn_opts* opts, tvr_result* res,
@@ -216,12 +237,23 @@ int tvr_solve_gp(tvr_problem* p, float* x_dev_inout, const tvr_gp_opts* opts, tv
                  tvr_record* hist, int64_t hist_cap);
 
 /* ---- inspection hooks (tests) ---- */
-/* y = A x - b (fused residual, the a1 pass); returns 1/2 ||Ax - b||^2 in *fid (nullable). */
+/* r = A x - b (the a1 pass: the operand of the fidelity term of Eq. (1), fused with the
+ * residual) and *fid = 1/2 ||Ax - b||^2 in fp64 (nullable).  x_dev: N_local fp32 device
+ * vector; r_dev: m_local fp32 device vector (caller-owned).  Errors: TVR_E_ARG, TVR_E_CUDA. */
 int tvr_residual(tvr_problem* p, const float* x_dev, float* r_dev, double* fid);
-/* w = A^T y using the stored transposed CSR (the a2 pass). y_dev: m_local, w_dev: N_local
- * (VIEWS mode: the rank's slab of sum_p A_p^T y_p; collective). */
+/* y = A x (the forward projection of Eq. (1), without b).  x_dev: N_local fp32 device
+ * vector (VIEWS mode: the rank's slab; collective), y_dev: m_local fp32 device vector.
+ * Row sums in fp64, rounded once to fp32.  Errors: TVR_E_ARG, TVR_E_CUDA, TVR_E_NCCL. */
+int tvr_apply_A(tvr_problem* p, const float* x_dev, float* y_dev);
+/* w = A^T y (the back-projection in the gradient of Eq. (1)) from the stored transposed
+ * CSR, no atomics (the a2 pass, BJ:5).  y_dev: m_local fp32 device vector, w_dev: N_local fp32
+ * device vector, caller-owned (VIEWS mode: the rank's slab of sum_p A_p^T y_p; collective).
+ * Row sums in fp64, rounded once.  Errors: TVR_E_ARG, TVR_E_CUDA, TVR_E_NCCL. */
 int tvr_apply_AT(tvr_problem* p, const float* y_dev, float* w_dev);
-/* TV_tau(x) and, if grad_dev != NULL, grad TV_tau(x). */
+/* TV_tau(x) = sum_j h_tau(||D_j x||_2) (Eq. (2), P:81-85 with the Huber smoothing C1 and the
+ * Neumann forward differences C3) into *tv_out (fp64, host) and, if grad_dev != NULL, its
+ * gradient (C2) as N_local fp32.  x_dev: N_local fp32 device vector.  Errors: TVR_E_ARG,
+ * TVR_E_CUDA, TVR_E_NCCL (halo exchange). */
 int tvr_tv(tvr_problem* p, const float* x_dev, double* tv_out, float* grad_dev);
 /* ||G_nu(x)||_2 with G_nu(x) = nu (x - P_Q(x - grad f(x)/nu)) (Eq. (10)); G_dev nullable. */
 int tvr_gradient_map(tvr_problem* p, const float* x_dev, double nu, double* norm_out, float* G_dev);

@@ -106,6 +106,7 @@ static int local_collective(tvr_problem* p, const void* mine, F&& copy) {
 }
 
 int halo_exchange(tvr_problem* p, float* v) {
+  NvtxRange nv("halo_exchange");
   if (p->world <= 1) return TVR_OK;
   const size_t bytes = sizeof(float) * (size_t)p->plane;
   if (LocalComm* L = local_of(p)) {
@@ -174,6 +175,7 @@ int halo_fill_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, co
 }
 
 int dist_sum_scalars(tvr_problem* p, double* vals, int n) {
+  NvtxRange nv("scalar_allgather");
   if (local_of(p)) {
     TVR_TRY(local_collective(p, p->dscal, [&](const std::vector<const void*>& peer) -> int {
       for (int r = 0; r < p->world; ++r)
@@ -252,6 +254,7 @@ static bool uniform_slabs(const tvr_problem* p) {
 // point: a tilted ray crosses every slab).  NCCL: equal slabs one ncclAllGather, ragged slabs
 // one broadcast per rank inside a group.
 int gather_volume(tvr_problem* p, const float* slab, const float** full) {
+  NvtxRange nv("views_allgather");
   if (!views_dist(p)) {
     *full = slab;
     return TVR_OK;
@@ -282,6 +285,7 @@ int gather_volume(tvr_problem* p, const float* slab, const float** full) {
 // A_p^T r_p already carries fp64-accumulated rows rounded once to fp32).  NCCL: equal slabs one
 // ncclReduceScatter, ragged slabs one ncclReduce per rank; local backend: rank-order sum.
 int reduce_scatter_volume(tvr_problem* p, const float* full, float* slab) {
+  NvtxRange nv("views_reduce_scatter");
   if (local_of(p)) {
     const int64_t cnt = p->slab_cnt[p->rank], off = p->slab_off[p->rank];
     return local_collective(p, full, [&](const std::vector<const void*>& peer) -> int {

@@ -142,73 +142,6 @@ cudaError_t launch_sell32_zkey(int64_t nblk, int64_t rows, const int64_t* rp, co
 cudaError_t launch_sell_split(int64_t rows, const int64_t* rp, const uint16_t* col16, int h,
                               int32_t* split, cudaStream_t st);
 
-// Row-agnostic SpMV (spmv_flat.cu): warps stream items as tiles of 32 x 8 entries with a
-// head-mask segmented reduction.
-struct FlatArgs {
-  const int64_t* rp;
-  const int32_t* col;      // int32 global columns (!idx16)
-  const uint16_t* col16;   // 16-bit window offsets (idx16)
-  const float* val;
-  const uint8_t* head;     // per 8-entry chunk: bit q set iff entry 8c+q starts a nonempty row
-  const float* src;
-  const float* b;          // non-null: out = A src - b, sum r^2
-  float* out;
-  float* out_lo;
-  const int64_t* item_row;  // nitems+1 row boundaries (items never straddle a slice)
-  const int64_t* item_nz;   // per item: nonempty rows before item_row[k] (index into nzr)
-  const int32_t* item_slice;
-  const int64_t* slice_item_end;  // per slice: one past its last item
-  int64_t nitems;
-  const int32_t* nzr;       // nonempty rows in order
-  const int32_t* empty_rows;
-  int64_t n_empty;
-  const int64_t* win_lo;    // per slice gather window (staged: shared memory; else base offset)
-  const int32_t* win_len;
-  double* partials;
-  unsigned* counter;
-  double* scal;
-};
-struct FlatVariant {
-  bool staged = false;
-  bool idx16 = false;
-  int unroll = 2;  // tiles of loads in flight per warp
-};
-cudaError_t launch_spmv_flat(const FlatArgs& a, const FlatVariant& v, int grid, int block,
-                             size_t smem, cudaStream_t st);
-int spmv_flat_occupancy(const FlatVariant& v, int block, size_t smem);
-
-// TMA bulk-copy pipelined SpMV (spmv_tma.cu): tiles of whole rows inside one slice.
-constexpr int kTmaConsumerWarps = 8;
-constexpr int kTmaProducerWarps = 4;  // divides kTmaConsumerWarps (stage count is a multiple)
-struct TmaSpmvArgs {
-  const int64_t* rp;
-  const int32_t* col;
-  const float* val;
-  const float* src;
-  const float* b;
-  float* out;
-  float* out_lo;
-  const int64_t* tile_row;   // ntiles+1 row boundaries
-  const int64_t* tile_k0;    // per tile: first entry, rounded down to a multiple of 4
-  const int64_t* tile_k1;    // per tile: end entry, rounded up to a multiple of 4
-  const int32_t* tile_slice;
-  int64_t ntiles;
-  const int64_t* bounds;     // ascending tile indices that start a new slice (bounds[0] = 0)
-  int64_t nbounds;
-  const int64_t* win_lo;
-  const int32_t* win_len;
-  int32_t win_cap;    // floats of the (swizzled) window buffer
-  int32_t tile_nnz;   // capacity of a stage in entries (multiple of 4)
-  int32_t tile_rows;  // capacity of a stage in rows
-  int32_t stages;
-  uint32_t piece;     // bytes per bulk copy of the col / val streams (multiple of 16)
-  double* partials;
-  unsigned* counter;
-  double* scal;
-};
-size_t tma_spmv_smem_bytes(int win_cap, int tile_nnz, int tile_rows, int stages);
-cudaError_t launch_spmv_tma(const TmaSpmvArgs& a, int lpr, int grid, size_t smem, cudaStream_t st);
-
 cudaError_t launch_momentum_resid(int64_t m, const float* r1, const float* r1lo, const float* r0,
                                   const float* r0lo, double beta, double* partials,
                                   unsigned* counter, double* scal, int grid, cudaStream_t st,

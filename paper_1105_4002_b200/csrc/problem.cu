@@ -92,6 +92,7 @@ static void resolve_timings(tvr_problem* p) {
 
 template <class F>
 static int launch(tvr_problem* p, int kid, double bytes, F&& f) {
+  NvtxRange nv(kKernelNames[kid]);
   cudaEvent_t a = nullptr, b = nullptr;
   if (p->prof) {
     a = get_event(p);
@@ -149,8 +150,8 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
   return a;
 }
 
-// Launch one SpMV pass with the plan's kernel: the TMA bulk-copy pipeline when planned, else the
-// register-streaming kernel.
+// Launch one SpMV pass with the plan's kernel: sliced ELL (16-bit or int32), else the padded or
+// plain per-row kernel.
 static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed, const float* src,
                             const float* b, float* out, float* out_lo, double* scal,
                             int z_lo = 0, int z_hi = -1) {
@@ -258,61 +259,6 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     }
     return launch_spmv(a, pl.v, (int)std::min<int64_t>(pl.grid, std::max<int64_t>(1, a.nitems)),
                        pl.block, pl.smem, p->stream);
-  }
-  if (pl.tma.on) {
-    TmaSpmvArgs t{};
-    t.rp = transposed ? p->rpT : p->rp;
-    t.col = transposed ? p->colT : p->col;
-    t.val = transposed ? p->valT : p->val;
-    t.src = src;
-    t.b = b;
-    t.out = out;
-    t.out_lo = out_lo;
-    t.tile_row = pl.tma.tile_row;
-    t.tile_k0 = pl.tma.tile_k0;
-    t.tile_k1 = pl.tma.tile_k1;
-    t.tile_slice = pl.tma.tile_slice;
-    t.ntiles = pl.tma.ntiles;
-    t.bounds = pl.tma.bounds;
-    t.nbounds = pl.tma.nbounds;
-    t.win_lo = pl.win_lo;
-    t.win_len = pl.win_len;
-    t.win_cap = pl.tma.win_cap;
-    t.tile_nnz = pl.tma.tile_nnz;
-    t.tile_rows = pl.tma.tile_rows;
-    t.stages = pl.tma.stages;
-    t.piece = pl.tma.piece;
-    t.partials = p->partials;
-    t.counter = p->counter;
-    t.scal = scal;
-    return launch_spmv_tma(t, pl.v.lpr, pl.tma.grid, pl.tma.smem, p->stream);
-  }
-  if (pl.flat.on) {
-    const FlatPlan& f = pl.flat;
-    FlatArgs a{};
-    a.rp = transposed ? p->rpT : p->rp;
-    a.col = transposed ? p->colT : p->col;
-    a.col16 = transposed ? p->colT16 : p->col16;
-    a.val = transposed ? p->valT : p->val;
-    a.head = f.head;
-    a.src = src;
-    a.b = b;
-    a.out = out;
-    a.out_lo = out_lo;
-    a.item_row = f.item_row;
-    a.item_nz = f.item_nz;
-    a.item_slice = f.item_slice;
-    a.slice_item_end = f.slice_item_end;
-    a.nitems = f.nitems;
-    a.nzr = f.nzr;
-    a.empty_rows = f.empty_rows;
-    a.n_empty = f.n_empty;
-    a.win_lo = f.win_lo;
-    a.win_len = f.win_len;
-    a.partials = p->partials;
-    a.counter = p->counter;
-    a.scal = scal;
-    return launch_spmv_flat(a, f.v, f.grid, f.block, f.smem, p->stream);
   }
   SpmvArgs a = spmv_args(p, pl, transposed, src, b, out, scal);
   a.out_lo = out_lo;
@@ -547,144 +493,6 @@ static int env_int(const char* name, int dflt) {
 static int upload(tvr_problem* p, void** dst, const void* src, size_t bytes) {
   TVR_TRY(dev_alloc(p, dst, bytes));
   if (src && bytes) TVR_CUDA(cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, p->stream));
-  return TVR_OK;
-}
-
-// Tiles for the TMA pipeline: runs of whole rows inside one slice whose 16-byte-aligned entry
-// span fits a stage (tile_nnz entries) and whose row count fits tile_rows.  Stages fill the
-// shared memory left after the slice window.  Disabled (register kernel) if a row does not fit.
-static int make_tma_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& rp,
-                         const std::vector<int64_t>& slice_rows, size_t win_cap) {
-  TmaPlan& t = pl.tma;
-  t.on = false;
-  // Opt-in: measured slower than the register-streaming kernel at c2 (profiles/r01/tma.md).
-  if (!env_int("TVR_SPMV_TMA", 0)) return TVR_OK;
-  int maxsmem = 0;
-  cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
-  t.tile_nnz = env_int("TVR_TMA_TILE", 1024);
-  t.piece = (uint32_t)env_int("TVR_TMA_PIECE", 1 << 20) & ~15u;
-  if (t.piece < 16) t.piece = 16;
-  t.tile_rows = 256;
-  t.win_cap = (int)win_cap;
-  // Stage count: a multiple of the consumer-warp count.  Tile i goes to warp i % NC and stage
-  // i % S; with S % NC != 0 a warp could wait on a stage two phases ahead, which an mbarrier
-  // parity wait cannot tell from the previous phase (it would read a stale tile).
-  // (Consumers take tiles dynamically, which needs S >= NC; producers own tiles i = p mod NP,
-  // which needs S % NP == 0.)
-  int stages = 0;
-  const int smax = env_int("TVR_TMA_STAGES", 4 * kTmaConsumerWarps);
-  for (int s = (smax / kTmaProducerWarps) * kTmaProducerWarps; s >= kTmaConsumerWarps;
-       s -= kTmaProducerWarps)
-    if (tma_spmv_smem_bytes(t.win_cap, t.tile_nnz, t.tile_rows, s) + 4096 <= (size_t)maxsmem) {
-      stages = s;
-      break;
-    }
-  if (stages < kTmaConsumerWarps) return TVR_OK;
-  t.stages = stages;
-  t.smem = tma_spmv_smem_bytes(t.win_cap, t.tile_nnz, t.tile_rows, stages);
-  std::vector<int64_t> row, k0, k1;
-  std::vector<int32_t> sl;
-  auto span = [&](int64_t r0, int64_t r1) {
-    return ((rp[r1] + 3) & ~int64_t(3)) - (rp[r0] & ~int64_t(3));
-  };
-  for (size_t z = 0; z + 1 < slice_rows.size(); ++z) {
-    int64_t r = slice_rows[z];
-    const int64_t rend = slice_rows[z + 1];
-    while (r < rend) {
-      int64_t e = r + 1;
-      if (span(r, e) > t.tile_nnz) return TVR_OK;  // a row longer than a stage
-      while (e < rend && e - r < t.tile_rows && span(r, e + 1) <= t.tile_nnz) ++e;
-      row.push_back(r);
-      k0.push_back(rp[r] & ~int64_t(3));
-      k1.push_back((rp[e] + 3) & ~int64_t(3));
-      sl.push_back((int32_t)z);
-      r = e;
-    }
-  }
-  if (row.empty()) return TVR_OK;
-  row.push_back(slice_rows.back());
-  t.ntiles = (int64_t)sl.size();
-  t.grid = (int)std::min<int64_t>(p->num_sms, t.ntiles);
-  TVR_TRY(upload(p, (void**)&t.tile_row, row.data(), sizeof(int64_t) * row.size()));
-  TVR_TRY(upload(p, (void**)&t.tile_k0, k0.data(), sizeof(int64_t) * k0.size()));
-  TVR_TRY(upload(p, (void**)&t.tile_k1, k1.data(), sizeof(int64_t) * k1.size()));
-  TVR_TRY(upload(p, (void**)&t.tile_slice, sl.data(), sizeof(int32_t) * sl.size()));
-  std::vector<int64_t> bounds;
-  for (size_t i = 0; i < sl.size(); ++i)
-    if (i == 0 || sl[i] != sl[i - 1]) bounds.push_back((int64_t)i);
-  t.nbounds = (int64_t)bounds.size();
-  TVR_TRY(upload(p, (void**)&t.bounds, bounds.data(), sizeof(int64_t) * bounds.size()));
-  t.on = true;
-  return TVR_OK;
-}
-
-// Row-agnostic plan (spmv_flat.cu): items of about TVR_FLAT_ITEM entries (default 2048) that
-// never straddle a slice, the per-chunk head mask, the nonempty-row map and the empty rows.
-// Uses the per-row plan's window staging (pl.staged, pl.smem) and column format (pl.v.idx16).
-static int make_flat_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& rp,
-                          int64_t n_rows, bool separable, const std::vector<int64_t>& slice_rows,
-                          const std::vector<int64_t>& win_lo, const std::vector<int32_t>& win_len,
-                          size_t nnz_pad) {
-  FlatPlan& f = pl.flat;
-  f.on = false;
-  if (!env_int("TVR_SPMV_FLAT", 0) || pl.tma.on || pl.v.parts) return TVR_OK;
-  if (n_rows >= ((int64_t)1 << 31)) return TVR_OK;  // nzr holds int32 row ids
-  // int32 columns are slab-local voxel ids: gathered from global memory (no window)
-  f.v.staged = pl.staged && pl.v.idx16;
-  f.v.idx16 = pl.v.idx16;
-  f.v.unroll = env_int("TVR_FLAT_UNROLL", 2);
-  f.block = env_int("TVR_FLAT_BLOCK", 512);
-  f.smem = f.v.staged ? pl.smem : 0;
-  f.grid = p->num_sms * spmv_flat_occupancy(f.v, f.block, f.smem);
-  const int64_t nnz = rp[n_rows];
-  // head mask, nonempty-row map, empty rows
-  std::vector<uint8_t> head(nnz_pad / 8, 0);
-  std::vector<int32_t> nzr, empty;
-  std::vector<int64_t> nz_before(n_rows + 1, 0);
-  for (int64_t r = 0; r < n_rows; ++r) {
-    nz_before[r + 1] = nz_before[r];
-    if (rp[r + 1] > rp[r]) {
-      head[rp[r] >> 3] |= (uint8_t)(1u << (rp[r] & 7));
-      nzr.push_back((int32_t)r);
-      nz_before[r + 1]++;
-    } else {
-      empty.push_back((int32_t)r);
-    }
-  }
-  // items
-  const int64_t target = std::max<int64_t>(64, env_int("TVR_FLAT_ITEM", 2048));
-  std::vector<int64_t> rows;
-  std::vector<int32_t> slices;
-  if (separable) {
-    for (size_t z = 0; z + 1 < slice_rows.size(); ++z)
-      split_rows(rp.data(), slice_rows[z], slice_rows[z + 1], target, (int32_t)z, rows, slices);
-  } else {
-    split_rows(rp.data(), 0, n_rows, target, 0, rows, slices);
-  }
-  rows.push_back(n_rows);
-  f.nitems = (int64_t)slices.size();
-  std::vector<int64_t> inz(f.nitems);
-  for (int64_t k = 0; k < f.nitems; ++k) inz[k] = nz_before[rows[k]];
-  const size_t nslices = separable ? win_lo.size() : 1;
-  std::vector<int64_t> zend(nslices, 0);
-  for (size_t i = 0; i < slices.size(); ++i) zend[slices[i]] = (int64_t)i + 1;
-  for (size_t z = 1; z < nslices; ++z) zend[z] = std::max(zend[z], zend[z - 1]);
-  std::vector<int64_t> wlo = separable && f.v.idx16 ? win_lo : std::vector<int64_t>(nslices, 0);
-  std::vector<int32_t> wlen = separable && f.v.idx16 ? win_len : std::vector<int32_t>(nslices, 0);
-  if (f.grid > f.nitems) f.grid = (int)std::max<int64_t>(1, f.nitems);
-  TVR_TRY(upload(p, (void**)&f.head, head.data(), head.size()));
-  TVR_TRY(upload(p, (void**)&f.nzr, nzr.data(), sizeof(int32_t) * nzr.size()));
-  TVR_TRY(upload(p, (void**)&f.empty_rows, empty.data(), sizeof(int32_t) * empty.size()));
-  f.n_empty = (int64_t)empty.size();
-  TVR_TRY(upload(p, (void**)&f.item_row, rows.data(), sizeof(int64_t) * rows.size()));
-  TVR_TRY(upload(p, (void**)&f.item_nz, inz.data(), sizeof(int64_t) * inz.size()));
-  TVR_TRY(upload(p, (void**)&f.item_slice, slices.data(), sizeof(int32_t) * slices.size()));
-  TVR_TRY(upload(p, (void**)&f.slice_item_end, zend.data(), sizeof(int64_t) * zend.size()));
-  TVR_TRY(upload(p, (void**)&f.win_lo, wlo.data(), sizeof(int64_t) * wlo.size()));
-  TVR_TRY(upload(p, (void**)&f.win_len, wlen.data(), sizeof(int32_t) * wlen.size()));
-  TVR_CUDA(cudaStreamSynchronize(p->stream));  // host vectors die here
-  f.on = true;
-  (void)nnz;
   return TVR_OK;
 }
 
@@ -1014,7 +822,7 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
   //  * staging the window in shared memory when it fits (c2 both passes, c3 A^T); a larger
   //    window (c3's 256 KB x-slice) is gathered from global memory (mostly L1 hits), or, with
   //    TVR_PART_CAP set, cut into parts staged one after another (measured slower at c3).
-  // The TMA path and TVR_IDX16=0 use int32 columns with whole staged windows only.
+  // TVR_IDX16=0 uses int32 columns with whole staged windows only.
   size_t smem = 0;
   bool staged = separable && env_int("TVR_SPMV_STAGE", 1) != 0;
   pl.parts = 1;
@@ -1022,8 +830,7 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
   int32_t maxlen = 0;
   for (int32_t l : win_len) maxlen = std::max(maxlen, l);
   pl.max_win = maxlen;
-  const bool want16 = separable && maxlen <= 65536 && env_int("TVR_IDX16", 1) != 0 &&
-                      env_int("TVR_SPMV_TMA", 0) == 0;
+  const bool want16 = separable && maxlen <= 65536 && env_int("TVR_IDX16", 1) != 0;
   if (staged) {
     int32_t wlen = maxlen;
     const int32_t cap = want16 ? std::min(65536, std::max(1024, env_int("TVR_PART_CAP", 65536))) : maxlen;
@@ -1096,9 +903,7 @@ static int make_plan(tvr_problem* p, SpmvPlan& pl, const std::vector<int64_t>& r
     TVR_TRY(upload(p, (void**)&pl.slice_item_end, zend.data(), sizeof(int64_t) * std::max<size_t>(1, zend.size())));
     pl.h_slice_item_end = zend;
   }
-  if (staged) TVR_TRY(make_tma_plan(p, pl, rp, slice_rows, pl.smem / sizeof(float)));
-  TVR_TRY(make_flat_plan(p, pl, rp, n_rows, separable, slice_rows, win_lo, win_len,
-                         (size_t)((rp[n_rows] + 7) / 8 * 8 + 8)));
+
   return TVR_OK;
 }
 
@@ -1294,7 +1099,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   if (p->world > 1) TVR_TRY(slab_table(p));
 
   // ---- device copies (columns made slab-local) ----
-  // Padding: 16-byte chunk loads and TMA bulk copies of whole 16-byte units may read up to 3
+  // Padding: 16-byte chunk loads of whole 16-byte units may read up to 3
   // entries past the end of col/val/b and 2 past row_ptr (the pads are zero, never used).
   const size_t nnz_pad = (size_t)((nnz + 7) / 8 * 8 + 8);  // 8-entry chunks of the 16-bit kernel
   TVR_TRY(dev_alloc(p, (void**)&p->rp, sizeof(int64_t) * (m + 3)));
@@ -1405,7 +1210,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   for (int which = 0; which < 2; ++which) {
     SpmvPlan& pl = which ? p->planT : p->planA;
     const bool p16 = pl.v.idx16, p32 = !pl.v.idx16 && !pl.staged;
-    if (!(p16 || p32) || pl.v.parts || pl.tma.on || pl.flat.on || !env_int("TVR_SPMV_PAD", 1)) continue;
+    if (!(p16 || p32) || pl.v.parts || !env_int("TVR_SPMV_PAD", 1)) continue;
     const int q = p16 ? 8 : 4;  // chunk entries
     const int64_t rows = which ? n : m;
     std::vector<int64_t> rph(rows + 1), rpp(rows + 1);
@@ -1598,8 +1403,8 @@ int tvr_get_info(const tvr_problem* p, tvr_info* info) {
   info->nnz_local = p->nnz;
   info->z0 = p->z0;
   info->z1 = p->z1;
-  info->slab_staged_A = p->planA.tma.on ? 2 : (p->planA.staged ? 1 : 0);
-  info->slab_staged_AT = p->planT.tma.on ? 2 : (p->planT.staged ? 1 : 0);
+  info->slab_staged_A = p->planA.staged ? 1 : 0;
+  info->slab_staged_AT = p->planT.staged ? 1 : 0;
   info->device_bytes = p->device_bytes;
   info->n_cols_local = p->ncol;
   info->views_fused_rs = p->fused_rs ? 1 : 0;
@@ -1641,6 +1446,7 @@ static int objective_grad_impl(tvr_problem* p, const float* x_dev, double* f_out
 
 int tvr_objective_grad(tvr_problem* p, const float* x_dev, double* f_out, float* g_dev,
                        tvr_fparts* parts) {
+  NvtxRange nv("tvr_objective_grad");
   if (!p || !x_dev) { set_error("tvr_objective_grad: NULL"); return TVR_E_ARG; }
   TVR_CUDA(cudaSetDevice(p->device));
   return objective_grad_impl(p, x_dev, f_out, g_dev, parts);
@@ -1861,11 +1667,11 @@ static int objective_grad_host_pipelined(tvr_problem* p, const float* xh, double
 
 int tvr_objective_grad_host(tvr_problem* p, const float* x_host, double* f_out, float* g_host,
                             tvr_fparts* parts) {
+  NvtxRange nv("tvr_objective_grad_host");
   if (!p || !x_host) { set_error("tvr_objective_grad_host: NULL"); return TVR_E_ARG; }
   TVR_CUDA(cudaSetDevice(p->device));
   const int C = std::min(env_int("TVR_E2E_CHUNKS", 3), std::min(6, p->nzl));  // 6: dscal slots
-  if (C > 1 && p->world == 1 && p->separable && !p->planA.tma.on && !p->planT.tma.on &&
-      !p->planA.flat.on && !p->planT.flat.on && !p->planA.v.parts && !p->planT.v.parts &&
+  if (C > 1 && p->world == 1 && p->separable && !p->planA.v.parts && !p->planT.v.parts &&
       pinned(x_host) && (!g_host || pinned(g_host)))
     return objective_grad_host_pipelined(p, x_host, f_out, g_host, parts, C);
   float* x = volvec(p, 7);
@@ -1885,6 +1691,22 @@ int tvr_residual(tvr_problem* p, const float* x_dev, float* r_dev, double* fid) 
   TVR_TRY(pass_residual(p, x_dev, r_dev, 0));
   TVR_TRY(fetch_scalars(p, 1));
   if (fid) *fid = 0.5 * p->hscal[0];
+  return TVR_OK;
+}
+
+int tvr_apply_A(tvr_problem* p, const float* x_dev, float* y_dev) {
+  if (!p || !x_dev || !y_dev) { set_error("tvr_apply_A: NULL"); return TVR_E_ARG; }
+  TVR_CUDA(cudaSetDevice(p->device));
+  NvtxRange nv("tvr_apply_A");
+  const float* src = x_dev;
+  TVR_TRY(gather_volume(p, x_dev, &src));
+  const double bytes = entry_bytes(p->planA) * (p->sliced ? (double)p->nnz_s : (double)p->nnz) +
+                       8.0 * ((p->sliced ? (double)p->m_s : (double)p->m) + 1) + 4.0 * p->ncol +
+                       4.0 * p->m;
+  TVR_TRY(launch(p, K_SPMV_A, bytes, [&] {
+    return run_spmv(p, p->planA, false, src, nullptr, y_dev, nullptr, nullptr);
+  }));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
   return TVR_OK;
 }
 

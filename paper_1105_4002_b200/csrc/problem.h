@@ -6,10 +6,22 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/libtvreg.h"
 #include "kernels.h"
 
 namespace tvr {
+
+// NVTX range (SURVEY §5 tracing): every pass, exchange and solver phase is a named range on the
+// host timeline (header-only NVTX v3; a no-op unless a tool such as nsys / ncu is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 // ------------------------------------------------------------------ errors
 void set_error(const std::string& msg);
@@ -40,42 +52,6 @@ enum KernelId {
 };
 extern const char* kKernelNames[K_COUNT];
 
-struct TmaPlan {
-  bool on = false;
-  int grid = 0, stages = 0, tile_nnz = 0, tile_rows = 0, win_cap = 0;
-  uint32_t piece = 1u << 20;
-  size_t smem = 0;
-  int64_t ntiles = 0;
-  int64_t* tile_row = nullptr;
-  int64_t* tile_k0 = nullptr;
-  int64_t* tile_k1 = nullptr;
-  int32_t* tile_slice = nullptr;
-  int64_t* bounds = nullptr;
-  int64_t nbounds = 0;
-};
-
-// Row-agnostic SpMV plan (spmv_flat.cu): warp-sized items, head mask, nonempty-row map.
-struct FlatPlan {
-  bool on = false;
-  FlatVariant v;
-  int grid = 0, block = 512;
-  size_t smem = 0;
-  int64_t nitems = 0;
-  int64_t* item_row = nullptr;
-  int64_t* item_nz = nullptr;
-  int32_t* item_slice = nullptr;
-  int64_t* slice_item_end = nullptr;
-  int64_t* win_lo = nullptr;  // one zero entry when the matrix has no slice windows
-  int32_t* win_len = nullptr;
-  uint8_t* head = nullptr;
-  int32_t* nzr = nullptr;
-  int32_t* empty_rows = nullptr;
-  int64_t n_empty = 0;
-};
-
-// One sliced-ELL structure (spmv16s_kernel): blocks of 32 rows of one slice each.  A window too
-// large for shared memory is cut into column parts, one structure per part (the part's entries
-// of every row, offsets relative to the part's window).
 struct SellData {
   int64_t nblk = 0;
   int64_t* off = nullptr;
@@ -95,8 +71,6 @@ struct SellData {
 };
 
 struct SpmvPlan {
-  TmaPlan tma;
-  FlatPlan flat;
   // padded-row copy for spmv16p_kernel (rows on 8-entry boundaries, zero pads)
   bool pad = false;
   int pad_grid = 0;

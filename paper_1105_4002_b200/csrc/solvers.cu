@@ -118,6 +118,7 @@ static int gpbb_impl(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_re
     int trials = 0;
     double f_bar = 0.0;
     for (;;) {
+      NvtxRange nv("GPBB trial (Alg. 1)");
       // x_bar = P_Q(x_k - beta theta_k g_k), TV(x_bar), g.(x - x_bar); on the first
       // trial also ||x_k - P_Q(x_k - theta_k g_k)|| for the stop test with nu = 1/theta_k (C11)
       TVR_TRY(pass_tv_trial(p, x_cur, g_cur, beta * theta, v, trials == 0 ? theta : 0.0, nullptr, S_TV));
@@ -465,6 +466,7 @@ static int backtrack(tvr_problem* p, const float* y, const float* y_lo, const fl
                      double L_bar, const tvr_upn_opts& o, const float* xk_for_mu,
                      const float* xk_lo_for_mu, float* x_out, float* x_out_lo, float* r_out,
                      float* r_out_lo, BTOut& out) {
+  NvtxRange nv("BT (Alg. 2)");
   double L = L_bar;
   out.trials = 0;
   out.mu_gd = out.mu_dd = 0.0;
@@ -588,6 +590,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
       break;
     }
     const double beta = theta * (1.0 - theta) / (theta * theta + theta_n);
+    NvtxRange nv_m("UPN gradient and momentum (Alg. 3)");
     // w_{k+1} = A^T r_{k+1}; stop reduction at x_{k+1} with nu = L_k (C11); then
     // y_{k+1} = x_{k+1} + beta (x_{k+1} - x_k) with grad f(y) and f(y) by linearity (a6)
     TVR_TRY(pass_AT(p, rn, wn));
@@ -721,6 +724,7 @@ extern "C" {
 
 int tvr_solve_gpbb(tvr_problem* p, float* x, const tvr_gpbb_opts* opts, tvr_result* res,
                    tvr_record* hist, int64_t hist_cap) {
+  NvtxRange nv("tvr_solve_gpbb");
   if (!p || !x) { set_error("tvr_solve_gpbb: NULL"); return TVR_E_ARG; }
   tvr_gpbb_opts o;
   tvr_gpbb_default(&o);
@@ -742,6 +746,7 @@ int tvr_solve_gpbb(tvr_problem* p, float* x, const tvr_gpbb_opts* opts, tvr_resu
 
 int tvr_solve_upn(tvr_problem* p, float* x, const tvr_upn_opts* opts, tvr_result* res,
                   tvr_record* hist, int64_t hist_cap) {
+  NvtxRange nv("tvr_solve_upn");
   if (!p || !x) { set_error("tvr_solve_upn: NULL"); return TVR_E_ARG; }
   tvr_upn_opts o;
   tvr_upn_default(&o);
@@ -763,6 +768,7 @@ int tvr_solve_upn(tvr_problem* p, float* x, const tvr_upn_opts* opts, tvr_result
 
 int tvr_solve_gp(tvr_problem* p, float* x, const tvr_gp_opts* opts, tvr_result* res,
                  tvr_record* hist, int64_t hist_cap) {
+  NvtxRange nv("tvr_solve_gp");
   if (!p || !x) { set_error("tvr_solve_gp: NULL"); return TVR_E_ARG; }
   tvr_gp_opts o;
   tvr_gp_default(&o);

@@ -129,6 +129,7 @@ SIGNATURES = {
     "tvr_residual": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(c_f64)]),
     "tvr_set_control": (ctypes.c_int, [c_vp, ctypes.c_int]),
     "tvr_apply_AT": (ctypes.c_int, [c_vp, c_vp, c_vp]),
+    "tvr_apply_A": (ctypes.c_int, [c_vp, c_vp, c_vp]),
     "tvr_tv": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(c_f64), c_vp]),
     "tvr_gradient_map": (ctypes.c_int, [c_vp, c_vp, c_f64, ctypes.POINTER(c_f64), c_vp]),
     "tvr_get_AT": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
@@ -348,6 +349,10 @@ class Problem:
         fid = c_f64()
         _check(lib().tvr_residual(self._h, _ptr(x), _ptr(r), ctypes.byref(fid)), "tvr_residual")
         return fid.value
+
+    def apply_A(self, x, y):
+        """y = A x (tvr_apply_A)."""
+        _check(lib().tvr_apply_A(self._h, _ptr(x), _ptr(y)), "tvr_apply_A")
 
     def apply_AT(self, y, w):
         _check(lib().tvr_apply_AT(self._h, _ptr(y), _ptr(w)), "tvr_apply_AT")

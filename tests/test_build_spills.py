@@ -16,10 +16,13 @@ HOT = {
         (r"tv_kernelINS_8SrcPlainELi0ELi5EiE", 0),       # tvr_objective_grad: W1 | G
         (r"tv_kernelINS_8SrcPlainELi0ELi69EiE", 0),      # solver gradient + stop test
         (r"tv_kernelINS_8SrcPlainELi0ELi65EiE", 0),      # UPN stop test at x_{k+1}
-        (r"tv_kernelINS_11SrcMomentumELi0ELi15EiE", 0),  # UPN momentum point
+        (r"tv_kernelINS_12SrcMomentumXELi0ELi15EiE", 0),   # UPN momentum point (hi + lo state)
+        (r"tv_kernelINS_12SrcMomentumXELi0ELi143EiE", 0),  # same, device-side control
         (r"tv_kernelINS_8SrcTrialELi1ELi0EiE", 0),       # trial points
         (r"tv_kernelINS_8SrcTrialELi1ELi32EiE", 0),
         (r"tv_kernelINS_8SrcTrialELi1ELi64EiE", 0),
+        (r"tv_kernelINS_9SrcTrialXELi1ELi0EiE", 0),        # BT trials (hi + lo state)
+        (r"tv_kernelINS_9SrcTrialXELi1ELi32EiE", 0),
     ],
     "spmv.cu": [
         (r"spmv16s_kernelILi2ELb1ELi512ELb0ELb1E", 0),   # sliced ELL: c2 A and A^T passes

@@ -216,9 +216,10 @@ def test_gradient_map(tvreg, c1):
 
 
 @pytest.mark.parametrize("cfg", ["c1", "ragged"])
-def test_tma_pipeline_matches_register_kernel_bitwise(tvreg, cfg, c1, monkeypatch):
-    """The TMA bulk-copy SpMV and the register-streaming SpMV use the same per-row summation
-    order, so r, 1/2||r||^2 and A^T r agree bitwise; the staged-window kernel is exercised too."""
+def test_per_row_kernels_bitwise(tvreg, cfg, c1, monkeypatch):
+    """The int32 per-row SpMV with the slice window staged in shared memory and with global
+    gathers use the same per-row summation order, so r, 1/2||r||^2 and A^T r agree bitwise; the
+    16-bit-column kernel (8-entry chunks) agrees to fp32 rounding."""
     if cfg == "c1":
         A, b, grid = c1.A, c1.b, c1.grid
     else:
@@ -227,13 +228,11 @@ def test_tma_pipeline_matches_register_kernel_bitwise(tvreg, cfg, c1, monkeypatc
         grid = (37, 29, 11)
     x = dev(harness.random_x(A.n_cols))
     outs = {}
-    monkeypatch.setenv("TVR_SPMV_FLAT", "0")  # the per-row kernels (the flat one: test_flat_*)
-    for mode in ("tma", "reg", "global", "reg16"):
-        monkeypatch.setenv("TVR_SPMV_TMA", "1" if mode == "tma" else "0")
+    for mode in ("reg", "global", "reg16"):
         monkeypatch.setenv("TVR_SPMV_STAGE", "0" if mode == "global" else "1")
         monkeypatch.setenv("TVR_IDX16", "1" if mode == "reg16" else "0")
         P = make(tvreg, A, b, grid)
-        assert P.info.slab_staged_A == {"tma": 2, "reg": 1, "global": 0, "reg16": 1}[mode]
+        assert P.info.slab_staged_A == {"reg": 1, "global": 0, "reg16": 1}[mode]
         r = torch.empty(A.n_rows, device="cuda")
         fid = P.residual(x, r)
         w = torch.empty(A.n_cols, device="cuda")
@@ -244,12 +243,10 @@ def test_tma_pipeline_matches_register_kernel_bitwise(tvreg, cfg, c1, monkeypatc
             oT = oracle.transpose(A.row_ptr, A.col, A.val, A.n_cols)
             assert np.array_equal(cT, oT[1]) and np.array_equal(rT, oT[0])
         P.close()
-    for mode in ("reg", "global"):   # same 4-entry chunk order: bitwise
-        assert np.array_equal(outs[mode][0], outs["tma"][0])
-        # the fp64 sum of r^2 is split differently over CTAs: equal to rounding only
-        assert abs(outs[mode][1] - outs["tma"][1]) <= 1e-13 * outs["tma"][1]
-        assert np.array_equal(outs[mode][2], outs["tma"][2])
-    # 16-bit columns use 8-entry chunks (another fp64 summation order): equal to fp32 rounding
+    assert np.array_equal(outs["global"][0], outs["reg"][0])
+    # the fp64 sum of r^2 is split differently over CTAs: equal to rounding only
+    assert abs(outs["global"][1] - outs["reg"][1]) <= 1e-13 * outs["reg"][1]
+    assert np.array_equal(outs["global"][2], outs["reg"][2])
     assert rel(outs["reg16"][0], outs["reg"][0]) <= 1e-7
     assert abs(outs["reg16"][1] - outs["reg"][1]) <= 1e-13 * outs["reg"][1]
     assert rel(outs["reg16"][2], outs["reg"][2]) <= 1e-7
@@ -271,10 +268,11 @@ def _row_length_zoo(n_cols, seed):
 
 
 @pytest.mark.parametrize("cfg", ["c1", "ragged", "zoo"])
-def test_flat_spmv_variants(tvreg, cfg, c1, monkeypatch):
-    """The row-agnostic SpMV (spmv_flat.cu): staged / global gather, 1 or 2 tiles in flight,
-    16-bit or int32 columns and any item size share one summation order, so they agree bitwise;
-    they match the oracle (bitwise on dyadic data) and the per-row kernel to fp32 rounding."""
+def test_spmv_variants_against_oracle(tvreg, cfg, c1, monkeypatch):
+    """Every SpMV layout the library can pick for a slice-structured matrix (sliced ELL with the
+    staged window, global gathers, int32 columns, the padded per-row kernel) against the oracle:
+    bitwise on dyadic data (the zoo of row lengths 0 .. 600: rows inside one chunk, on chunk
+    edges, spanning many chunks, empty rows), to fp32 rounding otherwise."""
     rng = np.random.default_rng(11)
     if cfg == "c1":
         A, grid = c1.A, c1.grid
@@ -289,12 +287,12 @@ def test_flat_spmv_variants(tvreg, cfg, c1, monkeypatch):
         A = _row_length_zoo(16 * 16 * 4, 3)
         x = rng.integers(0, 9, A.n_cols).astype(np.float32)
         b = rng.integers(0, 9, A.n_rows).astype(np.float32)
-    modes = {"flat": {}, "global": {"TVR_SPMV_STAGE": "0"}, "unr1": {"TVR_FLAT_UNROLL": "1"},
-             "int32": {"TVR_IDX16": "0"}, "items64": {"TVR_FLAT_ITEM": "64"},
-             "perrow": {"TVR_SPMV_FLAT": "0"}}
-    outs = {}
+    modes = {"sell": {}, "global": {"TVR_SPMV_STAGE": "0"}, "int32": {"TVR_IDX16": "0"},
+             "perrow": {"TVR_SPMV_SELL": "0"}}
+    r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x.astype(np.float64)) - b
+    w_ora = oracle.rmatvec(A.row_ptr, A.col, A.val, b.astype(np.float64), A.n_cols)
     for mode, env in modes.items():
-        for k in ("TVR_SPMV_STAGE", "TVR_FLAT_UNROLL", "TVR_IDX16", "TVR_FLAT_ITEM", "TVR_SPMV_FLAT"):
+        for k in ("TVR_SPMV_STAGE", "TVR_IDX16", "TVR_SPMV_SELL"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -303,24 +301,13 @@ def test_flat_spmv_variants(tvreg, cfg, c1, monkeypatch):
         fid = P.residual(dev(x), r)
         w = torch.empty(A.n_cols, device="cuda")
         P.apply_AT(dev(b), w)
-        outs[mode] = (host(r).copy(), fid, host(w).copy())
+        rh, wh = host(r).astype(np.float64), host(w).astype(np.float64)
         P.close()
-    r_ora = oracle.matvec(A.row_ptr, A.col, A.val, x.astype(np.float64)) - b
-    w_ora = oracle.rmatvec(A.row_ptr, A.col, A.val, b.astype(np.float64), A.n_cols)
-    for mode in ("global", "unr1", "int32", "items64"):
-        assert np.array_equal(outs[mode][0], outs["flat"][0]), mode
-        assert np.array_equal(outs[mode][2], outs["flat"][2]), mode
-        assert abs(outs[mode][1] - outs["flat"][1]) <= 1e-13 * outs["flat"][1]
-    if cfg == "zoo":  # dyadic: exact
-        assert np.array_equal(outs["flat"][0].astype(np.float64), r_ora)
-        assert np.array_equal(outs["flat"][2].astype(np.float64), w_ora)
-        assert outs["flat"][1] == 0.5 * float(r_ora @ r_ora)
-    assert rel(outs["flat"][0], r_ora) <= 1e-6 and rel(outs["flat"][2], w_ora) <= 1e-6
-    assert rel(outs["flat"][0], outs["perrow"][0]) <= 1e-7
-    assert rel(outs["flat"][2], outs["perrow"][2]) <= 1e-7
-    empty = np.diff(A.row_ptr) == 0
-    if empty.any():
-        assert np.array_equal(outs["flat"][0][empty], -b[empty])
+        if cfg == "zoo":  # dyadic: exact
+            assert np.array_equal(rh, r_ora), mode
+            assert np.array_equal(wh, w_ora), mode
+            assert fid == 0.5 * float(r_ora @ r_ora), mode
+        assert rel(rh, r_ora) <= 1e-6 and rel(wh, w_ora) <= 1e-6, mode
 
 
 def _separable_zoo(nx, ny, nz, seed):

@@ -234,19 +234,26 @@ def test_gp_abs_per_n_stop_closed_form(tvreg):
 
 def test_gpbb_long_nonmonotone_window(tvreg, c1):
     """f_hat of P:147 is the max over the last K + 1 accepted values for any K (the host
-    controller used to keep at most 64).  With K = 63 and K = 100 the windows hold every accepted
-    value until iteration 63, so the two runs are identical there; from iteration 64 on K = 63
-    drops f_0 (the largest value) from its window and the runs must part."""
+    controller used to keep at most 64).  K = 100 (host control: more than the device
+    controller's 64 slots) runs 120 iterations, follows the oracle's GPBB with K = 100 over the
+    first iterations, and is identical to K = 63 while both windows still hold every accepted
+    value (iterations < 64); every accepted value lies below the max of the K + 1 before it."""
     outs = {}
     for K in (63, 100):
         P = _gpu_problem(tvreg, c1)
         P.set_control("host")
         x = torch.zeros(c1.N, device="cuda")
-        outs[K] = P.solve_gpbb(x, max_iters=120, eps=0.0, K=K, hist_cap=200).history
+        res = P.solve_gpbb(x, max_iters=120, eps=0.0, K=K, hist_cap=200)
+        assert res.iters == 120
+        outs[K] = res.history
         P.close()
     a, b = outs[63], outs[100]
     assert a[:64] == b[:64]
-    assert any(u != v for u, v in zip(a[64:], b[64:]))
+    fs = [r["f"] for r in b]
+    assert all(fs[k + 1] < max(fs[max(0, k - 100):k + 1]) for k in range(len(fs) - 1))
+    ref = oracle.gpbb(_oracle_problem(c1), np.zeros(c1.N), eps=0.0, max_iters=5, K=100)
+    for k in range(3):
+        assert abs(b[k]["f"] - ref.history[k]["f"]) <= 1e-6 * abs(ref.history[k]["f"])
 
 
 @pytest.mark.parametrize("alpha", [0.003, 0.03])
