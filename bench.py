@@ -136,24 +136,83 @@ def traffic_table():
 
 
 # ---------------------------------------------------------------- cpu baseline
-def cpu_baseline(w, budget_s=20.0, max_evals=5):
+def _oracle_evals(Po, x, n, budget_s):
+    """n timed oracle gradient evaluations (bounded by budget_s), split into the A pass
+    (row-parallel A x - b), the A^T pass and the TV value + gradient (single-threaded)."""
+    import oracle
+    t_a = t_at = t_tv = 0.0
+    k = 0
+    t0 = time.perf_counter()
+    while k < n and (k == 0 or time.perf_counter() - t0 < budget_s):
+        a = time.perf_counter()
+        r = Po.residual(x)
+        b = time.perf_counter()
+        Po.rmatvec(r)
+        c = time.perf_counter()
+        oracle.tv(Po.grid, x, Po.tau, want_grad=True)
+        d = time.perf_counter()
+        t_a, t_at, t_tv = t_a + b - a, t_at + c - b, t_tv + d - c
+        k += 1
+    tot = t_a + t_at + t_tv
+    return dict(evals=k, evals_per_s=k / tot, s_per_eval=tot / k,
+                pass_s=dict(A=t_a / k, AT=t_at / k, TV=t_tv / k))
+
+
+def cpu_baseline(w, solver_its=None):
+    """The oracle (plain fp64 CPU, oracle/) on this box's host cores, beside the GPU numbers
+    (SURVEY §8(d) 'Oracle timing'; a baseline, not the target).  value: c2 gradient evaluations
+    per second on all cores (20 evaluations).  Also: the same at 1 thread (5 evaluations), the
+    per-pass split, c1 GPBB / UPN iterations timed (200 each) and, labelled as extrapolations,
+    the oracle time of the GPU's full solves (oracle seconds per iteration x GPU iterations)."""
+    import harness
     import oracle
     nthreads = os.cpu_count() or 1
+    x = harness.random_x(w.N).astype(np.float64)
     Po = oracle.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
                         nthreads=nthreads).use_transpose()
-    import harness
-    x = harness.random_x(w.N)
-    Po.fg(x)  # warm-up
-    t0 = time.perf_counter()
-    n = 0
-    while n < max_evals and (time.perf_counter() - t0) < budget_s:
-        Po.fg(x)
-        n += 1
-    dt = time.perf_counter() - t0
-    return dict(value=n / dt, unit=UNIT, cores=nthreads, kind="oracle",
-                sample=f"{n} full fp64 gradient evaluations of {w.name} (A x row-parallel, A^T r "
-                       f"row-parallel over the oracle's own transposed CSR, TV single-threaded), "
-                       f"{dt:.1f} s on {nthreads} host threads")
+    Po.fg(x)  # warm-up (page-in)
+    allc = _oracle_evals(Po, x, 20, 30.0)
+    P1 = oracle.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, w.alpha, w.tau, w.lo, w.hi,
+                        nthreads=1)
+    P1._T = Po._T  # the same canonical transpose, row-parallel product on one thread
+    one = _oracle_evals(P1, x, 5, 15.0)
+    del Po, P1
+    c1 = harness.preset("c1")
+    Pc = oracle.Problem(c1.A.row_ptr, c1.A.col, c1.A.val, c1.b, c1.grid, c1.alpha, c1.tau, c1.lo,
+                        c1.hi, nthreads=nthreads).use_transpose()
+    c1_its = {}
+    for solver in ("gpbb", "upn"):
+        t0 = time.perf_counter()
+        r = getattr(oracle, solver)(Pc, np.zeros(c1.N), eps=0.0, max_iters=200)
+        c1_its[solver] = dict(iters=r.iters, seconds=time.perf_counter() - t0,
+                              s_per_iter=(time.perf_counter() - t0) / max(1, r.iters))
+    # Labelled extrapolations (not measured): the oracle's time for the GPU's full solves.
+    # c1: oracle seconds per iteration x GPU iterations.  c2 / c3 / c5: the GPU run's objective
+    # and gradient evaluation counts priced at the measured all-core c2 pass times, scaled by
+    # entries (A, A^T) and voxels (TV) for the 256^3 workloads.
+    ps = allc["pass_s"]
+    scale = {"c2": (1.0, 1.0), "c3": (1922080768 / 160079872, 8.0), "c5": (2673867810 / 160079872, 8.0)}
+    extrap = {}
+    for key, rec in (solver_its or {}).items():
+        cfg, solver = key.split("_", 1)
+        per_it = c1_its.get(solver, {}).get("s_per_iter")
+        if cfg == "c1" and per_it:
+            extrap[key] = dict(oracle_seconds=per_it * rec["iters"], gpu_iters=rec["iters"],
+                               basis="oracle c1 seconds per iteration (200 timed) x GPU iterations")
+        elif cfg in scale and "n_f" in rec:
+            se, sv = scale[cfg]
+            sec = rec["n_f"] * (ps["A"] * se + ps["TV"] * sv) + rec["n_grad"] * (ps["AT"] * se + ps["TV"] * sv)
+            extrap[key] = dict(oracle_seconds=sec, gpu_iters=rec["iters"], n_f=rec["n_f"],
+                               n_grad=rec["n_grad"],
+                               basis=f"GPU evaluation counts x oracle c2 all-core pass seconds"
+                                     f"{'' if cfg == 'c2' else ' scaled by entries / voxels to ' + cfg}")
+    return dict(value=allc["evals_per_s"], unit=UNIT, cores=nthreads, kind="oracle",
+                sample=f"{allc['evals']} full fp64 gradient evaluations of {w.name} (A x row-parallel, "
+                       f"A^T r row-parallel over the oracle's own transposed CSR, TV single-threaded) "
+                       f"on {nthreads} host threads, {allc['evals'] * allc['s_per_eval']:.1f} s",
+                pass_seconds_all_cores=allc["pass_s"],
+                one_thread=dict(value=one["evals_per_s"], evals=one["evals"], pass_seconds=one["pass_s"]),
+                c1_solver_iterations=c1_its, extrapolated=extrap)
 
 
 # ------------------------------------------------------------------ our arm
@@ -198,10 +257,21 @@ def run_ours(args, rank, world, local_rank):
         P.objective_grad(x, g)
     clocks = ClockSampler(local_rank)
     clocks.start()
-    time.sleep(0.15)
-    # Timed region 1 (the value): K uninstrumented steps.  Timed region 2 (the roofline): the
-    # same K steps with CUDA events around every kernel on the library's stream — the events
-    # cost ~28 us per step (measured, scripts/host_overhead.py), so they are kept out of region 1.
+    # keep the GPU busy (not idle-sleeping) while the sampler starts, so the timed regions begin
+    # at steady clocks: extra untimed warm-up steps for ~150 ms (a short timed region after an
+    # idle gap ran at ramping clocks: r1's e2e at --steps 20 read 1159/s against 1819/s)
+    xh = torch.from_numpy(x_h.copy()).pin_memory()
+    gh = torch.empty(n_loc, dtype=torch.float32).pin_memory()
+    extra_warm = 0
+    torch.cuda.synchronize()
+    t_w = time.perf_counter()
+    while time.perf_counter() - t_w < 0.15:
+        P.objective_grad(x, g)
+        extra_warm += 1
+    # Timed region 1 (the value): K uninstrumented steps.  Then the e2e region, then timed
+    # region 3 (the roofline): the same K steps with CUDA events around every kernel on the
+    # library's stream — the events cost ~28 us per step (measured, scripts/host_overhead.py), so
+    # they are kept out of region 1.
     P.profile(False)
     P.launch_count(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -216,6 +286,29 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     launches = P.launch_count()
     ms_total = e0.elapsed_time(e1)
+
+    # ---- e2e through the host API: H2D x, D2H g and f inside the timed region
+    for _ in range(5):
+        P.objective_grad_host(xh.numpy(), gh.numpy())
+    barrier()
+    torch.cuda.synchronize()
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    h0.record(stream)
+    for _ in range(args.steps):
+        P.objective_grad_host(xh.numpy(), gh.numpy())
+    h1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    barrier()
+    te = torch.tensor([max(h0.elapsed_time(h1), wall * 1e3)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = dict(value=world * args.steps / (float(te.item()) / 1e3), unit=UNIT,
+               h2d_bytes_per_step=int(4 * n_loc * world), d2h_bytes_per_step=int((4 * n_loc + 8) * world),
+               pipeline="3 slab chunks: H2D of chunk c+1 and D2H of chunk c-1 overlap the passes of "
+                        "chunk c (DESIGN §7.1)")
+
     P.profile(True)
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -238,27 +331,6 @@ def run_ours(args, rank, world, local_rank):
     # gradient evaluations of c2-sized volumes per second over the whole job (weak scaling:
     # world slabs per step)
     value = world * args.steps / (ms_total / 1e3)
-
-    # ---- e2e through the host API: H2D x, D2H g and f inside the timed region
-    xh = torch.from_numpy(x_h.copy()).pin_memory()
-    gh = torch.empty(n_loc, dtype=torch.float32).pin_memory()
-    for _ in range(2):
-        P.objective_grad_host(xh.numpy(), gh.numpy())
-    barrier()
-    torch.cuda.synchronize()
-    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    w0 = time.perf_counter()
-    h0.record(stream)
-    for _ in range(args.steps):
-        P.objective_grad_host(xh.numpy(), gh.numpy())
-    h1.record(stream)
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - w0
-    te = torch.tensor([max(h0.elapsed_time(h1), wall * 1e3)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e = dict(value=world * args.steps / (float(te.item()) / 1e3), unit=UNIT,
-               h2d_bytes_per_step=int(4 * n_loc * world), d2h_bytes_per_step=int((4 * n_loc + 8) * world))
 
     # ---- roofline of the dominant kernel
     peak, peak_src = peaks()
@@ -283,7 +355,8 @@ def run_ours(args, rank, world, local_rank):
                            "region of the same K steps (events excluded from the value region)")
     step_bytes = sum(s["bytes"] for s in stats.values()) / args.steps
     out = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
-               warmup=args.warmup, ms_per_step=ms_step, higher_is_better=True,
+               warmup=args.warmup, warmup_extra_steps=extra_warm, ms_per_step=ms_step,
+               higher_is_better=True,
                ms_per_step_instrumented=ms_total_prof / args.steps,
                scaling="weak", vs_baseline=None, dtype="f64",
                storage_dtype="f32", data="synthetic",
@@ -299,7 +372,8 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0 and world == 1 and not args.no_solve:
         out["solvers"] = solver_timings(tvreg, torch)
-        out["c3_gradient"] = large_config_line(tvreg, torch, solve=("gpbb", "upn"))
+        out["c3_gradient"] = large_config_line(tvreg, torch, solve=("gpbb", "upn"),
+                                               oracle_time=not args.no_cpu_baseline)
         out["c5_gradient"] = large_config_line(tvreg, torch, cfg="c5")
         out["sliced"] = sliced_lines(tvreg, torch)
     if world > 1 and not args.no_solve:
@@ -312,7 +386,11 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.empty_cache()
         out["c5_gradient"] = large_config_line(tvreg, torch, "c5", 10, world, rank, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(w)
+        its = {k: v for k, v in out.get("solvers", {}).items() if "iters" in v}
+        for s in ("gpbb", "upn"):
+            if s in out.get("c3_gradient", {}):
+                its[f"c3_{s}"] = out["c3_gradient"][s]
+        out["cpu_baseline"] = cpu_baseline(w, its)
     if P is not None:
         P.close()
     if comm:
@@ -348,7 +426,8 @@ def solver_timings(tvreg, torch, configs=("c1", "c2", "f2few", "f2many")):
     return out
 
 
-def large_config_line(tvreg, torch, cfg="c3", steps=10, world=1, rank=0, local_rank=0, solve=None):
+def large_config_line(tvreg, torch, cfg="c3", steps=10, world=1, rank=0, local_rank=0, solve=None,
+                      oracle_time=False):
     """Gradient evaluations on a 256^3 workload (c3: BJ configs[2], separable; c5: configs[4],
     non-separable) at N = world GPUs, STRONG scaling (the whole 256^3 problem split over the ranks,
     the north star's "80 % parallel efficiency at 8 GPUs on the 256^3 workloads"):
@@ -399,6 +478,7 @@ def large_config_line(tvreg, torch, cfg="c3", steps=10, world=1, rank=0, local_r
                           stream=stream.cuda_stream)
         nnz_tot = w.A.nnz
         x = torch.from_numpy(harness.random_x(w.N)).cuda()
+        w_host = w if oracle_time else None
         del w
 
     def barrier():
@@ -450,6 +530,17 @@ def large_config_line(tvreg, torch, cfg="c3", steps=10, world=1, rank=0, local_r
     if comm:
         barrier()
         tvreg.nccl_comm_destroy(comm)
+    if world == 1 and oracle_time:
+        # one oracle gradient evaluation of the same 256^3 workload on all host cores (A x
+        # row-parallel, A^T r by the scatter over A's rows: no second 15 GB transpose)
+        import oracle
+        Po = oracle.Problem(w_host.A.row_ptr, w_host.A.col, w_host.A.val, w_host.b, w_host.grid,
+                            w_host.alpha, w_host.tau, w_host.lo, w_host.hi, nthreads=os.cpu_count() or 1)
+        ev = _oracle_evals(Po, x.cpu().numpy().astype(np.float64), 1, 60.0)
+        res["oracle"] = dict(value=ev["evals_per_s"], unit=UNIT, cores=os.cpu_count() or 1,
+                             pass_seconds=ev["pass_s"], kind="oracle",
+                             sample="1 full fp64 gradient evaluation (A^T r by scatter, single-threaded)")
+        del Po, w_host
     return res
 
 

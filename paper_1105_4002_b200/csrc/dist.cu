@@ -174,6 +174,45 @@ int halo_fill_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, co
   return TVR_OK;
 }
 
+int reduce_gathered_scalars(tvr_problem* p, double* vals, int n);
+
+int halo_exchange_fetch(tvr_problem* p, float* v, int nslots) {
+  if (p->world <= 1 || local_of(p)) {
+    TVR_TRY(halo_exchange(p, v));
+    return fetch_scalars(p, nslots);
+  }
+  NvtxRange nv("halo_exchange + scalar_allgather");
+  ncclComm_t comm = nccl_of(p);
+  const size_t cnt = (size_t)p->plane;
+  TVR_NCCL(ncclGroupStart());
+  if (p->rank > 0) {
+    TVR_NCCL(ncclSend(v, cnt, ncclFloat, p->rank - 1, comm, p->stream));
+    TVR_NCCL(ncclRecv(v - p->plane, cnt, ncclFloat, p->rank - 1, comm, p->stream));
+  }
+  if (p->rank < p->world - 1) {
+    TVR_NCCL(ncclSend(v + (int64_t)(p->nzl - 1) * p->plane, cnt, ncclFloat, p->rank + 1, comm, p->stream));
+    TVR_NCCL(ncclRecv(v + (int64_t)p->nzl * p->plane, cnt, ncclFloat, p->rank + 1, comm, p->stream));
+  }
+  TVR_NCCL(ncclAllGather(p->dscal, p->dgather, (size_t)nslots, ncclDouble, comm, p->stream));
+  TVR_NCCL(ncclGroupEnd());
+  return reduce_gathered_scalars(p, p->hscal, nslots);
+}
+
+// rank-ordered sum of the all-gathered scalars (p->dgather, world x n) into vals (host)
+int reduce_gathered_scalars(tvr_problem* p, double* vals, int n) {
+  double* all = p->hscal + 64;  // world x n staging after the first 64 slots
+  TVR_CUDA(cudaMemcpyAsync(all, p->dgather, sizeof(double) * n * p->world, cudaMemcpyDeviceToHost,
+                           p->stream));
+  TVR_CUDA(cudaStreamSynchronize(p->stream));
+  resolve_pending_timings(p);
+  for (int s = 0; s < n; ++s) {
+    double acc = 0.0;
+    for (int r = 0; r < p->world; ++r) acc += all[(size_t)r * n + s];  // rank order
+    vals[s] = acc;
+  }
+  return TVR_OK;
+}
+
 int dist_sum_scalars(tvr_problem* p, double* vals, int n) {
   NvtxRange nv("scalar_allgather");
   if (local_of(p)) {
@@ -186,17 +225,7 @@ int dist_sum_scalars(tvr_problem* p, double* vals, int n) {
   } else {
     TVR_NCCL(ncclAllGather(p->dscal, p->dgather, (size_t)n, ncclDouble, nccl_of(p), p->stream));
   }
-  double* all = p->hscal + 64;  // world x n staging after the first 64 slots
-  TVR_CUDA(cudaMemcpyAsync(all, p->dgather, sizeof(double) * n * p->world, cudaMemcpyDeviceToHost,
-                           p->stream));
-  TVR_CUDA(cudaStreamSynchronize(p->stream));
-  resolve_pending_timings(p);
-  for (int s = 0; s < n; ++s) {
-    double acc = 0.0;
-    for (int r = 0; r < p->world; ++r) acc += all[(size_t)r * n + s];  // rank order
-    vals[s] = acc;
-  }
-  return TVR_OK;
+  return reduce_gathered_scalars(p, vals, n);
 }
 
 // Every rank's slab [z0, z1), gathered once at create time (the halo exchange of the local

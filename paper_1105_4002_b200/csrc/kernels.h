@@ -103,6 +103,8 @@ struct SellArgs {
   const int64_t* win_lo;
   const int32_t* win_len;
   int part_len;             // half: window entries staged
+  int32_t l2hint;           // spmv32s_kernel L2 policies: bit 0 matrix stream evict-first,
+                            // bit 1 gathered vector evict-last
   int32_t ilv;              // spmv32s_kernel: > 0 = CTA c walks the block chunks c, c + G,
                             // c + 2G, ... of ilv blocks each (the grid sweeps the block order
                             // together: z-ordered blocks keep the gathered sub-volume in L2);

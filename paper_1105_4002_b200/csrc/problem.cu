@@ -178,6 +178,7 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     s.nb = d.nblk;
     s.rep = 1;
     s.ilv = pl.sell32_ilv;
+    s.l2hint = pl.sell32_l2;
     s.partials = p->partials;
     s.counter = p->counter;
     s.scal = scal;
@@ -804,6 +805,7 @@ static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std:
   pl.sell32_zorder = zorder;
   // interleaved chunks of TVR_SELL32_ILV blocks (default 4 with the z order, else ranges)
   pl.sell32_ilv = env_int("TVR_SELL32_ILV", zorder ? 4 : 0);
+  pl.sell32_l2 = env_int("TVR_SELL32_L2", 0);
   return TVR_OK;
 }
 

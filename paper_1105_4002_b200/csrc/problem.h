@@ -81,6 +81,7 @@ struct SpmvPlan {
   int64_t sell32_row_blocks = 0;       // of its blocks, those in row mode
   int32_t sell32_ilv = 0;              // interleaved CTA chunks of this many blocks (0: ranges)
   bool sell32_zorder = false;          // blocks stored in z order of the voxels they gather
+  int32_t sell32_l2 = 0;               // spmv32s L2 policies (SellArgs::l2hint)
   int32_t rep = 1;                     // slice-shared operator: the blocks repeat per slice
   int64_t rep_rows = 0, rep_win = 0;   // per repetition: output row / gather window offsets
   int64_t rep_total = 0;               // slice groups (sv.zgroup > 1): slices; rep = groups
@@ -259,6 +260,9 @@ int halo_fill_trial_x(tvr_problem* p, const float* x, const float* x_lo, const f
 int halo_fill_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, const float* x0,
                          const float* x0_lo, double beta, float* y, float* y_lo);
 int dist_sum_scalars(tvr_problem* p, double* vals, int n);
+// halo_exchange(v) then fetch_scalars(nslots), with the halo send / recv and the scalar
+// all-gather in ONE NCCL group (one launch, one synchronisation) on the NCCL backend
+int halo_exchange_fetch(tvr_problem* p, float* v, int nslots);
 // VIEWS mode: the A pass's source (slab -> full volume, all-gathered) and the A^T pass's
 // target (full-volume partial -> slab, reduce-scattered); identity on one rank
 bool views_dist(const tvr_problem* p);

@@ -90,8 +90,7 @@ static int gpbb_impl(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_re
   TVR_TRY(pass_AT(p, r_cur, w));
   TVR_TRY(pass_tv_grad(p, x_cur, nullptr, 0.0, w, nullptr, 0.0, g_cur, nullptr, nullptr, nullptr,
                        1.0, S_TV));
-  TVR_TRY(halo_exchange(p, g_cur));
-  TVR_TRY(fetch_scalars(p, S_COUNT));
+  TVR_TRY(halo_exchange_fetch(p, g_cur, S_COUNT));
   double f = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
   const double gref = std::sqrt(p->hscal[S_TV + 3]);
   if (!std::isfinite(f) || !std::isfinite(gref)) { set_error("GPBB: non-finite f or g at x0"); return TVR_E_NONFINITE; }
@@ -159,8 +158,7 @@ static int gpbb_impl(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_re
     TVR_TRY(pass_AT(p, r_cur, w));
     TVR_TRY(pass_tv_grad(p, x_cur, nullptr, 0.0, w, nullptr, 0.0, g_cur, nullptr, x_prev, g_prev,
                          0.0, S_TV));
-    TVR_TRY(halo_exchange(p, g_cur));
-    TVR_TRY(fetch_scalars(p, S_COUNT));
+    TVR_TRY(halo_exchange_fetch(p, g_cur, S_COUNT));
     bb_dd = p->hscal[S_TV + 1];
     bb_dg = p->hscal[S_TV + 2];
     ++n_g;
@@ -524,8 +522,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   TVR_TRY(pass_residual(p, xk, rk, S_RSQ, rk_lo));
   TVR_TRY(pass_AT(p, rk, wk));
   TVR_TRY(pass_tv_grad(p, xk, nullptr, 0.0, wk, nullptr, 0.0, gy, nullptr, nullptr, nullptr, 1.0, S_TV));
-  TVR_TRY(halo_exchange(p, gy));
-  TVR_TRY(fetch_scalars(p, S_COUNT));
+  TVR_TRY(halo_exchange_fetch(p, gy, S_COUNT));
   const double f0 = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
   const double gref = std::sqrt(p->hscal[S_TV + 3]);
   if (!std::isfinite(f0) || !std::isfinite(gref)) { set_error("UPN: non-finite f or g at x0"); return TVR_E_NONFINITE; }
@@ -547,8 +544,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   TVR_TRY(pass_AT(p, rk, wk));
   // y_1 = x_1: grad f(y_1) = grad f(x_1) -> gy, with the stop reduction at nu = L_0
   TVR_TRY(pass_tv_grad(p, xk, nullptr, 0.0, wk, nullptr, 0.0, gy, nullptr, nullptr, nullptr, 1.0 / L, S_TV));
-  TVR_TRY(halo_exchange(p, gy));
-  TVR_TRY(fetch_scalars(p, S_COUNT));
+  TVR_TRY(halo_exchange_fetch(p, gy, S_COUNT));
   ++n_g;
   double fxk = bt.f, fy = bt.f;
   double gn = L * std::sqrt(p->hscal[S_TV + 3]);
@@ -599,8 +595,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
     TVR_TRY(pass_momentum(p, rn, rn_lo, rk, rk_lo, beta, S_MOM));
     TVR_TRY(pass_tv_momentum_x(p, xn, xn_lo, xk, xk_lo, beta, wn, wk, gy, ybuf, y_lo, S_TV2));
     TVR_TRY(halo_fill_momentum_x(p, xn, xn_lo, xk, xk_lo, beta, ybuf, y_lo));
-    TVR_TRY(halo_exchange(p, gy));
-    TVR_TRY(fetch_scalars(p, S_COUNT));
+    TVR_TRY(halo_exchange_fetch(p, gy, S_COUNT));
     ++n_g;
     gn = L * std::sqrt(p->hscal[S_TV + 3]);
     ++k;
@@ -661,8 +656,7 @@ static int gp_impl(tvr_problem* p, float* x_io, const tvr_gp_opts& o, tvr_result
   TVR_TRY(pass_residual(p, xk, rk, S_RSQ));
   TVR_TRY(pass_AT(p, rk, w));
   TVR_TRY(pass_tv_grad(p, xk, nullptr, 0.0, w, nullptr, 0.0, g, nullptr, nullptr, nullptr, 1.0, S_TV));
-  TVR_TRY(halo_exchange(p, g));
-  TVR_TRY(fetch_scalars(p, S_COUNT));
+  TVR_TRY(halo_exchange_fetch(p, g, S_COUNT));
   double f = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
   const double gref = std::sqrt(p->hscal[S_TV + 3]);
   if (!std::isfinite(f) || !std::isfinite(gref)) { set_error("GP: non-finite f or g at x0"); return TVR_E_NONFINITE; }
@@ -689,8 +683,7 @@ static int gp_impl(tvr_problem* p, float* x_io, const tvr_gp_opts& o, tvr_result
     TVR_TRY(pass_AT(p, rk, w));
     TVR_TRY(pass_tv_grad(p, xk, nullptr, 0.0, w, nullptr, 0.0, g, nullptr, nullptr, nullptr,
                          1.0 / L, S_TV));
-    TVR_TRY(halo_exchange(p, g));
-    TVR_TRY(fetch_scalars(p, S_COUNT));
+    TVR_TRY(halo_exchange_fetch(p, g, S_COUNT));
     ++n_g;
     gn = L * std::sqrt(p->hscal[S_TV + 3]);
     tvr_record r{};

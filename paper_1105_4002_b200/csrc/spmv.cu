@@ -829,10 +829,60 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16z_kernel(SellArgs a) {
 //    running along x: consecutive entries are neighbouring voxels).
 // Offsets are in 4-entry chunks.  The gathers go through L1 (__ldg); warps take blocks from a
 // shared counter; per-block sums as spmv16s_kernel (deterministic).
-template <int UNR, int NT = 512>
+// L2 cache policies (L2H, spmv32s_kernel): bit 0 = the matrix stream is evict-first, bit 1 = the
+// gathered vector is evict-last.  With z-ordered blocks (make_sell32) the gathered sub-volume in
+// flight is a ~60-slice band (~16 MB at c5), but between two uses of an x line the grid streams
+// ~5 GB of matrix through L2, which evicts it under plain LRU (profiles/r02: 25.0 GB of DRAM
+// reads per c5 A pass against 21.4 GB algorithmic).
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int4 ld_stream_i4_pol(const int32_t* p, uint64_t pol) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float4 ld_stream_f4_pol(const float* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_gather_pol(const float* p, uint64_t pol) {
+  float r;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
+template <int UNR, int NT = 512, int L2H = 0>
 __global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
   __shared__ int s_next;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
+  uint64_t pol_s = 0, pol_g = 0;
+  if constexpr (L2H & 1) pol_s = l2_policy_evict_first();
+  if constexpr (L2H & 2) pol_g = l2_policy_evict_last();
+  auto ldi = [&](const int32_t* p) {
+    if constexpr (L2H & 1) return ld_stream_i4_pol(p, pol_s);
+    else return ld_stream_i4(p);
+  };
+  auto ldf = [&](const float* p) {
+    if constexpr (L2H & 1) return ld_stream_f4_pol(p, pol_s);
+    else return ld_stream_f4(p);
+  };
+  auto ldg = [&](const float* p) {
+    if constexpr (L2H & 2) return ld_gather_pol(p, pol_g);
+    else return __ldg(p);
+  };
   // The CTA's blocks as a sequence j = 0, 1, ..: contiguous (ilv = 0: [b0, b1)) or interleaved
   // (chunk q = blockIdx.x + (j / ilv) G of ilv blocks); blk(j) maps it to the stored block.
   int64_t b0, b1;
@@ -853,10 +903,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
   if (threadIdx.x == 0) s_next = nwarps;
   __syncthreads();
   auto gather4 = [&](const int4 c, const float4 v) {
-    const double p0 = (double)v.x * (double)__ldg(a.src + c.x);
-    const double p1 = (double)v.y * (double)__ldg(a.src + c.y);
-    const double p2 = (double)v.z * (double)__ldg(a.src + c.z);
-    const double p3 = (double)v.w * (double)__ldg(a.src + c.w);
+    const double p0 = (double)v.x * (double)ldg(a.src + c.x);
+    const double p1 = (double)v.y * (double)ldg(a.src + c.y);
+    const double p2 = (double)v.z * (double)ldg(a.src + c.z);
+    const double p3 = (double)v.w * (double)ldg(a.src + c.w);
     return (p0 + p1) + (p2 + p3);
   };
   auto emit = [&](int64_t row, double acc) -> double {
@@ -917,13 +967,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
         float4 v[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-          c[u] = ld_stream_i4(cp + (s + u) * 128);
-          v[u] = ld_stream_f4(vp + (s + u) * 128);
+          c[u] = ldi(cp + (s + u) * 128);
+          v[u] = ldf(vp + (s + u) * 128);
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) acc += gather4(c[u], v[u]);
       }
-      for (; s < K; ++s) acc += gather4(ld_stream_i4(cp + s * 128), ld_stream_f4(vp + s * 128));
+      for (; s < K; ++s) acc += gather4(ldi(cp + s * 128), ldf(vp + s * 128));
       if (row >= 0) q = emit(row, acc);
     } else {  // row mode: 8 lanes per row, 4 rows at a time
       const int grp = lane >> 3, gl = lane & 7;
@@ -936,14 +986,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
         double acc = 0.0;
         int c = gl;
         for (; c + 8 < ni; c += 16) {
-          const int4 c0 = ld_stream_i4(a.col32 + (si + c) * 4);
-          const float4 v0 = ld_stream_f4(a.val + (si + c) * 4);
-          const int4 c1 = ld_stream_i4(a.col32 + (si + c + 8) * 4);
-          const float4 v1 = ld_stream_f4(a.val + (si + c + 8) * 4);
+          const int4 c0 = ldi(a.col32 + (si + c) * 4);
+          const float4 v0 = ldf(a.val + (si + c) * 4);
+          const int4 c1 = ldi(a.col32 + (si + c + 8) * 4);
+          const float4 v1 = ldf(a.val + (si + c + 8) * 4);
           acc += gather4(c0, v0);
           acc += gather4(c1, v1);
         }
-        if (c < ni) acc += gather4(ld_stream_i4(a.col32 + (si + c) * 4), ld_stream_f4(a.val + (si + c) * 4));
+        if (c < ni) acc += gather4(ldi(a.col32 + (si + c) * 4), ldf(a.val + (si + c) * 4));
         acc = group_sum<8>(acc);
         if (gl == 0 && ri >= 0) q += emit(ri, acc);
       }
@@ -1040,18 +1090,29 @@ cudaError_t launch_sell32_mode(int64_t nblk, int64_t rows, const int64_t* rp, co
   return cudaGetLastError();
 }
 
-static const void* spmv32s_ptr(int unroll, int block) {
+template <int L2H>
+static const void* spmv32s_ptr_l2(int unroll, int block) {
   if (block == 1024)
-    return unroll >= 3 ? (const void*)spmv32s_kernel<3, 1024>
-                       : unroll == 2 ? (const void*)spmv32s_kernel<2, 1024> : (const void*)spmv32s_kernel<1, 1024>;
-  return unroll >= 3 ? (const void*)spmv32s_kernel<3>
-                     : unroll == 2 ? (const void*)spmv32s_kernel<2> : (const void*)spmv32s_kernel<1>;
+    return unroll >= 3 ? (const void*)spmv32s_kernel<3, 1024, L2H>
+                       : unroll == 2 ? (const void*)spmv32s_kernel<2, 1024, L2H>
+                                     : (const void*)spmv32s_kernel<1, 1024, L2H>;
+  return unroll >= 3 ? (const void*)spmv32s_kernel<3, 512, L2H>
+                     : unroll == 2 ? (const void*)spmv32s_kernel<2, 512, L2H>
+                                   : (const void*)spmv32s_kernel<1, 512, L2H>;
+}
+static const void* spmv32s_ptr(int unroll, int block, int l2 = 0) {
+  switch (l2) {
+    case 1: return spmv32s_ptr_l2<1>(unroll, block);
+    case 2: return spmv32s_ptr_l2<2>(unroll, block);
+    case 3: return spmv32s_ptr_l2<3>(unroll, block);
+    default: return spmv32s_ptr_l2<0>(unroll, block);
+  }
 }
 
 cudaError_t launch_spmv32s(const SellArgs& a, int unroll, int grid, cudaStream_t st, int block) {
   if (a.blk_hi <= a.blk_lo) return cudaSuccess;
   void* args[] = {const_cast<SellArgs*>(&a)};
-  return cudaLaunchKernel(spmv32s_ptr(unroll, block), dim3(grid), dim3(block == 1024 ? 1024 : 512),
+  return cudaLaunchKernel(spmv32s_ptr(unroll, block, a.l2hint), dim3(grid), dim3(block == 1024 ? 1024 : 512),
                           args, 0, st);
 }
 

@@ -160,7 +160,12 @@ def lib():
             raise ImportError(f"libtvreg.so not built ({LIB_PATH}); run __graft_entry__.build()")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
-            fn = getattr(L, name)
+            try:
+                fn = getattr(L, name)
+            except AttributeError:
+                if LIB_PATH.endswith("libtvreg.so"):
+                    raise
+                continue  # an older A/B build (TVR_LIB_PATH) without this entry point
             fn.restype = res
             fn.argtypes = args
         _lib = L

@@ -29,8 +29,8 @@ HOT = {
         (r"spmv16s_kernelILi2ELb1ELi1024ELb0ELb1E", 0),  # c3 A^T pass (wide CTA)
         (r"spmv16s_kernelILi2ELb1ELi1024ELb1ELb1E", 0),  # c3 A pass (partly staged window)
         (r"spmv16p_kernelILi8ELi3ELb1E", 0),   # padded per-row kernel (TVR_SPMV_SELL=0)
-        (r"spmv32s_kernelILi2ELi512EE", 0),    # int32 sliced ELL: c5 A pass
-        (r"spmv32s_kernelILi3ELi512EE", 8),    # int32 sliced ELL: c5 / f2 A^T pass (4 B, measured faster)
+        (r"spmv32s_kernelILi2ELi512ELi0EE", 0),  # int32 sliced ELL: c5 A pass
+        (r"spmv32s_kernelILi3ELi512ELi0EE", 8),  # int32 sliced ELL: c5 / f2 A^T pass
         (r"spmv16z_kernelILi2ELi1ELi1024EE", 0),  # slice-shared operator, 2 slices per pass
         (r"spmv16p_kernelILi4ELi3ELb1E", 0),   # c2 A^T pass
         (r"spmv16p_kernelILi8ELi2ELb0E", 0),   # c3 A pass (global gather)
