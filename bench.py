@@ -262,12 +262,19 @@ def run_ours(args, rank, world, local_rank):
     # idle gap ran at ramping clocks: r1's e2e at --steps 20 read 1159/s against 1819/s)
     xh = torch.from_numpy(x_h.copy()).pin_memory()
     gh = torch.empty(n_loc, dtype=torch.float32).pin_memory()
-    extra_warm = 0
+    # the count is fixed from rank 0's step time (every step is collective when world > 1, so
+    # every rank must run the same number)
     torch.cuda.synchronize()
     t_w = time.perf_counter()
-    while time.perf_counter() - t_w < 0.15:
+    P.objective_grad(x, g)
+    torch.cuda.synchronize()
+    n_w = torch.tensor([max(1, min(2000, int(0.15 / max(1e-6, time.perf_counter() - t_w))))],
+                       dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.broadcast(n_w, src=0)
+    extra_warm = 1 + int(n_w.item())
+    for _ in range(extra_warm - 1):
         P.objective_grad(x, g)
-        extra_warm += 1
     # Timed region 1 (the value): K uninstrumented steps.  Then the e2e region, then timed
     # region 3 (the roofline): the same K steps with CUDA events around every kernel on the
     # library's stream — the events cost ~28 us per step (measured, scripts/host_overhead.py), so

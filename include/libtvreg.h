@@ -280,9 +280,10 @@ int64_t tvr_launch_count(const tvr_problem* p, int reset);
  * solve is one CUDA graph with conditional while / if nodes; single-thread control kernels take
  * the same decisions in the same fp64 arithmetic (identical iterates), the host waits once; the
  * state rotates by device copies.  DEVICE applies to one-GPU problems (world == 1; others use
- * HOST).  AUTO (default): DEVICE below 2^28 matrix entries, where launch and synchronisation
- * latency is a visible part of an iteration (c1: -11 to -16 % per iteration; c2 UPN -7 %, GPBB
- * equal), HOST above (c3: the state copies cost 1-2 %).  The environment variable
+ * HOST).  AUTO (default): DEVICE where launch and synchronisation latency is a visible part of
+ * an iteration — GPBB below 2^28 matrix entries (c1 -16 % per iteration; c2 equal), UPN below 2^24
+ * (c1 -11 %; its extended-precision graph is slower than host control at c2) — HOST above (c3:
+ * the state copies cost 1-2 %).  The environment variable
  * TVR_CONTROL=host|device overrides. */
 enum { TVR_CONTROL_HOST = 0, TVR_CONTROL_DEVICE = 1, TVR_CONTROL_AUTO = 2 };
 int tvr_set_control(tvr_problem* p, int mode);

@@ -795,9 +795,12 @@ static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std:
   d.h_slice_end = zend;
   pl.sd.assign(1, d);
   pl.sv = SellVariant();
-  // steps in flight: 3 for A^T (c5 3.85 -> 3.69 ms), 2 for A (3: 5.21 -> 5.29 ms)
-  pl.sv.unroll = env_int("TVR_SELL32_UNROLL", transposed ? 3 : 2);
-  pl.sv.block = env_int("TVR_SELL32_BLOCK", 512);
+  // steps in flight: 3 for A^T (c5 3.85 -> 3.69 ms); for A 2 with row-ordered blocks (3: 5.21 ->
+  // 5.29 ms), 3 with the z order (4.72 -> 4.50 ms: the gathers now hit L2, latency-bound)
+  pl.sv.unroll = env_int("TVR_SELL32_UNROLL", transposed || zorder ? 3 : 2);
+  // 1024-thread CTAs (one per SM: 32 warps share the block counter) for a gathered volume larger
+  // than 32 MB (c5 A^T 3.80 -> 3.68 ms, A 4.72 -> 4.65 ms); 512 on small volumes (f2: slower)
+  pl.sv.block = env_int("TVR_SELL32_BLOCK", (double)p->ncol * 4.0 > 32.0 * (1 << 20) ? 1024 : 512);
   pl.pad_grid = (int)std::min<int64_t>((int64_t)p->num_sms * spmv32s_occupancy(pl.sv.unroll, pl.sv.block),
                                        std::max<int64_t>(1, nblk));
   pl.sell32 = true;

@@ -51,7 +51,7 @@ int copy_in(tvr_problem* p, float* dst, const float* src) {
 
 }  // namespace
 
-bool use_device_control(const tvr_problem* p);
+bool use_device_control(const tvr_problem* p, bool upn = false);
 static int gpbb_device(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_result* res,
                        Recorder& rec, double t0, double bytes0, float* x_cur, float* x_prev,
                        float* v, float* g_cur, float* g_prev, float* w, float* r_cur,
@@ -244,12 +244,15 @@ struct GraphGuard {
 
 }  // namespace
 
-bool use_device_control(const tvr_problem* p) {
+bool use_device_control(const tvr_problem* p, bool upn) {
   if (p->world > 1) return false;
   const char* e = std::getenv("TVR_CONTROL");
   if (e && *e) return std::string(e) == "device";
-  if (p->control == TVR_CONTROL_AUTO)  // by the stored matrix (the slice's, when slice-shared)
-    return (p->sliced ? p->nnz_s : p->nnz) < ((int64_t)1 << 28);  // c2 UPN 0.323 -> 0.301 s
+  // AUTO, by the stored matrix (the slice's, when slice-shared): GPBB below 2^28 entries (c1, c2:
+  // device and host equal at c2, 0.708 / 0.709 ms per iteration); UPN below 2^24 (c1 -11 %; at c2
+  // the extended-precision UPN graph runs 0.567 ms per iteration against 0.506 ms on the host)
+  if (p->control == TVR_CONTROL_AUTO)
+    return (p->sliced ? p->nnz_s : p->nnz) < ((int64_t)1 << (upn ? 24 : 28));
   return p->control == TVR_CONTROL_DEVICE;
 }
 
@@ -559,7 +562,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
     rec.add(r);
   }
   int status = TVR_OK;
-  if (!conv && k < o.max_iters && use_device_control(p)) {
+  if (!conv && k < o.max_iters && use_device_control(p, true)) {
     UpnState us{xk, xn, ybuf, gy, wk, wn, rk, rn, rk_lo, rn_lo, xk_lo, xn_lo, y_lo, L, mu, theta,
                 fxk, fy, gn, gref, k, n_f, n_g, n_ls, conv};
     TVR_TRY(upn_device(p, o, rec, us, &status));
