@@ -90,6 +90,8 @@ struct SellArgs {
   const int64_t* rp;        // spmv32s_kernel row-mode blocks: the CSR row pointer (lengths)
   const float* val;         // [step][lane][8] values (zero pads)
   const float* src;
+  const float* src_lo;      // non-null: A (src + src_lo), the lo part gathered from global
+                            // memory (extended-precision solver iterates)
   const float* b;           // non-null: out = A src - b, sum r^2
   float* out;
   float* out_lo;
@@ -124,6 +126,7 @@ struct SellVariant {
 cudaError_t launch_spmv16s(const SellArgs& a, const SellVariant& v, int grid, size_t smem,
                            cudaStream_t st);
 int spmv16s_occupancy(const SellVariant& v, size_t smem);
+bool spmv16s_lo_ok(const SellVariant& v);  // an extended-precision (src_lo) instantiation exists
 cudaError_t launch_sell_fill(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
                              const int64_t* rp, const int32_t* lo_off, const int32_t* hi_off,
                              uint16_t coff, const uint16_t* col16, const float* val,
@@ -191,11 +194,14 @@ cudaError_t launch_tv_trial(const TVArgs& a, const float* x, const float* g, dou
                             cudaStream_t st);
 // extended-precision iterates (hi + lo pairs; tv.cu SrcTrialX / SrcMomentumX): a.v_lo_out (and
 // a.xo_lo with a.xo) required
+// full: evaluate at the state hi + lo (with the A pass's lo gathers) instead of the hi part
 cudaError_t launch_tv_trial_x(const TVArgs& a, const float* x, const float* x_lo, const float* g,
-                              double s, cudaStream_t st);
+                              double s, cudaStream_t st, bool full);
 cudaError_t launch_tv_grad_momentum_x(const TVArgs& a, const float* x1, const float* x1_lo,
                                       const float* x0, const float* x0_lo, double beta,
-                                      cudaStream_t st);
+                                      cudaStream_t st, bool full);
+cudaError_t launch_tv_grad_plain_x(const TVArgs& a, const float* x, const float* x_lo,
+                                   cudaStream_t st);
 cudaError_t launch_halo_fill_trial_x(const float* x, const float* x_lo, const float* g, double s,
                                      double lo, double hi, int64_t plane, int nzl, int has_lo,
                                      int has_hi, float* v, float* v_lo, cudaStream_t st);

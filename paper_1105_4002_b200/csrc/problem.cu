@@ -154,7 +154,9 @@ static SpmvArgs spmv_args(tvr_problem* p, const SpmvPlan& pl, bool transposed, c
 // plain per-row kernel.
 static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed, const float* src,
                             const float* b, float* out, float* out_lo, double* scal,
-                            int z_lo = 0, int z_hi = -1) {
+                            int z_lo = 0, int z_hi = -1, const float* src_lo = nullptr) {
+  // src_lo (extended-precision solver iterates): the sliced-ELL kernels only (p->ext_eval)
+  if (src_lo && !(pl.sell32 || pl.sell)) return cudaErrorNotSupported;
   if (pl.sell32) {  // int32 sliced ELL (non-separable: no slice ranges)
     const SellData& d = pl.sd[0];
     SellArgs s{};
@@ -170,6 +172,7 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     s.rp = transposed ? p->rpT : p->rp;
     s.val = d.val;
     s.src = src;
+    s.src_lo = src_lo;
     s.b = b;
     s.out = out;
     s.out_lo = out_lo;
@@ -206,6 +209,7 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
       s.col16 = d.col16;
       s.val = d.val;
       s.src = src;
+      s.src_lo = src_lo;
       s.b = q == P - 1 ? b : nullptr;
       s.out = out;
       s.out_lo = q == P - 1 ? out_lo : nullptr;
@@ -283,9 +287,18 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
 static double entry_bytes(const SpmvPlan& pl) { return pl.v.idx16 ? 6.0 : 8.0; }
 
 // x: a slab volume vector.  VIEWS mode gathers the whole point first (gather_volume).
-int pass_residual(tvr_problem* p, const float* x, float* r, int slot, float* r_lo) {
+int pass_residual(tvr_problem* p, const float* x, float* r, int slot, float* r_lo,
+                  const float* x_lo) {
   const float* src = x;
   TVR_TRY(gather_volume(p, x, &src));
+  if (x_lo) {  // A (x + x_lo): extended-precision iterate evaluated whole (p->ext_eval)
+    const double nnz_hbm = p->sliced ? (double)p->nnz_s : (double)p->nnz;
+    const double bytes = entry_bytes(p->planA) * nnz_hbm + 8.0 * ((p->sliced ? p->m_s : p->m) + 1.0) +
+                         8.0 * p->ncol + 8.0 * p->m + (r_lo ? 4.0 * p->m : 0.0);
+    return launch(p, K_SPMV_A, bytes, [&] {
+      return run_spmv(p, p->planA, false, src, p->b, r, r_lo, p->dscal + slot, 0, -1, x_lo);
+    });
+  }
   // slice-shared operator: the one stored slice matrix is read from HBM once (L2 after that)
   const double nnz_hbm = p->sliced ? (double)p->nnz_s : (double)p->nnz;
   const double rows_hbm = p->sliced ? (double)p->m_s : (double)p->m;
@@ -382,6 +395,18 @@ int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, floa
   return launch(p, K_TV_TRIAL, bytes, [&] { return launch_tv_trial(a, x, g, s, p->stream); });
 }
 
+int pass_tv_grad_x(tvr_problem* p, const float* x, const float* x_lo, const float* w1, float* g,
+                   double stop_step, int slot, const double* dparam) {
+  TVArgs a = tv_args(p, slot);
+  a.dparam = dparam;
+  a.w1 = w1;
+  a.g_out = g;
+  a.stop_step = stop_step;
+  const double N = (double)n_local(p);
+  return launch(p, K_TV_GRAD, N * (12.0 + (g ? 4.0 : 0.0)),
+                [&] { return launch_tv_grad_plain_x(a, x, x_lo, p->stream); });
+}
+
 int pass_tv_trial_x(tvr_problem* p, const float* x, const float* x_lo, const float* g, double s,
                     float* v, float* v_lo, const float* xo, const float* xo_lo, int slot,
                     const double* dparam) {
@@ -396,7 +421,8 @@ int pass_tv_trial_x(tvr_problem* p, const float* x, const float* x_lo, const flo
   a.stop_step = 0.0;
   const double N = (double)n_local(p);
   const double bytes = N * (20.0 + (xo ? 8.0 : 0.0));
-  return launch(p, K_TV_TRIAL, bytes, [&] { return launch_tv_trial_x(a, x, x_lo, g, s, p->stream); });
+  return launch(p, K_TV_TRIAL, bytes,
+                [&] { return launch_tv_trial_x(a, x, x_lo, g, s, p->stream, p->ext_on); });
 }
 
 int pass_tv_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, const float* x0,
@@ -412,7 +438,7 @@ int pass_tv_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, cons
   a.v_lo_out = y_lo;
   const double N = (double)n_local(p);
   return launch(p, K_TV_GRAD, N * 36.0, [&] {
-    return launch_tv_grad_momentum_x(a, x1, x1_lo, x0, x0_lo, beta, p->stream);
+    return launch_tv_grad_momentum_x(a, x1, x1_lo, x0, x0_lo, beta, p->stream, p->ext_on);
   });
 }
 
@@ -1300,6 +1326,12 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   // the int32 columns are no longer read by any pass: release them (c3: 7.7 GB each)
   if (p->planA.v.idx16) { dev_free(p, p->col); p->col = nullptr; }
   if (p->planT.v.idx16) { dev_free(p, p->colT); p->colT = nullptr; }
+
+  // extended-precision evaluation of the UPN / GP iterates (A (x + x_lo)): the
+  // sliced-ELL A-pass kernels have the lo gathers; one rank or z-slabs (VIEWS would all-gather
+  // the lo parts too); TVR_EXT_EVAL=0 evaluates at the hi parts
+  p->ext_eval = !views_dist(p) && !sliced && env_int("TVR_EXT_EVAL", 1) != 0 &&
+                (p->planA.sell32 || (p->planA.sell && spmv16s_lo_ok(p->planA.sv)));
 
   // ---- work vectors ----
   const int NVOL = 13, NDAT = 4;  // 10-12: lo parts of the extended-precision solver iterates

@@ -175,7 +175,9 @@ struct tvr_problem {
   // floats), per-owner store targets (device array) and the owners' row bounds
   bool fused_rs = false;
   float* inbox = nullptr;
-  bool inbox_raw = false;            // NCCL backend: inbox from cudaMalloc (IPC-mappable), freed by dist_release
+  bool inbox_raw = false;  // NCCL backend: inbox from cudaMalloc (IPC-mappable), freed by dist_release
+  bool ext_eval = false;   // UPN / GP iterates can be evaluated at hi + lo (A pass lo gathers)
+  bool ext_on = false;     // ... and are, from this point of the current solve on
   int64_t inbox_stride = 0;
   float** out_peer_dev = nullptr;
   int64_t* out_bounds_dev = nullptr;
@@ -220,7 +222,7 @@ int64_t n_local(const tvr_problem* p);
 
 // pass functions (enqueue only; scalars land in p->dscal[slot..])
 int pass_residual(tvr_problem* p, const float* x, float* r, int slot,          // a1
-                  float* r_lo = nullptr);
+                  float* r_lo = nullptr, const float* x_lo = nullptr);  // x_lo: A (x + x_lo)
 int pass_AT(tvr_problem* p, const float* r, float* w);                          // a2
 int pass_tv_grad(tvr_problem* p, const float* x, const float* x0, double beta,  // a4
                  const float* w1, const float* w0, double wbeta, float* g, float* v_out,
@@ -238,6 +240,9 @@ int pass_tv_trial(tvr_problem* p, const float* x, const float* g, double s, floa
 int pass_tv_trial_x(tvr_problem* p, const float* x, const float* x_lo, const float* g, double s,
                     float* v, float* v_lo, const float* xo, const float* xo_lo, int slot,
                     const double* dparam = nullptr);
+// gradient w1 + alpha grad TV and the stop reduction at the extended-precision iterate x + x_lo
+int pass_tv_grad_x(tvr_problem* p, const float* x, const float* x_lo, const float* w1, float* g,
+                   double stop_step, int slot, const double* dparam = nullptr);
 // UPN point from (x1, x1_lo), (x0, x0_lo): gradient (w blend) at x1 + beta (x1 - x0) of the hi
 // parts, state y = (y, y_lo) from the full pairs
 int pass_tv_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, const float* x0,

@@ -338,6 +338,20 @@ __device__ __forceinline__ double chunk8_sum(const int4 c, const float4 v0, cons
   return ((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
 }
 
+// The lo parts of an extended-precision source (global gathers through L1): sum of v * x_lo.
+__device__ __forceinline__ double chunk8_sum_lo(const int4 c, const float4 v0, const float4 v1,
+                                                const float* __restrict__ lbase) {
+  const uint32_t cw[4] = {(uint32_t)c.x, (uint32_t)c.y, (uint32_t)c.z, (uint32_t)c.w};
+  const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+  double pr[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int cidx = (int)((cw[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+    pr[q] = (double)vv[q] * (double)__ldg(lbase + cidx);
+  }
+  return ((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
+}
+
 // Partly staged window (HALF): offsets below h come from shared memory, the rest from global
 // memory (L1) — for windows larger than shared memory (c3's 256 KB x-slice), so that part of the
 // gathers leaves the L1 tag / data pipe that global gathers saturate.
@@ -571,7 +585,7 @@ __device__ __forceinline__ void sell_cta_range(const SellArgs& a, int64_t& b0, i
   b1 = s_rng[1];
 }
 
-template <int UNR, bool STAGED, int NT = 512, bool HALF = false, bool DYN = true>
+template <int UNR, bool STAGED, int NT = 512, bool HALF = false, bool DYN = true, bool LO = false>
 __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
   extern __shared__ float stage[];
   __shared__ int s_next;
@@ -584,6 +598,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
     const int z = a.blk_slice[it - zb];
     const int64_t it_end = min(b1, zb + a.zend[z]);
     const float* gbase = a.src + a.win_lo[z] + rz * a.rep_win;
+    const float* lbase = LO ? a.src_lo + a.win_lo[z] + rz * a.rep_win : nullptr;
     const int64_t row_off = rz * a.rep_rows;
     if (STAGED || DYN) __syncthreads();  // previous segment done: window and counter reusable
     if (DYN && threadIdx.x == 0) s_next = nwarps;
@@ -630,9 +645,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
           vb[u] = ld_stream_f4(vp + (s + u) * 256 + 4);
         }
 #pragma unroll
-        for (int u = 0; u < UNR; ++u)
+        for (int u = 0; u < UNR; ++u) {
           acc += HALF ? chunk8_sum_part(c[u], va[u], vb[u], stage, gbase, a.part_len)
                       : chunk8_sum<STAGED>(c[u], va[u], vb[u], stage, gbase);
+          if constexpr (LO) acc += chunk8_sum_lo(c[u], va[u], vb[u], lbase);
+        }
       }
       for (; s < K; ++s) {
         const int4 c0 = ld_stream_i4(reinterpret_cast<const int32_t*>(cp + s * 256));
@@ -640,6 +657,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
         const float4 vb0 = ld_stream_f4(vp + s * 256 + 4);
         acc += HALF ? chunk8_sum_part(c0, va0, vb0, stage, gbase, a.part_len)
                     : chunk8_sum<STAGED>(c0, va0, vb0, stage, gbase);
+        if constexpr (LO) acc += chunk8_sum_lo(c0, va0, vb0, lbase);
       }
       double q = 0.0;
       if (row >= 0 && a.acc_out) {
@@ -864,7 +882,7 @@ __device__ __forceinline__ float ld_gather_pol(const float* p, uint64_t pol) {
   return r;
 }
 
-template <int UNR, int NT = 512, int L2H = 0>
+template <int UNR, int NT = 512, int L2H = 0, bool LO = false>
 __global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
   __shared__ int s_next;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
@@ -907,7 +925,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv32s_kernel(SellArgs a) {
     const double p1 = (double)v.y * (double)ldg(a.src + c.y);
     const double p2 = (double)v.z * (double)ldg(a.src + c.z);
     const double p3 = (double)v.w * (double)ldg(a.src + c.w);
-    return (p0 + p1) + (p2 + p3);
+    double t = (p0 + p1) + (p2 + p3);
+    if constexpr (LO) {  // extended-precision source: + the lo parts
+      const double q0 = (double)v.x * (double)__ldg(a.src_lo + c.x);
+      const double q1 = (double)v.y * (double)__ldg(a.src_lo + c.y);
+      const double q2 = (double)v.z * (double)__ldg(a.src_lo + c.z);
+      const double q3 = (double)v.w * (double)__ldg(a.src_lo + c.w);
+      t += (q0 + q1) + (q2 + q3);
+    }
+    return t;
   };
   auto emit = [&](int64_t row, double acc) -> double {
     if (a.b) {
@@ -1100,7 +1126,12 @@ static const void* spmv32s_ptr_l2(int unroll, int block) {
                      : unroll == 2 ? (const void*)spmv32s_kernel<2, 512, L2H>
                                    : (const void*)spmv32s_kernel<1, 512, L2H>;
 }
-static const void* spmv32s_ptr(int unroll, int block, int l2 = 0) {
+static const void* spmv32s_ptr(int unroll, int block, int l2 = 0, bool lo = false) {
+  if (lo)  // extended-precision source (no L2 policies)
+    return block == 1024 ? (unroll >= 3 ? (const void*)spmv32s_kernel<3, 1024, 0, true>
+                                        : (const void*)spmv32s_kernel<2, 1024, 0, true>)
+                         : (unroll >= 3 ? (const void*)spmv32s_kernel<3, 512, 0, true>
+                                        : (const void*)spmv32s_kernel<2, 512, 0, true>);
   switch (l2) {
     case 1: return spmv32s_ptr_l2<1>(unroll, block);
     case 2: return spmv32s_ptr_l2<2>(unroll, block);
@@ -1112,7 +1143,8 @@ static const void* spmv32s_ptr(int unroll, int block, int l2 = 0) {
 cudaError_t launch_spmv32s(const SellArgs& a, int unroll, int grid, cudaStream_t st, int block) {
   if (a.blk_hi <= a.blk_lo) return cudaSuccess;
   void* args[] = {const_cast<SellArgs*>(&a)};
-  return cudaLaunchKernel(spmv32s_ptr(unroll, block, a.l2hint), dim3(grid), dim3(block == 1024 ? 1024 : 512),
+  return cudaLaunchKernel(spmv32s_ptr(unroll, block, a.l2hint, a.src_lo != nullptr), dim3(grid),
+                          dim3(block == 1024 ? 1024 : 512),
                           args, 0, st);
 }
 
@@ -1177,9 +1209,32 @@ static cudaError_t dispatch16s(const SellVariant& v, F&& f) {
   return v.block == 1024 ? f(spmv16s_kernel<2, false, 1024>) : f(spmv16s_kernel<2, false, 512>);
 }
 
+// extended-precision source (a.src_lo): the default sliced-ELL configurations only (DYN, two
+// steps in flight, one slice per pass); spmv16s_lo_ok() tells the planner
+template <class F>
+static cudaError_t dispatch16s_lo(const SellVariant& v, F&& f) {
+  if (v.staged) return v.block == 1024 ? f(spmv16s_kernel<2, true, 1024, false, true, true>)
+                                       : f(spmv16s_kernel<2, true, 512, false, true, true>);
+  return v.block == 1024 ? f(spmv16s_kernel<2, false, 1024, false, true, true>)
+                         : f(spmv16s_kernel<2, false, 512, false, true, true>);
+}
+// (not the partly staged window: its lo instantiation spilled 312 bytes)
+bool spmv16s_lo_ok(const SellVariant& v) {
+  return v.zgroup == 1 && v.dyn && v.unroll == 2 && !v.half;
+}
+
 cudaError_t launch_spmv16s(const SellArgs& a, const SellVariant& v, int grid, size_t smem,
                            cudaStream_t st) {
   if (a.blk_hi <= a.blk_lo) return cudaSuccess;
+  if (a.src_lo) {
+    if (!spmv16s_lo_ok(v)) return cudaErrorNotSupported;
+    return dispatch16s_lo(v, [&](auto k) -> cudaError_t {
+      cudaError_t e = ensure_smem_attr((const void*)k, smem);
+      if (e != cudaSuccess) return e;
+      k<<<grid, v.block, smem, st>>>(a);
+      return cudaGetLastError();
+    });
+  }
   return dispatch16s(v, [&](auto k) -> cudaError_t {
     cudaError_t e = ensure_smem_attr((const void*)k, smem);
     if (e != cudaSuccess) return e;

@@ -142,9 +142,12 @@ def test_gp_parity_c1(tvreg, c1):
 
 @pytest.mark.parametrize("solver", ["gpbb", "upn"])
 @pytest.mark.parametrize("case", ["c1", "box"])
-def test_device_control_matches_host_control(tvreg, c1, case, solver):
+def test_device_control_matches_host_control(tvreg, c1, case, solver, monkeypatch):
     """f3: a solve as one CUDA graph with conditional nodes and device control kernels takes the
-    host controller's decisions in the same fp64 arithmetic: identical iterates, counts, history."""
+    host controller's decisions in the same fp64 arithmetic: identical iterates, counts, history.
+    (UPN's graph evaluates its hi + lo iterates whole from the start; the host controller switches
+    to that at a gradient-map ratio of TVR_EXT_EVAL_AT, set to 1 here: from the start too.)"""
+    monkeypatch.setenv("TVR_EXT_EVAL_AT", "1")
     kw = {} if case == "c1" else dict(alpha=0.03, tau=1e-2, hi=1.0)
     outs = {}
     for mode in ("host", "device"):
@@ -164,9 +167,10 @@ def test_device_control_matches_host_control(tvreg, c1, case, solver):
 
 
 @pytest.mark.parametrize("solver", ["gpbb", "upn"])
-def test_device_control_max_iters_and_restart(tvreg, c1, solver):
+def test_device_control_max_iters_and_restart(tvreg, c1, solver, monkeypatch):
     """max_iters stops the device loop like the host loop, and a second solve on the same problem
     starts from fresh controller state."""
+    monkeypatch.setenv("TVR_EXT_EVAL_AT", "1")
     P = _gpu_problem(tvreg, c1)
     res = []
     for mode in ("host", "device", "device"):
