@@ -261,3 +261,88 @@ def test_weak_slab_tiles_a_tall_volume():
             assert np.array_equal(sl.col, w.A.col + rank * nz * plane)
             assert sl.b.shape == (w.A.n_rows,)
     assert np.array_equal(harness.weak_slab("c1", 1, 0).b, w.b)  # world 1: the c1 workload itself
+
+
+# --------------------------------------------- bench.py's per-rank strong-scaling generators
+_TINY_SEP = dict(grid=(12, 10, 9), views=7, bins=17, n_ell=3)
+_TINY_TILT = dict(grid=(10, 9, 8), views=6, det=(5, 13), tilt=10.0, n_ell=3)
+
+
+def _strong_worker(rank, world, port, q):
+    """As bench.py's large_config_line at N > 1: each rank builds only its own rows
+    (harness.strong_slab / harness.views_block, the noise sigma of the views from an all-reduced
+    sum of y^2), then the P1 / P2 exchanges of csrc/dist.cu, here with the oracle's arithmetic."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        harness.PRESETS["tiny_sep"] = _TINY_SEP
+        harness.PRESETS["tiny_tilt"] = _TINY_TILT
+        alpha, tau = 0.01, 1e-2
+        out = {}
+        # P1: z-slab rows of the separable preset
+        sl = harness.strong_slab("tiny_sep", world, rank)
+        nx, ny, nz = sl.grid
+        plane = nx * ny
+        x = harness.random_x(nx * ny * nz).astype(np.float64)
+        xl = x[sl.z0 * plane:sl.z1 * plane]
+        col_loc = (sl.col - sl.z0 * plane).astype(np.int32)
+        r = oracle.matvec(sl.row_ptr, col_loc, sl.val, xl) - sl.b.astype(np.float64)
+        wl = oracle.rmatvec(sl.row_ptr, col_loc, sl.val, r, (sl.z1 - sl.z0) * plane)
+        tv_own, g_tv = _tv_slab(xl, (nx, ny), sl.z0, sl.z1, tau, rank, world)
+        s = _rank_ordered_sum([float(r @ r), tv_own], world)
+        out["sep"] = (sl.z0, 0.5 * s[0] + alpha * s[1], wl + alpha * g_tv)
+        # P2: view blocks of the tilted preset
+        vb = harness.views_block("tiny_tilt", world, rank)
+        s2 = torch.tensor([float(vb.y @ vb.y)], dtype=torch.float64)
+        dist.all_reduce(s2)
+        b = vb.data(float(s2.item()))
+        nx, ny, nz = vb.grid
+        plane, N = nx * ny, nx * ny * nz
+        bounds = [slab_bounds(nz, world, q_) for q_ in range(world)]
+        assert bounds[rank] == (vb.z0, vb.z1)
+        x = harness.random_x(N).astype(np.float64)
+        r = oracle.matvec(vb.A.row_ptr, vb.A.col, vb.A.val, x) - b.astype(np.float64)
+        w_part = torch.from_numpy(oracle.rmatvec(vb.A.row_ptr, vb.A.col, vb.A.val, r, N))
+        w_slab = None
+        for q_, (z0, z1) in enumerate(bounds):
+            piece = w_part[z0 * plane:z1 * plane].clone()
+            dist.reduce(piece, dst=q_)
+            if q_ == rank:
+                w_slab = piece.numpy()
+        tv_own, g_tv = _tv_slab(x[vb.z0 * plane:vb.z1 * plane], (nx, ny), vb.z0, vb.z1, tau,
+                                rank, world)
+        s = _rank_ordered_sum([float(r @ r), tv_own], world)
+        out["tilt"] = (vb.z0, 0.5 * s[0] + alpha * s[1], w_slab + alpha * g_tv)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_strong_scaling_generators_match_unsharded(world, monkeypatch):
+    """The per-rank rows bench.py builds for its N > 1 strong-scaling lines (c3 by z-slabs, c5 by
+    views) assemble, through the sharded exchanges, the oracle gradient of the single-process
+    workload (same rows, same b, same sigma)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_strong_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    monkeypatch.setitem(harness.PRESETS, "tiny_sep", _TINY_SEP)
+    monkeypatch.setitem(harness.PRESETS, "tiny_tilt", _TINY_TILT)
+    for key, name in (("sep", "tiny_sep"), ("tilt", "tiny_tilt")):
+        w = harness.preset(name)
+        Po = oracle.Problem(w.A.row_ptr, w.A.col, w.A.val, w.b, w.grid, 0.01, 1e-2)
+        f, g = Po.fg(harness.random_x(w.N))
+        parts = sorted([r[1][key] for r in res], key=lambda t: t[0])
+        fs = [p_[1] for p_ in parts]
+        assert all(fi == fs[0] for fi in fs)
+        assert abs(fs[0] - f) <= 1e-12 * abs(f), key
+        gs = np.concatenate([p_[2] for p_ in parts])
+        assert np.allclose(gs, g, rtol=1e-12, atol=1e-12 * np.abs(g).max()), key
