@@ -32,6 +32,12 @@ METRIC = "gradient evals/s & HBM GB/s (Ax, A^T r, grad TV_tau); GPBB/UPN time-to
 UNIT = "gradient evals/s"
 
 
+def _dist(world: int) -> bool:
+    """The multi-rank code path: world > 1 under torchrun, or TVR_BENCH_DIST=1 at world 1 (a 1-rank
+    NCCL communicator: exercises the N > 1 path, its generators and collectives, on one GPU)."""
+    return world > 1 or os.environ.get("TVR_BENCH_DIST") == "1"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -227,7 +233,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     stream = torch.cuda.current_stream()
     comm = None
-    if world > 1:
+    if _dist(world):
         # Weak scaling over z-slabs: every rank holds one full c2-sized slab of
         # a volume nz*world slices tall; the TV halo exchange and the rank-ordered scalar sum are
         # the real data-path collectives.  value = c2-sized gradient evaluations per second,
@@ -250,7 +256,7 @@ def run_ours(args, rank, world, local_rank):
     g = torch.empty(n_loc, device="cuda")
 
     def barrier():
-        if world > 1:
+        if _dist(world):
             dist.barrier()
 
     for _ in range(max(3, args.warmup)):
@@ -270,7 +276,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     n_w = torch.tensor([max(1, min(2000, int(0.15 / max(1e-6, time.perf_counter() - t_w))))],
                        dtype=torch.int64, device="cuda")
-    if world > 1:
+    if _dist(world):
         dist.broadcast(n_w, src=0)
     extra_warm = 1 + int(n_w.item())
     for _ in range(extra_warm - 1):
@@ -309,7 +315,7 @@ def run_ours(args, rank, world, local_rank):
     wall = time.perf_counter() - w0
     barrier()
     te = torch.tensor([max(h0.elapsed_time(h1), wall * 1e3)], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if _dist(world):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = dict(value=world * args.steps / (float(te.item()) / 1e3), unit=UNIT,
                h2d_bytes_per_step=int(4 * n_loc * world), d2h_bytes_per_step=int((4 * n_loc + 8) * world),
@@ -331,7 +337,7 @@ def run_ours(args, rank, world, local_rank):
     P.profile(False)
     clk = clocks.stop()
     t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if _dist(world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
@@ -377,13 +383,13 @@ def run_ours(args, rank, world, local_rank):
                kernels=ktab, step_hbm_gbs=step_bytes / (ms_step / 1e3) / 1e9,
                step_frac=step_bytes / (ms_step / 1e3) / 1e9 / peak)
 
-    if rank == 0 and world == 1 and not args.no_solve:
+    if rank == 0 and not _dist(world) and not args.no_solve:
         out["solvers"] = solver_timings(tvreg, torch)
         out["c3_gradient"] = large_config_line(tvreg, torch, solve=("gpbb", "upn"),
                                                oracle_time=not args.no_cpu_baseline)
         out["c5_gradient"] = large_config_line(tvreg, torch, cfg="c5")
         out["sliced"] = sliced_lines(tvreg, torch)
-    if world > 1 and not args.no_solve:
+    if _dist(world) and not args.no_solve:
         # strong scaling of the 256^3 workloads (every rank takes part; rank 0 reports)
         P.close()
         P = None
@@ -392,7 +398,7 @@ def run_ours(args, rank, world, local_rank):
                                                solve=("gpbb",))
         torch.cuda.empty_cache()
         out["c5_gradient"] = large_config_line(tvreg, torch, "c5", 10, world, rank, local_rank)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not _dist(world) and not args.no_cpu_baseline:
         its = {k: v for k, v in out.get("solvers", {}).items() if "iters" in v}
         for s in ("gpbb", "upn"):
             if s in out.get("c3_gradient", {}):
@@ -448,7 +454,7 @@ def large_config_line(tvreg, torch, cfg="c3", steps=10, world=1, rank=0, local_r
     import harness
     stream = torch.cuda.current_stream()
     comm = None
-    if world > 1:
+    if _dist(world):
         import torch.distributed as dist
         from paper_1105_4002_b200.dist import nccl_comm_from_process_group
         comm = nccl_comm_from_process_group(world, rank, local_rank)
@@ -489,11 +495,11 @@ def large_config_line(tvreg, torch, cfg="c3", steps=10, world=1, rank=0, local_r
         del w
 
     def barrier():
-        if world > 1:
+        if _dist(world):
             torch.distributed.barrier()
 
     def maxrank(v):
-        if world == 1:
+        if not _dist(world):
             return v
         t = torch.tensor([v], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -537,7 +543,7 @@ def large_config_line(tvreg, torch, cfg="c3", steps=10, world=1, rank=0, local_r
     if comm:
         barrier()
         tvreg.nccl_comm_destroy(comm)
-    if world == 1 and oracle_time:
+    if not _dist(world) and oracle_time:
         # one oracle gradient evaluation of the same 256^3 workload on all host cores (A x
         # row-parallel, A^T r by the scatter over A's rows: no second 15 GB transpose)
         import oracle
@@ -633,7 +639,7 @@ def main():
         if rank == 0:
             print(json.dumps(run_reference(args)), flush=True)
         return 0
-    if world > 1:
+    if _dist(world):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
@@ -641,7 +647,7 @@ def main():
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if _dist(world):
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0

@@ -457,17 +457,33 @@ static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnS
 
 // Extended-precision evaluation: the UPN / GP iterates are hi + lo pairs from the
 // start; the objective is evaluated at the fp32 hi part (plain A pass) until the gradient-map
-// ratio reaches TVR_EXT_EVAL_AT (default 3e-5, an order of magnitude above the hi-evaluation
-// floor seen at 256^3), then at hi + lo (the A pass also gathers the lo parts: +70 % on the c2 A
-// pass, so only the last stretch pays it).  The device-control graph (small problems) evaluates at
-// hi + lo throughout.
+// ratio reaches TVR_EXT_EVAL_AT (default 1e-4: down to there the hi evaluation follows the hi + lo
+// one iteration for iteration at 256^3) and progress slows (ExtEvalRule), then at hi + lo (the A
+// pass also gathers the lo parts: +70 % on the c2 A pass, so only the last stretch pays it).  The
+// device-control graph (small problems) evaluates at hi + lo throughout.
 static double ext_eval_at() {
   const char* e = std::getenv("TVR_EXT_EVAL_AT");
-  return (e && *e) ? std::atof(e) : 3e-5;
+  return (e && *e) ? std::atof(e) : 1e-4;
 }
-static void ext_eval_update(tvr_problem* p, double gn, double gref) {
-  if (p->ext_eval && !p->ext_on && gn <= ext_eval_at() * gref) p->ext_on = true;
-}
+// Switch rule: below the ratio TVR_EXT_EVAL_AT, once the gradient map has shrunk by less than
+// a factor 2 over the last 100 iterations (slow progress: where the hi evaluation stalls; a solve
+// still converging briskly, e.g. c3 without the box, keeps the cheaper pass to the end).
+// Returns true when the evaluation switches to hi + lo now: the caller then re-evaluates the
+// quantities it carries (objective, residuals, gradients) at hi + lo, so that no hi-evaluated
+// value meets a hi + lo one in a BT test or the mu_k quotient (mixing them broke BT at 256^3).
+struct ExtEvalRule {
+  std::deque<double> hist;  // gn of the last 100 iterations
+  bool update(tvr_problem* p, double gn, double gref) {
+    if (!p->ext_eval || p->ext_on) return false;
+    hist.push_back(gn);
+    if (hist.size() > 101) hist.pop_front();
+    if (gn <= ext_eval_at() * gref && hist.size() == 101 && gn > 0.5 * hist.front()) {
+      p->ext_on = true;
+      return true;
+    }
+    return false;
+  }
+};
 
 // -------------------------------------------------------------------- UPN
 namespace {
@@ -571,7 +587,19 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   ++n_g;
   double fxk = bt.f, fy = bt.f;
   double gn = L * std::sqrt(p->hscal[S_TV + 3]);
-  ext_eval_update(p, gn, gref);
+  double fx1 = bt.f;
+  ExtEvalRule ext_rule;
+  if (ext_rule.update(p, gn, gref)) {  // re-evaluate x_1 (= y_1) at hi + lo
+    TVR_TRY(pass_residual(p, xk, rk, S_RSQ, rk_lo, xk_lo));
+    TVR_TRY(pass_AT(p, rk, wk));
+    TVR_TRY(pass_tv_grad_x(p, xk, xk_lo, wk, gy, 1.0 / L, S_TV));
+    TVR_TRY(halo_exchange_fetch(p, gy, S_COUNT));
+    fx1 = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
+    gn = L * std::sqrt(p->hscal[S_TV + 3]);
+    ++n_f;
+    ++n_g;
+  }
+  fxk = fy = fx1;
   const float* y = xk;
   const float* ylo = xk_lo;
   int64_t k = 1;
@@ -624,7 +652,7 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
     TVR_TRY(halo_exchange_fetch(p, gy, S_COUNT));
     ++n_g;
     gn = L * std::sqrt(p->hscal[S_TV + 3]);
-    ext_eval_update(p, gn, gref);
+    const bool switched = ext_rule.update(p, gn, gref);
     ++k;
     std::swap(xk, xn);
     std::swap(xk_lo, xn_lo);
@@ -637,6 +665,23 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
     fy = 0.5 * p->hscal[S_MOM] + p->alpha * p->hscal[S_TV2];
     theta = theta_n;
     conv = stop_test(gn, gref, Nglob, o.eps, o.stop_mode);
+    if (switched && !conv && k < o.max_iters) {
+      // re-evaluate x_{k+1} (now xk), x_k (now xn) and y_{k+1} at hi + lo (same beta)
+      TVR_TRY(pass_residual(p, xk, rk, S_RSQ, rk_lo, xk_lo));
+      TVR_TRY(pass_AT(p, rk, wk));
+      TVR_TRY(pass_tv_grad_x(p, xk, xk_lo, wk, nullptr, 1.0 / L, S_TV));
+      TVR_TRY(fetch_scalars(p, S_COUNT));
+      fxk = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
+      TVR_TRY(pass_residual(p, xn, rn, S_RSQ, rn_lo, xn_lo));
+      TVR_TRY(pass_AT(p, rn, wn));
+      TVR_TRY(pass_momentum(p, rk, rk_lo, rn, rn_lo, beta, S_MOM));
+      TVR_TRY(pass_tv_momentum_x(p, xk, xk_lo, xn, xn_lo, beta, wk, wn, gy, ybuf, y_lo, S_TV2));
+      TVR_TRY(halo_fill_momentum_x(p, xk, xk_lo, xn, xn_lo, beta, ybuf, y_lo));
+      TVR_TRY(halo_exchange_fetch(p, gy, S_COUNT));
+      fy = 0.5 * p->hscal[S_MOM] + p->alpha * p->hscal[S_TV2];
+      n_f += 2;
+      n_g += 2;
+    }
     tvr_record r{};
     r.iter = k; r.f = fxk; r.gmap_rel = gref > 0 ? gn / gref : 0.0; r.gmap_abs_per_n = gn / Nglob;
     r.step_or_inv_L = 1.0 / L; r.mu = mu; r.L = L; r.ls_trials = bt.trials;
@@ -694,6 +739,7 @@ static int gp_impl(tvr_problem* p, float* x_io, const tvr_gp_opts& o, tvr_result
   bo.rho_L = o.rho_L;
   bo.bt_max = o.bt_max;
   double L = o.L0, gn = gref;
+  ExtEvalRule ext_rule;
   bool conv = false;
   int status = TVR_OK;
   for (;;) {
@@ -715,7 +761,16 @@ static int gp_impl(tvr_problem* p, float* x_io, const tvr_gp_opts& o, tvr_result
     TVR_TRY(halo_exchange_fetch(p, g, S_COUNT));
     ++n_g;
     gn = L * std::sqrt(p->hscal[S_TV + 3]);
-    ext_eval_update(p, gn, gref);
+    if (ext_rule.update(p, gn, gref)) {  // re-evaluate f and g at x_k at hi + lo
+      TVR_TRY(pass_residual(p, xk, rk, S_RSQ, nullptr, xk_lo));
+      TVR_TRY(pass_AT(p, rk, w));
+      TVR_TRY(pass_tv_grad_x(p, xk, xk_lo, w, g, 1.0 / L, S_TV));
+      TVR_TRY(halo_exchange_fetch(p, g, S_COUNT));
+      f = 0.5 * p->hscal[S_RSQ] + p->alpha * p->hscal[S_TV];
+      gn = L * std::sqrt(p->hscal[S_TV + 3]);
+      ++n_f;
+      ++n_g;
+    }
     tvr_record r{};
     r.iter = k; r.f = f; r.gmap_rel = gref > 0 ? gn / gref : 0.0; r.gmap_abs_per_n = gn / Nglob;
     r.step_or_inv_L = 1.0 / L; r.L = L; r.ls_trials = bt.trials;

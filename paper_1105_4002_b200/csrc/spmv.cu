@@ -571,14 +571,49 @@ __device__ __forceinline__ int64_t sell_lower(const SellArgs& a, int64_t lo, int
   return min(max(k, lo), hi);
 }
 
-// The CTA's virtual block range [b0, b1): searched once by thread 0, broadcast in shared memory.
+// First index in [lo, hi) with a[i] >= key (hi if none), a ascending, by a whole warp: 32 probes
+// per round (log32 of the range dependent loads instead of log2: the CTA-range search of a c2
+// pass is 2 x 16 dependent L2 loads with one thread, ~10 us before the CTA streams anything).
+__device__ __forceinline__ int64_t warp_lower_bound_i64(const int64_t* __restrict__ a, int64_t lo,
+                                                        int64_t hi, int64_t key) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = lo + lane * step;
+    const bool ge = p >= hi || __ldg(a + p) >= key;
+    const unsigned m = __ballot_sync(0xffffffffu, ge);
+    if (m == 0) {  // every probe below the key: the answer lies past the last one
+      lo = lo + 31 * step + 1;
+      continue;
+    }
+    const int f = __ffs(m) - 1;  // first probe at or past the answer
+    if (f == 0) return lo;
+    const int64_t pf = lo + f * step;
+    lo = lo + (f - 1) * step + 1;
+    hi = min(pf, hi);
+  }
+  return (hi - lo == 1 && __ldg(a + lo) >= key) ? lo : hi;
+}
+__device__ __forceinline__ int64_t sell_lower_warp(const SellArgs& a, int64_t lo, int64_t hi, int64_t t) {
+  const int64_t ws = a.cum[a.nb];
+  const int64_t z = ws > 0 ? t / ws : 0;
+  const int64_t k = z >= a.rep ? (int64_t)a.rep * a.nb
+                               : z * a.nb + warp_lower_bound_i64(a.cum, 0, a.nb, t - z * ws);
+  return min(max(k, lo), hi);
+}
+
+// The CTA's virtual block range [b0, b1): warps 0 and 1 search its two ends concurrently,
+// broadcast in shared memory (the same result as sell_lower).
 __device__ __forceinline__ void sell_cta_range(const SellArgs& a, int64_t& b0, int64_t& b1) {
   __shared__ int64_t s_rng[2];
-  if (threadIdx.x == 0) {
+  const int warp = threadIdx.x >> 5;
+  if (warp < 2) {
     const int64_t w0 = sell_work(a, a.blk_lo), W = sell_work(a, a.blk_hi) - w0;
-    const int64_t t0 = w0 + W * blockIdx.x / gridDim.x, t1 = w0 + W * (blockIdx.x + 1) / gridDim.x;
-    s_rng[0] = sell_lower(a, a.blk_lo, a.blk_hi, t0);
-    s_rng[1] = blockIdx.x + 1 == gridDim.x ? a.blk_hi : sell_lower(a, a.blk_lo, a.blk_hi, t1);
+    const int64_t t = w0 + W * (blockIdx.x + warp) / gridDim.x;
+    int64_t v;
+    if (warp == 1 && blockIdx.x + 1 == gridDim.x) v = a.blk_hi;
+    else v = sell_lower_warp(a, a.blk_lo, a.blk_hi, t);
+    if ((threadIdx.x & 31) == 0) s_rng[warp] = v;
   }
   __syncthreads();
   b0 = s_rng[0];
