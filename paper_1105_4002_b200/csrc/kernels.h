@@ -90,8 +90,9 @@ struct SellArgs {
   const int64_t* rp;        // spmv32s_kernel row-mode blocks: the CSR row pointer (lengths)
   const float* val;         // [step][lane][8] values (zero pads)
   const float* src;
-  const float* src_lo;      // non-null: A (src + src_lo), the lo part gathered from global
-                            // memory (extended-precision solver iterates)
+  const float* src_lo;      // non-null: A (src + src_lo) (extended-precision solver iterates,
+                            // DESIGN §5.3), the lo parts gathered from global memory, or staged
+  int32_t lo_off;           // > 0: after the hi window, lo_off floats on (spmv16s_kernel)
   const float* b;           // non-null: out = A src - b, sum r^2
   float* out;
   float* out_lo;

@@ -210,6 +210,10 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
       s.val = d.val;
       s.src = src;
       s.src_lo = src_lo;
+      // stage the lo window too when both fit (c2: 2 x 66 KB): the hi window occupies
+      // pl.smem bytes, the lo one the same amount after it
+      if (src_lo && pl.staged && !pl.sv.half && 2 * pl.smem + 2048 <= (size_t)p->max_smem_optin)
+        s.lo_off = (int32_t)(pl.smem / sizeof(float));
       s.b = q == P - 1 ? b : nullptr;
       s.out = out;
       s.out_lo = q == P - 1 ? out_lo : nullptr;
@@ -1118,6 +1122,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   if (p->device < 0) TVR_CUDA(cudaGetDevice(&p->device));
   TVR_CUDA(cudaSetDevice(p->device));
   TVR_CUDA(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device));
+  TVR_CUDA(cudaDeviceGetAttribute(&p->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device));
   if (user_stream) {
     p->stream = user_stream;
   } else {

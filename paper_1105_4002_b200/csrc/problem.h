@@ -178,6 +178,7 @@ struct tvr_problem {
   bool inbox_raw = false;  // NCCL backend: inbox from cudaMalloc (IPC-mappable), freed by dist_release
   bool ext_eval = false;   // UPN / GP iterates can be evaluated at hi + lo (A pass lo gathers)
   bool ext_on = false;     // ... and are, from this point of the current solve on
+  int max_smem_optin = 0;  // cudaDevAttrMaxSharedMemoryPerBlockOptin of the device
   int64_t inbox_stride = 0;
   float** out_peer_dev = nullptr;
   int64_t* out_bounds_dev = nullptr;

@@ -620,7 +620,9 @@ __device__ __forceinline__ void sell_cta_range(const SellArgs& a, int64_t& b0, i
   b1 = s_rng[1];
 }
 
-template <int UNR, bool STAGED, int NT = 512, bool HALF = false, bool DYN = true, bool LO = false>
+// LO: 0 = plain; 1 = + the lo parts gathered from global memory; 2 = + the lo window staged in
+// shared memory after the hi one (a.lo_off floats on; when both fit: c2)
+template <int UNR, bool STAGED, int NT = 512, bool HALF = false, bool DYN = true, int LO = 0>
 __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
   extern __shared__ float stage[];
   __shared__ int s_next;
@@ -633,11 +635,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
     const int z = a.blk_slice[it - zb];
     const int64_t it_end = min(b1, zb + a.zend[z]);
     const float* gbase = a.src + a.win_lo[z] + rz * a.rep_win;
-    const float* lbase = LO ? a.src_lo + a.win_lo[z] + rz * a.rep_win : nullptr;
+    const float* lbase = LO != 0 ? a.src_lo + a.win_lo[z] + rz * a.rep_win : nullptr;
     const int64_t row_off = rz * a.rep_rows;
     if (STAGED || DYN) __syncthreads();  // previous segment done: window and counter reusable
     if (DYN && threadIdx.x == 0) s_next = nwarps;
     if constexpr (STAGED) stage_window(stage, gbase, HALF ? min(a.win_len[z], a.part_len) : a.win_len[z]);
+    if constexpr (LO == 2) stage_window(stage + a.lo_off, lbase, a.win_len[z]);
     if (STAGED || DYN) __syncthreads();
     // DYN: warps take the segment's blocks from a shared counter (blocks are sorted by length
     // inside a slice, so this is longest-first list scheduling); the next block's descriptors are
@@ -683,7 +686,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
         for (int u = 0; u < UNR; ++u) {
           acc += HALF ? chunk8_sum_part(c[u], va[u], vb[u], stage, gbase, a.part_len)
                       : chunk8_sum<STAGED>(c[u], va[u], vb[u], stage, gbase);
-          if constexpr (LO) acc += chunk8_sum_lo(c[u], va[u], vb[u], lbase);
+          if constexpr (LO == 1) acc += chunk8_sum_lo(c[u], va[u], vb[u], lbase);
+          if constexpr (LO == 2) acc += chunk8_sum<true>(c[u], va[u], vb[u], stage + a.lo_off, lbase);
         }
       }
       for (; s < K; ++s) {
@@ -692,7 +696,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
         const float4 vb0 = ld_stream_f4(vp + s * 256 + 4);
         acc += HALF ? chunk8_sum_part(c0, va0, vb0, stage, gbase, a.part_len)
                     : chunk8_sum<STAGED>(c0, va0, vb0, stage, gbase);
-        if constexpr (LO) acc += chunk8_sum_lo(c0, va0, vb0, lbase);
+        if constexpr (LO == 1) acc += chunk8_sum_lo(c0, va0, vb0, lbase);
+        if constexpr (LO == 2) acc += chunk8_sum<true>(c0, va0, vb0, stage + a.lo_off, lbase);
       }
       double q = 0.0;
       if (row >= 0 && a.acc_out) {
@@ -1247,11 +1252,14 @@ static cudaError_t dispatch16s(const SellVariant& v, F&& f) {
 // extended-precision source (a.src_lo): the default sliced-ELL configurations only (DYN, two
 // steps in flight, one slice per pass); spmv16s_lo_ok() tells the planner
 template <class F>
-static cudaError_t dispatch16s_lo(const SellVariant& v, F&& f) {
-  if (v.staged) return v.block == 1024 ? f(spmv16s_kernel<2, true, 1024, false, true, true>)
-                                       : f(spmv16s_kernel<2, true, 512, false, true, true>);
-  return v.block == 1024 ? f(spmv16s_kernel<2, false, 1024, false, true, true>)
-                         : f(spmv16s_kernel<2, false, 512, false, true, true>);
+static cudaError_t dispatch16s_lo(const SellVariant& v, bool lo_staged, F&& f) {
+  if (v.staged && lo_staged)
+    return v.block == 1024 ? f(spmv16s_kernel<2, true, 1024, false, true, 2>)
+                           : f(spmv16s_kernel<2, true, 512, false, true, 2>);
+  if (v.staged) return v.block == 1024 ? f(spmv16s_kernel<2, true, 1024, false, true, 1>)
+                                       : f(spmv16s_kernel<2, true, 512, false, true, 1>);
+  return v.block == 1024 ? f(spmv16s_kernel<2, false, 1024, false, true, 1>)
+                         : f(spmv16s_kernel<2, false, 512, false, true, 1>);
 }
 // (not the partly staged window: its lo instantiation spilled 312 bytes)
 bool spmv16s_lo_ok(const SellVariant& v) {
@@ -1263,10 +1271,12 @@ cudaError_t launch_spmv16s(const SellArgs& a, const SellVariant& v, int grid, si
   if (a.blk_hi <= a.blk_lo) return cudaSuccess;
   if (a.src_lo) {
     if (!spmv16s_lo_ok(v)) return cudaErrorNotSupported;
-    return dispatch16s_lo(v, [&](auto k) -> cudaError_t {
-      cudaError_t e = ensure_smem_attr((const void*)k, smem);
+    // the lo window staged too when both windows fit (a.lo_off > 0 set by the caller)
+    const size_t sm = a.lo_off > 0 ? smem + sizeof(float) * (size_t)a.lo_off : smem;
+    return dispatch16s_lo(v, a.lo_off > 0, [&](auto k) -> cudaError_t {
+      cudaError_t e = ensure_smem_attr((const void*)k, sm);
       if (e != cudaSuccess) return e;
-      k<<<grid, v.block, smem, st>>>(a);
+      k<<<grid, v.block, sm, st>>>(a);
       return cudaGetLastError();
     });
   }

@@ -25,14 +25,15 @@ HOT = {
         (r"tv_kernelINS_9SrcTrialXILb1EEELi1ELi32EiE", 0),
     ],
     "spmv.cu": [
-        (r"spmv16s_kernelILi2ELb1ELi512ELb0ELb1ELb0E", 0),   # sliced ELL: c2 A and A^T passes
-        (r"spmv16s_kernelILi2ELb1ELi1024ELb0ELb1ELb0E", 0),  # c3 A^T pass (wide CTA)
-        (r"spmv16s_kernelILi2ELb1ELi1024ELb1ELb1ELb0E", 0),  # c3 A pass (partly staged window)
+        (r"spmv16s_kernelILi2ELb1ELi512ELb0ELb1ELi0E", 0),   # sliced ELL: c2 A and A^T passes
+        (r"spmv16s_kernelILi2ELb1ELi1024ELb0ELb1ELi0E", 0),  # c3 A^T pass (wide CTA)
+        (r"spmv16s_kernelILi2ELb1ELi1024ELb1ELb1ELi0E", 0),  # c3 A pass (partly staged window)
         (r"spmv16p_kernelILi8ELi3ELb1E", 0),   # padded per-row kernel (TVR_SPMV_SELL=0)
         (r"spmv32s_kernelILi2ELi512ELi0ELb0EE", 0),  # int32 sliced ELL: c5 A pass
         (r"spmv32s_kernelILi3ELi512ELi0ELb0EE", 8),  # int32 sliced ELL: c5 / f2 A^T pass
         (r"spmv32s_kernelILi3ELi1024ELi0ELb0EE", 0),  # c5 A / A^T (1024-thread CTAs)
-        (r"spmv16s_kernelILi2ELb1ELi1024ELb0ELb1ELb1EE", 0),  # extended-precision UPN A pass (c2, c3 parts)
+        (r"spmv16s_kernelILi2ELb1ELi1024ELb0ELb1ELi1EE", 0),  # extended-precision UPN A pass (c3 parts)
+        (r"spmv16s_kernelILi2ELb1ELi1024ELb0ELb1ELi2EE", 16),  # same, lo window staged (c2; 8 B)
         (r"spmv16z_kernelILi2ELi1ELi1024EE", 0),  # slice-shared operator, 2 slices per pass
         (r"spmv16p_kernelILi4ELi3ELb1E", 0),   # c2 A^T pass
         (r"spmv16p_kernelILi8ELi2ELb0E", 0),   # c3 A pass (global gather)
