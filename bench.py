@@ -397,7 +397,13 @@ def run_ours(args, rank, world, local_rank):
         out["c3_gradient"] = large_config_line(tvreg, torch, "c3", 10, world, rank, local_rank,
                                                solve=("gpbb",))
         torch.cuda.empty_cache()
-        out["c5_gradient"] = large_config_line(tvreg, torch, "c5", 10, world, rank, local_rank)
+        out["c5_gradient"] = large_config_line(tvreg, torch, "c5", 10, world, rank, local_rank,
+                                               solve=("gpbb",))
+        torch.cuda.empty_cache()
+        # the same with the solvers' volume vectors replicated (one all-gather of the gradient
+        # per iteration instead of one of the point per A pass; the same iterates bitwise)
+        out["c5_views_rep"] = large_config_line(tvreg, torch, "c5", 10, world, rank, local_rank,
+                                                solve=("gpbb",), shard="views_rep")
     if rank == 0 and not _dist(world) and not args.no_cpu_baseline:
         its = {k: v for k, v in out.get("solvers", {}).items() if "iters" in v}
         for s in ("gpbb", "upn"):
@@ -440,14 +446,16 @@ def solver_timings(tvreg, torch, configs=("c1", "c2", "f2few", "f2many")):
 
 
 def large_config_line(tvreg, torch, cfg="c3", steps=10, world=1, rank=0, local_rank=0, solve=None,
-                      oracle_time=False):
+                      oracle_time=False, shard="views"):
     """Gradient evaluations on a 256^3 workload (c3: BJ configs[2], separable; c5: configs[4],
     non-separable) at N = world GPUs, STRONG scaling (the whole 256^3 problem split over the ranks,
     the north star's "80 % parallel efficiency at 8 GPUs on the 256^3 workloads"):
       c3: z-slabs (P1): each rank builds only its slices' rows (harness.strong_slab), one TV halo
           exchange per evaluation and the rank-ordered scalar all-gather over NCCL;
       c5: views (P2): each rank traces only its views' rays (harness.views_block), the point is
-          all-gathered before the A pass and A^T r reduce-scattered to the slabs.
+          all-gathered before the A pass and A^T r reduce-scattered to the slabs (shard "views"),
+          or the solvers keep x and g whole on every rank (shard "views_rep": the gradient's
+          slab all-gathered once per gradient, trial points formed redundantly).
     value = whole-problem gradient evaluations per second (device time, max over ranks), so the
     parallel efficiency at N is value(N) / (N value(1)).  solve: optional solver names timed to
     REL 1e-6 from x0 = 0 on the same (sharded) problem (c3: configs[2]'s GPBB full solve)."""
@@ -466,7 +474,7 @@ def large_config_line(tvreg, torch, cfg="c3", steps=10, world=1, rank=0, local_r
             A, grid, z0, z1 = vb.A, vb.grid, vb.z0, vb.z1
             P = tvreg.Problem(A.row_ptr, A.col, A.val, b, grid, vb.alpha, vb.tau, vb.lo, vb.hi,
                               world=world, rank=rank, z0=z0, z1=z1, nccl_comm=comm,
-                              device=local_rank, stream=stream.cuda_stream, shard="views")
+                              device=local_rank, stream=stream.cuda_stream, shard=shard)
             nnz_loc = A.nnz
             del A, vb
         else:
@@ -528,7 +536,7 @@ def large_config_line(tvreg, torch, cfg="c3", steps=10, world=1, rank=0, local_r
     kt = {k: dict(ms_per_launch=v["ms"] / v["launches"],
                   achieved_gbs=v["bytes"] / v["ms"] / 1e6, frac=v["bytes"] / v["ms"] / 1e6 / peak)
           for k, v in st.items() if v["launches"]}
-    par = "single" if world == 1 else (f"views{world}" if cfg == "c5" else f"zslab{world}")
+    par = "single" if world == 1 else (f"{shard}{world}" if cfg == "c5" else f"zslab{world}")
     res = dict(workload=f"{cfg}: {grid[0]}^3, nnz {nnz_tot}", n_gpus=world, parallelism=par,
                scaling="strong" if world > 1 else "single", value=1e3 / ms, unit=UNIT,
                ms_per_step=ms, steps=steps, kernels_rank0=kt)

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define TVR_ABI_VERSION 4
+#define TVR_ABI_VERSION 5
 
 typedef enum {
   TVR_OK = 0,
@@ -73,7 +73,7 @@ typedef struct {
   int32_t nx, ny, nz; /* global volume; voxel j = (z*ny + y)*nx + x */
 } tvr_grid;
 
-enum { TVR_SHARD_NONE = 0, TVR_SHARD_ZSLAB = 1, TVR_SHARD_VIEWS = 2 };
+enum { TVR_SHARD_NONE = 0, TVR_SHARD_ZSLAB = 1, TVR_SHARD_VIEWS = 2, TVR_SHARD_VIEWS_REP = 3 };
 
 /* Distribution / placement.  NULL => one GPU, current device, a library-created stream.
  * ZSLAB (P1, slice-separable geometry): rank owns slices [z0, z1) and the rows
@@ -83,7 +83,13 @@ enum { TVR_SHARD_NONE = 0, TVR_SHARD_ZSLAB = 1, TVR_SHARD_VIEWS = 2 };
  *   [z0, z1) of every volume vector.  Before each A pass the slabs of the point are
  *   all-gathered into a full-volume buffer; the A^T pass produces a full-volume partial
  *   A_p^T r_p that is reduce-scattered (fp32 sum) to the slabs.
- * In both modes the TV stencil exchanges one halo slice with each z-neighbour over NCCL
+ * VIEWS_REP (P2 with replicated iterates): rows and slabs as VIEWS, but the
+ *   solvers keep every volume vector WHOLE on every rank: trial and momentum points are formed
+ *   redundantly outside the slab (no communication), so the A pass needs no all-gather; the
+ *   gradient's slab (stencil over the slab, after the A^T reduce-scatter) is all-gathered once
+ *   per gradient instead of the point once per A pass.  Same results as VIEWS, bitwise.  The
+ *   caller's vectors are still slabs [z0, z1).
+ * In ZSLAB / VIEWS the TV stencil exchanges one halo slice with each z-neighbour over NCCL
  * (nccl_comm from tvr_nccl_comm_init) and scalars are all-gathered and summed in rank order.
  * The slabs must tile [0, nz) in rank order (rank r's z1 = rank r+1's z0). */
 typedef struct {
@@ -141,6 +147,11 @@ typedef struct {
                                           it uses the collective reduce-scatter */
   int32_t slice_shared;                /* tvr_create_sliced: slices sharing the stored slice
                                           matrix (the slab's nz); 0 for tvr_create */
+  int32_t views_rep;                   /* VIEWS_REP with world > 1: the solvers' volume vectors
+                                          are whole on every rank */
+  int64_t point_allgathers;            /* VIEWS modes: all-gathers of a point before an A pass
+                                          so far (VIEWS: one per A pass; VIEWS_REP: only for a
+                                          caller's slab) */
 } tvr_info;
 int tvr_get_info(const tvr_problem* p, tvr_info* info);
 

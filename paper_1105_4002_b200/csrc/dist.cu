@@ -105,7 +105,7 @@ static int local_collective(tvr_problem* p, const void* mine, F&& copy) {
   return TVR_OK;
 }
 
-int halo_exchange(tvr_problem* p, float* v) {
+int halo_exchange_to(tvr_problem* p, const float* v, float* lo, float* hi) {
   NvtxRange nv("halo_exchange");
   if (p->world <= 1) return TVR_OK;
   const size_t bytes = sizeof(float) * (size_t)p->plane;
@@ -115,12 +115,11 @@ int halo_exchange(tvr_problem* p, float* v) {
       if (p->rank > 0) {  // lower halo = last owned plane of rank - 1
         const float* src = static_cast<const float*>(peer[p->rank - 1]);
         const int nzl_lo = (int)p->peer_nzl[p->rank - 1];
-        TVR_CUDA(cudaMemcpyAsync(v - p->plane, src + (int64_t)(nzl_lo - 1) * p->plane, bytes,
+        TVR_CUDA(cudaMemcpyAsync(lo, src + (int64_t)(nzl_lo - 1) * p->plane, bytes,
                                  cudaMemcpyDeviceToDevice, p->stream));
       }
       if (p->rank < p->world - 1) {  // upper halo = first owned plane of rank + 1
-        TVR_CUDA(cudaMemcpyAsync(v + (int64_t)p->nzl * p->plane, peer[p->rank + 1], bytes,
-                                 cudaMemcpyDeviceToDevice, p->stream));
+        TVR_CUDA(cudaMemcpyAsync(hi, peer[p->rank + 1], bytes, cudaMemcpyDeviceToDevice, p->stream));
       }
       return TVR_OK;
     });
@@ -130,27 +129,37 @@ int halo_exchange(tvr_problem* p, float* v) {
   TVR_NCCL(ncclGroupStart());
   if (p->rank > 0) {
     TVR_NCCL(ncclSend(v, cnt, ncclFloat, p->rank - 1, comm, p->stream));
-    TVR_NCCL(ncclRecv(v - p->plane, cnt, ncclFloat, p->rank - 1, comm, p->stream));
+    TVR_NCCL(ncclRecv(lo, cnt, ncclFloat, p->rank - 1, comm, p->stream));
   }
   if (p->rank < p->world - 1) {
     TVR_NCCL(ncclSend(v + (int64_t)(p->nzl - 1) * p->plane, cnt, ncclFloat, p->rank + 1, comm, p->stream));
-    TVR_NCCL(ncclRecv(v + (int64_t)p->nzl * p->plane, cnt, ncclFloat, p->rank + 1, comm, p->stream));
+    TVR_NCCL(ncclRecv(hi, cnt, ncclFloat, p->rank + 1, comm, p->stream));
   }
   TVR_NCCL(ncclGroupEnd());
   return TVR_OK;
 }
 
+int halo_exchange(tvr_problem* p, float* v) {
+  if (rep_dist(p)) return replicate_volume(p, v);
+  return halo_exchange_to(p, v, v - p->plane, v + (int64_t)p->nzl * p->plane);
+}
+
+// planes of a point recomputed outside the owned slab: the z-neighbours' halo planes (-1, nzl),
+// or in VIEWS_REP every plane of the replicated vector outside [z0, z1)
+static int fill_lo(const tvr_problem* p) { return rep_dist(p) ? p->z0 : (p->z0 > 0 ? 1 : 0); }
+static int fill_hi(const tvr_problem* p) { return rep_dist(p) ? p->nz - p->z1 : (p->z1 < p->nz ? 1 : 0); }
+
 int halo_fill_trial(tvr_problem* p, const float* x, const float* g, double s, float* v) {
   if (p->world <= 1) return TVR_OK;
-  TVR_CUDA(launch_halo_fill_trial(x, g, s, p->lo, p->hi, p->plane, p->nzl, p->z0 > 0,
-                                  p->z1 < p->nz, v, p->stream));
+  TVR_CUDA(launch_halo_fill_trial(x, g, s, p->lo, p->hi, p->plane, p->nzl, fill_lo(p),
+                                  fill_hi(p), v, p->stream));
   p->launches++;
   return TVR_OK;
 }
 
 int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double beta, float* y) {
   if (p->world <= 1) return TVR_OK;
-  TVR_CUDA(launch_halo_fill_momentum(x1, x0, beta, p->plane, p->nzl, p->z0 > 0, p->z1 < p->nz, y,
+  TVR_CUDA(launch_halo_fill_momentum(x1, x0, beta, p->plane, p->nzl, fill_lo(p), fill_hi(p), y,
                                      p->stream));
   p->launches++;
   return TVR_OK;
@@ -159,8 +168,8 @@ int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double 
 int halo_fill_trial_x(tvr_problem* p, const float* x, const float* x_lo, const float* g, double s,
                       float* v, float* v_lo) {
   if (p->world <= 1) return TVR_OK;
-  TVR_CUDA(launch_halo_fill_trial_x(x, x_lo, g, s, p->lo, p->hi, p->plane, p->nzl, p->z0 > 0,
-                                    p->z1 < p->nz, v, v_lo, p->stream));
+  TVR_CUDA(launch_halo_fill_trial_x(x, x_lo, g, s, p->lo, p->hi, p->plane, p->nzl, fill_lo(p),
+                                    fill_hi(p), v, v_lo, p->stream));
   p->launches++;
   return TVR_OK;
 }
@@ -168,8 +177,8 @@ int halo_fill_trial_x(tvr_problem* p, const float* x, const float* x_lo, const f
 int halo_fill_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, const float* x0,
                          const float* x0_lo, double beta, float* y, float* y_lo) {
   if (p->world <= 1) return TVR_OK;
-  TVR_CUDA(launch_halo_fill_momentum_x(x1, x1_lo, x0, x0_lo, beta, p->plane, p->nzl, p->z0 > 0,
-                                       p->z1 < p->nz, y, y_lo, p->stream));
+  TVR_CUDA(launch_halo_fill_momentum_x(x1, x1_lo, x0, x0_lo, beta, p->plane, p->nzl, fill_lo(p),
+                                       fill_hi(p), y, y_lo, p->stream));
   p->launches++;
   return TVR_OK;
 }
@@ -177,7 +186,7 @@ int halo_fill_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, co
 int reduce_gathered_scalars(tvr_problem* p, double* vals, int n);
 
 int halo_exchange_fetch(tvr_problem* p, float* v, int nslots) {
-  if (p->world <= 1 || local_of(p)) {
+  if (p->world <= 1 || local_of(p) || rep_dist(p)) {
     TVR_TRY(halo_exchange(p, v));
     return fetch_scalars(p, nslots);
   }
@@ -271,7 +280,22 @@ int slab_table(tvr_problem* p) {
 }
 
 // ---- VIEWS mode: rows split by projection views, volume vectors by z-slabs.
-bool views_dist(const tvr_problem* p) { return p->mode == TVR_SHARD_VIEWS && p->world > 1; }
+bool views_dist(const tvr_problem* p) {
+  return (p->mode == TVR_SHARD_VIEWS || p->mode == TVR_SHARD_VIEWS_REP) && p->world > 1;
+}
+// VIEWS_REP: the library's volume vectors are whole volumes on every rank (a slab pointer v is
+// base + z0 plane); a point is made whole once (replicate_volume after its owned slab is
+// written, or the trial / momentum fills over the planes outside the slab), so the A pass reads
+// it without an all-gather
+bool rep_dist(const tvr_problem* p) { return p->mode == TVR_SHARD_VIEWS_REP && p->world > 1; }
+
+// a slab pointer into one of the library's replicated volume vectors (not a caller's slab)
+static bool rep_internal(const tvr_problem* p, const float* slab) {
+  const float* base = slab - (int64_t)p->z0 * p->plane;
+  for (const float* b : p->vol_base)
+    if (b == base) return true;
+  return false;
+}
 
 static bool uniform_slabs(const tvr_problem* p) {
   for (int r = 1; r < p->world; ++r)
@@ -288,6 +312,11 @@ int gather_volume(tvr_problem* p, const float* slab, const float** full) {
     *full = slab;
     return TVR_OK;
   }
+  if (rep_dist(p) && rep_internal(p, slab)) {  // already whole on this rank
+    *full = slab - (int64_t)p->z0 * p->plane;
+    return TVR_OK;
+  }
+  ++p->n_gathers;
   if (local_of(p)) {
     TVR_TRY(local_collective(p, slab, [&](const std::vector<const void*>& peer) -> int {
       for (int r = 0; r < p->world; ++r)
@@ -307,6 +336,38 @@ int gather_volume(tvr_problem* p, const float* slab, const float** full) {
     TVR_NCCL(ncclGroupEnd());
   }
   *full = p->xfull;
+  return TVR_OK;
+}
+
+// VIEWS_REP: every rank's slab of the replicated vector v (slab pointer) lands in everybody's
+// copy, in place (the one all-gather of a gradient per iteration that replaces the all-gather of
+// the point before every A pass).  NCCL: equal slabs one in-place ncclAllGather, ragged slabs
+// one in-place broadcast per rank.
+int replicate_volume(tvr_problem* p, float* v) {
+  NvtxRange nv("views_rep_allgather");
+  float* full = v - (int64_t)p->z0 * p->plane;
+  if (local_of(p)) {
+    return local_collective(p, full, [&](const std::vector<const void*>& peer) -> int {
+      for (int r = 0; r < p->world; ++r) {
+        if (r == p->rank) continue;
+        TVR_CUDA(cudaMemcpyAsync(full + p->slab_off[r],
+                                 static_cast<const float*>(peer[r]) + p->slab_off[r],
+                                 sizeof(float) * p->slab_cnt[r], cudaMemcpyDeviceToDevice, p->stream));
+      }
+      return TVR_OK;
+    });
+  }
+  if (uniform_slabs(p)) {
+    TVR_NCCL(ncclAllGather(full + p->slab_off[p->rank], full, (size_t)p->slab_cnt[0], ncclFloat,
+                           nccl_of(p), p->stream));
+  } else {
+    TVR_NCCL(ncclGroupStart());
+    for (int r = 0; r < p->world; ++r) {
+      float* dst = full + p->slab_off[r];
+      TVR_NCCL(ncclBroadcast(dst, dst, (size_t)p->slab_cnt[r], ncclFloat, r, nccl_of(p), p->stream));
+    }
+    TVR_NCCL(ncclGroupEnd());
+  }
   return TVR_OK;
 }
 

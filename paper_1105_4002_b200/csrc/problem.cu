@@ -62,6 +62,17 @@ static void dev_free_all(tvr_problem* p) {
 
 int64_t n_local(const tvr_problem* p) { return p->plane * p->nzl; }
 float* volvec(tvr_problem* p, int i) { return p->vol[i]; }
+// first element and length of the allocation behind volume vector v (halo planes, or in VIEWS_REP
+// the whole replicated volume)
+void vol_extent(const tvr_problem* p, float* v, float** first, int64_t* count) {
+  if (rep_dist(p)) {
+    *first = v - (int64_t)p->z0 * p->plane;
+    *count = (int64_t)p->nz * p->plane;
+  } else {
+    *first = v - p->plane;
+    *count = (int64_t)(p->nzl + 2) * p->plane;
+  }
+}
 float* datvec(tvr_problem* p, int i) { return p->dat[i]; }
 
 // --------------------------------------------------------------- timing
@@ -1025,7 +1036,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     p->comm = dist->nccl_comm;
     p->device = dist->device;
     user_stream = (cudaStream_t)dist->cuda_stream;
-    if (p->mode == TVR_SHARD_ZSLAB || p->mode == TVR_SHARD_VIEWS) {
+    if (p->mode == TVR_SHARD_ZSLAB || p->mode == TVR_SHARD_VIEWS || p->mode == TVR_SHARD_VIEWS_REP) {
       p->z0 = dist->z0; p->z1 = dist->z1;
       if (p->z0 < 0 || p->z1 > grid.nz || p->z0 >= p->z1) { set_error("tvr_create: bad slab"); return TVR_E_ARG; }
     } else if (p->mode != TVR_SHARD_NONE) {
@@ -1045,7 +1056,7 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
     }
   }
   p->nzl = p->z1 - p->z0;
-  const bool views = p->mode == TVR_SHARD_VIEWS;
+  const bool views = p->mode == TVR_SHARD_VIEWS || p->mode == TVR_SHARD_VIEWS_REP;
   if (sliced && views) {
     set_error("tvr_create_sliced: VIEWS mode is not supported (use ZSLAB)");
     return TVR_E_ARG;
@@ -1340,18 +1351,22 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
 
   // ---- work vectors ----
   const int NVOL = 13, NDAT = 4;  // 10-12: lo parts of the extended-precision solver iterates
-  const size_t volbytes = sizeof(float) * (size_t)(p->plane * (p->nzl + 2));
+  // slab + one halo plane per side; VIEWS_REP: the whole volume, the slab at its z0 offset
+  const bool rep = rep_dist(p);
+  const size_t volbytes = sizeof(float) * (size_t)(p->plane * (rep ? p->nz : p->nzl + 2));
   for (int i = 0; i < NVOL; ++i) {
     float* q = nullptr;
     TVR_TRY(dev_alloc(p, (void**)&q, volbytes));
     TVR_CUDA(cudaMemsetAsync(q, 0, volbytes, p->stream));
-    p->vol.push_back(q + p->plane);
+    p->vol.push_back(q + (rep ? (int64_t)p->z0 * p->plane : p->plane));
+    if (rep) p->vol_base.push_back(q);
   }
   for (int i = 0; i < NDAT; ++i) {
     float* q = nullptr;
     TVR_TRY(dev_alloc(p, (void**)&q, sizeof(float) * std::max<int64_t>(m_full, 1)));
     p->dat.push_back(q);
   }
+  if (p->world > 1) TVR_TRY(dev_alloc(p, (void**)&p->xhalo, sizeof(float) * 2 * p->plane));
   if (views_dist(p)) {
     TVR_TRY(dev_alloc(p, (void**)&p->xfull, sizeof(float) * p->ncol));
     TVR_TRY(dev_alloc(p, (void**)&p->wfull, sizeof(float) * p->ncol));
@@ -1450,25 +1465,40 @@ int tvr_get_info(const tvr_problem* p, tvr_info* info) {
   info->device_bytes = p->device_bytes;
   info->n_cols_local = p->ncol;
   info->views_fused_rs = p->fused_rs ? 1 : 0;
+  info->views_rep = rep_dist(p) ? 1 : 0;
+  info->point_allgathers = p->n_gathers;
   info->slice_shared = p->sliced ? p->nzA : 0;
   return TVR_OK;
 }
 
 // Volume input from a caller pointer: in slab mode copied into an internal buffer whose halo
 // planes are then exchanged; on one GPU used in place.
-static int stage_volume(tvr_problem* p, const float* x_dev, int slot, const float** out) {
-  if (p->world == 1) { *out = x_dev; return TVR_OK; }
-  float* v = volvec(p, slot);
-  TVR_CUDA(cudaMemcpyAsync(v, x_dev, sizeof(float) * p->n, cudaMemcpyDeviceToDevice, p->stream));
-  TVR_TRY(halo_exchange(p, v));
-  *out = v;
-  return TVR_OK;
+// A caller's volume vector at world > 1: its boundary planes go to the neighbours and theirs land
+// in p->xhalo (planes -1 and nzl), so the stencil reads the caller's slab in place.
+static int exchange_caller_halo(tvr_problem* p, const float* x_dev) {
+  if (p->world == 1) return TVR_OK;
+  return halo_exchange_to(p, x_dev, p->xhalo, p->xhalo + p->plane);
+}
+
+// alpha grad TV(x) (+ w) on a caller's x after exchange_caller_halo (a4)
+static int pass_tv_caller(tvr_problem* p, const float* x, const float* w, float* g, double alpha) {
+  if (p->world == 1)
+    return pass_tv_grad(p, x, nullptr, 0.0, w, nullptr, 0.0, g, nullptr, nullptr, nullptr, 0.0, 1,
+                        alpha, nullptr);
+  TVArgs a = tv_args(p, 1);
+  a.alpha = alpha;
+  a.w1 = w;
+  a.g_out = g;
+  const double bytes = (double)n_local(p) * (4.0 + (w ? 4.0 : 0.0) + (g ? 4.0 : 0.0));
+  return launch(p, K_TV_GRAD, bytes, [&] {
+    return launch_tv_grad_plain_h(a, x, p->xhalo, p->xhalo + p->plane, p->stream);
+  });
 }
 
 static int objective_grad_impl(tvr_problem* p, const float* x_dev, double* f_out, float* g_dev,
                                tvr_fparts* parts) {
-  const float* x;
-  TVR_TRY(stage_volume(p, x_dev, 9, &x));
+  const float* x = x_dev;
+  TVR_TRY(exchange_caller_halo(p, x));
   float* r = datvec(p, 0);
   TVR_TRY(pass_residual(p, x, r, 0));
   float* w = nullptr;
@@ -1476,7 +1506,7 @@ static int objective_grad_impl(tvr_problem* p, const float* x_dev, double* f_out
     w = volvec(p, 8);
     TVR_TRY(pass_AT(p, r, w));
   }
-  TVR_TRY(pass_tv_grad(p, x, nullptr, 0.0, w, nullptr, 0.0, g_dev, nullptr, nullptr, nullptr, 0.0, 1));
+  TVR_TRY(pass_tv_caller(p, x, w, g_dev, p->alpha));
   TVR_TRY(fetch_scalars(p, 8));
   const double fid = 0.5 * p->hscal[0], tv = p->hscal[1];
   const double f = fid + p->alpha * tv;
@@ -1763,10 +1793,8 @@ int tvr_apply_AT(tvr_problem* p, const float* y_dev, float* w_dev) {
 int tvr_tv(tvr_problem* p, const float* x_dev, double* tv_out, float* grad_dev) {
   if (!p || !x_dev) { set_error("tvr_tv: NULL"); return TVR_E_ARG; }
   TVR_CUDA(cudaSetDevice(p->device));
-  const float* x;
-  TVR_TRY(stage_volume(p, x_dev, 9, &x));
-  TVR_TRY(pass_tv_grad(p, x, nullptr, 0.0, nullptr, nullptr, 0.0, grad_dev, nullptr, nullptr,
-                       nullptr, 0.0, 1, 1.0));
+  TVR_TRY(exchange_caller_halo(p, x_dev));
+  TVR_TRY(pass_tv_caller(p, x_dev, nullptr, grad_dev, 1.0));
   TVR_TRY(fetch_scalars(p, 8));
   if (tv_out) *tv_out = p->hscal[1];
   return TVR_OK;

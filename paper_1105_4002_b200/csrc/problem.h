@@ -164,8 +164,11 @@ struct tvr_problem {
   double* dscal = nullptr;  // 32 doubles
   double* hscal = nullptr;  // pinned mirror
 
-  // halo exchange staging (z-slab)
-  float* halo_send = nullptr;
+  // world > 1: the halo planes (-1, nzl) of a caller's vector (tvr_objective_grad / tvr_tv read the
+  // caller's slab in place; its neighbours' planes land here)
+  float* xhalo = nullptr;
+  std::vector<float*> vol_base;
+  int64_t n_gathers = 0;  // all-gathers of a point (gather_volume), tvr_info.point_allgathers  // VIEWS_REP: allocation base of each replicated volume vector
   // VIEWS mode with world > 1: full-volume gather target of the A pass and full-volume partial
   // A_p^T r_p before the reduce-scatter; per-rank slab offsets / sizes (elements)
   float* xfull = nullptr;
@@ -218,6 +221,7 @@ namespace tvr {
 int dev_alloc(tvr_problem* p, void** ptr, size_t bytes);
 void dev_free(tvr_problem* p, void* ptr);
 float* volvec(tvr_problem* p, int i);
+void vol_extent(const tvr_problem* p, float* v, float** first, int64_t* count);
 float* datvec(tvr_problem* p, int i);
 int64_t n_local(const tvr_problem* p);
 
@@ -258,6 +262,9 @@ int pass_gmap(tvr_problem* p, const float* x, const float* g, double nu, float* 
 int fetch_scalars(tvr_problem* p, int nslots);
 // halo planes of a volume vector from the z-neighbours (no-op on one GPU)
 int halo_exchange(tvr_problem* p, float* v);
+// the same exchange for a vector without halo room: v's boundary planes go to the neighbours,
+// theirs land in lo (plane -1) and hi (plane nzl)
+int halo_exchange_to(tvr_problem* p, const float* v, float* lo, float* hi);
 // recompute the halo planes of a trial / momentum point from its inputs' halo planes
 int halo_fill_trial(tvr_problem* p, const float* x, const float* g, double s, float* v);
 int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double beta, float* y);
@@ -271,7 +278,9 @@ int dist_sum_scalars(tvr_problem* p, double* vals, int n);
 int halo_exchange_fetch(tvr_problem* p, float* v, int nslots);
 // VIEWS mode: the A pass's source (slab -> full volume, all-gathered) and the A^T pass's
 // target (full-volume partial -> slab, reduce-scattered); identity on one rank
-bool views_dist(const tvr_problem* p);
+bool views_dist(const tvr_problem* p);  // VIEWS or VIEWS_REP with world > 1
+bool rep_dist(const tvr_problem* p);    // VIEWS_REP with world > 1
+int replicate_volume(tvr_problem* p, float* v);
 bool valid_comm(const void* comm);  // an NCCL or in-process thread communicator handle
 int slab_table(tvr_problem* p);     // every rank's slab, gathered at create time (collective)
 int setup_fused_rs(tvr_problem* p); // VIEWS: inboxes mapped on every peer (collective)

@@ -551,7 +551,12 @@ static int upn_impl(tvr_problem* p, float* x_io, const tvr_upn_opts& o, tvr_resu
   float* xk_lo = volvec(p, 10);
   float* xn_lo = volvec(p, 11);
   float* y_lo = volvec(p, 12);
-  TVR_CUDA(cudaMemsetAsync(xk_lo - p->plane, 0, sizeof(float) * p->plane * (p->nzl + 2), p->stream));
+  {
+    float* first;
+    int64_t cnt;
+    vol_extent(p, xk_lo, &first, &cnt);
+    TVR_CUDA(cudaMemsetAsync(first, 0, sizeof(float) * cnt, p->stream));
+  }
   p->ext_on = p->ext_eval && ext_eval_at() >= 1.0;
 
   TVR_TRY(copy_in(p, xk, x_io));
@@ -720,7 +725,12 @@ static int gp_impl(tvr_problem* p, float* x_io, const tvr_gp_opts& o, tvr_result
   float* rn = datvec(p, 1);
   float* xk_lo = volvec(p, 10);  // extended-precision iterates (as UPN)
   float* xn_lo = volvec(p, 11);
-  TVR_CUDA(cudaMemsetAsync(xk_lo - p->plane, 0, sizeof(float) * p->plane * (p->nzl + 2), p->stream));
+  {
+    float* first;
+    int64_t cnt;
+    vol_extent(p, xk_lo, &first, &cnt);
+    TVR_CUDA(cudaMemsetAsync(first, 0, sizeof(float) * cnt, p->stream));
+  }
   p->ext_on = p->ext_eval && ext_eval_at() >= 1.0;
 
   TVR_TRY(copy_in(p, xk, x_io));

@@ -34,6 +34,7 @@ STATUS_NAMES = {v: k for k, v in globals().items() if k.startswith("TVR_") and i
 TVR_SHARD_NONE = 0
 TVR_SHARD_ZSLAB = 1
 TVR_SHARD_VIEWS = 2
+TVR_SHARD_VIEWS_REP = 3
 TVR_CONTROL_HOST = 0
 TVR_CONTROL_DEVICE = 1
 TVR_CONTROL_AUTO = 2
@@ -61,7 +62,7 @@ class tvr_info(ctypes.Structure):
     _fields_ = [("m_local", c_i64), ("n_local", c_i64), ("nnz_local", c_i64), ("z0", c_i32),
                 ("z1", c_i32), ("slab_staged_A", c_i32), ("slab_staged_AT", c_i32),
                 ("device_bytes", c_i64), ("n_cols_local", c_i64), ("views_fused_rs", c_i32),
-                ("slice_shared", c_i32)]
+                ("slice_shared", c_i32), ("views_rep", c_i32), ("point_allgathers", c_i64)]
 
 
 class tvr_fparts(ctypes.Structure):
@@ -282,7 +283,8 @@ class Problem:
                  z0: int | None = None, z1: int | None = None, nccl_comm: int | None = None,
                  device: int = -1, stream: int | None = None, shard: str | None = None,
                  sliced: bool = False):
-        """shard: None (ZSLAB when world > 1 or z0 is given, else NONE), "zslab" or "views"
+        """shard: None (ZSLAB when world > 1 or z0 is given, else NONE), "zslab", "views" or
+        "views_rep" (VIEWS with the solvers' volume vectors replicated on every rank)
         (rows of any geometry, global columns; see tvr_dist in include/libtvreg.h).
         sliced: the CSR is ONE slice's matrix (n_cols = nx*ny) applied to every slice of the
         slab, b has m_s * slab-slices entries (tvr_create_sliced)."""
@@ -300,7 +302,8 @@ class Problem:
         if shard is None:
             mode = TVR_SHARD_ZSLAB if (world > 1 or z0 is not None) else TVR_SHARD_NONE
         else:
-            mode = {"none": TVR_SHARD_NONE, "zslab": TVR_SHARD_ZSLAB, "views": TVR_SHARD_VIEWS}[shard]
+            mode = {"none": TVR_SHARD_NONE, "zslab": TVR_SHARD_ZSLAB, "views": TVR_SHARD_VIEWS,
+                    "views_rep": TVR_SHARD_VIEWS_REP}[shard]
         if mode != TVR_SHARD_NONE or stream is not None or device >= 0:
             dist = tvr_dist(world, rank, mode,
                             0 if z0 is None else z0, nz if z1 is None else z1,
@@ -419,6 +422,12 @@ class Problem:
         """Gradient projection with BT steps (the paper's comparator, Eq. (6))."""
         o = tvr_gp_opts(max_iters, eps, stop_mode, L0, rho_L, bt_max)
         return self._solve(lib().tvr_solve_gp, o, x, hist_cap)
+
+    def get_info(self) -> tvr_info:
+        """tvr_get_info now (self.info is the snapshot taken at creation)."""
+        info = tvr_info()
+        _check(lib().tvr_get_info(self._h, ctypes.byref(info)), "tvr_get_info")
+        return info
 
     # ---- timing
     def profile(self, on: bool = True):

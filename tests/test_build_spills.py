@@ -23,6 +23,15 @@ HOT = {
         (r"tv_kernelINS_8SrcTrialELi1ELi64EiE", 0),
         (r"tv_kernelINS_9SrcTrialXILb1EEELi1ELi0EiE", 0),  # BT trials (hi + lo state)
         (r"tv_kernelINS_9SrcTrialXILb1EEELi1ELi32EiE", 0),
+        # row-tiled stencil (K = 4; one-warp rows: c2, two-warp rows: c3 / c5)
+        (r"tv_row_kernelINS_8SrcPlainELi0ELi5ELi4ELi7ELi1E", 0),   # tvr_objective_grad
+        (r"tv_row_kernelINS_8SrcPlainELi0ELi5ELi4ELi7ELi2E", 0),
+        (r"tv_row_kernelINS_8SrcPlainELi0ELi69ELi4ELi7ELi1E", 0),  # solver gradient + stop test
+        (r"tv_row_kernelINS_8SrcPlainELi0ELi69ELi4ELi7ELi2E", 0),
+        (r"tv_row_kernelINS_8SrcTrialELi1ELi0ELi4ELi7ELi1E", 0),   # trial points
+        (r"tv_row_kernelINS_8SrcTrialELi1ELi64ELi4ELi7ELi2E", 0),
+        (r"tv_row_kernelINS_12SrcMomentumXILb1EEELi0ELi15ELi4ELi7ELi1E", 0),  # UPN momentum point
+        (r"tv_row_kernelINS_9SrcTrialXILb1EEELi1ELi32ELi4ELi7ELi1E", 0),     # UPN BT trial
     ],
     "spmv.cu": [
         (r"spmv16s_kernelILi2ELb1ELi512ELb0ELb1ELi0E", 0),   # sliced ELL: c2 A and A^T passes

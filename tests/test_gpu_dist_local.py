@@ -223,3 +223,53 @@ def test_views_fused_reduce_scatter_matches_collective(tvreg, world, monkeypatch
         outs[fused] = (res[0][1], torch.cat([r[2] for r in sorted(res, key=lambda t: t[0])]))
     assert outs["1"][0] == outs["0"][0]
     assert torch.equal(outs["1"][1], outs["0"][1])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("solver", ["gpbb", "upn", "gp"])
+def test_views_rep_solvers_equal_views(tvreg, world, solver):
+    """VIEWS_REP (x, g and the trial / momentum points kept whole on every rank: the points are
+    formed redundantly outside the slab, the gradient's slab is all-gathered once per gradient,
+    the A pass reads the whole point without an all-gather) takes exactly the steps of VIEWS
+    (the all-gather of the point before every A pass): identical iterations, objective and
+    iterate, bitwise; the gradient too.  Against the oracle's solve of the whole problem."""
+    grid, views = (14, 12, 10), 9
+    A = harness.siddon_tilted(*grid, views, 7, 17, 10.0)
+    b = harness.simulate_data(A, harness.phantom(*grid, 3))
+    alpha, tau = 0.01, 1e-2
+    x0 = harness.random_x(A.n_cols)
+    plane = grid[0] * grid[1]
+    iters = {"gpbb": 20000, "upn": 20000, "gp": 300}[solver]
+    outs = {}
+    for shard in ("views", "views_rep"):
+        comm = tvreg.local_comm_create(world)
+
+        def rank_fn(r):
+            lv = local_views(A.row_ptr, A.col, A.val, b, grid, views, world, r)
+            P = tvreg.Problem(lv.row_ptr, lv.col, lv.val, lv.b, grid, alpha, tau, world=world,
+                              rank=r, z0=lv.z0, z1=lv.z1, nccl_comm=comm, shard=shard)
+            xl = torch.from_numpy(np.ascontiguousarray(x0[lv.z0 * plane:lv.z1 * plane])).cuda()
+            g = torch.empty(P.n, device="cuda")
+            f, _ = P.objective_grad(xl, g)
+            n0 = P.get_info().point_allgathers
+            assert n0 == 1 and P.info.views_rep == (shard == "views_rep")  # a caller's slab
+            x = torch.zeros(P.n, device="cuda")
+            res = getattr(P, f"solve_{solver}")(x, max_iters=iters, eps=1e-6)
+            # VIEWS all-gathers the point before every A pass (at least one per objective
+            # evaluation), VIEWS_REP never in a solve
+            ng = P.get_info().point_allgathers - n0
+            assert ng == 0 if shard == "views_rep" else ng >= res.n_f
+            return lv.z0, (f, res.iters, res.f, res.n_f, res.converged), g.cpu(), x.cpu()
+
+        res = _run_ranks(world, rank_fn)
+        tvreg.local_comm_destroy(comm)
+        res.sort(key=lambda t: t[0])
+        assert all(r[1] == res[0][1] for r in res)  # every rank: the same branches and values
+        outs[shard] = (res[0][1], torch.cat([r[2] for r in res]), torch.cat([r[3] for r in res]))
+    assert outs["views_rep"][0] == outs["views"][0]
+    assert torch.equal(outs["views_rep"][1], outs["views"][1])
+    assert torch.equal(outs["views_rep"][2], outs["views"][2])
+    if solver != "gp":
+        assert outs["views_rep"][0][4]
+        _solve_parity(_oracle(A, b, grid, alpha, tau), outs["views_rep"][2],
+                      outs["views_rep"][0][2], solver, 1e-6)

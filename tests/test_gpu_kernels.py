@@ -128,8 +128,12 @@ def test_spmv_real_values(tvreg, cfg, c1):
 
 
 # -------------------------------------------------------------------- TV
+# row-tiled stencil (K voxels per lane, 7 owned rows per tile): K = 1 (32, 31, 1, 2 wide),
+# K = 2 (64), K = 4 (128 with ragged tiles, 100 and 96 with idle lanes), K = 8 (256, 200);
+# the 32x8 xy-tile kernel where K does not divide nx (37)
 @pytest.mark.parametrize("grid", [(32, 32, 32), (37, 29, 19), (31, 7, 16), (1, 1, 5), (64, 3, 2),
-                                  (2, 1, 1)])
+                                  (2, 1, 1), (128, 20, 9), (100, 15, 7), (96, 8, 3), (256, 9, 5),
+                                  (200, 13, 4)])
 @pytest.mark.parametrize("tau", [1e-4, 1e-1])
 def test_tv_value_and_gradient(tvreg, grid, tau):
     N = grid[0] * grid[1] * grid[2]
