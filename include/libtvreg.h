@@ -152,6 +152,9 @@ typedef struct {
   int64_t point_allgathers;            /* VIEWS modes: all-gathers of a point before an A pass
                                           so far (VIEWS: one per A pass; VIEWS_REP: only for a
                                           caller's slab) */
+  int64_t gather_layout_blocks[3];     /* non-separable A pass (int32 sliced ELL with block
+                                          modes): 32-ray blocks gathering from the point laid out
+                                          row-major, with x / y swapped, in 8x4 bricks */
 } tvr_info;
 int tvr_get_info(const tvr_problem* p, tvr_info* info);
 

@@ -138,6 +138,18 @@ cudaError_t launch_sell_fill32(int64_t nslots, const int32_t* perm, const int64_
                                const int32_t* blk_k, const int64_t* row_start, const int64_t* rp,
                                const int32_t* col, const float* val, int32_t* cols, float* vals,
                                cudaStream_t st);
+// gather layouts of the non-separable A pass (spmv.cu): xs = [x | x_yx | x_bricks] (3N floats);
+// per-row mapped and sorted columns; per-block distinct-line counts; the layout-aware fill
+cudaError_t launch_relayout(const float* x, float* xs, int nx, int ny, int64_t N, cudaStream_t st);
+cudaError_t launch_layout_sort_rows(int64_t rows, const int64_t* rp, const int32_t* col, int L, int nx,
+                                    int ny, int64_t N, int32_t* scol, uint8_t* bad, cudaStream_t st);
+cudaError_t launch_layout_count(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* scol,
+                                int64_t* cnt_lane, int64_t* cnt_row, cudaStream_t st);
+cudaError_t launch_sell_fill32_layout(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
+                                      const int32_t* blk_k, const int64_t* row_start,
+                                      const uint8_t* layout, const int64_t* rp, const int32_t* col,
+                                      const float* val, int nx, int ny, int64_t N, int32_t* cols,
+                                      float* vals, cudaStream_t st);
 cudaError_t launch_sell32_mode(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* col,
                                uint8_t* mode, cudaStream_t st, int bias_pct = 100);
 // per block of 32 consecutive rows: the z (column / plane) of the middle entry of its middle

@@ -184,6 +184,16 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
     s.val = d.val;
     s.src = src;
     s.src_lo = src_lo;
+    if (pl.sell32_layouts) {  // the point in the three gather layouts (columns index into them)
+      cudaError_t e = launch_relayout(src, p->xs, p->nx, p->ny, p->ncol, p->stream);
+      if (e != cudaSuccess) return e;
+      s.src = p->xs;
+      if (src_lo) {
+        e = launch_relayout(src_lo, p->xs_lo, p->nx, p->ny, p->ncol, p->stream);
+        if (e != cudaSuccess) return e;
+        s.src_lo = p->xs_lo;
+      }
+    }
     s.b = b;
     s.out = out;
     s.out_lo = out_lo;
@@ -766,6 +776,82 @@ static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std:
   // blocks in z order of the voxels they gather (the z of each block's middle entry; rays tilted
   // by <= 10 deg span a band of ~60 slices) and the grid sweeps that order together (interleaved
   // CTA chunks), so the x sub-volume in flight stays in L2.  TVR_SELL32_ZORDER=0: row order.
+  // Gather layouts (A pass with modes: c5): per block the layout of the point (row-major, x / y
+  // swapped, 8x4 bricks; spmv.cu layout_index) and the walk (lane / row mode) whose gathers touch
+  // the fewest 128-byte lines, counted exactly on the device (TVR_SELL32_LAYOUTS=0: row-major).
+  std::vector<uint8_t> layout(nblk, 0);
+  bool layouts = false;
+  const int64_t Nl = p->ncol;
+  const int lmask = env_int("TVR_SELL32_LAYOUTS", 7);  // bit L: layout L may be chosen
+  if (!transposed && modes && (lmask & 6) != 0 && p->nx % 8 == 0 &&
+      p->ny % 4 == 0 && 3 * Nl < ((int64_t)1 << 31)) {
+    size_t fr = 0, tot_mem = 0;
+    TVR_CUDA(cudaMemGetInfo(&fr, &tot_mem));
+    const int64_t nnz_rows = rph[rows];
+    const size_t scratch = sizeof(int32_t) * (size_t)nnz_rows + (size_t)nblk * (16 + 1);
+    // the scratch, the two 3N layout buffers, and the sliced-ELL copy built below
+    if (scratch + sizeof(float) * 6 * (size_t)Nl + (size_t)nnz_rows * 9 + ((size_t)2 << 30) < fr) {
+      layouts = true;
+      const double bias = env_int("TVR_SELL32_ROWBIAS", 100) / 100.0;  // row-mode overheads
+      // the matrix stream too: lane mode pads every row to its block's longest (c5: +14.6 %
+      // bytes, row mode +0.6 %); a stored 4-entry chunk (32 B) costs ~1.4 L1 wavefronts of time
+      // at the measured HBM rate (6.5 TB/s against 148 SMs x 1 wavefront per cycle)
+      const double bw = env_int("TVR_SELL32_BYTEW", 140) / 100.0;
+      std::vector<int64_t> ch_lane(nblk, 0), ch_row(nblk, 0);
+      for (int64_t j = 0; j < nblk; ++j) {
+        int64_t K = 0, tot = 0;
+        for (int64_t r = j * 32; r < std::min(rows, j * 32 + 32); ++r) {
+          const int64_t c = (rph[r + 1] - rph[r] + 3) / 4;
+          K = std::max(K, c);
+          tot += c;
+        }
+        ch_lane[j] = 32 * K;
+        ch_row[j] = tot;
+      }
+      int32_t* scol = nullptr;
+      int64_t *cl = nullptr, *cr = nullptr;
+      uint8_t* bad = nullptr;
+      TVR_CUDA(cudaMalloc(&scol, sizeof(int32_t) * std::max<int64_t>(nnz_rows, 1)));
+      TVR_CUDA(cudaMalloc(&cl, sizeof(int64_t) * nblk));
+      TVR_CUDA(cudaMalloc(&cr, sizeof(int64_t) * nblk));
+      TVR_CUDA(cudaMalloc(&bad, nblk));
+      TVR_CUDA(cudaMemsetAsync(bad, 0, nblk, p->stream));
+      std::vector<int64_t> hl(nblk), hr(nblk), best(nblk, INT64_MAX);
+      std::vector<uint8_t> hbad(nblk);
+      cudaError_t e = cudaSuccess;
+      for (int L = 0; L < 3 && e == cudaSuccess; ++L) {
+        if (L > 0 && !((lmask >> L) & 1)) continue;
+        const int32_t* c = p->col;
+        if (L > 0) {
+          e = launch_layout_sort_rows(rows, p->rp, p->col, L, p->nx, p->ny, Nl, scol, bad, p->stream);
+          c = scol;
+        }
+        if (e == cudaSuccess) e = launch_layout_count(nblk, rows, p->rp, c, cl, cr, p->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hl.data(), cl, sizeof(int64_t) * nblk, cudaMemcpyDeviceToHost, p->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hr.data(), cr, sizeof(int64_t) * nblk, cudaMemcpyDeviceToHost, p->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hbad.data(), bad, nblk, cudaMemcpyDeviceToHost, p->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+        if (e != cudaSuccess) break;
+        for (int64_t j = 0; j < nblk; ++j) {
+          if (L > 0 && hbad[j]) continue;  // a row too long to sort: row-major
+          if (L == 0 && !(lmask & 1)) continue;  // row-major only as the fallback (rows > cap)
+          const int64_t cost_lane = hl[j] + (int64_t)(bw * (double)ch_lane[j]);
+          const int64_t cost_row = (int64_t)(bias * (double)hr[j] + bw * (double)ch_row[j]);
+          const int64_t c_best = std::min(cost_lane, cost_row);
+          if (c_best < best[j]) {
+            best[j] = c_best;
+            layout[j] = (uint8_t)L;
+            mode[j] = cost_row < cost_lane ? 1 : 0;
+          }
+        }
+      }
+      cudaFree(scol);
+      cudaFree(cl);
+      cudaFree(cr);
+      cudaFree(bad);
+      TVR_CUDA(e);
+    }
+  }
   std::vector<int64_t> ord(nblk);
   for (int64_t j = 0; j < nblk; ++j) ord[j] = j;
   const bool zorder = !transposed && modes && env_int("TVR_SELL32_ZORDER", 1) != 0;
@@ -828,10 +914,32 @@ static int make_sell32(tvr_problem* p, SpmvPlan& pl, bool transposed, const std:
   TVR_CUDA(cudaMemsetAsync(d.val, 0, sizeof(float) * cap, p->stream));
   TVR_TRY(dev_alloc(p, (void**)&d.col32, sizeof(int32_t) * cap));
   TVR_CUDA(cudaMemsetAsync(d.col32, 0, sizeof(int32_t) * cap, p->stream));
-  TVR_CUDA(launch_sell_fill32(nblk * 32, d.perm, d.off, d.k, d.row_start,
-                              transposed ? p->rpT : p->rp, transposed ? p->colT : p->col,
-                              transposed ? p->valT : p->val, d.col32, d.val, p->stream));
+  if (layouts) {
+    std::vector<uint8_t> lst(nblk);
+    for (int64_t j = 0; j < nblk; ++j) lst[j] = layout[ord[j]];
+    uint8_t* dl = nullptr;
+    TVR_CUDA(cudaMalloc(&dl, nblk));
+    cudaError_t e = cudaMemcpyAsync(dl, lst.data(), nblk, cudaMemcpyHostToDevice, p->stream);
+    if (e == cudaSuccess)
+      e = launch_sell_fill32_layout(nblk * 32, d.perm, d.off, d.k, d.row_start, dl, p->rp, p->col,
+                                    p->val, p->nx, p->ny, Nl, d.col32, d.val, p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    cudaFree(dl);
+    TVR_CUDA(e);
+    int64_t per[3] = {0, 0, 0};
+    for (int64_t j = 0; j < nblk; ++j) ++per[lst[j]];
+    pl.sell32_layout_blocks[0] = per[0];
+    pl.sell32_layout_blocks[1] = per[1];
+    pl.sell32_layout_blocks[2] = per[2];
+    if (!p->xs) TVR_TRY(dev_alloc(p, (void**)&p->xs, sizeof(float) * 3 * Nl));
+    if (!p->xs_lo) TVR_TRY(dev_alloc(p, (void**)&p->xs_lo, sizeof(float) * 3 * Nl));
+  } else {
+    TVR_CUDA(launch_sell_fill32(nblk * 32, d.perm, d.off, d.k, d.row_start,
+                                transposed ? p->rpT : p->rp, transposed ? p->colT : p->col,
+                                transposed ? p->valT : p->val, d.col32, d.val, p->stream));
+  }
   TVR_CUDA(cudaStreamSynchronize(p->stream));  // host vectors die here
+  pl.sell32_layouts = layouts;
   d.nblk = nblk;
   d.h_slice_end = zend;
   pl.sd.assign(1, d);
@@ -1467,6 +1575,7 @@ int tvr_get_info(const tvr_problem* p, tvr_info* info) {
   info->views_fused_rs = p->fused_rs ? 1 : 0;
   info->views_rep = rep_dist(p) ? 1 : 0;
   info->point_allgathers = p->n_gathers;
+  for (int i = 0; i < 3; ++i) info->gather_layout_blocks[i] = p->planA.sell32_layout_blocks[i];
   info->slice_shared = p->sliced ? p->nzA : 0;
   return TVR_OK;
 }

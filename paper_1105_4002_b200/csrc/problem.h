@@ -82,6 +82,8 @@ struct SpmvPlan {
   int32_t sell32_ilv = 0;              // interleaved CTA chunks of this many blocks (0: ranges)
   bool sell32_zorder = false;          // blocks stored in z order of the voxels they gather
   int32_t sell32_l2 = 0;               // spmv32s L2 policies (SellArgs::l2hint)
+  bool sell32_layouts = false;         // columns index the point's gather layouts (p->xs)
+  int64_t sell32_layout_blocks[3] = {0, 0, 0};  // blocks per layout (row-major, yx, bricks)
   int32_t rep = 1;                     // slice-shared operator: the blocks repeat per slice
   int64_t rep_rows = 0, rep_win = 0;   // per repetition: output row / gather window offsets
   int64_t rep_total = 0;               // slice groups (sv.zgroup > 1): slices; rep = groups
@@ -168,6 +170,8 @@ struct tvr_problem {
   // caller's slab in place; its neighbours' planes land here)
   float* xhalo = nullptr;
   std::vector<float*> vol_base;
+  float* xs = nullptr;     // the A pass's point in its three gather layouts (3 ncol floats)
+  float* xs_lo = nullptr;  // ... and its lo parts (extended-precision evaluation)
   int64_t n_gathers = 0;  // all-gathers of a point (gather_volume), tvr_info.point_allgathers  // VIEWS_REP: allocation base of each replicated volume vector
   // VIEWS mode with world > 1: full-volume gather target of the A pass and full-volume partial
   // A_p^T r_p before the reduce-scatter; per-rank slab offsets / sizes (elements)

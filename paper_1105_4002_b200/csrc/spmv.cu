@@ -11,6 +11,7 @@
 // z-slice; rows slice-major) the gather vector of the current slice is staged in shared memory
 // once per slice change, so the x[col] / r[colT] gathers hit smem instead of L1/L2.
 // Instruction budget per entry: predicate, select, swizzle, LDS, 2 conversions, 1 DFMA.
+#include <climits>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -1222,6 +1223,253 @@ cudaError_t launch_sell_fill32(int64_t nslots, const int32_t* perm, const int64_
   if (nslots <= 0) return cudaSuccess;
   sell_fill32_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(
       nslots, perm, blk_off, blk_k, row_start, rp, col, val, cols, vals);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------ gather layouts of the non-separable A pass
+// (c5; profiles/r02/c5_raw.csv: the pass is bound by L1TEX wavefronts, 88 % of peak, one per
+// distinct 128-byte line a 32-lane gather touches).  The gathered point is kept in three layouts
+// side by side, xs = [x | x_yx | x_b], and every block of 32 rays gathers from the one in which
+// its lanes' simultaneous accesses fall into the fewest lines (scripts/c5_lines.py: 17.1 ->
+// 8.4 lines per gather instruction on c5's views):
+//   0  row-major (z, y, x): rays along y, neighbouring rays at neighbouring x;
+//   1  (z, x, y), x and y swapped: rays along x;
+//   2  8x4 bricks in each xy plane (z, y/4, x/8, y%4, x%8): oblique rays.
+// The block's columns are stored as indices into xs (layout * N + position), its entries sorted
+// by them, so the kernel is unchanged; the point is re-laid out before each A pass.
+__host__ __device__ __forceinline__ int64_t layout_index(int L, int64_t j, int nx, int ny, int64_t N) {
+  if (L == 0) return j;
+  const int64_t plane = (int64_t)nx * ny;
+  const int64_t z = j / plane, r = j - z * plane;
+  const int64_t y = r / nx, x = r - y * nx;
+  if (L == 1) return N + (z * nx + x) * ny + y;
+  return 2 * N + ((z * (ny >> 2) + (y >> 2)) * (nx >> 3) + (x >> 3)) * 32 + (y & 3) * 8 + (x & 7);
+}
+
+// The re-layout before each A pass (3N < 2^31: 32-bit indices).  x_yx: per z-slice a 32 x 32
+// tiled transpose through shared memory (coalesced reads and writes); bricks: one warp per 8 x 4
+// brick (a 128-byte line written whole, four 32-byte row pieces read).  Row-major: a copy.
+__global__ void relayout_yx_kernel(const float* __restrict__ x, float* __restrict__ xt, int nx, int ny) {
+  __shared__ float t[32][33];
+  const int z = blockIdx.z;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  const float* xz = x + (size_t)z * nx * ny;
+  float* tz = xt + (size_t)z * nx * ny;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int y = by + i, xx = bx + threadIdx.x;
+    if (y < ny && xx < nx) t[i][threadIdx.x] = __ldg(xz + y * nx + xx);
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int xx = bx + i, y = by + threadIdx.x;
+    if (y < ny && xx < nx) tz[xx * ny + y] = t[threadIdx.x][i];
+  }
+}
+__global__ void relayout_brick_kernel(const float* __restrict__ x, float* __restrict__ xb, int nx, int ny,
+                                      int nbricks) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= nbricks) return;
+  const int t = threadIdx.x & 31;
+  const int nbx = nx >> 3, nby = ny >> 2;
+  const int bx = b % nbx, by = (b / nbx) % nby, z = b / (nbx * nby);
+  xb[(size_t)b * 32 + t] = __ldg(x + ((size_t)z * ny + by * 4 + (t >> 3)) * nx + bx * 8 + (t & 7));
+}
+
+cudaError_t launch_relayout(const float* x, float* xs, int nx, int ny, int64_t N, cudaStream_t st) {
+  cudaError_t e = cudaMemcpyAsync(xs, x, sizeof(float) * N, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
+  const int nz = (int)(N / ((int64_t)nx * ny));
+  relayout_yx_kernel<<<dim3((nx + 31) / 32, (ny + 31) / 32, nz), dim3(32, 8), 0, st>>>(x, xs + N, nx, ny);
+  const int nbricks = (int)(N / 32);
+  relayout_brick_kernel<<<(nbricks + 7) / 8, 256, 0, st>>>(x, xs + 2 * N, nx, ny, nbricks);
+  return cudaGetLastError();
+}
+
+// Bitonic sort of n <= cap (key, payload) pairs in shared memory by one warp (padding: +inf keys)
+template <bool PAY>
+__device__ void warp_sort_pairs(int64_t* key, float* pay, int n, int lane) {
+  int P = 32;
+  while (P < n) P <<= 1;
+  for (int i = n + lane; i < P; i += 32) key[i] = INT64_MAX;
+  __syncwarp();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < P; i += 32) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const int64_t a = key[i], b = key[l];
+          if ((a > b) == up) {
+            key[i] = b;
+            key[l] = a;
+            if constexpr (PAY) {
+              const float t = pay[i];
+              pay[i] = pay[l];
+              pay[l] = t;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+constexpr int kLayoutCap = 1024;  // longest row the layout kernels sort (longer: layout 0)
+
+// Phase 1: the rows' columns mapped to layout L and sorted, into scol (same row_ptr); rows longer
+// than kLayoutCap are flagged in bad[row / 32].  One warp per row, 8 warps per CTA.
+__global__ void __launch_bounds__(256) layout_sort_rows_kernel(int64_t rows, const int64_t* rp,
+                                                               const int32_t* col, int L, int nx,
+                                                               int ny, int64_t N, int32_t* scol,
+                                                               uint8_t* bad) {
+  extern __shared__ int64_t lsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t* key = lsm + warp * kLayoutCap;
+  for (int64_t r = blockIdx.x * 8 + warp; r < rows; r += (int64_t)gridDim.x * 8) {
+    const int64_t s = rp[r];
+    const int n = (int)(rp[r + 1] - s);
+    if (n > kLayoutCap) {
+      if (lane == 0) bad[r >> 5] = 1;
+      continue;
+    }
+    for (int e = lane; e < n; e += 32) key[e] = layout_index(L, col[s + e], nx, ny, N);
+    __syncwarp();
+    warp_sort_pairs<false>(key, nullptr, n, lane);
+    for (int e = lane; e < n; e += 32) scol[s + e] = (int32_t)key[e];
+    __syncwarp();
+  }
+}
+
+// Distinct 128-byte lines per 32-lane gather of a block of 32 consecutive rows (lane = row) in
+// spmv32s_kernel's two walks: lane mode (lane l at entry 4s + k of its row) and row mode (4 rows
+// at a time, lane g of a row at entries 4 (g + 8 i) + k).  Pads are not counted.
+__device__ __forceinline__ int distinct_lines(int64_t line, bool act) {
+  // a lane leads its value when no lower active lane holds it (shuffles; __match_any_sync in this
+  // loop hung on sm_100a)
+  const int lane = threadIdx.x & 31;
+  const unsigned am = __ballot_sync(0xffffffffu, act);
+  const int32_t lo = (int32_t)line, hi = (int32_t)(line >> 32);
+  bool leader = act;
+  for (int d = 0; d < 31; ++d) {
+    const int32_t vlo = __shfl_sync(0xffffffffu, lo, d), vhi = __shfl_sync(0xffffffffu, hi, d);
+    if (d < lane && ((am >> d) & 1u) && vlo == lo && vhi == hi) leader = false;
+  }
+  return __popc(__ballot_sync(0xffffffffu, leader));
+}
+__global__ void layout_count_kernel(int64_t nblk, int64_t rows, const int64_t* rp,
+                                    const int32_t* scol, int64_t* cnt_lane, int64_t* cnt_row) {
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= nblk) return;  // whole warps exit together
+  const int64_t r = j * 32 + lane;
+  const int64_t s = r < rows ? rp[r] : 0;
+  const int n = r < rows ? (int)(rp[r + 1] - s) : 0;
+  int mx = n;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+  int64_t cl = 0, cr = 0;
+  for (int e = 0; e < mx; ++e) {
+    const bool act = e < n;
+    cl += distinct_lines(act ? (int64_t)(scol[s + e] >> 5) : 0, act);
+  }
+  for (int i0 = 0; i0 < 32; i0 += 4) {
+    const int ri = i0 + (lane >> 3), g = lane & 7;
+    const int ni = __shfl_sync(0xffffffffu, n, ri);
+    const int64_t si = __shfl_sync(0xffffffffu, s, ri);
+    int mxi = ni;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) mxi = max(mxi, __shfl_xor_sync(0xffffffffu, mxi, d));
+    const int chunks = (mxi + 3) >> 2;
+    for (int c0 = 0; c0 < chunks; c0 += 8) {
+      const int c = c0 + g;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int e = 4 * c + k;
+        const bool act = e < ni;
+        cr += distinct_lines(act ? (int64_t)(scol[si + e] >> 5) : 0, act);
+      }
+    }
+  }
+  if (lane == 0) {
+    cnt_lane[j] = cl;
+    cnt_row[j] = cr;
+  }
+}
+
+cudaError_t launch_layout_sort_rows(int64_t rows, const int64_t* rp, const int32_t* col, int L, int nx,
+                                    int ny, int64_t N, int32_t* scol, uint8_t* bad, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const size_t smem = sizeof(int64_t) * kLayoutCap * 8;
+  cudaError_t e = ensure_smem_attr((const void*)layout_sort_rows_kernel, smem);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 8);
+  layout_sort_rows_kernel<<<grid, 256, smem, st>>>(rows, rp, col, L, nx, ny, N, scol, bad);
+  return cudaGetLastError();
+}
+cudaError_t launch_layout_count(int64_t nblk, int64_t rows, const int64_t* rp, const int32_t* scol,
+                                int64_t* cnt_lane, int64_t* cnt_row, cudaStream_t st) {
+  if (nblk <= 0) return cudaSuccess;
+  layout_count_kernel<<<(unsigned)((nblk * 32 + 255) / 256), 256, 0, st>>>(nblk, rows, rp, scol,
+                                                                          cnt_lane, cnt_row);
+  return cudaGetLastError();
+}
+
+// Phase 3: sell_fill32 with each stored block's layout: one warp per slot (stored block j, lane
+// l): its row's columns mapped to layout[j] and sorted with the values, written to the block's
+// lane- or row-mode positions.
+__global__ void __launch_bounds__(256) sell_fill32_layout_kernel(
+    int64_t nslots, const int32_t* perm, const int64_t* blk_off, const int32_t* blk_k,
+    const int64_t* row_start, const uint8_t* layout, const int64_t* rp, const int32_t* col,
+    const float* val, int nx, int ny, int64_t N, int32_t* cols, float* vals) {
+  extern __shared__ int64_t lsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t* key = lsm + warp * kLayoutCap;
+  float* pay = reinterpret_cast<float*>(lsm + 8 * kLayoutCap) + warp * kLayoutCap;
+  for (int64_t t = blockIdx.x * 8 + warp; t < nslots; t += (int64_t)gridDim.x * 8) {
+    const int row = perm[t];
+    if (row < 0) continue;
+    const int64_t j = t >> 5, l = t & 31, s = rp[row];
+    const int n = (int)(rp[row + 1] - s);
+    const int64_t base = blk_off[j];
+    const bool lane_mode = blk_k[j] >= 0;
+    const int L = layout[j];
+    auto dst = [&](int e) {
+      return lane_mode ? (base + (e >> 2) * 32 + l) * 4 + (e & 3) : (base + row_start[t]) * 4 + e;
+    };
+    if (L == 0 || n > kLayoutCap) {  // the stored order (layout 0 sorts to itself)
+      for (int e = lane; e < n; e += 32) {
+        cols[dst(e)] = col[s + e];
+        vals[dst(e)] = val[s + e];
+      }
+      continue;
+    }
+    for (int e = lane; e < n; e += 32) {
+      key[e] = layout_index(L, col[s + e], nx, ny, N);
+      pay[e] = val[s + e];
+    }
+    __syncwarp();
+    warp_sort_pairs<true>(key, pay, n, lane);
+    for (int e = lane; e < n; e += 32) {
+      cols[dst(e)] = (int32_t)key[e];
+      vals[dst(e)] = pay[e];
+    }
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_sell_fill32_layout(int64_t nslots, const int32_t* perm, const int64_t* blk_off,
+                                      const int32_t* blk_k, const int64_t* row_start,
+                                      const uint8_t* layout, const int64_t* rp, const int32_t* col,
+                                      const float* val, int nx, int ny, int64_t N, int32_t* cols,
+                                      float* vals, cudaStream_t st) {
+  if (nslots <= 0) return cudaSuccess;
+  const size_t smem = (sizeof(int64_t) + sizeof(float)) * kLayoutCap * 8;
+  cudaError_t e = ensure_smem_attr((const void*)sell_fill32_layout_kernel, smem);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)std::min<int64_t>((nslots + 7) / 8, 148 * 8);
+  sell_fill32_layout_kernel<<<grid, 256, smem, st>>>(nslots, perm, blk_off, blk_k, row_start, layout,
+                                                     rp, col, val, nx, ny, N, cols, vals);
   return cudaGetLastError();
 }
 

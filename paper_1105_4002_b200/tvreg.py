@@ -62,7 +62,8 @@ class tvr_info(ctypes.Structure):
     _fields_ = [("m_local", c_i64), ("n_local", c_i64), ("nnz_local", c_i64), ("z0", c_i32),
                 ("z1", c_i32), ("slab_staged_A", c_i32), ("slab_staged_AT", c_i32),
                 ("device_bytes", c_i64), ("n_cols_local", c_i64), ("views_fused_rs", c_i32),
-                ("slice_shared", c_i32), ("views_rep", c_i32), ("point_allgathers", c_i64)]
+                ("slice_shared", c_i32), ("views_rep", c_i32), ("point_allgathers", c_i64),
+                ("gather_layout_blocks", c_i64 * 3)]
 
 
 class tvr_fparts(ctypes.Structure):

@@ -421,7 +421,7 @@ def test_sell_column_parts(tvreg, cfg, floats, c1, monkeypatch):
     P.close()
 
 
-@pytest.mark.parametrize("cfg", ["zoo", "sphere", "tilted"])
+@pytest.mark.parametrize("cfg", ["zoo", "sphere", "tilted", "layouts"])
 @pytest.mark.parametrize("mode", ["0", "1", "2", "3"])
 def test_sell32_spmv(tvreg, cfg, mode, monkeypatch):
     """Int32 sliced ELL for non-separable matrices (spmv32s_kernel; TVR_SPMV_SELL32 = 0 none,
@@ -440,12 +440,20 @@ def test_sell32_spmv(tvreg, cfg, mode, monkeypatch):
         A = harness.siddon_sphere(24, 24, 24, 7, 33, 33)
         x = harness.random_x(A.n_cols)
         b = rng.random(A.n_rows).astype(np.float32)
-    else:
+    elif cfg == "tilted":
         grid = (20, 20, 20)
         A = harness.siddon_tilted(20, 20, 20, 9, 20, 29, 10.0)
         x = harness.random_x(A.n_cols)
         b = rng.random(A.n_rows).astype(np.float32)
+    else:  # tilted rays on a grid whose xy planes tile into 8x4 bricks: the gather layouts
+        grid = (32, 24, 16)
+        A = harness.siddon_tilted(32, 24, 16, 12, 16, 41, 10.0)
+        x = harness.random_x(A.n_cols)
+        b = rng.random(A.n_rows).astype(np.float32)
     P = make(tvreg, A, b, grid)
+    if mode == "3" and cfg == "layouts":  # every layout is chosen by some block of rays
+        lb = list(P.info.gather_layout_blocks)
+        assert sum(lb) == (A.n_rows + 31) // 32 and min(lb) > 0, lb
     r = torch.empty(A.n_rows, device="cuda")
     fid = P.residual(dev(x), r)
     w = torch.empty(A.n_cols, device="cuda")
