@@ -275,3 +275,35 @@ def test_solver_parity_c4_recipe_desk(tvreg, solver, alpha):
     res = getattr(P, f"solve_{solver}")(x, max_iters=20000, eps=1e-6)
     assert res.converged and ref.converged
     _check_parity(Po, x.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("solver", ["upn", "gp"])
+def test_solver_parity_gather_layouts_extended(tvreg, solver, monkeypatch):
+    """Non-separable rays (c5's geometry at desk size) through the int32 sliced ELL with block
+    modes and the gather layouts (row-major / x-y swapped / bricks), with the extended-precision
+    evaluation on from the start (the A pass also gathers the lo parts from the re-laid-out lo
+    vector): the converged reconstruction against the oracle's."""
+    monkeypatch.setenv("TVR_SPMV_SELL32", "3")
+    monkeypatch.setenv("TVR_EXT_EVAL_AT", "1")
+    grid = (32, 24, 16)
+    A = harness.siddon_tilted(*grid, 12, 16, 41, 10.0)
+    xt = harness.phantom(*grid, 4)
+    b = harness.simulate_data(A, xt)
+    alpha, tau = 0.01, 1e-2
+    Po = oracle.Problem(A.row_ptr, A.col, A.val, b, grid, alpha, tau, 0.0, np.inf, nthreads=4)
+    P = tvreg.Problem(A.row_ptr, A.col, A.val, b, grid, alpha, tau, 0.0, np.inf)
+    lb = list(P.info.gather_layout_blocks)
+    assert min(lb) > 0, lb
+    x = torch.zeros(A.n_cols, device="cuda")
+    if solver == "upn":
+        ref = oracle.upn(Po, np.zeros(A.n_cols), eps=1e-6, max_iters=20000)
+        res = P.solve_upn(x, max_iters=20000, eps=1e-6)
+        assert res.converged and ref.converged
+        _check_parity(Po, x.cpu().numpy(), ref)
+    else:  # GP (Eq. (6)): 150 iterations follow the oracle's trajectory
+        ref = oracle.gp(Po, np.zeros(A.n_cols), eps=0.0, max_iters=150)
+        res = P.solve_gp(x, max_iters=150, eps=0.0, hist_cap=200)
+        h, oh = res.history, ref.history
+        assert len(h) == 150
+        for k in range(150):
+            assert abs(h[k]["f"] - oh[k]["f"]) <= 1e-6 * abs(oh[k]["f"])
