@@ -155,6 +155,12 @@ typedef struct {
   int64_t gather_layout_blocks[3];     /* non-separable A pass (int32 sliced ELL with block
                                           modes): 32-ray blocks gathering from the point laid out
                                           row-major, with x / y swapped, in 8x4 bricks */
+  int64_t dist_graph_solves;           /* solves run as one CUDA graph WITH the NCCL exchanges
+                                          captured in it (device control on an NCCL
+                                          communicator, tvr_set_control) */
+  int64_t dist_graph_exchanges;        /* ... and the captured exchange groups those graphs
+                                          executed (one per line-search / BT trial, one per
+                                          accepted gradient) */
 } tvr_info;
 int tvr_get_info(const tvr_problem* p, tvr_info* info);
 
@@ -293,14 +299,26 @@ int64_t tvr_launch_count(const tvr_problem* p, int reset);
  * / BT trial runs on the host after a device->host fetch of the pass reductions.  DEVICE: a whole
  * solve is one CUDA graph with conditional while / if nodes; single-thread control kernels take
  * the same decisions in the same fp64 arithmetic (identical iterates), the host waits once; the
- * state rotates by device copies.  DEVICE applies to one-GPU problems (world == 1; others use
- * HOST).  AUTO (default): DEVICE where launch and synchronisation latency is a visible part of
+ * state rotates by device copies.  With an NCCL communicator (world > 1) DEVICE captures the
+ * exchanges in the graph as well: the halo send / recv of the gradient and the scalar all-gather
+ * are one NCCL group per decision point, the gathered partials are summed in rank order by a
+ * device kernel (the host sum's arithmetic), trial / momentum halo planes are recomputed from
+ * device-side step parameters — no host synchronisation per trial.  It
+ * is opt-in there (AUTO keeps HOST at world > 1; the in-process thread communicator synchronises
+ * on the host and always uses HOST).  TVR_DIST_GRAPH_FORCE=1 takes this path on a one-rank NCCL
+ * communicator too (tests).  AUTO (default): DEVICE where launch and synchronisation latency is a visible part of
  * an iteration — GPBB below 2^28 matrix entries (c1 -16 % per iteration; c2 equal), UPN below 2^24
  * (c1 -11 %; its extended-precision graph is slower than host control at c2) — HOST above (c3:
  * the state copies cost 1-2 %).  The environment variable
  * TVR_CONTROL=host|device overrides. */
 enum { TVR_CONTROL_HOST = 0, TVR_CONTROL_DEVICE = 1, TVR_CONTROL_AUTO = 2 };
 int tvr_set_control(tvr_problem* p, int mode);
+
+/* Inspection hook of the distributed device control: out_dev[s] = sum over r (in rank order,
+ * starting from +0.0) of gathered_dev[r * n + s], the kernel the solver graphs run after the
+ * scalar all-gather (fixed-order fp64 sums).  Device pointers; synchronises
+ * cuda_stream (NULL: the default stream).  TVR_E_ARG on NULL / non-positive sizes. */
+int tvr_rank_sum(const double* gathered_dev, int world, int n, double* out_dev, void* cuda_stream);
 
 /* In-process thread communicator (testing the multi-rank paths on one GPU): ranks are host
  * threads of one process, each with its own tvr_problem (same or different devices); every

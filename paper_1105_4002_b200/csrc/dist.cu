@@ -149,36 +149,39 @@ int halo_exchange(tvr_problem* p, float* v) {
 static int fill_lo(const tvr_problem* p) { return rep_dist(p) ? p->z0 : (p->z0 > 0 ? 1 : 0); }
 static int fill_hi(const tvr_problem* p) { return rep_dist(p) ? p->nz - p->z1 : (p->z1 < p->nz ? 1 : 0); }
 
-int halo_fill_trial(tvr_problem* p, const float* x, const float* g, double s, float* v) {
+int halo_fill_trial(tvr_problem* p, const float* x, const float* g, double s, float* v,
+                    const double* dparam) {
   if (p->world <= 1) return TVR_OK;
   TVR_CUDA(launch_halo_fill_trial(x, g, s, p->lo, p->hi, p->plane, p->nzl, fill_lo(p),
-                                  fill_hi(p), v, p->stream));
+                                  fill_hi(p), v, p->stream, dparam));
   p->launches++;
   return TVR_OK;
 }
 
-int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double beta, float* y) {
+int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double beta, float* y,
+                       const double* dparam) {
   if (p->world <= 1) return TVR_OK;
   TVR_CUDA(launch_halo_fill_momentum(x1, x0, beta, p->plane, p->nzl, fill_lo(p), fill_hi(p), y,
-                                     p->stream));
+                                     p->stream, dparam));
   p->launches++;
   return TVR_OK;
 }
 
 int halo_fill_trial_x(tvr_problem* p, const float* x, const float* x_lo, const float* g, double s,
-                      float* v, float* v_lo) {
+                      float* v, float* v_lo, const double* dparam) {
   if (p->world <= 1) return TVR_OK;
   TVR_CUDA(launch_halo_fill_trial_x(x, x_lo, g, s, p->lo, p->hi, p->plane, p->nzl, fill_lo(p),
-                                    fill_hi(p), v, v_lo, p->stream));
+                                    fill_hi(p), v, v_lo, p->stream, dparam));
   p->launches++;
   return TVR_OK;
 }
 
 int halo_fill_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, const float* x0,
-                         const float* x0_lo, double beta, float* y, float* y_lo) {
+                         const float* x0_lo, double beta, float* y, float* y_lo,
+                         const double* dparam) {
   if (p->world <= 1) return TVR_OK;
   TVR_CUDA(launch_halo_fill_momentum_x(x1, x1_lo, x0, x0_lo, beta, p->plane, p->nzl, fill_lo(p),
-                                       fill_hi(p), y, y_lo, p->stream));
+                                       fill_hi(p), y, y_lo, p->stream, dparam));
   p->launches++;
   return TVR_OK;
 }
@@ -205,6 +208,51 @@ int halo_exchange_fetch(tvr_problem* p, float* v, int nslots) {
   TVR_NCCL(ncclAllGather(p->dscal, p->dgather, (size_t)nslots, ncclDouble, comm, p->stream));
   TVR_NCCL(ncclGroupEnd());
   return reduce_gathered_scalars(p, p->hscal, nslots);
+}
+
+// Device-side rank-ordered sum (solver graphs at world > 1): out[s] =
+// ((0 + all[0][s]) + all[1][s]) + ..., the host sum of reduce_gathered_scalars operation for
+// operation, so every rank's control kernels read bitwise the scalars the host controller sums.
+__global__ void rank_sum_kernel(const double* __restrict__ all, int world, int n,
+                                double* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  double acc = 0.0;
+  for (int r = 0; r < world; ++r) acc = __dadd_rn(acc, all[(size_t)r * n + s]);
+  out[s] = acc;
+}
+
+bool nccl_backend(const tvr_problem* p) { return p->comm && !local_of(p); }
+
+// The exchanges of halo_exchange_fetch without the host: the halo planes of v (nullable) and the
+// scalar all-gather in one NCCL group (VIEWS_REP: the in-place all-gather of v, then the scalars),
+// the rank-ordered sum on the device into p->dsum.  Enqueue only -- capturable into the solver
+// graphs.  Runs the all-gather on a one-rank communicator too (the forced path of the tests).
+int dist_scalars_dev(tvr_problem* p, float* v, int nslots) {
+  NvtxRange nv("halo_exchange + scalar_allgather (device sum)");
+  ncclComm_t comm = nccl_of(p);
+  const size_t cnt = (size_t)p->plane;
+  if (v && rep_dist(p)) {
+    TVR_TRY(replicate_volume(p, v));
+    v = nullptr;
+  }
+  TVR_NCCL(ncclGroupStart());
+  if (v && p->world > 1) {
+    if (p->rank > 0) {
+      TVR_NCCL(ncclSend(v, cnt, ncclFloat, p->rank - 1, comm, p->stream));
+      TVR_NCCL(ncclRecv(v - p->plane, cnt, ncclFloat, p->rank - 1, comm, p->stream));
+    }
+    if (p->rank < p->world - 1) {
+      TVR_NCCL(ncclSend(v + (int64_t)(p->nzl - 1) * p->plane, cnt, ncclFloat, p->rank + 1, comm, p->stream));
+      TVR_NCCL(ncclRecv(v + (int64_t)p->nzl * p->plane, cnt, ncclFloat, p->rank + 1, comm, p->stream));
+    }
+  }
+  TVR_NCCL(ncclAllGather(p->dscal, p->dgather, (size_t)nslots, ncclDouble, comm, p->stream));
+  TVR_NCCL(ncclGroupEnd());
+  rank_sum_kernel<<<1, 64, 0, p->stream>>>(p->dgather, p->world, nslots, p->dsum);
+  TVR_CUDA(cudaGetLastError());
+  p->launches++;
+  return TVR_OK;
 }
 
 // rank-ordered sum of the all-gathered scalars (p->dgather, world x n) into vals (host)
@@ -520,6 +568,15 @@ void dist_release(tvr_problem* p) {
 using namespace tvr;
 
 extern "C" {
+
+int tvr_rank_sum(const double* gathered_dev, int world, int n, double* out_dev, void* cuda_stream) {
+  if (!gathered_dev || !out_dev || world < 1 || n < 1) { set_error("tvr_rank_sum: bad arguments"); return TVR_E_ARG; }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  rank_sum_kernel<<<(n + 63) / 64, 64, 0, st>>>(gathered_dev, world, n, out_dev);
+  TVR_CUDA(cudaGetLastError());
+  TVR_CUDA(cudaStreamSynchronize(st));
+  return TVR_OK;
+}
 
 int tvr_nccl_unique_id_size(void) { return (int)sizeof(ncclUniqueId); }
 

@@ -220,18 +220,20 @@ cudaError_t launch_tv_grad_plain_x(const TVArgs& a, const float* x, const float*
                                    cudaStream_t st);
 cudaError_t launch_halo_fill_trial_x(const float* x, const float* x_lo, const float* g, double s,
                                      double lo, double hi, int64_t plane, int nzl, int n_lo,
-                                     int n_hi, float* v, float* v_lo, cudaStream_t st);
+                                     int n_hi, float* v, float* v_lo, cudaStream_t st,
+                                     const double* dparam = nullptr);
 cudaError_t launch_halo_fill_momentum_x(const float* x1, const float* x1_lo, const float* x0,
                                         const float* x0_lo, double beta, int64_t plane, int nzl,
                                         int n_lo, int n_hi, float* v, float* v_lo,
-                                        cudaStream_t st);
+                                        cudaStream_t st, const double* dparam = nullptr);
 int tv_num_blocks(int nx, int ny, int nzl);
 int tv_set_grid(int num_sms);  // size the persistent stencil grid for the current device
 cudaError_t launch_halo_fill_trial(const float* x, const float* g, double s, double lo, double hi,
                                    int64_t plane, int nzl, int n_lo, int n_hi, float* v,
-                                   cudaStream_t st);
+                                   cudaStream_t st, const double* dparam = nullptr);
 cudaError_t launch_halo_fill_momentum(const float* x1, const float* x0, double beta, int64_t plane,
-                                      int nzl, int n_lo, int n_hi, float* v, cudaStream_t st);
+                                      int nzl, int n_lo, int n_hi, float* v, cudaStream_t st,
+                                      const double* dparam = nullptr);
 
 cudaError_t build_transpose(int64_t m, int64_t n, int64_t nnz, const int64_t* rp,
                             const int32_t* col, const float* val, int64_t* rowT, int32_t* colT,

@@ -1157,6 +1157,10 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
                 "(tvr_nccl_comm_init or tvr_local_comm_create)");
       return TVR_E_ARG;
     }
+    if (p->world == 1 && p->comm && !valid_comm(p->comm)) {
+      set_error("tvr_create: nccl_comm is not a libtvreg communicator handle");
+      return TVR_E_ARG;
+    }
     if (p->world == 1 && (p->z0 != 0 || p->z1 != grid.nz)) {
       // one rank owns every slice: no neighbour would fill the halo planes of a partial slab
       set_error("tvr_create: a single rank (world == 1) must own every slice (z0 = 0, z1 = nz)");
@@ -1493,7 +1497,10 @@ static int create_impl(tvr_problem* p, const tvr_csr* A, const float* b_host, tv
   TVR_TRY(dev_alloc(p, (void**)&p->dscal, sizeof(double) * 64));
   TVR_CUDA(cudaMemsetAsync(p->dscal, 0, sizeof(double) * 64, p->stream));
   TVR_CUDA(cudaMallocHost((void**)&p->hscal, sizeof(double) * 64 * (std::max(1, p->world) + 1)));
-  if (p->world > 1) TVR_TRY(dev_alloc(p, (void**)&p->dgather, sizeof(double) * 64 * p->world));
+  if (p->world > 1 || p->comm) {
+    TVR_TRY(dev_alloc(p, (void**)&p->dgather, sizeof(double) * 64 * p->world));
+    TVR_TRY(dev_alloc(p, (void**)&p->dsum, sizeof(double) * 64));
+  }
   TVR_CUDA(cudaStreamSynchronize(p->stream));
   return TVR_OK;
 }
@@ -1575,6 +1582,8 @@ int tvr_get_info(const tvr_problem* p, tvr_info* info) {
   info->views_fused_rs = p->fused_rs ? 1 : 0;
   info->views_rep = rep_dist(p) ? 1 : 0;
   info->point_allgathers = p->n_gathers;
+  info->dist_graph_solves = p->n_dist_graph;
+  info->dist_graph_exchanges = p->n_dist_exch;
   for (int i = 0; i < 3; ++i) info->gather_layout_blocks[i] = p->planA.sell32_layout_blocks[i];
   info->slice_shared = p->sliced ? p->nzA : 0;
   return TVR_OK;

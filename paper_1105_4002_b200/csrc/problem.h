@@ -215,6 +215,8 @@ struct tvr_problem {
   int64_t launches = 0;
   double bytes_total = 0;  // algorithmic bytes of every pass launched
   double* dgather = nullptr;  // world x 64 scalars (dist)
+  double* dsum = nullptr;     // 64 scalars: rank-ordered sums taken on the device (solver graphs)
+  int64_t n_dist_graph = 0, n_dist_exch = 0;  // tvr_info.dist_graph_solves / _exchanges
 
   std::vector<void*> allocs;
   int64_t device_bytes = 0;
@@ -270,12 +272,21 @@ int halo_exchange(tvr_problem* p, float* v);
 // theirs land in lo (plane -1) and hi (plane nzl)
 int halo_exchange_to(tvr_problem* p, const float* v, float* lo, float* hi);
 // recompute the halo planes of a trial / momentum point from its inputs' halo planes
-int halo_fill_trial(tvr_problem* p, const float* x, const float* g, double s, float* v);
-int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double beta, float* y);
+// (dparam: the step / beta read on the device from dparam[0], as the stencil's device-control variants)
+int halo_fill_trial(tvr_problem* p, const float* x, const float* g, double s, float* v,
+                    const double* dparam = nullptr);
+int halo_fill_momentum(tvr_problem* p, const float* x1, const float* x0, double beta, float* y,
+                       const double* dparam = nullptr);
 int halo_fill_trial_x(tvr_problem* p, const float* x, const float* x_lo, const float* g, double s,
-                      float* v, float* v_lo);
+                      float* v, float* v_lo, const double* dparam = nullptr);
 int halo_fill_momentum_x(tvr_problem* p, const float* x1, const float* x1_lo, const float* x0,
-                         const float* x0_lo, double beta, float* y, float* y_lo);
+                         const float* x0_lo, double beta, float* y, float* y_lo,
+                         const double* dparam = nullptr);
+// NCCL communicator (not the in-process thread backend): its collectives are stream work only
+bool nccl_backend(const tvr_problem* p);
+// halo planes of v (nullable) + scalar all-gather + rank-ordered sum ON THE DEVICE into p->dsum;
+// enqueue only (capturable)
+int dist_scalars_dev(tvr_problem* p, float* v, int nslots);
 int dist_sum_scalars(tvr_problem* p, double* vals, int n);
 // halo_exchange(v) then fetch_scalars(nslots), with the halo send / recv and the scalar
 // all-gather in ONE NCCL group (one launch, one synchronisation) on the NCCL backend

@@ -233,6 +233,21 @@ int capture_body(tvr_problem* p, cudaGraph_t body, double* bytes, F&& f) {
   return TVR_OK;
 }
 
+// dst <- src for the library's volume vectors: with the halo planes (VIEWS_REP: the whole
+// replicated volume) when the copy replaces a pointer swap of vectors whose halos are read later
+int copy_vol(tvr_problem* p, float* dst, const float* src, bool with_halo) {
+  if (with_halo && p->world > 1) {
+    float *d0, *s0;
+    int64_t cnt;
+    vol_extent(p, dst, &d0, &cnt);
+    vol_extent(p, const_cast<float*>(src), &s0, &cnt);
+    TVR_CUDA(cudaMemcpyAsync(d0, s0, sizeof(float) * cnt, cudaMemcpyDeviceToDevice, p->stream));
+  } else {
+    TVR_CUDA(cudaMemcpyAsync(dst, src, sizeof(float) * p->n, cudaMemcpyDeviceToDevice, p->stream));
+  }
+  return TVR_OK;
+}
+
 struct GraphGuard {
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ex = nullptr;
@@ -244,9 +259,25 @@ struct GraphGuard {
 
 }  // namespace
 
+// The solver graphs carry the exchanges (dist_scalars_dev, the halo fills with device-side
+// parameters, the VIEWS collectives inside the passes) when the communicator is NCCL's: world > 1,
+// or a one-rank NCCL communicator with TVR_DIST_GRAPH_FORCE=1 (the path's test on one GPU).
+static bool dist_graph(const tvr_problem* p) {
+  if (!nccl_backend(p)) return false;
+  if (p->world > 1) return true;
+  const char* e = std::getenv("TVR_DIST_GRAPH_FORCE");
+  return e && *e == '1';
+}
+
 bool use_device_control(const tvr_problem* p, bool upn) {
-  if (p->world > 1) return false;
   const char* e = std::getenv("TVR_CONTROL");
+  if (p->world > 1) {
+    // captured NCCL exchanges: opt-in (no multi-GPU measurement behind an AUTO rule yet); the
+    // thread communicator synchronises on the host and cannot be captured
+    if (!nccl_backend(p)) return false;
+    if (e && *e) return std::string(e) == "device";
+    return p->control == TVR_CONTROL_DEVICE;
+  }
   if (e && *e) return std::string(e) == "device";
   // AUTO, by the stored matrix (the slice's, when slice-shared): GPBB below 2^28 entries (c1, c2:
   // device and host equal at c2, 0.708 / 0.709 ms per iteration); UPN below 2^24 (c1 -11 %; at c2
@@ -302,6 +333,9 @@ static int gpbb_device(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_
   TVR_CUDA(cudaGraphConditionalHandleCreate(&h.acc, body, 0, 0));
   const size_t vb = sizeof(float) * p->n, db = sizeof(float) * p->m;
   double bytes_ls = 0.0, bytes_acc = 0.0;
+  // world > 1 (NCCL): every decision reads the rank-ordered sums dist_scalars_dev leaves in dsum
+  const bool dg = dist_graph(p);
+  const double* sc = dg ? p->dsum : p->dscal;
   TVR_TRY(capture_body(p, body, nullptr, [&]() -> int {
     TVR_CUDA(launch_gpbb_begin(d, h, p->stream));
     TVR_TRY(capture_conditional(p, h.ls, cudaGraphCondTypeWhile, &body_ls));
@@ -313,20 +347,23 @@ static int gpbb_device(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_
   TVR_TRY(capture_body(p, body_ls, &bytes_ls, [&]() -> int {
     TVR_TRY(pass_tv_trial(p, x_cur, g_cur, 0.0, v, 1.0 /* stop: decided on the device */, nullptr,
                           S_TV, d->dparam));
+    TVR_TRY(halo_fill_trial(p, x_cur, g_cur, 0.0, v, d->dparam));
     TVR_TRY(pass_residual(p, v, r_trial, S_RSQ));
-    TVR_CUDA(launch_gpbb_ls(d, p->dscal, h, p->stream));
+    if (dg) TVR_TRY(dist_scalars_dev(p, nullptr, S_COUNT));
+    TVR_CUDA(launch_gpbb_ls(d, sc, h, p->stream));
     return TVR_OK;
   }));
   // accepted step: rotate the state by copies, gradient at x_{k+1} with BB reductions
   TVR_TRY(capture_body(p, body_acc, &bytes_acc, [&]() -> int {
     TVR_CUDA(cudaMemcpyAsync(x_prev, x_cur, vb, cudaMemcpyDeviceToDevice, p->stream));
     TVR_CUDA(cudaMemcpyAsync(g_prev, g_cur, vb, cudaMemcpyDeviceToDevice, p->stream));
-    TVR_CUDA(cudaMemcpyAsync(x_cur, v, vb, cudaMemcpyDeviceToDevice, p->stream));
+    TVR_TRY(copy_vol(p, x_cur, v, true));  // the trial's halo planes are x_{k+1}'s
     TVR_CUDA(cudaMemcpyAsync(r_cur, r_trial, db, cudaMemcpyDeviceToDevice, p->stream));
     TVR_TRY(pass_AT(p, r_cur, w));
     TVR_TRY(pass_tv_grad(p, x_cur, nullptr, 0.0, w, nullptr, 0.0, g_cur, nullptr, x_prev, g_prev,
                          0.0, S_TV));
-    TVR_CUDA(launch_gpbb_accept(d, p->dscal, p->stream));
+    if (dg) TVR_TRY(dist_scalars_dev(p, g_cur, S_COUNT));  // g_{k+1}'s halo planes + BB sums
+    TVR_CUDA(launch_gpbb_accept(d, sc, p->stream));
     return TVR_OK;
   }));
   TVR_CUDA(cudaGraphInstantiate(&gg.ex, gg.g, 0));
@@ -341,6 +378,11 @@ static int gpbb_device(tvr_problem* p, float* x_io, const tvr_gpbb_opts& o, tvr_
   rec.n = hd.n_rec;
   p->bytes_total += (double)hd.ls_execs * bytes_ls + (double)hd.n_g * (bytes_acc + 4.0 * vb + 2.0 * db);
   p->launches += 2 * hd.ls_execs + 3 * hd.n_g;
+  if (dg) {
+    ++p->n_dist_graph;
+    p->n_dist_exch += hd.ls_execs + hd.n_g;
+    p->launches += hd.ls_execs + hd.n_g;  // the rank-sum kernels
+  }
   if (res) {
     res->converged = hd.conv ? 1 : 0;
     res->iters = hd.k;
@@ -382,8 +424,8 @@ static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnS
   hd.rec = drec;
   const size_t vb = sizeof(float) * p->n, db = sizeof(float) * p->m;
   // y_1 = x_1 lives in ybuf (and y_lo) from here on
-  TVR_CUDA(cudaMemcpyAsync(st.ybuf, st.xk, vb, cudaMemcpyDeviceToDevice, p->stream));
-  TVR_CUDA(cudaMemcpyAsync(st.y_lo, st.xk_lo, vb, cudaMemcpyDeviceToDevice, p->stream));
+  TVR_TRY(copy_vol(p, st.ybuf, st.xk, true));
+  TVR_TRY(copy_vol(p, st.y_lo, st.xk_lo, true));
   TVR_CUDA(cudaMemcpyAsync(d, &hd, sizeof(hd), cudaMemcpyHostToDevice, p->stream));
   TVR_CUDA(cudaStreamSynchronize(p->stream));
 
@@ -402,6 +444,8 @@ static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnS
   TVR_CUDA(cudaGraphConditionalHandleCreate(&h.bt, body, 0, 0));
   TVR_CUDA(cudaGraphConditionalHandleCreate(&h.rest, body, 0, 0));
   double bytes_bt = 0.0, bytes_rest = 0.0;
+  const bool dg = dist_graph(p);  // as gpbb_device
+  const double* sc = dg ? p->dsum : p->dscal;
   TVR_TRY(capture_body(p, body, nullptr, [&]() -> int {
     TVR_CUDA(launch_upn_bt_begin(d, h, p->stream));
     TVR_TRY(capture_conditional(p, h.bt, cudaGraphCondTypeWhile, &body_bt));
@@ -413,8 +457,10 @@ static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnS
   TVR_TRY(capture_body(p, body_bt, &bytes_bt, [&]() -> int {
     TVR_TRY(pass_tv_trial_x(p, st.ybuf, st.y_lo, st.gy, 0.0, st.xn, st.xn_lo, st.xk, st.xk_lo,
                             S_TV, d->dp_trial));
+    TVR_TRY(halo_fill_trial_x(p, st.ybuf, st.y_lo, st.gy, 0.0, st.xn, st.xn_lo, d->dp_trial));
     TVR_TRY(pass_residual(p, st.xn, st.rn, S_RSQ, st.rn_lo, p->ext_on ? st.xn_lo : nullptr));
-    TVR_CUDA(launch_upn_bt(d, p->dscal, h, p->stream));
+    if (dg) TVR_TRY(dist_scalars_dev(p, nullptr, S_COUNT));
+    TVR_CUDA(launch_upn_bt(d, sc, h, p->stream));
     return TVR_OK;
   }));
   // w_{k+1}, stop reduction at x_{k+1}, y_{k+1} with f(y), grad f(y) by linearity (a6)
@@ -429,12 +475,15 @@ static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnS
     TVR_TRY(pass_momentum(p, st.rn, st.rn_lo, st.rk, st.rk_lo, 0.0, S_MOM, d->dp_mom));
     TVR_TRY(pass_tv_momentum_x(p, st.xn, st.xn_lo, st.xk, st.xk_lo, 0.0, st.wn, st.wk, st.gy,
                                st.ybuf, st.y_lo, S_TV2, d->dp_mom));
-    TVR_CUDA(cudaMemcpyAsync(st.xk, st.xn, vb, cudaMemcpyDeviceToDevice, p->stream));
-    TVR_CUDA(cudaMemcpyAsync(st.xk_lo, st.xn_lo, vb, cudaMemcpyDeviceToDevice, p->stream));
+    TVR_TRY(halo_fill_momentum_x(p, st.xn, st.xn_lo, st.xk, st.xk_lo, 0.0, st.ybuf, st.y_lo,
+                                 d->dp_mom));
+    if (dg) TVR_TRY(dist_scalars_dev(p, st.gy, S_COUNT));  // grad f(y_{k+1})'s halo planes + sums
+    TVR_TRY(copy_vol(p, st.xk, st.xn, true));
+    TVR_TRY(copy_vol(p, st.xk_lo, st.xn_lo, true));
     TVR_CUDA(cudaMemcpyAsync(st.rk, st.rn, db, cudaMemcpyDeviceToDevice, p->stream));
     TVR_CUDA(cudaMemcpyAsync(st.rk_lo, st.rn_lo, db, cudaMemcpyDeviceToDevice, p->stream));
     TVR_CUDA(cudaMemcpyAsync(st.wk, st.wn, vb, cudaMemcpyDeviceToDevice, p->stream));
-    TVR_CUDA(launch_upn_end(d, p->dscal, h, p->stream));
+    TVR_CUDA(launch_upn_end(d, sc, h, p->stream));
     return TVR_OK;
   }));
   TVR_CUDA(cudaGraphInstantiate(&gg.ex, gg.g, 0));
@@ -447,6 +496,11 @@ static int upn_device(tvr_problem* p, const tvr_upn_opts& o, Recorder& rec, UpnS
   rec.n += hd.n_rec;
   p->bytes_total += (double)hd.bt_execs * bytes_bt + (double)hd.n_g * (bytes_rest + 6.0 * vb + 4.0 * db);
   p->launches += 2 * hd.bt_execs + 5 * hd.n_g;
+  if (dg) {
+    ++p->n_dist_graph;
+    p->n_dist_exch += hd.bt_execs + hd.n_g;
+    p->launches += hd.bt_execs + hd.n_g;
+  }
   st.L = hd.L; st.mu = hd.mu; st.theta = hd.theta; st.fxk = hd.fxk; st.fy = hd.fy; st.gn = hd.gn;
   st.k = hd.k; st.n_f += hd.n_f; st.n_g += hd.n_g; st.n_ls += hd.n_ls; st.conv = hd.conv != 0;
   if (hd.status == TVR_E_NONFINITE) { set_error("UPN: non-finite objective"); *status = TVR_E_NONFINITE; }

@@ -63,7 +63,8 @@ class tvr_info(ctypes.Structure):
                 ("z1", c_i32), ("slab_staged_A", c_i32), ("slab_staged_AT", c_i32),
                 ("device_bytes", c_i64), ("n_cols_local", c_i64), ("views_fused_rs", c_i32),
                 ("slice_shared", c_i32), ("views_rep", c_i32), ("point_allgathers", c_i64),
-                ("gather_layout_blocks", c_i64 * 3)]
+                ("gather_layout_blocks", c_i64 * 3), ("dist_graph_solves", c_i64),
+                ("dist_graph_exchanges", c_i64)]
 
 
 class tvr_fparts(ctypes.Structure):
@@ -144,6 +145,7 @@ SIGNATURES = {
     "tvr_nccl_comm_init": (ctypes.c_int, [ctypes.POINTER(c_vp), c_vp, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int]),
     "tvr_nccl_comm_destroy": (ctypes.c_int, [c_vp]),
+    "tvr_rank_sum": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp]),
     "tvr_local_comm_create": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.c_int]),
     "tvr_local_comm_destroy": (ctypes.c_int, [c_vp]),
     "tvr_set_allocator": (ctypes.c_int, [ALLOC_FN, FREE_FN, c_vp]),
@@ -243,6 +245,12 @@ def nccl_comm_init(uid: bytes, world: int, rank: int, device: int) -> int:
 
 def nccl_comm_destroy(comm: int):
     _check(lib().tvr_nccl_comm_destroy(comm), "tvr_nccl_comm_destroy")
+
+
+def rank_sum(gathered_dev: int, world: int, n: int, out_dev: int, stream: int | None = None):
+    """tvr_rank_sum: out[s] = rank-ordered sum of gathered[r * n + s] on the device (device
+    pointers as ints)."""
+    _check(lib().tvr_rank_sum(gathered_dev, world, n, out_dev, stream), "tvr_rank_sum")
 
 
 def local_comm_create(world: int) -> int:
