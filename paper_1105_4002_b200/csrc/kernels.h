@@ -112,10 +112,15 @@ struct SellArgs {
                             // c + 2G, ... of ilv blocks each (the grid sweeps the block order
                             // together: z-ordered blocks keep the gathered sub-volume in L2);
                             // 0 = one contiguous work-balanced range per CTA
+  const int64_t* cta_tab;   // non-null: the CTA ranges of a full-range launch with cta_tab_grid
+  int32_t cta_tab_grid;     // CTAs, precomputed at plan time (sell_cta_range's search results)
   double* partials;
   unsigned* counter;
   double* scal;
 };
+// tab[i], i = 0..grid: first virtual block of CTA i of a `grid`-CTA launch over [a.blk_lo,
+// a.blk_hi) (tab[grid] = a.blk_hi): exactly what the kernels' own range search returns
+cudaError_t launch_sell_cta_table(const SellArgs& a, int grid, int64_t* tab, cudaStream_t st);
 struct SellVariant {
   bool staged = true;
   bool half = false;

@@ -262,6 +262,10 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
         continue;
       }
       const int g = (int)std::min<int64_t>(pl.pad_grid, std::max<int64_t>(1, s.blk_hi - s.blk_lo));
+      if (z_hi < 0 && d.cta_tab && d.cta_tab_grid == g) {  // full range: plan-time CTA ranges
+        s.cta_tab = d.cta_tab;
+        s.cta_tab_grid = g;
+      }
       cudaError_t e = launch_spmv16s(s, pl.sv, g, pl.smem, p->stream);
       if (e != cudaSuccess) return e;
     }
@@ -746,6 +750,25 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
   pl.smem = smem;
   pl.pad_grid = (int)std::min<int64_t>((int64_t)p->num_sms * spmv16s_occupancy(v, smem),
                                        std::max<int64_t>(1, nblk * pl.rep));
+  // the CTA ranges of the full-range launch, searched once here instead of by every CTA of
+  // every launch (TVR_SELL_CTA_TAB=0: off)
+  const char* ct = std::getenv("TVR_SELL_CTA_TAB");
+  if (!(ct && *ct == '0')) {
+    for (auto& d : pl.sd) {
+      const int64_t hi = d.nblk * pl.rep;
+      if (hi <= 0) continue;
+      const int g = (int)std::min<int64_t>(pl.pad_grid, hi);
+      TVR_TRY(dev_alloc(p, (void**)&d.cta_tab, sizeof(int64_t) * (g + 1)));
+      SellArgs s{};
+      s.cum = d.cum;
+      s.nb = d.nblk;
+      s.rep = pl.rep;
+      s.blk_lo = 0;
+      s.blk_hi = hi;
+      TVR_CUDA(launch_sell_cta_table(s, g, d.cta_tab, p->stream));
+      d.cta_tab_grid = g;
+    }
+  }
   pl.sell = true;
   return TVR_OK;
 }

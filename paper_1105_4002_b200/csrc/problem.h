@@ -67,6 +67,8 @@ struct SellData {
   float* val = nullptr;
   int64_t* win_lo = nullptr;   // the plan's windows, shifted to the part
   int32_t* win_len = nullptr;
+  int64_t* cta_tab = nullptr;  // CTA ranges of the full-range launch (SellArgs::cta_tab)
+  int32_t cta_tab_grid = 0;
   std::vector<int64_t> h_slice_end;  // per slice: one past its last block
 };
 

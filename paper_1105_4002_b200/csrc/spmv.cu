@@ -606,6 +606,13 @@ __device__ __forceinline__ int64_t sell_lower_warp(const SellArgs& a, int64_t lo
 // The CTA's virtual block range [b0, b1): warps 0 and 1 search its two ends concurrently,
 // broadcast in shared memory (the same result as sell_lower).
 __device__ __forceinline__ void sell_cta_range(const SellArgs& a, int64_t& b0, int64_t& b1) {
+  // plan-time table of the same search (full-range launches): one load instead of the 2 x 4
+  // dependent probe rounds before the CTA streams anything
+  if (a.cta_tab && a.cta_tab_grid == (int32_t)gridDim.x) {
+    b0 = __ldg(a.cta_tab + blockIdx.x);
+    b1 = __ldg(a.cta_tab + blockIdx.x + 1);
+    return;
+  }
   __shared__ int64_t s_rng[2];
   const int warp = threadIdx.x >> 5;
   if (warp < 2) {
@@ -619,6 +626,22 @@ __device__ __forceinline__ void sell_cta_range(const SellArgs& a, int64_t& b0, i
   __syncthreads();
   b0 = s_rng[0];
   b1 = s_rng[1];
+}
+
+__global__ void sell_cta_table_kernel(SellArgs a, int grid, int64_t* tab) {
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // boundary, one per warp
+  if (i > grid) return;
+  const int64_t w0 = sell_work(a, a.blk_lo), W = sell_work(a, a.blk_hi) - w0;
+  int64_t v;
+  if (i == grid) v = a.blk_hi;
+  else v = sell_lower_warp(a, a.blk_lo, a.blk_hi, w0 + W * i / grid);
+  if ((threadIdx.x & 31) == 0) tab[i] = v;
+}
+cudaError_t launch_sell_cta_table(const SellArgs& a, int grid, int64_t* tab, cudaStream_t st) {
+  SellArgs b = a;
+  b.cta_tab = nullptr;
+  sell_cta_table_kernel<<<(grid + 1 + 7) / 8, 256, 0, st>>>(b, grid, tab);
+  return cudaGetLastError();
 }
 
 // LO: 0 = plain; 1 = + the lo parts gathered from global memory; 2 = + the lo window staged in
