@@ -3,7 +3,45 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <utility>
+
 namespace tvr {
+
+// Programmatic dependent launch (sm_90+): a kernel launched with launch_pdl may become resident
+// while its predecessor in the stream drains (after every predecessor CTA has issued pdl_trigger
+// or exited); it must call pdl_wait() before touching anything a predecessor writes -- the wait
+// returns once the predecessor grid has completed and its writes are visible.  Both are no-ops
+// in a launch without the attribute.  Eager launches only: under stream capture (solver and
+// pipeline graphs) the attribute is left off.  TVR_PDL=0 turns it off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TVR_PDL");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (pdl_enabled() && cudaStreamIsCapturing(st, &cs) == cudaSuccess &&
+      cs == cudaStreamCaptureStatusNone) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 constexpr int kMaxScalars = 8;  // fp64 scalars one reduction launch may produce
 

@@ -651,8 +651,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
   extern __shared__ float stage[];
   __shared__ int s_next;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
+  pdl_trigger();  // the next kernel may take this SM as soon as this CTA leaves it
   int64_t b0, b1;
-  sell_cta_range(a, b0, b1);
+  sell_cta_range(a, b0, b1);  // plan data only
+  pdl_wait();     // the gathered vector / partial sums are the previous kernel's
   double sq = 0.0;  // static assignment: this thread's rows; DYN: the CTA's total (thread 0)
   for (int64_t it = b0; it < b1;) {
     const int64_t rz = it / a.nb, zb = rz * a.nb;  // repetition (slice-shared operator) and base
@@ -1547,15 +1549,13 @@ cudaError_t launch_spmv16s(const SellArgs& a, const SellVariant& v, int grid, si
     return dispatch16s_lo(v, a.lo_off > 0, [&](auto k) -> cudaError_t {
       cudaError_t e = ensure_smem_attr((const void*)k, sm);
       if (e != cudaSuccess) return e;
-      k<<<grid, v.block, sm, st>>>(a);
-      return cudaGetLastError();
+      return launch_pdl(k, dim3(grid), dim3(v.block), sm, st, a);
     });
   }
   return dispatch16s(v, [&](auto k) -> cudaError_t {
     cudaError_t e = ensure_smem_attr((const void*)k, smem);
     if (e != cudaSuccess) return e;
-    k<<<grid, v.block, smem, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(k, dim3(grid), dim3(v.block), smem, st, a);
   });
 }
 
