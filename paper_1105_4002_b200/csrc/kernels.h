@@ -93,6 +93,8 @@ struct SellArgs {
   const float* src_lo;      // non-null: A (src + src_lo) (extended-precision solver iterates,
                             // DESIGN §5.3), the lo parts gathered from global memory, or staged
   int32_t lo_off;           // > 0: after the hi window, lo_off floats on (spmv16s_kernel)
+  int32_t dual_off;         // > 0: a second window (the CTA's next slice segment) is staged
+                            // dual_off floats on and walked together with the first
   const float* b;           // non-null: out = A src - b, sum r^2
   float* out;
   float* out_lo;
@@ -112,6 +114,7 @@ struct SellArgs {
                             // c + 2G, ... of ilv blocks each (the grid sweeps the block order
                             // together: z-ordered blocks keep the gathered sub-volume in L2);
                             // 0 = one contiguous work-balanced range per CTA
+  long long* cta_prof;      // diagnostic (TVR_SELL_PROF=1): per CTA start ns, end ns, SM id
   const int64_t* cta_tab;   // non-null: the CTA ranges of a full-range launch with cta_tab_grid
   int32_t cta_tab_grid;     // CTAs, precomputed at plan time (sell_cta_range's search results)
   double* partials;

@@ -1,6 +1,7 @@
 // libtvreg: problem creation, device memory, SpMV plans, pass functions and the C ABI
 // entry points other than the solvers (solvers.cu) and NCCL plumbing (dist.cu).
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -235,6 +236,13 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
       // pl.smem bytes, the lo one the same amount after it
       if (src_lo && pl.staged && !pl.sv.half && 2 * pl.smem + 2048 <= (size_t)p->max_smem_optin)
         s.lo_off = (int32_t)(pl.smem / sizeof(float));
+      // two slice windows side by side when they fit (c1, c2): a CTA whose block range crosses a
+      // slice boundary stages both segments at once (spmv16s_kernel DUAL; opt-in, TVR_SELL_DUAL=1:
+      // c2 A^T 160.2 -> 158.5 us, A pass equal -- the second 66 KB window costs the streaming loads L1)
+      static const bool dual_on = [] { const char* v = std::getenv("TVR_SELL_DUAL"); return v && *v == '1'; }();
+      if (dual_on && !src_lo && pl.staged && !pl.sv.half && pl.sv.dyn && pl.sv.zgroup <= 1 && pl.rep == 1 &&
+          P == 1 && 2 * pl.smem + 2048 <= (size_t)p->max_smem_optin)
+        s.dual_off = (int32_t)(pl.smem / sizeof(float));
       s.b = q == P - 1 ? b : nullptr;
       s.out = out;
       s.out_lo = q == P - 1 ? out_lo : nullptr;
@@ -266,8 +274,27 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
         s.cta_tab = d.cta_tab;
         s.cta_tab_grid = g;
       }
+      // diagnostic: per-CTA start / end times and SM ids of every full-range launch on stderr
+      static const bool cta_prof = [] { const char* v = std::getenv("TVR_SELL_PROF"); return v && *v == '1'; }();
+      static long long* prof_buf = nullptr;
+      if (cta_prof && z_hi < 0) {
+        if (!prof_buf) cudaMalloc(&prof_buf, sizeof(long long) * 3 * 1024);
+        s.cta_prof = prof_buf;
+      }
       cudaError_t e = launch_spmv16s(s, pl.sv, g, pl.smem, p->stream);
       if (e != cudaSuccess) return e;
+      if (s.cta_prof) {
+        std::vector<long long> hb(3 * 1024);
+        cudaMemcpyAsync(hb.data(), prof_buf, sizeof(long long) * 3 * g, cudaMemcpyDeviceToHost, p->stream);
+        cudaStreamSynchronize(p->stream);
+        const long long* prof_buf = hb.data();
+        long long t0 = prof_buf[0], t1 = 0;
+        for (int i = 0; i < g; ++i) { t0 = std::min(t0, prof_buf[3 * i]); t1 = std::max(t1, prof_buf[3 * i + 1]); }
+        std::fprintf(stderr, "SELLPROF %s part %d grid %d span_ns %lld :", transposed ? "AT" : "A", q, g, t1 - t0);
+        for (int i = 0; i < g; ++i)
+          std::fprintf(stderr, " %lld,%lld,%lld", prof_buf[3 * i] - t0, prof_buf[3 * i + 1] - t0, prof_buf[3 * i + 2]);
+        std::fprintf(stderr, "\n");
+      }
     }
     return cudaSuccess;
   }
@@ -552,6 +579,134 @@ static int upload(tvr_problem* p, void** dst, const void* src, size_t bytes) {
   return TVR_OK;
 }
 
+// CTA block ranges by SIMULATED MAKESPAN (round 2).  The sliced-ELL kernel walks a CTA's range
+// slice segment by slice segment (barrier, window restage), and inside a segment its warps take
+// blocks from a counter in stored order (longest rows of the slice first).  Equal work sums do
+// not finish together: a range that ends a few blocks into the next slice leaves most warps idle
+// while a handful run that slice's longest blocks (c2 A pass: CTA times 128-150 us around a
+// 139 us mean, the slow ones exactly those ranges, scripts/sell_prof.py).  So the ranges are cut
+// where the kernel's own schedule -- list scheduling of block costs (steps + blk_cost) on
+// `nwarps` warps per segment, seg_cost per segment -- reaches a common makespan T, the smallest
+// T (bisection) that needs no more than `grid` CTAs.  tab[i] = first block of CTA i, tab[grid] =
+// nblk.
+static std::vector<int64_t> makespan_partition(const std::vector<int32_t>& k,
+                                               const std::vector<int32_t>& slice, int nwarps,
+                                               int grid, double blk_cost, double seg_cost,
+                                               double lambda) {
+  const int64_t nb = (int64_t)k.size();
+  std::vector<double> heap((size_t)nwarps);
+  // Incremental cost of a range that grows block by block: lambda x simulated makespan +
+  // (1 - lambda) x work sum per warp (the pass is bandwidth-bound, so a CTA's idle warps are
+  // partly made up by the other SMs: measured CTA times lie between the two models).
+  struct Sim {
+    double seg_base, seg_max, work;
+    int cur_slice;
+    int64_t taken;
+  };
+  auto reset = [&](Sim& m, int sl) {
+    m.seg_base = seg_cost;
+    m.seg_max = 0.0;
+    m.work = seg_cost * nwarps;
+    m.cur_slice = sl;
+    m.taken = 0;
+    std::fill(heap.begin(), heap.end(), 0.0);
+  };
+  // cost if block i were added (does not modify); commit = true adds it
+  auto add = [&](Sim& m, int64_t i, bool commit) -> double {
+    double sb = m.seg_base, sm = m.seg_max, wk = m.work;
+    const bool new_seg = slice[i] != m.cur_slice;
+    if (new_seg) {  // barrier: the next segment starts when the current one has drained
+      sb = m.seg_base + m.seg_max + seg_cost;
+      sm = 0.0;
+      wk += seg_cost * nwarps;
+    }
+    const double c = (double)k[i] + blk_cost;
+    const double fin = (new_seg ? 0.0 : heap.front()) + c;  // earliest-free warp takes the block
+    wk += c;
+    const double cost = lambda * (sb + std::max(sm, fin)) + (1.0 - lambda) * wk / nwarps;
+    if (commit) {
+      if (new_seg) {
+        std::fill(heap.begin(), heap.end(), 0.0);
+        m.cur_slice = slice[i];
+      }
+      std::pop_heap(heap.begin(), heap.end(), std::greater<double>());
+      heap.back() = fin;
+      std::push_heap(heap.begin(), heap.end(), std::greater<double>());
+      m.seg_base = sb;
+      m.seg_max = std::max(sm, fin);
+      m.work = wk;
+      ++m.taken;
+    }
+    return cost;
+  };
+  auto range_cost = [&](int64_t b0, int64_t b1) -> double {
+    if (b1 <= b0) return 0.0;
+    Sim m;
+    reset(m, slice[b0]);
+    double c = 0.0;
+    for (int64_t i = b0; i < b1; ++i) c = add(m, i, true);
+    return c;
+  };
+  auto cut = [&](double T, std::vector<int64_t>* out) -> int64_t {
+    // greedy: extend the current CTA block by block while its cost stays <= T
+    int64_t ctas = 0, i = 0;
+    if (out) out->assign(1, 0);
+    Sim m;
+    while (i < nb) {
+      ++ctas;
+      reset(m, slice[i]);
+      while (i < nb) {
+        if (m.taken > 0 && add(m, i, false) > T) break;
+        add(m, i, true);
+        ++i;
+      }
+      if (out) out->push_back(i);
+    }
+    return ctas;
+  };
+  double total = 0.0, longest = 0.0;
+  for (int64_t i = 0; i < nb; ++i) {
+    total += k[i] + blk_cost;
+    longest = std::max(longest, (double)k[i] + blk_cost);
+  }
+  double lo = total / ((double)grid * nwarps), hi = 2.0 * lo + 4.0 * (longest + seg_cost) + 1.0;
+  while (cut(hi, nullptr) > grid) hi *= 2.0;
+  for (int it = 0; it < 40 && hi - lo > 1e-3 * hi; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (cut(mid, nullptr) <= grid) hi = mid;
+    else lo = mid;
+  }
+  std::vector<int64_t> tab;
+  cut(hi, &tab);
+  // the greedy cut may need fewer CTAs than the grid has (its count jumps with T): halve the
+  // costliest ranges until every CTA has one
+  while ((int64_t)tab.size() - 1 < grid) {
+    size_t worst = 0;
+    double wc = -1.0;
+    for (size_t c = 0; c + 1 < tab.size(); ++c) {
+      if (tab[c + 1] - tab[c] < 2) continue;
+      const double rc = range_cost(tab[c], tab[c + 1]);
+      if (rc > wc) { wc = rc; worst = c; }
+    }
+    if (wc < 0.0) break;  // nothing left to split
+    const int64_t b0 = tab[worst], b1 = tab[worst + 1];
+    int64_t best = b0 + 1;
+    double bc = 1e300;
+    int64_t lo_b = b0 + 1, hi_b = b1 - 1;  // the cut where both halves cost the same (bisection)
+    while (lo_b <= hi_b) {
+      const int64_t mid = (lo_b + hi_b) / 2;
+      const double c0 = range_cost(b0, mid), c1 = range_cost(mid, b1);
+      if (std::max(c0, c1) < bc) { bc = std::max(c0, c1); best = mid; }
+      if (c0 < c1) lo_b = mid + 1;
+      else hi_b = mid - 1;
+    }
+    tab.insert(tab.begin() + (std::ptrdiff_t)worst + 1, best);
+  }
+  tab.resize((size_t)grid + 1, nb);
+  tab[(size_t)grid] = nb;
+  return tab;
+}
+
 // One sliced-ELL structure: per slice (prow / psl: the per-row plan's items), rows stably sorted
 // by 8-entry chunk count of `lens` (descending) in blocks of 32; entries [lo_off, hi_off) of each
 // row with coff subtracted from the offsets; the windows shifted by coff and clipped to part_h
@@ -605,6 +760,8 @@ static int build_sell_data(tvr_problem* p, SpmvPlan& pl, bool transposed,
   TVR_TRY(upload(p, (void**)&d.off, off.data(), sizeof(int64_t) * off.size()));
   TVR_TRY(upload(p, (void**)&d.k, kk.data(), sizeof(int32_t) * kk.size()));
   TVR_TRY(upload(p, (void**)&d.slice, sl.data(), sizeof(int32_t) * sl.size()));
+  d.h_k = kk;
+  d.h_slice = sl;
   TVR_TRY(upload(p, (void**)&d.cum, cum.data(), sizeof(int64_t) * cum.size()));
   TVR_TRY(upload(p, (void**)&d.zend, zend.data(), sizeof(int64_t) * zend.size()));
   TVR_TRY(upload(p, (void**)&d.win_lo, wl.data(), sizeof(int64_t) * wl.size()));
@@ -759,13 +916,29 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
       if (hi <= 0) continue;
       const int g = (int)std::min<int64_t>(pl.pad_grid, hi);
       TVR_TRY(dev_alloc(p, (void**)&d.cta_tab, sizeof(int64_t) * (g + 1)));
-      SellArgs s{};
-      s.cum = d.cum;
-      s.nb = d.nblk;
-      s.rep = pl.rep;
-      s.blk_lo = 0;
-      s.blk_hi = hi;
-      TVR_CUDA(launch_sell_cta_table(s, g, d.cta_tab, p->stream));
+      // one repetition, counter-scheduled warps: ranges of equal simulated makespan
+      // (TVR_SELL_MAKESPAN=0: the work-sum split); else the kernels' own search, tabulated
+      // -- where a CTA has few enough blocks for its schedule's tails to matter (c2: 290-440 per
+      // CTA, A 165.5 -> 162.1 us, A^T 160.2 -> 158.6 us; c3's 1,800-3,500 per CTA: work sums, the
+      // model's error there cost the A pass 1.7 %)
+      const int mk = env_int("TVR_SELL_MAKESPAN", 1);
+      if (pl.rep == 1 && v.dyn && mk != 0 && (int64_t)d.h_k.size() == d.nblk &&
+          (mk == 2 || d.nblk < (int64_t)1024 * g)) {
+        const std::vector<int64_t> tab = makespan_partition(
+            d.h_k, d.h_slice, v.block / 32, g, (double)env_int("TVR_SELL_BLKCOST", 2),
+            (double)env_int("TVR_SELL_SEGCOST", 3), 0.01 * env_int("TVR_SELL_MK_LAMBDA", 50));
+        TVR_CUDA(cudaMemcpyAsync(d.cta_tab, tab.data(), sizeof(int64_t) * (g + 1),
+                                 cudaMemcpyHostToDevice, p->stream));
+        TVR_CUDA(cudaStreamSynchronize(p->stream));  // tab is a local
+      } else {
+        SellArgs s{};
+        s.cum = d.cum;
+        s.nb = d.nblk;
+        s.rep = pl.rep;
+        s.blk_lo = 0;
+        s.blk_hi = hi;
+        TVR_CUDA(launch_sell_cta_table(s, g, d.cta_tab, p->stream));
+      }
       d.cta_tab_grid = g;
     }
   }

@@ -69,6 +69,7 @@ struct SellData {
   int32_t* win_len = nullptr;
   int64_t* cta_tab = nullptr;  // CTA ranges of the full-range launch (SellArgs::cta_tab)
   int32_t cta_tab_grid = 0;
+  std::vector<int32_t> h_k, h_slice;  // host copies: chunk steps and slice of every block
   std::vector<int64_t> h_slice_end;  // per slice: one past its last block
 };
 

@@ -34,6 +34,7 @@ __device__ __forceinline__ int swz(int c) { return c + (c >> 5); }
 // The block size is a multiple of 32, so slot swz(i + blockDim) = swz(i) + blockDim * 33 / 32:
 // both addresses advance by a constant (a few instructions per copy instead of a recomputed
 // 64-bit address and swizzle).
+template <bool WAIT = true>
 __device__ __forceinline__ void stage_window(float* stage, const float* __restrict__ g, int len) {
   const int step = blockDim.x;
   uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + swz(threadIdx.x));
@@ -43,7 +44,7 @@ __device__ __forceinline__ void stage_window(float* stage, const float* __restri
 #pragma unroll 4
   for (; n > 0; --n, dst += dstep, src += step)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  if constexpr (WAIT) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // Accumulate the (up to) 4 entries of one lane's 16-byte chunk that fall inside the row:
@@ -655,6 +656,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
   int64_t b0, b1;
   sell_cta_range(a, b0, b1);  // plan data only
   pdl_wait();     // the gathered vector / partial sums are the previous kernel's
+  if (a.cta_prof && threadIdx.x == 0) {
+    long long t;
+    unsigned sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    a.cta_prof[3 * blockIdx.x] = t;
+    a.cta_prof[3 * blockIdx.x + 2] = sm;
+  }
   double sq = 0.0;  // static assignment: this thread's rows; DYN: the CTA's total (thread 0)
   for (int64_t it = b0; it < b1;) {
     const int64_t rz = it / a.nb, zb = rz * a.nb;  // repetition (slice-shared operator) and base
@@ -663,37 +672,60 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
     const float* gbase = a.src + a.win_lo[z] + rz * a.rep_win;
     const float* lbase = LO != 0 ? a.src_lo + a.win_lo[z] + rz * a.rep_win : nullptr;
     const int64_t row_off = rz * a.rep_rows;
+    // DUAL (a.dual_off > 0: two windows fit, one repetition): the CTA's next slice segment
+    // [it_end, it2_end) is staged beside this one and both are walked from ONE block counter --
+    // no barrier, restage and idle warps where the CTA's range crosses a slice boundary.  The
+    // next slice's blocks (its longest rows) are taken first, this slice's tail (its shortest)
+    // last, so the CTA still ends on short blocks.
+    int64_t it2_end = it_end;
+    if constexpr (STAGED && DYN && !HALF && LO == 0) {
+      if (a.dual_off > 0 && it_end < b1) it2_end = min(b1, a.zend[a.blk_slice[it_end]]);
+    }
+    const int64_t n2 = it2_end - it_end, ntot = it2_end - it;
     if (STAGED || DYN) __syncthreads();  // previous segment done: window and counter reusable
     if (DYN && threadIdx.x == 0) s_next = nwarps;
+    if constexpr (STAGED && DYN && !HALF && LO == 0) {
+      if (n2 > 0) {  // both windows' copies in flight together
+        const int z2 = a.blk_slice[it_end];
+        stage_window<false>(stage + a.dual_off, a.src + a.win_lo[z2], a.win_len[z2]);
+      }
+    }
     if constexpr (STAGED) stage_window(stage, gbase, HALF ? min(a.win_len[z], a.part_len) : a.win_len[z]);
     if constexpr (LO == 2) stage_window(stage + a.lo_off, lbase, a.win_len[z]);
     if (STAGED || DYN) __syncthreads();
     // DYN: warps take the segment's blocks from a shared counter (blocks are sorted by length
     // inside a slice, so this is longest-first list scheduling); the next block's descriptors are
     // loaded while the current block streams
-    int64_t k = it + warp;
+    // position j of the walk -> block: the second segment's n2 blocks first, then this one's
+    int64_t j = warp;
+    int64_t k = j < n2 ? it_end + j : it + (j - n2);
     int64_t off = 0;
     int K = 0, row = -1;
-    if (k < it_end) {
+    if (j < ntot) {
       off = a.blk_off[k - zb];
       K = a.blk_k[k - zb];
       row = a.perm[(k - zb) * 32 + lane];
     }
-    while (k < it_end) {
-      int64_t kn;
+    while (j < ntot) {
+      int64_t jn;
       if constexpr (DYN) {
         int nx = 0;
         if (lane == 0) nx = atomicAdd(&s_next, 1);
-        kn = it + __shfl_sync(0xffffffffu, nx, 0);
+        jn = __shfl_sync(0xffffffffu, nx, 0);
       } else {
-        kn = k + nwarps;
+        jn = j + nwarps;
       }
+      const int64_t kn = jn < n2 ? it_end + jn : it + (jn - n2);
       int64_t off_n = 0;
       int K_n = 0, row_n = -1;
-      if (kn < it_end) {
+      if (jn < ntot) {
         off_n = a.blk_off[kn - zb];
         K_n = a.blk_k[kn - zb];
         row_n = a.perm[(kn - zb) * 32 + lane];
+      }
+      const float* win = stage;  // the staged window this block gathers from
+      if constexpr (STAGED && DYN && !HALF && LO == 0) {
+        if (j < n2) win = stage + a.dual_off;
       }
       const uint16_t* cp = a.col16 + (off * 32 + lane) * 8;
       const float* vp = a.val + (off * 32 + lane) * 8;
@@ -711,7 +743,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
           acc += HALF ? chunk8_sum_part(c[u], va[u], vb[u], stage, gbase, a.part_len)
-                      : chunk8_sum<STAGED>(c[u], va[u], vb[u], stage, gbase);
+                      : chunk8_sum<STAGED>(c[u], va[u], vb[u], win, gbase);
           if constexpr (LO == 1) acc += chunk8_sum_lo(c[u], va[u], vb[u], lbase);
           if constexpr (LO == 2) acc += chunk8_sum<true>(c[u], va[u], vb[u], stage + a.lo_off, lbase);
         }
@@ -721,7 +753,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
         const float4 va0 = ld_stream_f4(vp + s * 256);
         const float4 vb0 = ld_stream_f4(vp + s * 256 + 4);
         acc += HALF ? chunk8_sum_part(c0, va0, vb0, stage, gbase, a.part_len)
-                    : chunk8_sum<STAGED>(c0, va0, vb0, stage, gbase);
+                    : chunk8_sum<STAGED>(c0, va0, vb0, win, gbase);
         if constexpr (LO == 1) acc += chunk8_sum_lo(c0, va0, vb0, lbase);
         if constexpr (LO == 2) acc += chunk8_sum<true>(c0, va0, vb0, stage + a.lo_off, lbase);
       }
@@ -749,12 +781,21 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
           sq += q;
         }
       }
+      j = jn;
       k = kn;
       off = off_n;
       K = K_n;
       row = row_n;
     }
-    it = it_end;
+    it = it2_end;
+  }
+  if (a.cta_prof) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.cta_prof[3 * blockIdx.x + 1] = t;
+    }
   }
   if (a.scal) {
     if constexpr (DYN) {  // the CTA's blocks in block order: deterministic whatever warp ran them
@@ -1552,10 +1593,11 @@ cudaError_t launch_spmv16s(const SellArgs& a, const SellVariant& v, int grid, si
       return launch_pdl(k, dim3(grid), dim3(v.block), sm, st, a);
     });
   }
+  const size_t smd = a.dual_off > 0 ? smem + sizeof(float) * (size_t)a.dual_off : smem;
   return dispatch16s(v, [&](auto k) -> cudaError_t {
-    cudaError_t e = ensure_smem_attr((const void*)k, smem);
+    cudaError_t e = ensure_smem_attr((const void*)k, smd);
     if (e != cudaSuccess) return e;
-    return launch_pdl(k, dim3(grid), dim3(v.block), smem, st, a);
+    return launch_pdl(k, dim3(grid), dim3(v.block), smd, st, a);
   });
 }
 
