@@ -314,6 +314,16 @@ int64_t tvr_launch_count(const tvr_problem* p, int reset);
 enum { TVR_CONTROL_HOST = 0, TVR_CONTROL_DEVICE = 1, TVR_CONTROL_AUTO = 2 };
 int tvr_set_control(tvr_problem* p, int mode);
 
+/* Inspection hook of the plan builder (host only, no GPU): the CTA block ranges of a sliced-ELL
+ * pass (DESIGN §5.2 "CTA ranges by simulated makespan").  blk_steps[i] /
+ * blk_slice[i]: 8-entry chunk steps and slice of stored block i (slices ascending); a CTA's range
+ * is walked slice segment by slice segment, nwarps warps taking blocks in order.  tab_out
+ * (grid + 1 entries): tab_out[c] = first block of CTA c, tab_out[grid] = nblk, non-decreasing.
+ * Cost of a range = lambda x list-scheduled makespan + (1 - lambda) x work sum / nwarps, block
+ * cost = steps + blk_cost, seg_cost per segment.  TVR_E_ARG on NULL / out-of-range arguments. */
+int tvr_sell_partition(const int32_t* blk_steps, const int32_t* blk_slice, int64_t nblk, int nwarps,
+                       int grid, double blk_cost, double seg_cost, double lambda, int64_t* tab_out);
+
 /* Inspection hook of the distributed device control: out_dev[s] = sum over r (in rank order,
  * starting from +0.0) of gathered_dev[r * n + s], the kernel the solver graphs run after the
  * scalar all-gather (fixed-order fp64 sums).  Device pointers; synchronises

@@ -1764,6 +1764,19 @@ int tvr_create_sliced(tvr_problem** out, const tvr_csr* A_slice, const float* b_
   return TVR_OK;
 }
 
+int tvr_sell_partition(const int32_t* blk_steps, const int32_t* blk_slice, int64_t nblk, int nwarps,
+                       int grid, double blk_cost, double seg_cost, double lambda, int64_t* tab_out) {
+  if (!blk_steps || !blk_slice || !tab_out || nblk < 0 || nwarps < 1 || grid < 1 ||
+      !(lambda >= 0.0 && lambda <= 1.0) || !(blk_cost >= 0.0) || !(seg_cost >= 0.0)) {
+    set_error("tvr_sell_partition: bad arguments");
+    return TVR_E_ARG;
+  }
+  const std::vector<int32_t> k(blk_steps, blk_steps + nblk), sl(blk_slice, blk_slice + nblk);
+  const std::vector<int64_t> tab = makespan_partition(k, sl, nwarps, grid, blk_cost, seg_cost, lambda);
+  std::copy(tab.begin(), tab.end(), tab_out);
+  return TVR_OK;
+}
+
 int tvr_get_info(const tvr_problem* p, tvr_info* info) {
   if (!p || !info) { set_error("tvr_get_info: NULL"); return TVR_E_ARG; }
   info->m_local = p->m;

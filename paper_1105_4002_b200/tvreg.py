@@ -146,6 +146,8 @@ SIGNATURES = {
                                           ctypes.c_int]),
     "tvr_nccl_comm_destroy": (ctypes.c_int, [c_vp]),
     "tvr_rank_sum": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp]),
+    "tvr_sell_partition": (ctypes.c_int, [c_vp, c_vp, c_i64, ctypes.c_int, ctypes.c_int, c_f64,
+                                          c_f64, c_f64, c_vp]),
     "tvr_local_comm_create": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.c_int]),
     "tvr_local_comm_destroy": (ctypes.c_int, [c_vp]),
     "tvr_set_allocator": (ctypes.c_int, [ALLOC_FN, FREE_FN, c_vp]),
@@ -251,6 +253,17 @@ def rank_sum(gathered_dev: int, world: int, n: int, out_dev: int, stream: int | 
     """tvr_rank_sum: out[s] = rank-ordered sum of gathered[r * n + s] on the device (device
     pointers as ints)."""
     _check(lib().tvr_rank_sum(gathered_dev, world, n, out_dev, stream), "tvr_rank_sum")
+
+
+def sell_partition(blk_steps, blk_slice, nwarps: int, grid: int, blk_cost: float = 2.0,
+                   seg_cost: float = 3.0, lam: float = 0.5) -> np.ndarray:
+    """tvr_sell_partition (host only): CTA block ranges of a sliced-ELL pass."""
+    k = np.ascontiguousarray(blk_steps, np.int32)
+    sl = np.ascontiguousarray(blk_slice, np.int32)
+    tab = np.empty(grid + 1, np.int64)
+    _check(lib().tvr_sell_partition(k.ctypes.data, sl.ctypes.data, len(k), nwarps, grid, blk_cost,
+                                    seg_cost, lam, tab.ctypes.data), "tvr_sell_partition")
+    return tab
 
 
 def local_comm_create(world: int) -> int:
