@@ -93,8 +93,6 @@ struct SellArgs {
   const float* src_lo;      // non-null: A (src + src_lo) (extended-precision solver iterates,
                             // DESIGN §5.3), the lo parts gathered from global memory, or staged
   int32_t lo_off;           // > 0: after the hi window, lo_off floats on (spmv16s_kernel)
-  int32_t dual_off;         // > 0: a second window (the CTA's next slice segment) is staged
-                            // dual_off floats on and walked together with the first
   const float* b;           // non-null: out = A src - b, sum r^2
   float* out;
   float* out_lo;

@@ -236,13 +236,6 @@ static cudaError_t run_spmv(tvr_problem* p, const SpmvPlan& pl, bool transposed,
       // pl.smem bytes, the lo one the same amount after it
       if (src_lo && pl.staged && !pl.sv.half && 2 * pl.smem + 2048 <= (size_t)p->max_smem_optin)
         s.lo_off = (int32_t)(pl.smem / sizeof(float));
-      // two slice windows side by side when they fit (c1, c2): a CTA whose block range crosses a
-      // slice boundary stages both segments at once (spmv16s_kernel DUAL; opt-in, TVR_SELL_DUAL=1:
-      // c2 A^T 160.2 -> 158.5 us, A pass equal -- the second 66 KB window costs the streaming loads L1)
-      static const bool dual_on = [] { const char* v = std::getenv("TVR_SELL_DUAL"); return v && *v == '1'; }();
-      if (dual_on && !src_lo && pl.staged && !pl.sv.half && pl.sv.dyn && pl.sv.zgroup <= 1 && pl.rep == 1 &&
-          P == 1 && 2 * pl.smem + 2048 <= (size_t)p->max_smem_optin)
-        s.dual_off = (int32_t)(pl.smem / sizeof(float));
       s.b = q == P - 1 ? b : nullptr;
       s.out = out;
       s.out_lo = q == P - 1 ? out_lo : nullptr;

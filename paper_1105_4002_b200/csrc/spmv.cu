@@ -672,60 +672,37 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
     const float* gbase = a.src + a.win_lo[z] + rz * a.rep_win;
     const float* lbase = LO != 0 ? a.src_lo + a.win_lo[z] + rz * a.rep_win : nullptr;
     const int64_t row_off = rz * a.rep_rows;
-    // DUAL (a.dual_off > 0: two windows fit, one repetition): the CTA's next slice segment
-    // [it_end, it2_end) is staged beside this one and both are walked from ONE block counter --
-    // no barrier, restage and idle warps where the CTA's range crosses a slice boundary.  The
-    // next slice's blocks (its longest rows) are taken first, this slice's tail (its shortest)
-    // last, so the CTA still ends on short blocks.
-    int64_t it2_end = it_end;
-    if constexpr (STAGED && DYN && !HALF && LO == 0) {
-      if (a.dual_off > 0 && it_end < b1) it2_end = min(b1, a.zend[a.blk_slice[it_end]]);
-    }
-    const int64_t n2 = it2_end - it_end, ntot = it2_end - it;
     if (STAGED || DYN) __syncthreads();  // previous segment done: window and counter reusable
     if (DYN && threadIdx.x == 0) s_next = nwarps;
-    if constexpr (STAGED && DYN && !HALF && LO == 0) {
-      if (n2 > 0) {  // both windows' copies in flight together
-        const int z2 = a.blk_slice[it_end];
-        stage_window<false>(stage + a.dual_off, a.src + a.win_lo[z2], a.win_len[z2]);
-      }
-    }
     if constexpr (STAGED) stage_window(stage, gbase, HALF ? min(a.win_len[z], a.part_len) : a.win_len[z]);
     if constexpr (LO == 2) stage_window(stage + a.lo_off, lbase, a.win_len[z]);
     if (STAGED || DYN) __syncthreads();
     // DYN: warps take the segment's blocks from a shared counter (blocks are sorted by length
     // inside a slice, so this is longest-first list scheduling); the next block's descriptors are
     // loaded while the current block streams
-    // position j of the walk -> block: the second segment's n2 blocks first, then this one's
-    int64_t j = warp;
-    int64_t k = j < n2 ? it_end + j : it + (j - n2);
+    int64_t k = it + warp;
     int64_t off = 0;
     int K = 0, row = -1;
-    if (j < ntot) {
+    if (k < it_end) {
       off = a.blk_off[k - zb];
       K = a.blk_k[k - zb];
       row = a.perm[(k - zb) * 32 + lane];
     }
-    while (j < ntot) {
-      int64_t jn;
+    while (k < it_end) {
+      int64_t kn;
       if constexpr (DYN) {
         int nx = 0;
         if (lane == 0) nx = atomicAdd(&s_next, 1);
-        jn = __shfl_sync(0xffffffffu, nx, 0);
+        kn = it + __shfl_sync(0xffffffffu, nx, 0);
       } else {
-        jn = j + nwarps;
+        kn = k + nwarps;
       }
-      const int64_t kn = jn < n2 ? it_end + jn : it + (jn - n2);
       int64_t off_n = 0;
       int K_n = 0, row_n = -1;
-      if (jn < ntot) {
+      if (kn < it_end) {
         off_n = a.blk_off[kn - zb];
         K_n = a.blk_k[kn - zb];
         row_n = a.perm[(kn - zb) * 32 + lane];
-      }
-      const float* win = stage;  // the staged window this block gathers from
-      if constexpr (STAGED && DYN && !HALF && LO == 0) {
-        if (j < n2) win = stage + a.dual_off;
       }
       const uint16_t* cp = a.col16 + (off * 32 + lane) * 8;
       const float* vp = a.val + (off * 32 + lane) * 8;
@@ -743,7 +720,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
           acc += HALF ? chunk8_sum_part(c[u], va[u], vb[u], stage, gbase, a.part_len)
-                      : chunk8_sum<STAGED>(c[u], va[u], vb[u], win, gbase);
+                      : chunk8_sum<STAGED>(c[u], va[u], vb[u], stage, gbase);
           if constexpr (LO == 1) acc += chunk8_sum_lo(c[u], va[u], vb[u], lbase);
           if constexpr (LO == 2) acc += chunk8_sum<true>(c[u], va[u], vb[u], stage + a.lo_off, lbase);
         }
@@ -753,7 +730,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
         const float4 va0 = ld_stream_f4(vp + s * 256);
         const float4 vb0 = ld_stream_f4(vp + s * 256 + 4);
         acc += HALF ? chunk8_sum_part(c0, va0, vb0, stage, gbase, a.part_len)
-                    : chunk8_sum<STAGED>(c0, va0, vb0, win, gbase);
+                    : chunk8_sum<STAGED>(c0, va0, vb0, stage, gbase);
         if constexpr (LO == 1) acc += chunk8_sum_lo(c0, va0, vb0, lbase);
         if constexpr (LO == 2) acc += chunk8_sum<true>(c0, va0, vb0, stage + a.lo_off, lbase);
       }
@@ -781,13 +758,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
           sq += q;
         }
       }
-      j = jn;
       k = kn;
       off = off_n;
       K = K_n;
       row = row_n;
     }
-    it = it2_end;
+    it = it_end;
   }
   if (a.cta_prof) {
     __syncthreads();
@@ -1593,11 +1569,10 @@ cudaError_t launch_spmv16s(const SellArgs& a, const SellVariant& v, int grid, si
       return launch_pdl(k, dim3(grid), dim3(v.block), sm, st, a);
     });
   }
-  const size_t smd = a.dual_off > 0 ? smem + sizeof(float) * (size_t)a.dual_off : smem;
   return dispatch16s(v, [&](auto k) -> cudaError_t {
-    cudaError_t e = ensure_smem_attr((const void*)k, smd);
+    cudaError_t e = ensure_smem_attr((const void*)k, smem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(k, dim3(grid), dim3(v.block), smd, st, a);
+    return launch_pdl(k, dim3(grid), dim3(v.block), smem, st, a);
   });
 }
 
