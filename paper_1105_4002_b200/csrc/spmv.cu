@@ -801,8 +801,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16z_kernel(SellArgs a) {
   extern __shared__ float stage[];
   __shared__ int s_next;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
+  pdl_trigger();  // launched through launch_pdl like spmv16s_kernel: the wait is mandatory
   int64_t b0, b1;
   sell_cta_range(a, b0, b1);
+  pdl_wait();
   for (int64_t it = b0; it < b1;) {
     const int64_t rz = it / a.nb, zb = rz * a.nb;
     const int z = a.blk_slice[it - zb];
