@@ -606,10 +606,11 @@ __device__ __forceinline__ int64_t sell_lower_warp(const SellArgs& a, int64_t lo
 
 // The CTA's virtual block range [b0, b1): warps 0 and 1 search its two ends concurrently,
 // broadcast in shared memory (the same result as sell_lower).
+template <bool USE_TAB = true>
 __device__ __forceinline__ void sell_cta_range(const SellArgs& a, int64_t& b0, int64_t& b1) {
   // plan-time table of the same search (full-range launches): one load instead of the 2 x 4
   // dependent probe rounds before the CTA streams anything
-  if (a.cta_tab && a.cta_tab_grid == (int32_t)gridDim.x) {
+  if (USE_TAB && a.cta_tab && a.cta_tab_grid == (int32_t)gridDim.x) {
     b0 = __ldg(a.cta_tab + blockIdx.x);
     b1 = __ldg(a.cta_tab + blockIdx.x + 1);
     return;
@@ -654,9 +655,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = NT >> 5;
   pdl_trigger();  // the next kernel may take this SM as soon as this CTA leaves it
   int64_t b0, b1;
-  sell_cta_range(a, b0, b1);  // plan data only
+  sell_cta_range<LO != 2>(a, b0, b1);  // plan data only (LO == 2: no registers for the table path)
   pdl_wait();     // the gathered vector / partial sums are the previous kernel's
-  if (a.cta_prof && threadIdx.x == 0) {
+  if (LO == 0 && a.cta_prof && threadIdx.x == 0) {  // (the lo variants have no registers to spare)
     long long t;
     unsigned sm;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -765,7 +766,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmv16s_kernel(SellArgs a) {
     }
     it = it_end;
   }
-  if (a.cta_prof) {
+  if (LO == 0 && a.cta_prof) {
     __syncthreads();
     if (threadIdx.x == 0) {
       long long t;
