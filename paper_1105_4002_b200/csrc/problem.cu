@@ -918,7 +918,8 @@ static int make_sell(tvr_problem* p, SpmvPlan& pl, bool transposed, const std::v
       if (pl.rep == 1 && v.dyn && mk != 0 && (int64_t)d.h_k.size() == d.nblk &&
           (mk == 2 || d.nblk < (int64_t)1024 * g)) {
         const std::vector<int64_t> tab = makespan_partition(
-            d.h_k, d.h_slice, v.block / 32, g, (double)env_int("TVR_SELL_BLKCOST", 2),
+            d.h_k, d.h_slice, v.block / 32, g,
+            (double)env_int("TVR_SELL_MK_BLKCOST", 4),  // c2 A 160.2 -> 158.9 us against 2 (6: 159.8)
             (double)env_int("TVR_SELL_SEGCOST", 3), 0.01 * env_int("TVR_SELL_MK_LAMBDA", 50));
         TVR_CUDA(cudaMemcpyAsync(d.cta_tab, tab.data(), sizeof(int64_t) * (g + 1),
                                  cudaMemcpyHostToDevice, p->stream));
