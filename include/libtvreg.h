@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define TVR_ABI_VERSION 5
+#define TVR_ABI_VERSION 6
 
 typedef enum {
   TVR_OK = 0,

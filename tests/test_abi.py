@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(tvreg.SIGNATURES), set(names) ^ set(tvreg.SIGNATURES)
-    assert L.tvr_abi_version() == 5
+    assert L.tvr_abi_version() == 6
 
 
 def test_defaults_match_the_paper():
